@@ -1,0 +1,359 @@
+"""Brute-force CPU oracle for the chunk schedule of the AutoOverlap hot path.
+
+TEST INFRASTRUCTURE ONLY (see oracle/numeric.py header for who may import it).  This
+module shares no code with the C++ planner (paper_2601_20595_b200/csrc/planner.cpp);
+tests compare the two canonical JSON exports byte for byte.
+
+It follows, step by step, the paper's chunk-scheduling pipeline (§5.1-§5.2)
+as made concrete by SURVEY.md §8(c) rules 1-9 and the readings Q1-Q20 listed in
+DESIGN.md, deliberately by enumeration rather than closed forms:
+
+  1. Chunks    -- "a chunk is a logical block of data that is communicated as a unit"
+                  (P:288); row membership is enumerated row by row.
+  2. Plans     -- the communication schedule `schedule := [rank, List[CommOp]]`
+                  built as explicit per-rank op lists: the 1-D swizzle AllGather of
+                  Lst.2 (peer = (i + rank) mod W, reading Q1) and the owner-
+                  rotation ReduceScatter swizzle.
+  3. Arrival   -- a chunk's position = 1 + index of the op that delivers it, found by
+                  scanning the issuer's op list (P:295 push/pull: the op is recorded on
+                  exactly one side).
+  4. Deps      -- "for each tile, we determine which chunks it reads and writes based on
+                  its tile index and the tensor layout": tile rows are enumerated.
+  5. Group     -- a tile joins the latest chunk it needs.
+  6. Order     -- "reorder the sequence of waves so that each chunk is consumed as soon
+                  as it arrives, and apply an intra-chunk swizzle".
+  7. CTAs      -- static persistent stride `tile_id += NUM_SMS` of Lst.1.
+  8. Waits     -- "the minimal set of synchronization points ... a tile that consumes a
+                  given chunk cannot start until the corresponding communication operator
+                  has completed": one wait per (CTA, chunk) first use.
+  9. Signals   -- "global-memory signals": per-chunk flag words.
+
+Canonical export: JSON, sorted keys, no whitespace, integers only, strings only for
+enum names.  Parity: not applicable (exact).
+"""
+from __future__ import annotations
+
+import json
+import math
+
+# Tile shapes the kernel library implements, in the planner's candidate order
+# (BM, BN, cta_group).  Shared *specification* with the C++ planner (Q19);
+# each side types it independently.
+TILE_CANDIDATES = [(128, 256, 1), (128, 128, 1)]
+
+BK = 64  # K-block of the mainloop (TMA 128-B swizzle => 64 bf16), DESIGN.md
+
+
+def _ceil_div(a, b):
+    return -(-a // b)
+
+
+def default_desc(**kw):
+    d = dict(op="ag_gemm", world_size=2, rank=0, M=512, N=512, K=512, chunk_rows=64,
+             backend="ce", dir="push", chunk_order="shard_major", intra="row", group_m=1,
+             tile_m=0, tile_n=0, n_cta=0, comm_ctas=0, n_slices=1)
+    d.update(kw)
+    return d
+
+
+def validate(desc, sm_count=148):
+    """Violations as data.  Returns a list of strings, empty = valid."""
+    v = []
+    W, r = desc["world_size"], desc["rank"]
+    M, N, K, C = desc["M"], desc["N"], desc["K"], desc["chunk_rows"]
+    if desc["op"] not in ("ag_gemm", "gemm_rs"):
+        v.append("op")
+    if W < 1 or W > 8:
+        v.append("world_size")
+    if not (0 <= r < max(W, 1)):
+        v.append("rank")
+    if M < 0 or N < 0 or K < 0:
+        v.append("shape")
+    if W >= 1 and M % W != 0:
+        v.append("M % world_size")
+    S = M // W if W >= 1 else 0
+    if C <= 0 or C % 8 != 0 or (S > 0 and S % C != 0):
+        v.append("chunk_rows")
+    if K % 8 != 0:
+        v.append("K % 8")
+    if N % 8 != 0:
+        v.append("N % 8")
+    if desc["backend"] not in ("ce", "tma", "ldst"):
+        v.append("backend")
+    if desc["dir"] not in ("push", "pull"):
+        v.append("dir")
+    if desc["dir"] == "pull" and desc["op"] == "gemm_rs":
+        v.append("pull with gemm_rs")
+    if desc["chunk_order"] not in ("shard_major", "chunk_major"):
+        v.append("chunk_order")
+    if desc["intra"] not in ("row", "col", "grouped"):
+        v.append("intra")
+    if desc["intra"] == "grouped" and desc["group_m"] < 1:
+        v.append("group_m")
+    if desc["comm_ctas"] < 0 or desc["comm_ctas"] >= sm_count:
+        v.append("comm_ctas")
+    if desc["n_cta"] < 0:
+        v.append("n_cta")
+    if desc["n_slices"] < 1 or desc["n_slices"] > 64:
+        v.append("n_slices")
+    if (desc["tile_m"] == 0) != (desc["tile_n"] == 0):
+        v.append("tile")
+    if desc["tile_m"] and (desc["tile_m"], desc["tile_n"]) not in [(a, b) for a, b, _ in TILE_CANDIDATES]:
+        v.append("tile")
+    if not v and pick_tile(desc, sm_count) is None:
+        v.append("no tile shape fits")
+    return v
+
+
+def n_workers(desc, sm_count):
+    return desc["n_cta"] if desc["n_cta"] > 0 else sm_count - desc["comm_ctas"]
+
+
+def pick_tile(desc, sm_count):
+    """Tile shape: explicit, else argmax of wave-quantization utilization
+    util = T / (ceil(T/n) * n) (Fig.2a), ties -> larger BM*BN, then BN.
+    Enumerates every candidate (brute force over the candidate list)."""
+    W, M, N = desc["world_size"], desc["M"], desc["N"]
+    S = M // W
+    cands = TILE_CANDIDATES
+    if desc["tile_m"]:
+        cands = [c for c in TILE_CANDIDATES if (c[0], c[1]) == (desc["tile_m"], desc["tile_n"])]
+    best = None
+    for bm, bn, cg in cands:
+        if S % bm != 0:
+            continue
+        n = max(1, n_workers(desc, sm_count) // cg)
+        T = (M // bm) * _ceil_div(N, bn)
+        util = (T / (_ceil_div(T, n) * n)) if T > 0 else 1.0
+        key = (util, bm * bn, bn)
+        if best is None or key > best[0]:
+            best = (key, (bm, bn, cg))
+    return None if best is None else best[1]
+
+
+def _chunks(desc):
+    """Rule 1 by enumeration: row -> chunk membership, chunk -> (row0, rows, src/owner)."""
+    W, M, C = desc["world_size"], desc["M"], desc["chunk_rows"]
+    S = M // W
+    n_chunks = M // C if C > 0 else 0
+    row_chunk = [None] * M
+    rows_of = [[] for _ in range(n_chunks)]
+    for i in range(M):
+        g = i // C
+        row_chunk[i] = g
+        rows_of[g].append(i)
+    chunks = []
+    for g in range(n_chunks):
+        rows = rows_of[g]
+        row0 = rows[0]
+        owner = row0 // S  # the shard holding row0 (AG source / RS owner)
+        assert all(x // S == owner for x in rows), "chunk spans shards"
+        chunks.append((row0, len(rows), owner))
+    return chunks, row_chunk
+
+
+def _shard_chunks(chunks, p):
+    """Chunks of shard p in row order (their index j inside the shard)."""
+    return [g for g, (_, _, o) in enumerate(chunks) if o == p]
+
+
+def _build_plans(desc, chunks):
+    """Per-rank op lists -- 1-D swizzle AllGather (Lst.2) for AG, owner-rotation
+    ReduceScatter for RS.  Op dicts use SPEC's P2P fields."""
+    W = desc["world_size"]
+    plans = []
+    for q in range(W):
+        ops = []
+        if desc["op"] == "ag_gemm":
+            # Lst.2: for i in range(mesh): peer = (i + rank) % mesh; skip self (Q1).
+            peers = [(i + q) % W for i in range(W) if (i + q) % W != q]
+            if desc["dir"] == "push":
+                # push: q sends its own shard's chunks to each peer
+                per_peer = [(p, _shard_chunks(chunks, q)) for p in peers]
+            else:
+                # pull: q fetches each peer's shard chunks (Lst.2 TransferOp.PULL)
+                per_peer = [(p, _shard_chunks(chunks, p)) for p in peers]
+            seq = []
+            if desc["chunk_order"] == "shard_major":
+                for p, gs in per_peer:
+                    for g in gs:
+                        seq.append((p, g))
+            else:
+                n_c = len(per_peer[0][1]) if per_peer else 0
+                for j in range(n_c):
+                    for p, gs in per_peer:
+                        seq.append((p, gs[j]))
+            for p, g in seq:
+                row0, rows, _ = chunks[g]
+                ops.append({"accumulate": 0, "deps": [], "direction": desc["dir"], "dst_chunk": [row0, rows],
+                            "peer": p, "src_chunk": [row0, rows], "tensor": "A", "variant": "p2p"})
+        else:
+            # RS: owners q+1, ..., q+W-1, then q itself (own rows last, SURVEY rule 3)
+            owners = [(q + e + 1) % W for e in range(W)]
+            seq = []
+            if desc["chunk_order"] == "shard_major":
+                for o in owners:
+                    for g in _shard_chunks(chunks, o):
+                        seq.append((o, g))
+            else:
+                n_c = len(_shard_chunks(chunks, 0)) if W > 0 else 0
+                for j in range(n_c):
+                    for o in owners:
+                        seq.append((o, _shard_chunks(chunks, o)[j]))
+            for o, g in seq:
+                row0, rows, _ = chunks[g]
+                ops.append({"accumulate": 1, "deps": [], "direction": "push", "dst_chunk": [row0, rows],
+                            "peer": o, "src_chunk": [row0, rows], "tensor": "P", "variant": "p2p"})
+        plans.append(ops)
+    return plans
+
+
+def _arrival_pos(desc, chunks, plans):
+    """Rule 2/3: arrival position of every chunk at this rank, by scanning op lists."""
+    W, r = desc["world_size"], desc["rank"]
+    pos = []
+    for g, (row0, rows, owner) in enumerate(chunks):
+        if desc["op"] == "ag_gemm":
+            if owner == r:
+                pos.append(0)
+                continue
+            found = None
+            if desc["dir"] == "push":
+                for idx, op in enumerate(plans[owner]):
+                    if op["peer"] == r and op["src_chunk"] == [row0, rows]:
+                        found = idx
+                        break
+            else:
+                for idx, op in enumerate(plans[r]):
+                    if op["peer"] == owner and op["src_chunk"] == [row0, rows]:
+                        found = idx
+                        break
+            assert found is not None
+            pos.append(1 + found)
+        else:
+            found = None
+            for idx, op in enumerate(plans[r]):
+                if op["src_chunk"] == [row0, rows]:
+                    found = idx
+                    break
+            assert found is not None
+            pos.append(found)
+    return pos
+
+
+def _intra_key(desc, mb, nb):
+    if desc["intra"] == "row":
+        return (mb, nb)
+    if desc["intra"] == "col":
+        return (nb, mb)
+    gm = desc["group_m"]
+    return (mb // gm, nb, mb)
+
+
+def plan(desc, sm_count=148):
+    """Build the full canonical schedule for desc['rank'] (raises on invalid desc)."""
+    viol = validate(desc, sm_count)
+    if viol:
+        raise ValueError("invalid desc: " + ", ".join(viol))
+    W, r = desc["world_size"], desc["rank"]
+    M, N, K, C = desc["M"], desc["N"], desc["K"], desc["chunk_rows"]
+    S = M // W
+    bm, bn, cg = pick_tile(desc, sm_count)
+    nw = n_workers(desc, sm_count)
+    n_cta = max(1, nw // cg)
+    chunks, row_chunk = _chunks(desc)
+    plans = _build_plans(desc, chunks)
+    pos = _arrival_pos(desc, chunks, plans)
+    is_ag = desc["op"] == "ag_gemm"
+
+    n_mb, n_nb = M // bm, _ceil_div(N, bn)
+    T = n_mb * n_nb
+    deps = []
+    tile_chunks = []
+    group = []
+    for t in range(T):
+        mb, nb = divmod(t, n_nb)
+        gs = sorted({row_chunk[i] for i in range(mb * bm, min(M, (mb + 1) * bm))})
+        assert gs == list(range(gs[0], gs[-1] + 1))
+        tile_chunks.append(gs)
+        grp = max(pos[g] for g in gs)
+        group.append(grp)
+        deps.append([t, gs[0], gs[-1], grp])
+
+    keyed = []
+    for t in range(T):
+        mb, nb = divmod(t, n_nb)
+        keyed.append(((group[t],) + _intra_key(desc, mb, nb), t))
+    keyed.sort(key=lambda x: x[0])
+    order = [t for _, t in keyed]
+
+    reduce_items = []
+    tiles_per_chunk = []
+    if not is_ag:
+        tiles_per_chunk = [sum(1 for t in range(T) if g in tile_chunks[t]) for g in range(len(chunks))]
+        own = []
+        for t in range(T):
+            mb, nb = divmod(t, n_nb)
+            if (mb * bm) // S == r:
+                latest_j = max(_shard_chunks(chunks, r).index(g) for g in tile_chunks[t])
+                own.append(((latest_j,) + _intra_key(desc, mb, nb), t))
+        own.sort(key=lambda x: x[0])
+        reduce_items = [[t, tile_chunks[t][0], tile_chunks[t][-1]] for _, t in own]
+
+    # CTA assignment: position k -> CTA k mod n_cta; reduce items continue the stride.
+    work = [("tile", t) for t in order] + [("reduce", it[0]) for it in reduce_items]
+    waits = []
+    for c in range(n_cta):
+        seen = set()
+        lst = []
+        for k in range(c, len(work), n_cta):
+            kind, t = work[k]
+            need = []
+            if is_ag and kind == "tile":
+                need = [g for g in tile_chunks[t] if chunks[g][2] != r]
+            elif (not is_ag) and kind == "reduce":
+                need = list(tile_chunks[t])
+            for g in need:
+                if g not in seen:
+                    seen.add(g)
+                    lst.append([k, g])
+        waits.append([c, lst])
+
+    if is_ag:
+        contrib = [0 if chunks[g][2] == r else (1 if desc["backend"] == "ce" else desc["n_slices"])
+                   for g in range(len(chunks))]
+    else:
+        contrib = [W if chunks[g][2] == r else 0 for g in range(len(chunks))]
+
+    if is_ag:
+        tensors = {"A": {"elem_bytes": 2, "shape": [M, K]}, "C": {"elem_bytes": 2, "shape": [M, N]}}
+        owner_regions = [{"A": [[p * S, S]]} for p in range(W)]
+    else:
+        tensors = {"C": {"elem_bytes": 2, "shape": [M, N]}, "P": {"elem_bytes": 4, "shape": [M, N]}}
+        owner_regions = [{"P": [[0, M]]} for p in range(W)]
+
+    out = {
+        "op": desc["op"], "world_size": W, "rank": r, "M": M, "N": N, "K": K, "chunk_rows": C,
+        "tile": [bm, bn, cg], "backend": desc["backend"], "dir": desc["dir"],
+        "chunk_order": desc["chunk_order"], "intra": desc["intra"], "group_m": desc["group_m"],
+        "n_cta": n_cta, "comm_ctas": desc["comm_ctas"],
+        "n_slices": 1 if desc["backend"] == "ce" else desc["n_slices"],
+        "tensors": tensors, "owner_regions": owner_regions, "plans": plans,
+        "chunks": [[g, chunks[g][0], chunks[g][1], chunks[g][2], pos[g]] for g in range(len(chunks))],
+        "deps": deps, "order": order, "waits": waits, "contrib": contrib,
+    }
+    if not is_ag:
+        out["tiles_per_chunk"] = tiles_per_chunk
+        out["reduce_items"] = reduce_items
+    return out
+
+
+def export_json(p) -> str:
+    """Canonical export: sorted keys, no whitespace (byte-exact contract)."""
+    return json.dumps(p, sort_keys=True, separators=(",", ":"))
+
+
+def sm_utilization(n_tiles, sm_count):
+    """tile_count / (wave_count * sm_count)."""
+    waves = math.ceil(n_tiles / sm_count)
+    return n_tiles / (waves * sm_count)

@@ -1,0 +1,192 @@
+/*
+ * autooverlap.h -- C ABI of the B200-native AutoOverlap hot path (arXiv 2601.20595).
+ *
+ * The library runs ONE persistent fused kernel per op that overlaps a tensor-parallel
+ * collective with the GEMM that consumes or produces it, at communication-chunk
+ * granularity (§5):
+ *
+ *   ao_ag_gemm : AllGather -> GEMM.   C_r[M, N] = concat_p(A_p)[M, K] . B_r[N, K]^T
+ *                Each chunk of every rank's row shard A_p is pushed to the peers (Lst.2,
+ *                P:249-265); tiles spin on per-chunk ready flags and the tile order
+ *                follows chunk arrival.
+ *   ao_gemm_rs : GEMM -> ReduceScatter.  C_shard_r[S, N] = (sum_s A_s . B_s^T)[rS:(r+1)S, :]
+ *                Finished fp32 partial tiles are pushed into the owner's slots per chunk;
+ *                the owner's epilogue fuses the peer reduction.
+ *
+ * The calls follow the paper's statement of the user API: register symmetric
+ * buffers (ao_ctx_*), build a chunk schedule (ao_plan_*: chunk size, chunk->tile mapping,
+ * transfer backend), run the op with the local kernel's signature plus
+ * rank / world size.
+ *
+ * Conventions
+ *  - Every call returns ao_status; no C++ exception crosses the ABI.  On failure
+ *    ao_last_error() returns a thread-local human-readable detail.
+ *  - All matrices are bf16, row-major, contiguous, 16-byte aligned DEVICE pointers on the
+ *    ctx's device, owned by the caller.  Layouts follow Lst.1: A [rows, K],
+ *    B [N, K] (nn.Linear weight), C [rows, N].
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All op
+ *    calls are asynchronous; device-side spin timeouts surface through
+ *    ao_ctx_check_async() (or the next op call).
+ *  - Collective semantics: every rank of a world must issue the same sequence of ops,
+ *    with plans built from descs that differ only in `rank` (equal ao_plan_hash).
+ *  - There is no CPU fallback: on a device that is not sm_100 the ctx/plan calls return
+ *    AO_ERR_UNSUPPORTED.
+ */
+#ifndef AUTOOVERLAP_H
+#define AUTOOVERLAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AO_VERSION_MAJOR 0
+#define AO_VERSION_MINOR 1
+#define AO_MAX_WORLD 8
+#define AO_HANDLE_BYTES 256
+
+typedef enum {
+  AO_OK = 0,
+  AO_ERR_INVALID_ARG = 1, /* desc/pointer validation failed; ao_last_error lists violations */
+  AO_ERR_UNSUPPORTED = 2, /* not an sm_100 device, or a feature not built (e.g. PULL execution) */
+  AO_ERR_CUDA = 3,        /* a CUDA runtime/driver call failed */
+  AO_ERR_OOM = 4,
+  AO_ERR_PEER = 5,        /* handle / plan mismatch across ranks */
+  AO_ERR_TIMEOUT = 6,     /* a device spin-wait on a chunk flag expired */
+  AO_ERR_STATE = 7        /* call order violated (e.g. op before ao_ctx_import_handles) */
+} ao_status;
+
+typedef enum { AO_OP_AG_GEMM = 0, AO_OP_GEMM_RS = 1 } ao_op;
+/* Transfer backends of P:397 / Fig.7.  CE = copy-engine peer memcpy on a side
+ * stream with stream-memop flags; TMA = cp.async.bulk peer copies issued from
+ * communication warps; LDST = 16-byte vector ld/st over NVSwitch from CUDA cores. */
+typedef enum { AO_BACKEND_CE = 0, AO_BACKEND_TMA = 1, AO_BACKEND_LDST = 2 } ao_backend;
+/* a P2P op recorded on the source side is a push, on the destination side a pull. */
+typedef enum { AO_DIR_PUSH = 0, AO_DIR_PULL = 1 } ao_dir;
+/* Order of a rank's ops: all chunks for peer r+1, then r+2, ... (shard-major, the Lst.2
+ * rotation) or chunk j for every peer before chunk j+1 (chunk-major).  DESIGN.md Q3. */
+typedef enum { AO_CHUNK_SHARD_MAJOR = 0, AO_CHUNK_CHUNK_MAJOR = 1 } ao_chunk_order;
+/* Intra-chunk tile swizzle (Fig.6): row-major, column-major, Triton GROUP_M. */
+typedef enum { AO_INTRA_ROW = 0, AO_INTRA_COL = 1, AO_INTRA_GROUPED = 2 } ao_intra;
+/* GEMM-RS wire format of the partials.  FP32 is the conforming default (Q14). */
+typedef enum { AO_WIRE_FP32 = 0, AO_WIRE_BF16 = 1 } ao_wire;
+
+typedef struct ao_ctx ao_ctx;
+typedef struct ao_plan ao_plan;
+
+/* Opaque per-rank handle for the symmetric workspace (IPC handle + metadata).  The caller
+ * moves these between processes (e.g. torch.distributed.all_gather_object). */
+typedef struct {
+  unsigned char bytes[AO_HANDLE_BYTES];
+} ao_handle_blob;
+
+/* The chunk schedule description (the plan's whole config surface).
+ * Integer fields hold the enums above.  0 in tile_m/tile_n/n_cta/timeout_ns = default. */
+typedef struct {
+  uint32_t struct_size; /* = sizeof(ao_plan_desc); ABI versioning */
+  int32_t op;           /* ao_op */
+  int32_t world_size;   /* W, 1..AO_MAX_WORLD */
+  int32_t rank;         /* r, 0..W-1 */
+  int64_t M;            /* AG: gathered rows (S = M/W per rank).  RS: rows of A and of the partial */
+  int64_t N;            /* AG: this rank's columns of B/C.  RS: columns of C */
+  int64_t K;            /* AG: reduction dim.  RS: this rank's K shard */
+  int32_t chunk_rows;   /* C: rows per chunk; must divide S and be a multiple of 8 */
+  int32_t backend;      /* ao_backend */
+  int32_t dir;          /* ao_dir (PULL: AG only) */
+  int32_t chunk_order;  /* ao_chunk_order */
+  int32_t intra;        /* ao_intra */
+  int32_t group_m;      /* GROUP_M for AO_INTRA_GROUPED */
+  int32_t tile_m;       /* BM (0 = planner picks by wave-quantization utilization) */
+  int32_t tile_n;       /* BN (0 together with tile_m) */
+  int32_t n_cta;        /* persistent GEMM CTAs (0 = SMs - comm_ctas) */
+  int32_t comm_ctas;    /* TMA/LDST: 0 = co-located comm warps, >0 = dedicated comm CTAs */
+  int32_t n_slices;     /* TMA/LDST: slices (flag words) per chunk; CE uses 1 */
+  int32_t rs_wire;      /* ao_wire (RS only) */
+  uint64_t timeout_ns;  /* device spin bound (0 = 5 s) */
+} ao_plan_desc;
+
+/* ---- status / version ---------------------------------------------------------------- */
+const char* ao_status_string(ao_status s);
+const char* ao_last_error(void); /* thread-local detail of the last failing call ("" if none) */
+ao_status ao_version(int* major, int* minor);
+
+/* ---- plans (host-only part: no GPU needed) ---------------------------------------------
+ * ao_plan_desc_init: fills defaults (AG, W=1, CE, PUSH, SHARD_MAJOR, ROW, ...).
+ * ao_plan_validate: checks a desc against the rules in DESIGN.md "Validation"
+ *   (M % W, S % chunk_rows, K % 8, N % 8, tile shape, PULL only with AG, ...); returns
+ *   AO_OK with *n_violations = 0 when valid, AO_ERR_INVALID_ARG otherwise; a ';'-separated
+ *   list of violations is written to report (truncated to cap, NUL-terminated).
+ * ao_plan_create_host: builds the chunk table, chunk->tile dependency table, tile order,
+ *   per-CTA minimal wait lists and signal counts for a device with `sm_count`
+ *   SMs, without binding to a ctx.  The result can be exported / hashed, not launched.
+ * ao_plan_export_json: canonical JSON (sorted keys, no whitespace, integers only; the
+ *   bit-exact contract checked against the oracle).  Writes min(cap, needed) bytes incl.
+ *   the NUL; *needed = bytes required incl. NUL.
+ * ao_plan_hash: FNV-1a 64 of the rank-independent part of the schedule.
+ * ao_plan_workspace_bytes: symmetric workspace a ctx needs to run this desc (both epoch
+ *   parities, data + flags). */
+ao_status ao_plan_desc_init(ao_plan_desc* desc);
+ao_status ao_plan_validate(const ao_plan_desc* desc, int sm_count, char* report, size_t cap,
+                           int* n_violations);
+ao_status ao_plan_create_host(const ao_plan_desc* desc, int sm_count, ao_plan** out);
+ao_status ao_plan_export_json(const ao_plan* plan, char* buf, size_t cap, size_t* needed);
+ao_status ao_plan_hash(const ao_plan* plan, uint64_t* out);
+ao_status ao_plan_info(const ao_plan* plan, int32_t* tile_m, int32_t* tile_n, int32_t* cta_group,
+                       int32_t* n_cta, int32_t* n_tiles, int32_t* n_chunks);
+ao_status ao_plan_workspace_bytes(const ao_plan_desc* desc, size_t* bytes);
+ao_status ao_plan_destroy(ao_plan* plan);
+
+/* ---- symmetric memory (one ctx per rank) ------------------------------------------------
+ * ao_ctx_create: selects `device`, checks it is sm_100, cudaMallocs the symmetric workspace
+ *   (`workspace_bytes` of data, split in two epoch parities, plus flag words) and a
+ *   host-mapped error word.  The workspace is owned by the library.
+ * ao_ctx_export_handle: this rank's handle (cudaIpc memory handle + pid/device/size).
+ * ao_ctx_import_handles: `all` has world_size entries indexed by rank (own entry ignored).
+ *   Handles from the same process (loopback: several ranks on one GPU) are mapped
+ *   directly; others through cudaIpcOpenMemHandle (NVLink P2P).  Fails with AO_ERR_PEER
+ *   on a world/size mismatch.
+ * ao_ctx_check_async: AO_ERR_TIMEOUT if a device spin-wait expired since the last check
+ *   (detail in ao_last_error), else AO_OK.  Does not synchronize. */
+ao_status ao_ctx_create(int device, int rank, int world_size, size_t workspace_bytes, ao_ctx** out);
+ao_status ao_ctx_export_handle(ao_ctx* ctx, ao_handle_blob* out);
+ao_status ao_ctx_import_handles(ao_ctx* ctx, const ao_handle_blob* all);
+ao_status ao_ctx_check_async(ao_ctx* ctx);
+ao_status ao_ctx_destroy(ao_ctx* ctx);
+
+/* ---- plans bound to a ctx, and the ops -------------------------------------------------
+ * ao_plan_create: ao_plan_create_host with the ctx's SM count, plus device copies of the
+ *   tables.  The ctx must outlive the plan.
+ * ao_ag_gemm: A_shard [M/W, K] (this rank's rows), B [N, K], C [M, N];
+ *   A_gathered_out (nullable) [M, K] receives concat_p A_p (bit-exact copy).
+ * ao_gemm_rs: A [M, K], B [N, K] (this rank's K shard), C_shard [M/W, N].
+ * ao_*_group: ONE fused launch for n ranks of a world that live in this process on the
+ *   same device (loopback).  plans[i] must belong to distinct ctxs of one world; the
+ *   pointer arrays are indexed like plans.  The n=1 case equals the single-rank call. */
+ao_status ao_plan_create(ao_ctx* ctx, const ao_plan_desc* desc, ao_plan** out);
+ao_status ao_ag_gemm(ao_plan* plan, const void* A_shard, const void* B, void* C, void* A_gathered_out,
+                     void* stream);
+ao_status ao_gemm_rs(ao_plan* plan, const void* A, const void* B, void* C_shard, void* stream);
+ao_status ao_ag_gemm_group(int n, ao_plan* const* plans, const void* const* A_shards,
+                           const void* const* Bs, void* const* Cs, void* const* A_gathered_outs,
+                           void* stream);
+ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
+                           void* const* C_shards, void* stream);
+
+/* ---- plain local GEMM through the same tcgen05 mainloop (no communication) -------------
+ * C[M, N] = A[M, K] . B[N, K]^T, bf16 in / fp32 accumulate / bf16 out (Lst.1's local
+ * kernel).  Used for W = 1 and as the GEMM-only reference of the fused ops.
+ * tile_n: 0 = 256.  Requires M % 128 == 0, N % 8 == 0, K % 8 == 0. */
+ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                  int32_t tile_n, void* stream);
+
+/* ---- test hooks (deterministic fault injection; see tests/) ----------------------------
+ * ao_debug_set: key "skip_wait" = index of a wait (global over CTAs) the kernel must skip
+ * (-1 = none); "delay_ns" = nanosleep before each transfer/signal (fuzzes arrival order). */
+ao_status ao_debug_set(const char* key, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOOVERLAP_H */

@@ -1,0 +1,206 @@
+"""Python binding of the C ABI (include/autooverlap.h) -- same names, marshalling only.
+
+PyTorch is used for device memory, streams and the process group (IPC-handle exchange);
+it never computes any step of the hot path.  Tensors are passed to the library as raw
+device pointers together with torch's current CUDA stream.
+
+    ctx   = Context(device, rank, world_size, workspace_bytes)
+    ctx.import_handles(all_blobs)                  # blobs from every rank
+    plan  = Plan(ctx, desc)                        # desc: dict (oracle desc keys)
+    ag_gemm(plan, A_shard, B, C)                   # AllGather -> GEMM
+    gemm_rs(plan, A, B, C_shard)                   # GEMM -> ReduceScatter
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _native as N
+from ._native import AOError, check, lib, make_desc  # noqa: F401
+
+
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else int(t.data_ptr()))
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _require_bf16_cuda(*ts):
+    import torch
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError("operands must be contiguous bf16 CUDA tensors")
+
+
+# ----------------------------------------------------------------------------- plans
+def validate(desc: dict, sm_count: int = 148):
+    d = make_desc(desc)
+    buf = ctypes.create_string_buffer(4096)
+    n = ctypes.c_int(0)
+    lib().ao_plan_validate(ctypes.byref(d), sm_count, buf, len(buf), ctypes.byref(n))
+    v = buf.value.decode()
+    return [] if n.value == 0 else v.split(";")
+
+
+def workspace_bytes(desc: dict) -> int:
+    d = make_desc(desc)
+    out = ctypes.c_size_t(0)
+    check(lib().ao_plan_workspace_bytes(ctypes.byref(d), ctypes.byref(out)))
+    return out.value
+
+
+class Plan:
+    """A chunk schedule.  Plan(None, desc, sm_count) is host-only (export / hash);
+    Plan(ctx, desc) is bound to a ctx and can be launched."""
+
+    def __init__(self, ctx, desc: dict, sm_count: int = 148):
+        self.desc = dict(desc)
+        self.ctx = ctx
+        d = make_desc(desc)
+        h = ctypes.c_void_p()
+        if ctx is None:
+            check(lib().ao_plan_create_host(ctypes.byref(d), sm_count, ctypes.byref(h)))
+        else:
+            check(lib().ao_plan_create(ctx.handle, ctypes.byref(d), ctypes.byref(h)))
+        self.handle = h
+
+    def export_json(self) -> str:
+        need = ctypes.c_size_t(0)
+        check(lib().ao_plan_export_json(self.handle, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        check(lib().ao_plan_export_json(self.handle, buf, need.value, ctypes.byref(need)))
+        return buf.value.decode()
+
+    def hash(self) -> int:
+        out = ctypes.c_uint64(0)
+        check(lib().ao_plan_hash(self.handle, ctypes.byref(out)))
+        return out.value
+
+    def info(self) -> dict:
+        vals = [ctypes.c_int32(0) for _ in range(6)]
+        check(lib().ao_plan_info(self.handle, *[ctypes.byref(v) for v in vals]))
+        keys = ["tile_m", "tile_n", "cta_group", "n_cta", "n_tiles", "n_chunks"]
+        return {k: v.value for k, v in zip(keys, vals)}
+
+    def close(self):
+        if self.handle:
+            lib().ao_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def plan_json(desc: dict, sm_count: int = 148) -> str:
+    p = Plan(None, desc, sm_count)
+    try:
+        return p.export_json()
+    finally:
+        p.close()
+
+
+# ------------------------------------------------------------------------- contexts
+class Context:
+    def __init__(self, device: int, rank: int, world_size: int, workspace: int):
+        h = ctypes.c_void_p()
+        check(lib().ao_ctx_create(int(device), int(rank), int(world_size), int(workspace), ctypes.byref(h)))
+        self.handle = h
+        self.device, self.rank, self.world_size = device, rank, world_size
+
+    def export_handle(self) -> bytes:
+        b = N.HandleBlob()
+        check(lib().ao_ctx_export_handle(self.handle, ctypes.byref(b)))
+        return bytes(b.bytes)
+
+    def import_handles(self, blobs):
+        arr = (N.HandleBlob * self.world_size)()
+        for i, raw in enumerate(blobs):
+            ctypes.memmove(arr[i].bytes, raw, N.AO_HANDLE_BYTES)
+        check(lib().ao_ctx_import_handles(self.handle, arr))
+
+    def check_async(self):
+        check(lib().ao_ctx_check_async(self.handle))
+
+    def close(self):
+        if self.handle:
+            lib().ao_ctx_destroy(self.handle)
+            self.handle = None
+
+
+def loopback_world(device: int, world_size: int, workspace: int):
+    """W ranks of one world inside this process on one GPU (SURVEY.md T4 loopback)."""
+    ctxs = [Context(device, r, world_size, workspace) for r in range(world_size)]
+    blobs = [c.export_handle() for c in ctxs]
+    for c in ctxs:
+        c.import_handles(blobs)
+    return ctxs
+
+
+def dist_world(device: int, workspace: int, group=None):
+    """One rank per process: exchange IPC handles over torch.distributed (plumbing only)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ctx = Context(device, rank, world, workspace)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, ctx.export_handle(), group=group)
+    ctx.import_handles(blobs)
+    dist.barrier(group)
+    return ctx
+
+
+# ------------------------------------------------------------------------------ ops
+def ag_gemm(plan: Plan, A_shard, B, C, A_gathered_out=None, stream=None):
+    """ao_ag_gemm: C[M, N] = concat_p(A_p) . B^T for this rank."""
+    _require_bf16_cuda(A_shard, B, C, A_gathered_out)
+    check(lib().ao_ag_gemm(plan.handle, _ptr(A_shard), _ptr(B), _ptr(C), _ptr(A_gathered_out), _stream(stream)))
+
+
+def gemm_rs(plan: Plan, A, B, C_shard, stream=None):
+    """ao_gemm_rs: C_shard[S, N] = (sum_s A_s . B_s^T)[rank rows]."""
+    _require_bf16_cuda(A, B, C_shard)
+    check(lib().ao_gemm_rs(plan.handle, _ptr(A), _ptr(B), _ptr(C_shard), _stream(stream)))
+
+
+def _arr(ts):
+    return (ctypes.c_void_p * len(ts))(*[0 if t is None else int(t.data_ptr()) for t in ts])
+
+
+def _plans(plans):
+    return (ctypes.c_void_p * len(plans))(*[p.handle.value for p in plans])
+
+
+def ag_gemm_group(plans, A_shards, Bs, Cs, A_gathered_outs=None, stream=None):
+    """ao_ag_gemm_group: one fused launch for co-located ranks (loopback)."""
+    _require_bf16_cuda(*A_shards, *Bs, *Cs)
+    n = len(plans)
+    gouts = A_gathered_outs if A_gathered_outs is not None else [None] * n
+    check(lib().ao_ag_gemm_group(n, _plans(plans), _arr(A_shards), _arr(Bs), _arr(Cs), _arr(gouts), _stream(stream)))
+
+
+def gemm_rs_group(plans, As, Bs, C_shards, stream=None):
+    _require_bf16_cuda(*As, *Bs, *C_shards)
+    check(lib().ao_gemm_rs_group(len(plans), _plans(plans), _arr(As), _arr(Bs), _arr(C_shards), _stream(stream)))
+
+
+def gemm(A, B, C=None, tile_n: int = 0, stream=None):
+    """ao_gemm: C = A . B^T through the same tcgen05 mainloop (no communication)."""
+    import torch
+    if C is None:
+        C = torch.empty(A.shape[0], B.shape[0], dtype=torch.bfloat16, device=A.device)
+    _require_bf16_cuda(A, B, C)
+    check(lib().ao_gemm(A.device.index, _ptr(A), _ptr(B), _ptr(C), A.shape[0], B.shape[0], A.shape[1], tile_n,
+                        _stream(stream)))
+    return C
+
+
+def debug_set(key: str, value: int):
+    check(lib().ao_debug_set(key.encode(), int(value)))

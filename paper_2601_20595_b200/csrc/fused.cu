@@ -1,0 +1,550 @@
+// fused.cu -- the persistent fused kernel: tcgen05 GEMM mainloop + chunk waits (AG) or
+// partial pushes + owner reduction (RS) + in-kernel transfer backends (TMA / LD-ST).
+//
+// Method (§5.2):
+//  * the tile scheduler follows the planner's chunk-ordered tile list (Fig.6);
+//  * a tile that consumes a chunk waits on that chunk's global-memory signal, once per
+//    (CTA, chunk) (minimal waits) -- producer warp, ld.acquire.sys spin;
+//  * communication is issued from inside the fused kernel: co-located
+//    communication warps or dedicated communication CTAs ("specialized SMs", Fig.7b/c)
+//    push chunks with cp.async.bulk (TMA backend) or 16-byte ld/st (LDST backend);
+//  * GEMM-RS: each finished fp32 partial tile is written into its owner's slot; the last
+//    tile of a chunk releases the owner's flag; the owner's epilogue warps then run the
+//    fused reduction of the chunk (ascending source rank) and store bf16.
+//
+// Warp roles of a GEMM CTA (256 threads, 1 CTA / SM):
+//   warp 0      TMA producer (+ AG chunk waits)
+//   warp 1      TMEM allocator + tcgen05.mma issuer
+//   warps 2..5  epilogue (TMEM -> registers -> global; RS signals + reduce items)
+//   warps 6..7  co-located communication warps (AG, TMA/LDST backends)
+#include <cuda_runtime.h>
+
+#include "kernel_args.h"
+#include "ptx.cuh"
+
+namespace ao {
+namespace dev {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kThreads = 256;
+constexpr int kCommWarp0 = 6;
+constexpr int kColocCommWarps = 2;
+constexpr int kCommBufs = 2;
+constexpr uint32_t kColocBufBytes = 8192;
+constexpr uint32_t kCtaBufBytes = 12288;
+constexpr int kOperandBudget = 196608;  // bytes of smem for the A/B stage ring
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStageA = kBM * kBK * 2;
+  static constexpr int kStageB = BN * kBK * 2;
+  static constexpr int kStage = kStageA + kStageB;
+  static constexpr int kStages = kOperandBudget / kStage;
+  static constexpr int kTmemCols = 2 * BN;
+};
+
+struct SmemLayout {
+  uint32_t off_a, off_b, off_comm, off_bar, off_slot, total;
+};
+
+template <int BN>
+__host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm) {
+  SmemLayout L{};
+  L.off_a = 0;
+  L.off_b = Cfg<BN>::kStages * Cfg<BN>::kStageA;
+  L.off_comm = Cfg<BN>::kStages * Cfg<BN>::kStage;
+  const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : 0;
+  L.off_bar = L.off_comm + comm;
+  const uint32_t nbars = 2 * Cfg<BN>::kStages + 4 + 8 * kCommBufs;
+  L.off_slot = L.off_bar + nbars * 8;
+  L.total = L.off_slot + 16 + 1024;  // + alignment slack
+  return L;
+}
+__host__ __device__ constexpr SmemLayout comm_cta_layout() {
+  SmemLayout L{};
+  L.off_comm = 0;
+  L.off_bar = 8 * kCommBufs * kCtaBufBytes;
+  L.off_slot = L.off_bar + 8 * kCommBufs * 8;
+  L.total = L.off_slot + 16 + 1024;
+  return L;
+}
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Bounded spin on a flag word until it reaches `target` (an epoch).  On timeout the first
+// failure is recorded in the host-mapped ErrorInfo and the wait is abandoned (no hang).
+__device__ __noinline__ void spin_flag(const uint32_t* p, uint32_t target, const KernelArgs& A, int rank, int cta,
+                                       int g) {
+  uint32_t v = ld_acquire_sys(p);
+  if (v >= target) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t ns = 32;
+  while (true) {
+    v = ld_acquire_sys(p);
+    if (v >= target) return;
+    if (globaltimer() - t0 > A.timeout_ns) {
+      if (atomicCAS(const_cast<uint32_t*>(&A.err->flag), 0u, 1u) == 0u) {
+        A.err->rank = rank;
+        A.err->cta = cta;
+        A.err->chunk = g;
+        A.err->epoch = target;
+        A.err->seen = v;
+        __threadfence_system();
+      }
+      return;
+    }
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+__device__ __forceinline__ int4 ld_nc_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(int4* p, const int4& v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// ---- communication workers (AG in-kernel backends) -----------------------------------------
+// Each worker is one warp; worker w handles items w, w + n_workers, ... of this rank's
+// ordered item list (plan order, so early chunks go first on every worker).
+template <int COMM>
+__device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, int n_workers, uint8_t* staging,
+                            uint32_t buf_bytes, uint64_t* bars) {
+  const int lane = lane_id();
+  uint32_t phase_bits = 0;
+  for (int i = worker; i < R.n_comm_items; i += n_workers) {
+    const CommItem it = R.comm_items[i];
+    const char* src = R.A_shard + it.src_off;
+    char* dst = R.peer_data[it.peer] + it.dst_off;
+    if constexpr (COMM == COMM_LDST) {
+      const int4* s = reinterpret_cast<const int4*>(src);
+      int4* d = reinterpret_cast<int4*>(dst);
+      const int64_t n = it.bytes / 16;
+      constexpr int U = 8;
+      for (int64_t base = 0; base < n; base += 32 * U) {
+        int4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = base + u * 32 + lane;
+          if (j < n) v[u] = ld_nc_v4(s + j);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = base + u * 32 + lane;
+          if (j < n) st_v4(d + j, v[u]);
+        }
+      }
+      __threadfence_system();
+      __syncwarp();
+    } else {
+      if (lane == 0) {
+        const int64_t npieces = (it.bytes + buf_bytes - 1) / buf_bytes;
+        auto piece_len = [&](int64_t p) -> uint32_t {
+          const int64_t rem = it.bytes - p * int64_t(buf_bytes);
+          return uint32_t(rem < int64_t(buf_bytes) ? rem : int64_t(buf_bytes));
+        };
+        // prologue: load piece 0
+        {
+          const uint32_t n0 = piece_len(0);
+          mbar_arrive_expect_tx(&bars[0], n0);
+          bulk_g2s(staging, src, n0, &bars[0]);
+        }
+        for (int64_t p = 0; p < npieces; ++p) {
+          const int b = int(p & 1);
+          if (p + 1 < npieces) {
+            const int nb = b ^ 1;
+            bulk_wait_read<0>();  // the store that last used buffer nb has read it
+            const uint32_t n1 = piece_len(p + 1);
+            mbar_arrive_expect_tx(&bars[nb], n1);
+            bulk_g2s(staging + nb * buf_bytes, src + (p + 1) * int64_t(buf_bytes), n1, &bars[nb]);
+          }
+          mbar_wait(&bars[b], (phase_bits >> b) & 1);
+          phase_bits ^= (1u << b);
+          bulk_s2g(dst + p * int64_t(buf_bytes), staging + b * buf_bytes, piece_len(p));
+          bulk_commit();
+        }
+        bulk_wait<0>();  // writes performed
+        fence_proxy_async_global();
+        fence_sys();
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      if (A.delay_ns) __nanosleep((uint32_t(i) * 2654435761u) % A.delay_ns);
+      st_release_sys(R.peer_flags[it.peer] + it.g * R.n_slices + it.slice, R.epoch);
+    }
+    __syncwarp();
+  }
+}
+
+template <int BN, int MODE, int COMM>
+__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constant__ KernelArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int gemm_ctas = args.n_group * args.ctas_per_rank;
+
+  // ------------------------------------------------------------------ dedicated comm CTA
+  if (int(blockIdx.x) >= gemm_ctas) {
+    if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {
+      const SmemLayout L = comm_cta_layout();
+      uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar) + warp * kCommBufs;
+      if (lane == 0) {
+        for (int b = 0; b < kCommBufs; ++b) mbar_init(&bars[b], 1);
+        fence_barrier_init();
+      }
+      __syncwarp();
+      const int idx = blockIdx.x - gemm_ctas;
+      const int grp = idx / args.comm_ctas_per_rank;
+      const int c = idx % args.comm_ctas_per_rank;
+      comm_worker<COMM>(args.rk[grp], args, c * 8 + warp, args.comm_ctas_per_rank * 8,
+                        smem + L.off_comm + warp * kCommBufs * kCtaBufBytes, kCtaBufBytes, bars);
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ GEMM CTA
+  using C_ = Cfg<BN>;
+  constexpr bool kTmaComm = (MODE == MODE_AG && COMM == COMM_TMA);
+  constexpr SmemLayout L = gemm_layout<BN>(kTmaComm);
+  const int grp = blockIdx.x / args.ctas_per_rank;
+  const int cta = blockIdx.x % args.ctas_per_rank;
+  const int n_cta = args.ctas_per_rank;
+  const RankArgs& R = args.rk[grp];
+
+  uint8_t* sA = smem + L.off_a;
+  uint8_t* sB = smem + L.off_b;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+  uint64_t* empty = full + C_::kStages;
+  uint64_t* tfull = empty + C_::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* commbars = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.off_slot);
+
+  if (warp == 0 && lane == 0 && R.K > 0) {
+    prefetch_tmap(&R.tmA);
+    prefetch_tmap(&R.tmB);
+    if (MODE == MODE_AG) prefetch_tmap(&R.tmA_loc);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < C_::kStages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], 4);
+      }
+      for (int b = 0; b < 8 * kCommBufs; ++b) mbar_init(&commbars[b], 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(tmem_slot, C_::kTmemCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int64_t K = R.K, N = R.N, S = R.S;
+  const int nkb = int((K + kBK - 1) / kBK);
+  const int n_tiles = R.n_tiles;
+
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_b = policy_evict_last();
+      const uint64_t pol_a = policy_evict_first();
+      uint32_t stage = 0, phase = 0;
+      int wp = 0, we = 0;
+      if constexpr (MODE == MODE_AG) {
+        wp = R.wait_off[cta];
+        we = R.wait_off[cta + 1];
+      }
+      for (int k = cta; k < n_tiles; k += n_cta) {
+        if constexpr (MODE == MODE_AG) {
+          bool waited = false;
+          while (wp < we && R.waits[wp].x == k) {
+            const int g = R.waits[wp].y;
+            if (!(grp == 0 && wp == args.skip_wait)) {
+              for (int s = 0; s < R.n_slices; ++s)
+                spin_flag(R.flags + g * R.n_slices + s, R.epoch, args, R.rank, cta, g);
+            }
+            ++wp;
+            waited = true;
+          }
+          if (waited) fence_proxy_async_global();  // generic-proxy arrivals -> TMA reads
+        }
+        const int t = R.order[k];
+        const int mb = t / R.n_nb;
+        const int nb = t - mb * R.n_nb;
+        const CUtensorMap* mA = &R.tmA;
+        int arow = mb * kBM;
+        if constexpr (MODE == MODE_AG) {
+          if (int64_t(mb) * kBM / S == R.rank) {
+            mA = &R.tmA_loc;
+            arow -= int(R.rank * S);
+          }
+        }
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C_::kStage);
+          tma_load_2d(sA + stage * C_::kStageA, mA, &full[stage], kb * kBK, arow, pol_a);
+          tma_load_2d(sB + stage * C_::kStageB, &R.tmB, &full[stage], kb * kBK, nb * BN, pol_b);
+          if (++stage == C_::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    constexpr uint32_t idesc = make_idesc_bf16(kBM, BN);
+    uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+    for (int k = cta; k < n_tiles; k += n_cta) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint64_t ad = make_smem_desc_sw128(smem_u32(sA + stage * C_::kStageA));
+          const uint64_t bd = make_smem_desc_sw128(smem_u32(sB + stage * C_::kStageB));
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)  // +32 B per K=16 step inside the swizzle atom
+            mma_bf16_ss(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == C_::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) mma_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else if (warp < kCommWarp0) {
+    // ================================================================ epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int etid = threadIdx.x - 64;
+    uint32_t acc = 0, acc_phase = 0;
+    for (int k = cta; k < n_tiles; k += n_cta) {
+      const int t = R.order[k];
+      const int mb = t / R.n_nb;
+      const int nb = t - mb * R.n_nb;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = int64_t(mb) * kBM + q * 32 + lane;
+      const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+      const int64_t col_base = int64_t(nb) * BN;
+      int owner = 0;
+      char* rs_base = nullptr;
+      if constexpr (MODE == MODE_RS) {
+        owner = int(int64_t(mb) * kBM / S);
+        // owner's data half: slot[rank] of [S, N] fp32
+        rs_base = R.peer_data[owner] + (int64_t(R.rank) * S * N + (row - owner * S) * N) * 4;
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tb + cc * 32, v);
+        tmem_wait_ld();
+        if (nkb == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        }
+        const int64_t col0 = col_base + cc * 32;
+        const int64_t valid = N - col0;  // multiple of 8
+        if (valid <= 0) continue;
+        if constexpr (MODE == MODE_RS) {
+          float* dst = reinterpret_cast<float*>(rs_base) + col0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j * 4 < valid)
+              st_v4(reinterpret_cast<int4*>(dst + j * 4), make_int4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+          }
+        } else {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(R.C) + row * N + col0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (j * 8 < valid) {
+              int4 o;
+              o.x = pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+              o.y = pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+              o.z = pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+              o.w = pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+              st_v4(reinterpret_cast<int4*>(dst + j * 8), o);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if constexpr (MODE == MODE_RS) {
+        // RS-3: all partial rows of this tile are written; count the tile into each of
+        // its chunks; the last contributor releases the owner's flag[g][rank].
+        __threadfence_system();
+        named_bar_sync(1, 128);
+        if (etid == 0) {
+          const int glo = int(int64_t(mb) * kBM / R.crows);
+          const int ghi = int((int64_t(mb) * kBM + kBM - 1) / R.crows);
+          for (int g = glo; g <= ghi; ++g) {
+            uint32_t old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.counters + g) : "memory");
+            if (int(old) + 1 == R.tiles_per_chunk[g]) {
+              R.counters[g] = 0;
+              if (args.delay_ns) __nanosleep((uint32_t(g) * 2654435761u) % args.delay_ns);
+              st_release_sys(R.peer_flags[owner] + g * R.W + R.rank, R.epoch);
+            }
+          }
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+
+    if constexpr (MODE == MODE_RS) {
+      // RS-4: reduce items (own-row tiles, chunk order), after this CTA's GEMM tiles.
+      int wp = R.wait_off[cta];
+      const int we = R.wait_off[cta + 1];
+      const int n_work = n_tiles + R.n_items;
+      int k = cta;
+      while (k < n_tiles) k += n_cta;
+      const char* own = R.peer_data[R.rank];
+      const int64_t slot_stride = S * N;  // floats
+      for (; k < n_work; k += n_cta) {
+        if (etid == 0) {
+          while (wp < we && R.waits[wp].x == k) {
+            const int g = R.waits[wp].y;
+            if (!(grp == 0 && wp == args.skip_wait)) {
+              for (int s = 0; s < R.W; ++s) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, cta, g);
+            }
+            ++wp;
+          }
+        }
+        named_bar_sync(1, 128);
+        const int t = R.reduce_items[k - n_tiles];
+        const int mb = t / R.n_nb;
+        const int nb = t - mb * R.n_nb;
+        const int64_t lr0 = int64_t(mb) * kBM - int64_t(R.rank) * S;
+        const int64_t c0 = int64_t(nb) * BN;
+        const int64_t valid = (N - c0) < BN ? (N - c0) : BN;
+        const int per_row = BN / 4;
+        const float* slots = reinterpret_cast<const float*>(own);
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(R.C);
+        for (int idx = etid; idx < kBM * per_row; idx += 128) {
+          const int rr = idx / per_row;
+          const int c4 = idx - rr * per_row;
+          if (c4 * 4 >= valid) continue;
+          const int64_t off = (lr0 + rr) * N + c0 + c4 * 4;
+          float4 a = __ldcg(reinterpret_cast<const float4*>(slots + off));
+          for (int s = 1; s < R.W; ++s) {  // ascending source rank
+            const float4 b = __ldcg(reinterpret_cast<const float4*>(slots + s * slot_stride + off));
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+          }
+          uint2 o;
+          o.x = pack_bf16x2(a.x, a.y);
+          o.y = pack_bf16x2(a.z, a.w);
+          *reinterpret_cast<uint2*>(out + off) = o;
+        }
+      }
+    }
+  } else {
+    // ================================================================ co-located comm warps
+    if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {
+      if (args.comm_ctas_per_rank == 0) {
+        const int cw = warp - kCommWarp0;
+        comm_worker<COMM>(R, args, cta * kColocCommWarps + cw, n_cta * kColocCommWarps,
+                          smem + L.off_comm + cw * kCommBufs * kColocBufBytes, kColocBufBytes,
+                          commbars + cw * kCommBufs);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C_::kTmemCols);
+  }
+}
+
+}  // namespace dev
+
+// ------------------------------------------------------------------------------- launcher
+namespace {
+template <int BN, int MODE, int COMM>
+cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
+  auto kern = dev::fused_kernel<BN, MODE, COMM>;
+  constexpr bool tma_comm = (MODE == MODE_AG && COMM == COMM_TMA);
+  const size_t smem_gemm = dev::gemm_layout<BN>(tma_comm).total;
+  const size_t smem_comm = (MODE == MODE_AG && COMM != COMM_NONE) ? dev::comm_cta_layout().total : 0;
+  const size_t smem = smem_gemm > smem_comm ? smem_gemm : smem_comm;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(args.n_group * (args.ctas_per_rank + args.comm_ctas_per_rank));
+  cfg.blockDim = dim3(dev::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (spin-waits, H3)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args);
+}
+
+template <int BN>
+cudaError_t launch_bn(const KernelArgs& args, int comm, cudaStream_t stream) {
+  switch (args.mode) {
+    case MODE_GEMM:
+      return launch_one<BN, MODE_GEMM, COMM_NONE>(args, stream);
+    case MODE_RS:
+      return launch_one<BN, MODE_RS, COMM_NONE>(args, stream);
+    case MODE_AG:
+      if (comm == COMM_TMA) return launch_one<BN, MODE_AG, COMM_TMA>(args, stream);
+      if (comm == COMM_LDST) return launch_one<BN, MODE_AG, COMM_LDST>(args, stream);
+      return launch_one<BN, MODE_AG, COMM_NONE>(args, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_fused(const KernelArgs& args, int bn, int comm, cudaStream_t stream) {
+  if (bn == 256) return launch_bn<256>(args, comm, stream);
+  if (bn == 128) return launch_bn<128>(args, comm, stream);
+  return cudaErrorInvalidValue;
+}
+
+size_t fused_smem_bytes(int bn, int mode, int comm, bool comm_cta) {
+  if (comm_cta) return dev::comm_cta_layout().total;
+  const bool tc = mode == MODE_AG && comm == COMM_TMA;
+  return bn == 256 ? dev::gemm_layout<256>(tc).total : dev::gemm_layout<128>(tc).total;
+}
+
+}  // namespace ao

@@ -1,0 +1,72 @@
+// kernel_args.h -- parameter block of the fused persistent kernel (host <-> device).
+//
+// One launch carries n_group ranks of the same world that live on the same device
+// (loopback) -- or a single rank in the one-process-per-GPU deployment.  The block index
+// selects the rank group: CTAs [g*ctas_per_rank, (g+1)*ctas_per_rank) are rank g's GEMM
+// workers (plan CTA c = blockIdx % ctas_per_rank); dedicated communication CTAs follow.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "autooverlap.h"
+
+namespace ao {
+
+enum KernelMode : int { MODE_GEMM = 0, MODE_AG = 1, MODE_RS = 2 };
+enum CommKind : int { COMM_NONE = 0, COMM_TMA = 1, COMM_LDST = 2 };
+
+// Host-mapped record of the first device-side spin timeout.
+struct ErrorInfo {
+  volatile uint32_t flag;
+  int32_t rank, cta, chunk;
+  uint32_t epoch, seen, target, pad;
+};
+
+// A communication work item of the in-kernel AG backends: copy `bytes` bytes at byte
+// offset `off` of chunk `g` from the local shard to rank `peer`'s gathered buffer, then
+// release flag word g*n_slices + slice at `peer`.
+struct CommItem {
+  int32_t peer, g, slice, pad;
+  int64_t src_off, dst_off, bytes;  // byte offsets (src: local shard, dst: gathered buffer)
+};
+
+struct alignas(64) RankArgs {
+  CUtensorMap tmA;      // AG: gathered buffer (current parity) [M, K]; RS/GEMM: A [M, K]
+  CUtensorMap tmA_loc;  // AG: local shard [S, K]
+  CUtensorMap tmB;      // B [N, K]
+  const int* order;            // [n_tiles] tile ids in execution order
+  const int* wait_off;         // [n_cta + 1] CSR offsets into waits
+  const int2* waits;           // (position k, chunk g)
+  const int* tiles_per_chunk;  // RS [n_chunks]
+  const int* reduce_items;     // RS [n_items] tile ids
+  const CommItem* comm_items;  // AG in-kernel comm [n_comm_items]
+  void* C;                     // AG/GEMM: C [M, N] bf16.  RS: C_shard [S, N] bf16
+  const char* A_shard;         // AG: local shard (source of pushes)
+  uint32_t* flags;             // this rank's flag words (current parity)
+  uint32_t* peer_flags[AO_MAX_WORLD];  // every rank's flag words (current parity)
+  char* peer_data[AO_MAX_WORLD];       // every rank's data half (current parity)
+  uint32_t* counters;                  // RS: local per-chunk completion counters
+  int64_t M, N, K, S;
+  int32_t rank, W, crows, n_chunks, n_tiles, n_items, n_nb, n_slices, n_comm_items, n_cta;
+  uint32_t epoch;
+  int32_t pad;
+};
+
+struct KernelArgs {
+  RankArgs rk[AO_MAX_WORLD];
+  int32_t n_group;
+  int32_t ctas_per_rank;       // GEMM CTAs per rank (== plan n_cta)
+  int32_t comm_ctas_per_rank;  // dedicated comm CTAs per rank
+  int32_t mode;                // KernelMode
+  uint64_t timeout_ns;
+  ErrorInfo* err;              // host-mapped
+  int32_t skip_wait;           // debug: CSR index of a wait of rank group 0 to skip (-1 none)
+  uint32_t delay_ns;           // debug: sleep before each comm signal
+};
+
+// Host-side launcher (fused.cu).
+cudaError_t launch_fused(const KernelArgs& args, int bn, int comm, cudaStream_t stream);
+size_t fused_smem_bytes(int bn, int mode, int comm, bool comm_cta);
+
+}  // namespace ao

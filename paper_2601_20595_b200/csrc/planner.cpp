@@ -1,0 +1,433 @@
+// planner.cpp -- host chunk-schedule planner (closed forms; see planner.h).
+// Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, Qn = DESIGN.md reading n.
+#include "planner.h"
+
+#include <algorithm>
+#include <map>
+#include <sstream>
+#include <tuple>
+
+namespace ao {
+
+const TileShape kTileCandidates[] = {{128, 256, 1}, {128, 128, 1}};
+const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[0]);
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static const char* op_name(int op) { return op == AO_OP_AG_GEMM ? "ag_gemm" : "gemm_rs"; }
+static const char* backend_name(int b) { return b == AO_BACKEND_CE ? "ce" : (b == AO_BACKEND_TMA ? "tma" : "ldst"); }
+static const char* dir_name(int d) { return d == AO_DIR_PUSH ? "push" : "pull"; }
+static const char* chunk_order_name(int o) { return o == AO_CHUNK_SHARD_MAJOR ? "shard_major" : "chunk_major"; }
+static const char* intra_name(int i) { return i == AO_INTRA_ROW ? "row" : (i == AO_INTRA_COL ? "col" : "grouped"); }
+
+static int workers(const ao_plan_desc& d, int sm_count) { return d.n_cta > 0 ? d.n_cta : sm_count - d.comm_ctas; }
+
+std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
+  std::vector<std::string> v;
+  if (d.struct_size != sizeof(ao_plan_desc)) v.push_back("struct_size");
+  if (d.op != AO_OP_AG_GEMM && d.op != AO_OP_GEMM_RS) v.push_back("op");
+  const int W = d.world_size;
+  if (W < 1 || W > AO_MAX_WORLD) v.push_back("world_size");
+  if (!(d.rank >= 0 && d.rank < std::max(W, 1))) v.push_back("rank");
+  if (d.M < 0 || d.N < 0 || d.K < 0) v.push_back("shape");
+  if (W >= 1 && d.M % W != 0) v.push_back("M % world_size");
+  const int64_t S = W >= 1 ? d.M / W : 0;
+  if (d.chunk_rows <= 0 || d.chunk_rows % 8 != 0 || (S > 0 && S % d.chunk_rows != 0)) v.push_back("chunk_rows");
+  if (d.K % 8 != 0) v.push_back("K % 8");
+  if (d.N % 8 != 0) v.push_back("N % 8");
+  if (d.backend < AO_BACKEND_CE || d.backend > AO_BACKEND_LDST) v.push_back("backend");
+  if (d.dir != AO_DIR_PUSH && d.dir != AO_DIR_PULL) v.push_back("dir");
+  if (d.dir == AO_DIR_PULL && d.op == AO_OP_GEMM_RS) v.push_back("pull with gemm_rs");
+  if (d.chunk_order != AO_CHUNK_SHARD_MAJOR && d.chunk_order != AO_CHUNK_CHUNK_MAJOR) v.push_back("chunk_order");
+  if (d.intra < AO_INTRA_ROW || d.intra > AO_INTRA_GROUPED) v.push_back("intra");
+  if (d.intra == AO_INTRA_GROUPED && d.group_m < 1) v.push_back("group_m");
+  if (d.comm_ctas < 0 || d.comm_ctas >= sm_count) v.push_back("comm_ctas");
+  if (d.n_cta < 0) v.push_back("n_cta");
+  if (d.n_slices < 1 || d.n_slices > 64) v.push_back("n_slices");
+  if (d.rs_wire != AO_WIRE_FP32 && d.rs_wire != AO_WIRE_BF16) v.push_back("rs_wire");
+  if ((d.tile_m == 0) != (d.tile_n == 0)) v.push_back("tile");
+  if (d.tile_m != 0) {
+    bool ok = false;
+    for (int i = 0; i < kNumTileCandidates; ++i)
+      if (kTileCandidates[i].bm == d.tile_m && kTileCandidates[i].bn == d.tile_n) ok = true;
+    if (!ok) v.push_back("tile");
+  }
+  if (v.empty()) {
+    TileShape t;
+    if (!pick_tile(d, sm_count, &t)) v.push_back("no tile shape fits");
+  }
+  return v;
+}
+
+// Q19: explicit tile, else argmax of util = T / (ceil(T/n) * n);
+// ties -> larger BM*BN, then larger BN.
+bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
+  const int64_t S = d.M / d.world_size;
+  bool have = false;
+  double best_u = -1;
+  int64_t best_area = -1, best_bn = -1;
+  for (int i = 0; i < kNumTileCandidates; ++i) {
+    const TileShape c = kTileCandidates[i];
+    if (d.tile_m != 0 && !(c.bm == d.tile_m && c.bn == d.tile_n)) continue;
+    if (S % c.bm != 0) continue;
+    const int64_t n = std::max(1, workers(d, sm_count) / c.cg);
+    const int64_t T = (d.M / c.bm) * ceil_div(d.N, c.bn);
+    const double u = T > 0 ? double(T) / double(ceil_div(T, n) * n) : 1.0;
+    const int64_t area = int64_t(c.bm) * c.bn;
+    if (!have || std::make_tuple(u, area, int64_t(c.bn)) > std::make_tuple(best_u, best_area, best_bn)) {
+      have = true;
+      best_u = u;
+      best_area = area;
+      best_bn = c.bn;
+      *out = c;
+    }
+  }
+  return have;
+}
+
+size_t data_bytes_per_parity(const ao_plan_desc& d) {
+  if (d.op == AO_OP_AG_GEMM) return size_t(d.M) * size_t(d.K) * 2;  // gathered A
+  const size_t eb = d.rs_wire == AO_WIRE_BF16 ? 2 : 4;
+  return size_t(d.M) * size_t(d.N) * eb;  // W slots of [S, N]
+}
+
+size_t flag_words_needed(const ao_plan_desc& d) {
+  const size_t nch = d.chunk_rows > 0 ? size_t(d.M / d.chunk_rows) : 0;
+  if (d.op == AO_OP_AG_GEMM) return nch * size_t(d.backend == AO_BACKEND_CE ? 1 : d.n_slices);
+  return nch * size_t(d.world_size);
+}
+
+uint64_t fnv1a64(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// ---------------------------------------------------------------------------------------
+// canonical JSON writer: keys sorted bytewise (== Python json.dumps(sort_keys=True) for
+// ASCII keys), separators (',', ':'), integers only.
+namespace {
+struct Obj {
+  std::map<std::string, std::string> kv;
+  void put(const std::string& k, const std::string& raw) { kv[k] = raw; }
+  void put(const std::string& k, int64_t v) { kv[k] = std::to_string(v); }
+  void put_str(const std::string& k, const std::string& s) { kv[k] = "\"" + s + "\""; }
+  std::string str() const {
+    std::string o = "{";
+    bool first = true;
+    for (auto& e : kv) {
+      if (!first) o += ",";
+      first = false;
+      o += "\"" + e.first + "\":" + e.second;
+    }
+    return o + "}";
+  }
+};
+template <class T>
+std::string int_list(const T& v) {
+  std::string o = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i) o += ",";
+    o += std::to_string(v[i]);
+  }
+  return o + "]";
+}
+template <class T>
+std::string list_of(const std::vector<T>& v) {
+  std::string o = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i) o += ",";
+    o += int_list(v[i]);
+  }
+  return o + "]";
+}
+}  // namespace
+
+static std::string rank_independent_key(const HostPlan& p) {
+  const ao_plan_desc& d = p.desc;
+  Obj o;
+  o.put_str("op", op_name(d.op));
+  o.put("world_size", p.W);
+  o.put("M", p.M);
+  o.put("N", p.N);
+  o.put("K", p.K);
+  o.put("chunk_rows", p.C);
+  o.put("tile", int_list(std::vector<int>{p.tile.bm, p.tile.bn, p.tile.cg}));
+  o.put_str("backend", backend_name(d.backend));
+  o.put_str("dir", dir_name(d.dir));
+  o.put_str("chunk_order", chunk_order_name(d.chunk_order));
+  o.put_str("intra", intra_name(d.intra));
+  o.put("group_m", d.group_m);
+  o.put("n_cta", p.n_cta);
+  o.put("comm_ctas", d.comm_ctas);
+  o.put("n_slices", d.backend == AO_BACKEND_CE ? 1 : d.n_slices);
+  o.put("rs_wire", d.rs_wire);
+  return o.str();
+}
+
+std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPlan* p) {
+  std::vector<std::string> viol = validate_desc(d, sm_count);
+  if (!viol.empty()) return viol;
+  HostPlan& P = *p;
+  P = HostPlan{};
+  P.desc = d;
+  P.sm_count = sm_count;
+  P.W = d.world_size;
+  P.rank = d.rank;
+  P.M = d.M;
+  P.N = d.N;
+  P.K = d.K;
+  P.S = d.M / d.world_size;
+  P.C = d.chunk_rows;
+  P.is_ag = d.op == AO_OP_AG_GEMM;
+  pick_tile(d, sm_count, &P.tile);
+  P.n_cta = std::max(1, workers(d, sm_count) / P.tile.cg);
+  P.n_chunks = int(P.M / P.C);
+  P.n_c = int(P.S / P.C);
+  P.n_mb = int(P.M / P.tile.bm);
+  P.n_nb = int(ceil_div(P.N, P.tile.bn));
+  P.n_tiles = P.n_mb * P.n_nb;
+  const int W = P.W, r = P.rank, n_c = P.n_c;
+
+  // Rule 1: chunk g covers rows [gC, (g+1)C); src/owner = floor(gC / S); j = index in shard.
+  auto owner_of = [&](int g) { return int((int64_t(g) * P.C) / P.S); };
+  auto j_of = [&](int g) { return int((int64_t(g) * P.C - int64_t(owner_of(g)) * P.S) / P.C); };
+
+  // Rule 2/3: per-rank op lists and arrival positions (closed forms).
+  P.plans.assign(W, {});
+  for (int q = 0; q < W; ++q) {
+    std::vector<P2POp>& ops = P.plans[q];
+    if (P.is_ag) {
+      // Lst.2: peer = (i + rank) mod W for i = 1..W-1 (Q1); push sends own shard, pull
+      // fetches the peer's shard.
+      auto emit = [&](int dstep, int j) {
+        const int peer = (q + dstep) % W;
+        const int src = d.dir == AO_DIR_PUSH ? q : peer;
+        const int g = src * n_c + j;
+        ops.push_back(P2POp{peer, int64_t(g) * P.C, P.C, d.dir, 0});
+      };
+      if (d.chunk_order == AO_CHUNK_SHARD_MAJOR) {
+        for (int ds = 1; ds < W; ++ds)
+          for (int j = 0; j < n_c; ++j) emit(ds, j);
+      } else {
+        for (int j = 0; j < n_c; ++j)
+          for (int ds = 1; ds < W; ++ds) emit(ds, j);
+      }
+    } else {
+      // owners q+1, ..., q+W-1, then q (own rows last)
+      auto emit = [&](int e, int j) {
+        const int o = (q + e + 1) % W;
+        const int g = o * n_c + j;
+        ops.push_back(P2POp{o, int64_t(g) * P.C, P.C, AO_DIR_PUSH, 1});
+      };
+      if (d.chunk_order == AO_CHUNK_SHARD_MAJOR) {
+        for (int e = 0; e < W; ++e)
+          for (int j = 0; j < n_c; ++j) emit(e, j);
+      } else {
+        for (int j = 0; j < n_c; ++j)
+          for (int e = 0; e < W; ++e) emit(e, j);
+      }
+    }
+  }
+  P.chunks.resize(P.n_chunks);
+  for (int g = 0; g < P.n_chunks; ++g) {
+    const int src = owner_of(g), j = j_of(g);
+    int pos;
+    if (P.is_ag) {
+      if (src == r) {
+        pos = 0;
+      } else {
+        const int dstep = d.dir == AO_DIR_PUSH ? (r - src + W) % W : (src - r + W) % W;
+        const int idx = d.chunk_order == AO_CHUNK_SHARD_MAJOR ? (dstep - 1) * n_c + j : j * (W - 1) + (dstep - 1);
+        pos = 1 + idx;
+      }
+    } else {
+      const int dd = (src - r + W) % W;
+      const int e = dd == 0 ? W - 1 : dd - 1;
+      pos = d.chunk_order == AO_CHUNK_SHARD_MAJOR ? e * n_c + j : j * W + e;
+    }
+    P.chunks[g] = {g, int(int64_t(g) * P.C), P.C, src, pos};
+  }
+
+  // Rule 4/5: deps and groups.
+  const int BM = P.tile.bm;
+  P.deps.resize(P.n_tiles);
+  std::vector<int> glo_of(P.n_tiles), ghi_of(P.n_tiles);
+  for (int t = 0; t < P.n_tiles; ++t) {
+    const int mb = t / P.n_nb;
+    const int64_t r0 = int64_t(mb) * BM, r1 = std::min<int64_t>(P.M, int64_t(mb + 1) * BM);
+    const int glo = int(r0 / P.C), ghi = int(ceil_div(r1, P.C) - 1);
+    int grp = 0;
+    for (int g = glo; g <= ghi; ++g) grp = std::max(grp, P.chunks[g][4]);
+    P.deps[t] = {t, glo, ghi, grp};
+    glo_of[t] = glo;
+    ghi_of[t] = ghi;
+  }
+
+  // Rule 6: stable sort by (group, intra key).
+  auto intra_key = [&](int t) {
+    const int mb = t / P.n_nb, nb = t % P.n_nb;
+    if (d.intra == AO_INTRA_ROW) return std::make_tuple(mb, nb, 0);
+    if (d.intra == AO_INTRA_COL) return std::make_tuple(nb, mb, 0);
+    return std::make_tuple(mb / d.group_m, nb, mb);
+  };
+  P.order.resize(P.n_tiles);
+  for (int t = 0; t < P.n_tiles; ++t) P.order[t] = t;
+  std::stable_sort(P.order.begin(), P.order.end(), [&](int a, int b) {
+    return std::make_tuple(P.deps[a][3], intra_key(a)) < std::make_tuple(P.deps[b][3], intra_key(b));
+  });
+
+  // RS: tiles_per_chunk and reduce items (own-row tiles by (latest j, intra key)).
+  if (!P.is_ag) {
+    P.tiles_per_chunk.assign(P.n_chunks, 0);
+    for (int g = 0; g < P.n_chunks; ++g) {
+      const int64_t r0 = int64_t(g) * P.C, r1 = r0 + P.C - 1;
+      const int mb_lo = int(r0 / BM), mb_hi = int(r1 / BM);
+      P.tiles_per_chunk[g] = (mb_hi - mb_lo + 1) * P.n_nb;
+    }
+    std::vector<int> own;
+    for (int t = 0; t < P.n_tiles; ++t)
+      if ((int64_t(t / P.n_nb) * BM) / P.S == r) own.push_back(t);
+    std::stable_sort(own.begin(), own.end(), [&](int a, int b) {
+      return std::make_tuple(j_of(ghi_of[a]), intra_key(a)) < std::make_tuple(j_of(ghi_of[b]), intra_key(b));
+    });
+    for (int t : own) P.reduce_items.push_back({t, glo_of[t], ghi_of[t]});
+  }
+
+  // Rules 7/8: CTA k mod n_cta; one wait per (CTA, chunk) first use.
+  const int n_work = P.n_tiles + int(P.reduce_items.size());
+  P.waits.assign(P.n_cta, {});
+  std::vector<int> seen(P.n_chunks, -1);
+  for (int c = 0; c < P.n_cta; ++c) {
+    for (int k = c; k < n_work; k += P.n_cta) {
+      int glo, ghi;
+      bool need;
+      if (k < P.n_tiles) {
+        const int t = P.order[k];
+        glo = glo_of[t];
+        ghi = ghi_of[t];
+        need = P.is_ag;
+      } else {
+        const auto& it = P.reduce_items[k - P.n_tiles];
+        glo = it[1];
+        ghi = it[2];
+        need = true;
+      }
+      if (!need) continue;
+      for (int g = glo; g <= ghi; ++g) {
+        if (P.is_ag && P.chunks[g][3] == r) continue;
+        if (seen[g] == c) continue;
+        seen[g] = c;
+        P.waits[c].push_back({k, g});
+      }
+    }
+  }
+
+  // Rule 9: signal words per chunk at this rank.
+  P.contrib.resize(P.n_chunks);
+  const int ns = d.backend == AO_BACKEND_CE ? 1 : d.n_slices;
+  for (int g = 0; g < P.n_chunks; ++g) {
+    const bool own = P.chunks[g][3] == r;
+    P.contrib[g] = P.is_ag ? (own ? 0 : ns) : (own ? W : 0);
+  }
+
+  // ---- canonical export ---------------------------------------------------------------
+  Obj o;
+  o.put_str("op", op_name(d.op));
+  o.put("world_size", W);
+  o.put("rank", r);
+  o.put("M", P.M);
+  o.put("N", P.N);
+  o.put("K", P.K);
+  o.put("chunk_rows", P.C);
+  o.put("tile", int_list(std::vector<int>{P.tile.bm, P.tile.bn, P.tile.cg}));
+  o.put_str("backend", backend_name(d.backend));
+  o.put_str("dir", dir_name(d.dir));
+  o.put_str("chunk_order", chunk_order_name(d.chunk_order));
+  o.put_str("intra", intra_name(d.intra));
+  o.put("group_m", d.group_m);
+  o.put("n_cta", P.n_cta);
+  o.put("comm_ctas", d.comm_ctas);
+  o.put("n_slices", ns);
+  {
+    Obj tens;
+    if (P.is_ag) {
+      Obj a, c;
+      a.put("elem_bytes", 2);
+      a.put("shape", int_list(std::vector<int64_t>{P.M, P.K}));
+      c.put("elem_bytes", 2);
+      c.put("shape", int_list(std::vector<int64_t>{P.M, P.N}));
+      tens.put("A", a.str());
+      tens.put("C", c.str());
+    } else {
+      Obj c, pp;
+      c.put("elem_bytes", 2);
+      c.put("shape", int_list(std::vector<int64_t>{P.M, P.N}));
+      pp.put("elem_bytes", 4);
+      pp.put("shape", int_list(std::vector<int64_t>{P.M, P.N}));
+      tens.put("C", c.str());
+      tens.put("P", pp.str());
+    }
+    o.put("tensors", tens.str());
+  }
+  {
+    std::string s = "[";
+    for (int q = 0; q < W; ++q) {
+      if (q) s += ",";
+      Obj reg;
+      if (P.is_ag)
+        reg.put("A", "[" + int_list(std::vector<int64_t>{int64_t(q) * P.S, P.S}) + "]");
+      else
+        reg.put("P", "[" + int_list(std::vector<int64_t>{0, P.M}) + "]");
+      s += reg.str();
+    }
+    o.put("owner_regions", s + "]");
+  }
+  {
+    std::string s = "[";
+    for (int q = 0; q < W; ++q) {
+      if (q) s += ",";
+      s += "[";
+      for (size_t i = 0; i < P.plans[q].size(); ++i) {
+        const P2POp& op = P.plans[q][i];
+        if (i) s += ",";
+        Obj e;
+        e.put("accumulate", op.accumulate);
+        e.put("deps", "[]");
+        e.put_str("direction", dir_name(op.direction));
+        e.put("dst_chunk", int_list(std::vector<int64_t>{op.row0, op.rows}));
+        e.put("peer", op.peer);
+        e.put("src_chunk", int_list(std::vector<int64_t>{op.row0, op.rows}));
+        e.put_str("tensor", P.is_ag ? "A" : "P");
+        e.put_str("variant", "p2p");
+        s += e.str();
+      }
+      s += "]";
+    }
+    o.put("plans", s + "]");
+  }
+  o.put("chunks", list_of(P.chunks));
+  o.put("deps", list_of(P.deps));
+  o.put("order", int_list(P.order));
+  {
+    std::string s = "[";
+    for (int c = 0; c < P.n_cta; ++c) {
+      if (c) s += ",";
+      s += "[" + std::to_string(c) + "," + list_of(P.waits[c]) + "]";
+    }
+    o.put("waits", s + "]");
+  }
+  o.put("contrib", int_list(P.contrib));
+  if (!P.is_ag) {
+    o.put("tiles_per_chunk", int_list(P.tiles_per_chunk));
+    o.put("reduce_items", list_of(P.reduce_items));
+  }
+  P.json = o.str();
+  P.hash = fnv1a64(rank_independent_key(P));
+  return {};
+}
+
+}  // namespace ao

@@ -1,0 +1,737 @@
+// runtime.cpp -- host runtime and C ABI of libautooverlap (see include/autooverlap.h).
+//
+//  * symmetric workspace per rank: cudaMalloc'd [data parity 0 | data parity 1 |
+//    flags parity 0 | flags parity 1], exported with cudaIpcGetMemHandle and mapped by the
+//    peers (cudaIpcOpenMemHandle, NVLink P2P) -- or mapped directly when the peer ctx lives
+//    in the same process (loopback: several ranks on one GPU).  NVSHMEM's symmetric heap of
+//    the paper is replaced by this.
+//  * epochs: every op call advances the ctx epoch; data and flags of epoch e live in parity
+//    e % 2, flags are written with the absolute epoch value (Q10/Q11).
+//  * copy-engine backend (Fig.7a): the source rank's side stream issues one peer
+//    cudaMemcpyAsync per chunk followed by cuStreamWriteValue32(flag, epoch) -- a
+//    global-memory signal written without any SM.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "autooverlap.h"
+#include "kernel_args.h"
+#include "planner.h"
+
+// --------------------------------------------------------------------------- error state
+namespace {
+thread_local std::string g_last_error;
+
+ao_status fail(ao_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define AO_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t _e = (call);                                                                  \
+    if (_e != cudaSuccess) return fail(AO_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), \
+                                       __FILE__, __LINE__);                                   \
+  } while (0)
+
+constexpr size_t kFlagWordsPerParity = size_t(1) << 18;  // 1 MiB of u32 per parity
+constexpr size_t kCounterWords = size_t(1) << 16;
+constexpr uint32_t kBlobMagic = 0x414f5648u;  // "AOVH"
+
+// ------------------------------------------------------------------ driver entry points
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct DriverFns {
+  PFN_encodeTiled encode = nullptr;
+  PFN_writeValue32 write32 = nullptr;
+};
+
+ao_status get_driver(DriverFns** out) {
+  static DriverFns fns;
+  static bool loaded = false;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!loaded) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    AO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) return fail(AO_ERR_CUDA, "cuTensorMapEncodeTiled not found");
+    fns.encode = reinterpret_cast<PFN_encodeTiled>(p);
+    p = nullptr;
+    AO_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q));
+    if (!p) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 not found");
+    fns.write32 = reinterpret_cast<PFN_writeValue32>(p);
+    loaded = true;
+  }
+  *out = &fns;
+  return AO_OK;
+}
+
+uint64_t host_id() {
+  char h[256] = {0};
+  gethostname(h, sizeof h - 1);
+  return ao::fnv1a64(std::string(h));
+}
+
+struct Blob {
+  uint32_t magic, version;
+  int32_t pid, device, rank, world;
+  uint64_t data_half, total, raw_ptr, host;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(Blob) <= AO_HANDLE_BYTES, "blob too large");
+
+struct DebugKnobs {
+  int64_t skip_wait = -1;
+  int64_t delay_ns = 0;
+};
+DebugKnobs g_debug;
+
+}  // namespace
+
+// ------------------------------------------------------------------------------- objects
+struct ao_ctx {
+  int device = 0, rank = 0, W = 1, sm_count = 0;
+  size_t data_half = 0;
+  size_t total = 0;
+  char* base = nullptr;
+  uint32_t* counters = nullptr;
+  ao::ErrorInfo* err_host = nullptr;
+  ao::ErrorInfo* err_dev = nullptr;
+  bool imported = false;
+  char* peer_base[AO_MAX_WORLD] = {};
+  bool peer_opened[AO_MAX_WORLD] = {};
+  uint32_t epoch = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+
+  char* data(int q, uint32_t parity) const { return peer_base[q] + parity * data_half; }
+  uint32_t* flags(int q, uint32_t parity) const {
+    return reinterpret_cast<uint32_t*>(peer_base[q] + 2 * data_half + parity * kFlagWordsPerParity * 4);
+  }
+};
+
+struct ao_plan {
+  ao::HostPlan hp;
+  ao_ctx* ctx = nullptr;
+  int device = -1;
+  char* d_tables = nullptr;
+  const int* d_order = nullptr;
+  const int* d_wait_off = nullptr;
+  const int2* d_waits = nullptr;
+  const int* d_tpc = nullptr;
+  const int* d_items = nullptr;
+  const ao::CommItem* d_comm = nullptr;
+  int n_comm = 0;
+  int comm_kind = ao::COMM_NONE;
+};
+
+namespace {
+
+ao_status upload_tables(ao_plan* p) {
+  const ao::HostPlan& hp = p->hp;
+  std::vector<int> wait_off(hp.n_cta + 1, 0);
+  std::vector<int2> waits;
+  for (int c = 0; c < hp.n_cta; ++c) {
+    for (auto& w : hp.waits[c]) waits.push_back(make_int2(w[0], w[1]));
+    wait_off[c + 1] = int(waits.size());
+  }
+  std::vector<int> items;
+  for (auto& it : hp.reduce_items) items.push_back(it[0]);
+  // in-kernel comm items (AG push, TMA / LDST backends)
+  std::vector<ao::CommItem> comm;
+  if (hp.is_ag && hp.desc.backend != AO_BACKEND_CE && hp.desc.dir == AO_DIR_PUSH) {
+    const int64_t row_bytes = hp.K * 2;
+    const int64_t chunk_bytes = int64_t(hp.C) * row_bytes;
+    const int ns = hp.desc.n_slices;
+    const int64_t slice = ((chunk_bytes + ns - 1) / ns + 15) / 16 * 16;
+    for (const ao::P2POp& op : hp.plans[hp.rank]) {
+      const int g = int(op.row0 / hp.C);
+      for (int s = 0; s < ns; ++s) {
+        ao::CommItem it{};
+        it.peer = op.peer;
+        it.g = g;
+        it.slice = s;
+        const int64_t off = std::min<int64_t>(int64_t(s) * slice, chunk_bytes);
+        it.bytes = std::max<int64_t>(0, std::min<int64_t>(slice, chunk_bytes - off));
+        it.src_off = (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes + off;
+        it.dst_off = op.row0 * row_bytes + off;
+        comm.push_back(it);
+      }
+    }
+    p->comm_kind = hp.desc.backend == AO_BACKEND_TMA ? ao::COMM_TMA : ao::COMM_LDST;
+  }
+  p->n_comm = int(comm.size());
+
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t o_order = 0;
+  const size_t o_woff = o_order + al(hp.order.size() * 4 + 4);
+  const size_t o_waits = o_woff + al(wait_off.size() * 4);
+  const size_t o_tpc = o_waits + al(waits.size() * 8 + 8);
+  const size_t o_items = o_tpc + al(hp.tiles_per_chunk.size() * 4 + 4);
+  const size_t o_comm = o_items + al(items.size() * 4 + 4);
+  const size_t total = o_comm + al(comm.size() * sizeof(ao::CommItem) + 16);
+  std::vector<char> h(total, 0);
+  memcpy(h.data() + o_order, hp.order.data(), hp.order.size() * 4);
+  memcpy(h.data() + o_woff, wait_off.data(), wait_off.size() * 4);
+  if (!waits.empty()) memcpy(h.data() + o_waits, waits.data(), waits.size() * 8);
+  if (!hp.tiles_per_chunk.empty()) memcpy(h.data() + o_tpc, hp.tiles_per_chunk.data(), hp.tiles_per_chunk.size() * 4);
+  if (!items.empty()) memcpy(h.data() + o_items, items.data(), items.size() * 4);
+  if (!comm.empty()) memcpy(h.data() + o_comm, comm.data(), comm.size() * sizeof(ao::CommItem));
+  AO_CUDA(cudaMalloc(&p->d_tables, total));
+  AO_CUDA(cudaMemcpy(p->d_tables, h.data(), total, cudaMemcpyHostToDevice));
+  p->d_order = reinterpret_cast<const int*>(p->d_tables + o_order);
+  p->d_wait_off = reinterpret_cast<const int*>(p->d_tables + o_woff);
+  p->d_waits = reinterpret_cast<const int2*>(p->d_tables + o_waits);
+  p->d_tpc = reinterpret_cast<const int*>(p->d_tables + o_tpc);
+  p->d_items = reinterpret_cast<const int*>(p->d_tables + o_items);
+  p->d_comm = reinterpret_cast<const ao::CommItem*>(p->d_tables + o_comm);
+  return AO_OK;
+}
+
+ao_status encode_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  DriverFns* drv;
+  ao_status s = get_driver(&drv);
+  if (s != AO_OK) return s;
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+  cuuint32_t box[2] = {cuuint32_t(ao::kBK), cuuint32_t(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = drv->encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(AO_ERR_INVALID_ARG, "cuTensorMapEncodeTiled failed (%d) for %p [%lld x %lld]", int(r), ptr,
+                (long long)rows, (long long)cols);
+  return AO_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+ao_status check_device_sm100(int device, int* sm_count) {
+  cudaDeviceProp prop;
+  AO_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(AO_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only", device,
+                prop.major, prop.minor);
+  *sm_count = prop.multiProcessorCount;
+  return AO_OK;
+}
+
+ao_status take_async_error(ao_ctx* ctx) {
+  if (ctx && ctx->err_host && ctx->err_host->flag) {
+    const ao::ErrorInfo e = *ctx->err_host;
+    ctx->err_host->flag = 0;
+    return fail(AO_ERR_TIMEOUT, "device spin-wait timed out: rank %d cta %d chunk %d epoch %u (flag held %u)", e.rank,
+                e.cta, e.chunk, e.epoch, e.seen);
+  }
+  return AO_OK;
+}
+
+// Fill the rank-dependent part of the kernel args for one call.
+ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, const void* B, void* C) {
+  const ao::HostPlan& hp = p->hp;
+  ao_ctx* ctx = p->ctx;
+  const uint32_t par = epoch & 1;
+  memset(R, 0, sizeof(*R));
+  R->order = p->d_order;
+  R->wait_off = p->d_wait_off;
+  R->waits = p->d_waits;
+  R->tiles_per_chunk = p->d_tpc;
+  R->reduce_items = p->d_items;
+  R->comm_items = p->d_comm;
+  R->n_comm_items = p->n_comm;
+  R->C = C;
+  R->M = hp.M;
+  R->N = hp.N;
+  R->K = hp.K;
+  R->S = hp.S;
+  R->rank = hp.rank;
+  R->W = hp.W;
+  R->crows = hp.C;
+  R->n_chunks = hp.n_chunks;
+  R->n_tiles = hp.n_tiles;
+  R->n_items = int(hp.reduce_items.size());
+  R->n_nb = hp.n_nb;
+  R->n_slices = hp.desc.backend == AO_BACKEND_CE ? 1 : hp.desc.n_slices;
+  R->n_cta = hp.n_cta;
+  R->epoch = epoch;
+  R->counters = ctx ? ctx->counters : nullptr;
+  if (ctx) {
+    for (int q = 0; q < hp.W; ++q) {
+      R->peer_data[q] = ctx->data(q, par);
+      R->peer_flags[q] = ctx->flags(q, par);
+    }
+    R->flags = R->peer_flags[hp.rank];
+  }
+  const int bn = hp.tile.bn;
+  ao_status s;
+  if (hp.K > 0) {
+    if (hp.is_ag && ctx) {
+      s = encode_2d(&R->tmA, R->peer_data[hp.rank], hp.M, hp.K, 128);
+      if (s != AO_OK) return s;
+      s = encode_2d(&R->tmA_loc, A, hp.S, hp.K, 128);
+      if (s != AO_OK) return s;
+      R->A_shard = static_cast<const char*>(A);
+    } else {
+      s = encode_2d(&R->tmA, A, hp.M, hp.K, 128);
+      if (s != AO_OK) return s;
+    }
+    s = encode_2d(&R->tmB, B, hp.N, hp.K, bn);
+    if (s != AO_OK) return s;
+  }
+  R->C = C;
+  return AO_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char* ao_status_string(ao_status s) {
+  switch (s) {
+    case AO_OK: return "AO_OK";
+    case AO_ERR_INVALID_ARG: return "AO_ERR_INVALID_ARG";
+    case AO_ERR_UNSUPPORTED: return "AO_ERR_UNSUPPORTED";
+    case AO_ERR_CUDA: return "AO_ERR_CUDA";
+    case AO_ERR_OOM: return "AO_ERR_OOM";
+    case AO_ERR_PEER: return "AO_ERR_PEER";
+    case AO_ERR_TIMEOUT: return "AO_ERR_TIMEOUT";
+    case AO_ERR_STATE: return "AO_ERR_STATE";
+  }
+  return "AO_ERR_UNKNOWN";
+}
+
+const char* ao_last_error(void) { return g_last_error.c_str(); }
+
+ao_status ao_version(int* major, int* minor) {
+  if (major) *major = AO_VERSION_MAJOR;
+  if (minor) *minor = AO_VERSION_MINOR;
+  return AO_OK;
+}
+
+ao_status ao_debug_set(const char* key, int64_t value) {
+  if (!key) return fail(AO_ERR_INVALID_ARG, "null key");
+  if (!strcmp(key, "skip_wait")) g_debug.skip_wait = value;
+  else if (!strcmp(key, "delay_ns")) g_debug.delay_ns = value;
+  else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
+  return AO_OK;
+}
+
+ao_status ao_plan_desc_init(ao_plan_desc* d) {
+  if (!d) return fail(AO_ERR_INVALID_ARG, "null desc");
+  memset(d, 0, sizeof(*d));
+  d->struct_size = sizeof(ao_plan_desc);
+  d->op = AO_OP_AG_GEMM;
+  d->world_size = 1;
+  d->rank = 0;
+  d->chunk_rows = 128;
+  d->backend = AO_BACKEND_CE;
+  d->dir = AO_DIR_PUSH;
+  d->chunk_order = AO_CHUNK_SHARD_MAJOR;
+  d->intra = AO_INTRA_ROW;
+  d->group_m = 1;
+  d->n_slices = 1;
+  d->rs_wire = AO_WIRE_FP32;
+  return AO_OK;
+}
+
+ao_status ao_plan_validate(const ao_plan_desc* d, int sm_count, char* report, size_t cap, int* n_violations) {
+  if (!d) return fail(AO_ERR_INVALID_ARG, "null desc");
+  std::vector<std::string> v = ao::validate_desc(*d, sm_count > 0 ? sm_count : 148);
+  std::string joined;
+  for (size_t i = 0; i < v.size(); ++i) joined += (i ? ";" : "") + v[i];
+  if (report && cap) {
+    strncpy(report, joined.c_str(), cap - 1);
+    report[cap - 1] = 0;
+  }
+  if (n_violations) *n_violations = int(v.size());
+  if (!v.empty()) return fail(AO_ERR_INVALID_ARG, "invalid plan desc: %s", joined.c_str());
+  return AO_OK;
+}
+
+ao_status ao_plan_create_host(const ao_plan_desc* d, int sm_count, ao_plan** out) {
+  if (!d || !out) return fail(AO_ERR_INVALID_ARG, "null argument");
+  std::unique_ptr<ao_plan> p(new ao_plan());
+  std::vector<std::string> v = ao::build_plan(*d, sm_count > 0 ? sm_count : 148, &p->hp);
+  if (!v.empty()) {
+    std::string joined;
+    for (size_t i = 0; i < v.size(); ++i) joined += (i ? ";" : "") + v[i];
+    return fail(AO_ERR_INVALID_ARG, "invalid plan desc: %s", joined.c_str());
+  }
+  *out = p.release();
+  return AO_OK;
+}
+
+ao_status ao_plan_export_json(const ao_plan* p, char* buf, size_t cap, size_t* needed) {
+  if (!p) return fail(AO_ERR_INVALID_ARG, "null plan");
+  const std::string& s = p->hp.json;
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return AO_OK;
+}
+
+ao_status ao_plan_hash(const ao_plan* p, uint64_t* out) {
+  if (!p || !out) return fail(AO_ERR_INVALID_ARG, "null argument");
+  *out = p->hp.hash;
+  return AO_OK;
+}
+
+ao_status ao_plan_info(const ao_plan* p, int32_t* tile_m, int32_t* tile_n, int32_t* cta_group, int32_t* n_cta,
+                       int32_t* n_tiles, int32_t* n_chunks) {
+  if (!p) return fail(AO_ERR_INVALID_ARG, "null plan");
+  if (tile_m) *tile_m = p->hp.tile.bm;
+  if (tile_n) *tile_n = p->hp.tile.bn;
+  if (cta_group) *cta_group = p->hp.tile.cg;
+  if (n_cta) *n_cta = p->hp.n_cta;
+  if (n_tiles) *n_tiles = p->hp.n_tiles;
+  if (n_chunks) *n_chunks = p->hp.n_chunks;
+  return AO_OK;
+}
+
+ao_status ao_plan_workspace_bytes(const ao_plan_desc* d, size_t* bytes) {
+  if (!d || !bytes) return fail(AO_ERR_INVALID_ARG, "null argument");
+  *bytes = 2 * ao::data_bytes_per_parity(*d);
+  return AO_OK;
+}
+
+ao_status ao_plan_destroy(ao_plan* p) {
+  if (!p) return AO_OK;
+  if (p->d_tables) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    cudaFree(p->d_tables);
+    cudaSetDevice(cur);
+  }
+  delete p;
+  return AO_OK;
+}
+
+// ---------------------------------------------------------------------------- contexts
+ao_status ao_ctx_create(int device, int rank, int world_size, size_t workspace_bytes, ao_ctx** out) {
+  if (!out) return fail(AO_ERR_INVALID_ARG, "null out");
+  if (world_size < 1 || world_size > AO_MAX_WORLD || rank < 0 || rank >= world_size)
+    return fail(AO_ERR_INVALID_ARG, "bad rank/world (%d/%d)", rank, world_size);
+  int sm = 0;
+  AO_CUDA(cudaSetDevice(device));
+  ao_status s = check_device_sm100(device, &sm);
+  if (s != AO_OK) return s;
+  std::unique_ptr<ao_ctx> c(new ao_ctx());
+  c->device = device;
+  c->rank = rank;
+  c->W = world_size;
+  c->sm_count = sm;
+  c->data_half = (workspace_bytes / 2 + 4095) / 4096 * 4096;
+  c->total = 2 * c->data_half + 2 * kFlagWordsPerParity * 4;
+  cudaError_t e = cudaMalloc(&c->base, c->total);
+  if (e != cudaSuccess) return fail(AO_ERR_OOM, "cudaMalloc(%zu): %s", c->total, cudaGetErrorString(e));
+  AO_CUDA(cudaMemset(c->base + 2 * c->data_half, 0, 2 * kFlagWordsPerParity * 4));
+  AO_CUDA(cudaMalloc(&c->counters, kCounterWords * 4));
+  AO_CUDA(cudaMemset(c->counters, 0, kCounterWords * 4));
+  AO_CUDA(cudaHostAlloc(&c->err_host, sizeof(ao::ErrorInfo), cudaHostAllocMapped));
+  memset(c->err_host, 0, sizeof(ao::ErrorInfo));
+  AO_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+  AO_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  AO_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+  AO_CUDA(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  AO_CUDA(cudaDeviceSynchronize());
+  c->peer_base[rank] = c->base;
+  if (world_size == 1) c->imported = true;
+  *out = c.release();
+  return AO_OK;
+}
+
+ao_status ao_ctx_export_handle(ao_ctx* c, ao_handle_blob* out) {
+  if (!c || !out) return fail(AO_ERR_INVALID_ARG, "null argument");
+  memset(out, 0, sizeof(*out));
+  Blob b{};
+  b.magic = kBlobMagic;
+  b.version = AO_VERSION_MAJOR * 100 + AO_VERSION_MINOR;
+  b.pid = int32_t(getpid());
+  b.device = c->device;
+  b.rank = c->rank;
+  b.world = c->W;
+  b.data_half = c->data_half;
+  b.total = c->total;
+  b.raw_ptr = reinterpret_cast<uint64_t>(c->base);
+  b.host = host_id();
+  AO_CUDA(cudaSetDevice(c->device));
+  AO_CUDA(cudaIpcGetMemHandle(&b.ipc, c->base));
+  memcpy(out->bytes, &b, sizeof b);
+  return AO_OK;
+}
+
+ao_status ao_ctx_import_handles(ao_ctx* c, const ao_handle_blob* all) {
+  if (!c || !all) return fail(AO_ERR_INVALID_ARG, "null argument");
+  AO_CUDA(cudaSetDevice(c->device));
+  const uint64_t me = host_id();
+  for (int q = 0; q < c->W; ++q) {
+    if (q == c->rank) continue;
+    Blob b;
+    memcpy(&b, all[q].bytes, sizeof b);
+    if (b.magic != kBlobMagic) return fail(AO_ERR_PEER, "handle %d: bad magic", q);
+    if (b.rank != q || b.world != c->W) return fail(AO_ERR_PEER, "handle %d: rank/world mismatch (%d/%d)", q, b.rank, b.world);
+    if (b.data_half != c->data_half || b.total != c->total)
+      return fail(AO_ERR_PEER, "handle %d: workspace size mismatch (%llu vs %llu)", q,
+                  (unsigned long long)b.data_half, (unsigned long long)c->data_half);
+    if (b.pid == int32_t(getpid()) && b.host == me) {
+      if (b.device != c->device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(AO_ERR_CUDA, "peer access %d->%d: %s", c->device, b.device, cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+      c->peer_base[q] = reinterpret_cast<char*>(b.raw_ptr);
+      c->peer_opened[q] = false;
+    } else {
+      void* p = nullptr;
+      AO_CUDA(cudaIpcOpenMemHandle(&p, b.ipc, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_base[q] = static_cast<char*>(p);
+      c->peer_opened[q] = true;
+    }
+  }
+  c->imported = true;
+  return AO_OK;
+}
+
+ao_status ao_ctx_check_async(ao_ctx* c) {
+  if (!c) return fail(AO_ERR_INVALID_ARG, "null ctx");
+  return take_async_error(c);
+}
+
+ao_status ao_ctx_destroy(ao_ctx* c) {
+  if (!c) return AO_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int q = 0; q < c->W; ++q)
+    if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
+  if (c->base) cudaFree(c->base);
+  if (c->counters) cudaFree(c->counters);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  delete c;
+  return AO_OK;
+}
+
+ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
+  if (!c || !d || !out) return fail(AO_ERR_INVALID_ARG, "null argument");
+  if (d->world_size != c->W || d->rank != c->rank)
+    return fail(AO_ERR_INVALID_ARG, "desc rank/world (%d/%d) != ctx (%d/%d)", d->rank, d->world_size, c->rank, c->W);
+  AO_CUDA(cudaSetDevice(c->device));
+  ao_plan* p = nullptr;
+  ao_status s = ao_plan_create_host(d, c->sm_count, &p);
+  if (s != AO_OK) return s;
+  std::unique_ptr<ao_plan> guard(p);
+  if (ao::data_bytes_per_parity(*d) > c->data_half)
+    return fail(AO_ERR_INVALID_ARG, "workspace too small: plan needs %zu bytes per parity, ctx has %zu",
+                ao::data_bytes_per_parity(*d), c->data_half);
+  if (ao::flag_words_needed(*d) > kFlagWordsPerParity)
+    return fail(AO_ERR_INVALID_ARG, "too many chunk flags (%zu)", ao::flag_words_needed(*d));
+  if (size_t(p->hp.n_chunks) > kCounterWords) return fail(AO_ERR_INVALID_ARG, "too many chunks");
+  if (d->rs_wire != AO_WIRE_FP32 && d->op == AO_OP_GEMM_RS)
+    return fail(AO_ERR_UNSUPPORTED, "bf16 RS wire is not implemented (non-conforming, DESIGN.md Q14)");
+  if (d->op == AO_OP_AG_GEMM && d->dir == AO_DIR_PULL && d->world_size > 1)
+    return fail(AO_ERR_UNSUPPORTED, "PULL schedules are planned/exported but not executed yet");
+  p->ctx = c;
+  p->device = c->device;
+  s = upload_tables(p);
+  if (s != AO_OK) return s;
+  *out = guard.release();
+  return AO_OK;
+}
+
+// ------------------------------------------------------------------------------ op calls
+static ao_status launch_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
+                              void* const* Cs, void* const* Gouts, void* stream_v, int mode) {
+  if (n < 1 || n > AO_MAX_WORLD || !plans) return fail(AO_ERR_INVALID_ARG, "bad group size %d", n);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  ao_plan* p0 = plans[0];
+  if (!p0 || !p0->ctx) return fail(AO_ERR_STATE, "plan is not bound to a ctx");
+  const ao::HostPlan& h0 = p0->hp;
+  if ((mode == ao::MODE_AG) != h0.is_ag) return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is %s", h0.is_ag ? "ag_gemm" : "gemm_rs");
+  for (int i = 0; i < n; ++i) {
+    ao_plan* p = plans[i];
+    if (!p || !p->ctx) return fail(AO_ERR_STATE, "plan %d not bound", i);
+    if (!p->ctx->imported) return fail(AO_ERR_STATE, "ctx of rank %d: handles not imported", p->ctx->rank);
+    if (p->hp.hash != h0.hash) return fail(AO_ERR_PEER, "plan hash mismatch inside group");
+    if (p->ctx->device != p0->ctx->device) return fail(AO_ERR_INVALID_ARG, "group spans devices");
+    for (int j = 0; j < i; ++j)
+      if (plans[j]->ctx == p->ctx) return fail(AO_ERR_INVALID_ARG, "two plans of one ctx in a group");
+    if (!aligned16(As[i]) || !aligned16(Bs[i]) || !aligned16(Cs[i]))
+      return fail(AO_ERR_INVALID_ARG, "operands must be 16-byte aligned device pointers");
+    ao_status s = take_async_error(p->ctx);
+    if (s != AO_OK) return s;
+  }
+  AO_CUDA(cudaSetDevice(p0->ctx->device));
+  if (h0.M == 0 || h0.N == 0) return AO_OK;
+
+  std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
+  memset(ka.get(), 0, sizeof(ao::KernelArgs));
+  ka->n_group = n;
+  ka->ctas_per_rank = h0.n_cta;
+  ka->mode = mode;
+  ka->timeout_ns = h0.desc.timeout_ns ? h0.desc.timeout_ns : 5000000000ull;
+  ka->err = p0->ctx->err_dev;
+  ka->skip_wait = int32_t(g_debug.skip_wait);
+  ka->delay_ns = uint32_t(g_debug.delay_ns);
+  const bool ce = mode == ao::MODE_AG && h0.desc.backend == AO_BACKEND_CE && h0.W > 1;
+  const int comm = mode == ao::MODE_AG ? p0->comm_kind : ao::COMM_NONE;
+  ka->comm_ctas_per_rank = (comm != ao::COMM_NONE) ? h0.desc.comm_ctas : 0;
+  std::vector<uint32_t> epochs(n);
+  for (int i = 0; i < n; ++i) {
+    ao_ctx* c = plans[i]->ctx;
+    epochs[i] = ++c->epoch;
+    if (epochs[i] != epochs[0]) return fail(AO_ERR_STATE, "ranks of a group disagree on the epoch");
+    ao_status s = fill_rank(&ka->rk[i], plans[i], epochs[i], As[i], Bs[i], Cs[i]);
+    if (s != AO_OK) return s;
+  }
+  DriverFns* drv = nullptr;
+  if (ce) {
+    ao_status s = get_driver(&drv);
+    if (s != AO_OK) return s;
+    // CE backend: every source rank pushes its chunks in plan order on its side stream.
+    for (int i = 0; i < n; ++i) {
+      ao_plan* p = plans[i];
+      ao_ctx* c = p->ctx;
+      const ao::HostPlan& hp = p->hp;
+      const uint32_t par = epochs[i] & 1;
+      AO_CUDA(cudaEventRecord(c->ev_start, stream));
+      AO_CUDA(cudaStreamWaitEvent(c->side, c->ev_start, 0));
+      const int64_t row_bytes = hp.K * 2;
+      for (const ao::P2POp& op : hp.plans[hp.rank]) {
+        const int g = int(op.row0 / hp.C);
+        const char* src = static_cast<const char*>(As[i]) + (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes;
+        char* dst = c->data(op.peer, par) + op.row0 * row_bytes;
+        if (row_bytes > 0) AO_CUDA(cudaMemcpyAsync(dst, src, size_t(op.rows * row_bytes), cudaMemcpyDeviceToDevice, c->side));
+        CUresult r = drv->write32(c->side, reinterpret_cast<CUdeviceptr>(c->flags(op.peer, par) + g), epochs[i], 0);
+        if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
+      }
+      AO_CUDA(cudaEventRecord(c->ev_done, c->side));
+    }
+  }
+  cudaError_t e = ao::launch_fused(*ka, h0.tile.bn, comm, stream);
+  if (e != cudaSuccess) return fail(AO_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(e));
+  if (ce)
+    for (int i = 0; i < n; ++i) AO_CUDA(cudaStreamWaitEvent(stream, plans[i]->ctx->ev_done, 0));
+  // optional gathered-A output (bit-exact copy of concat_p A_p)
+  if (mode == ao::MODE_AG && Gouts) {
+    for (int i = 0; i < n; ++i) {
+      if (!Gouts[i]) continue;
+      const ao::HostPlan& hp = plans[i]->hp;
+      const size_t rb = size_t(hp.K) * 2, shard = size_t(hp.S) * rb;
+      char* out = static_cast<char*>(Gouts[i]);
+      const char* gath = plans[i]->ctx->data(hp.rank, epochs[i] & 1);
+      if (hp.rank > 0) AO_CUDA(cudaMemcpyAsync(out, gath, hp.rank * shard, cudaMemcpyDeviceToDevice, stream));
+      AO_CUDA(cudaMemcpyAsync(out + hp.rank * shard, As[i], shard, cudaMemcpyDeviceToDevice, stream));
+      const size_t tail = size_t(hp.W - 1 - hp.rank) * shard;
+      if (tail)
+        AO_CUDA(cudaMemcpyAsync(out + (hp.rank + 1) * shard, gath + (hp.rank + 1) * shard, tail,
+                                cudaMemcpyDeviceToDevice, stream));
+    }
+  }
+  return AO_OK;
+}
+
+ao_status ao_ag_gemm_group(int n, ao_plan* const* plans, const void* const* A_shards, const void* const* Bs,
+                           void* const* Cs, void* const* Gouts, void* stream) {
+  return launch_group(n, plans, A_shards, Bs, Cs, Gouts, stream, ao::MODE_AG);
+}
+
+ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
+                           void* const* C_shards, void* stream) {
+  return launch_group(n, plans, As, Bs, C_shards, nullptr, stream, ao::MODE_RS);
+}
+
+ao_status ao_ag_gemm(ao_plan* plan, const void* A_shard, const void* B, void* C, void* A_gathered_out, void* stream) {
+  void* g[1] = {A_gathered_out};
+  return launch_group(1, &plan, &A_shard, &B, &C, g, stream, ao::MODE_AG);
+}
+
+ao_status ao_gemm_rs(ao_plan* plan, const void* A, const void* B, void* C_shard, void* stream) {
+  return launch_group(1, &plan, &A, &B, &C_shard, nullptr, stream, ao::MODE_RS);
+}
+
+// ----------------------------------------------------------------------- plain GEMM entry
+ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int32_t tile_n,
+                  void* stream_v) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int64_t, int64_t, int64_t, int>, ao_plan*> cache;
+  if (M < 0 || N < 0 || K < 0 || M % 128 != 0 || N % 8 != 0 || K % 8 != 0)
+    return fail(AO_ERR_INVALID_ARG, "ao_gemm needs M %% 128 == 0, N %% 8 == 0, K %% 8 == 0 (M=%lld N=%lld K=%lld)",
+                (long long)M, (long long)N, (long long)K);
+  if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return fail(AO_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
+  if (M == 0 || N == 0) return AO_OK;
+  const int bn = tile_n ? tile_n : 256;
+  AO_CUDA(cudaSetDevice(device));
+  ao_plan* p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(device, M, N, K, bn);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      p = it->second;
+    } else {
+      int sm = 0;
+      ao_status s = check_device_sm100(device, &sm);
+      if (s != AO_OK) return s;
+      ao_plan_desc d;
+      ao_plan_desc_init(&d);
+      d.M = M;
+      d.N = N;
+      d.K = K;
+      d.chunk_rows = int32_t(std::min<int64_t>(M, 1 << 30));
+      d.tile_m = 128;
+      d.tile_n = bn;
+      s = ao_plan_create_host(&d, sm, &p);
+      if (s != AO_OK) return s;
+      p->device = device;
+      s = upload_tables(p);
+      if (s != AO_OK) {
+        ao_plan_destroy(p);
+        return s;
+      }
+      cache[key] = p;
+    }
+  }
+  std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
+  memset(ka.get(), 0, sizeof(ao::KernelArgs));
+  ka->n_group = 1;
+  ka->ctas_per_rank = p->hp.n_cta;
+  ka->mode = ao::MODE_GEMM;
+  ka->timeout_ns = 5000000000ull;
+  ka->skip_wait = -1;
+  ao_status s = fill_rank(&ka->rk[0], p, 0, A, B, C);
+  if (s != AO_OK) return s;
+  cudaError_t e = ao::launch_fused(*ka, bn, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));
+  if (e != cudaSuccess) return fail(AO_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+  return AO_OK;
+}
+
+}  // extern "C"

@@ -38,7 +38,7 @@ def ag_inputs(world_size: int, M: int, K: int, N_loc: int, salt: int = 0):
     assert M % world_size == 0
     S = M // world_size
     A = [_randn((S, K), 1000 + r + salt) for r in range(world_size)]
-    B = [_randn((N_loc, K), 2000 + r + salt, 1.0 / math.sqrt(K)) for r in range(world_size)]
+    B = [_randn((N_loc, K), 2000 + r + salt, 1.0 / math.sqrt(max(K, 1))) for r in range(world_size)]
     return A, B
 
 
@@ -47,7 +47,7 @@ def rs_inputs(world_size: int, M: int, K_loc: int, N: int, salt: int = 0):
 
     Returns (As, Bs): As[s] is rank s's K-shard of the activation [M, K_loc], Bs[s] is
     rank s's row-parallel weight shard [N, K_loc]; B ~ N(0,1)/sqrt(W*K_loc)."""
-    K_total = world_size * K_loc
+    K_total = max(world_size * K_loc, 1)
     A = [_randn((M, K_loc), 1000 + s + salt) for s in range(world_size)]
     B = [_randn((N, K_loc), 2000 + s + salt, 1.0 / math.sqrt(K_total)) for s in range(world_size)]
     return A, B

@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 CPU oracle, element by element.
+
+Tolerance (BASELINE.json north star): |gpu - oracle| <= 1e-2 * max(1, |oracle|) per element
+and relative Frobenius error <= 2e-3.  Integer/provenance and copy results are bit-exact.
+Multi-rank cases run in loopback (W ranks of one world on this GPU, one fused launch).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import numeric as on
+from synthetic import inputs as si
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ao():
+    from paper_2601_20595_b200 import build
+    build.build(verbose=False)
+    import paper_2601_20595_b200.api as api
+    return api
+
+
+def _dev(ts):
+    return [t.cuda() for t in ts]
+
+
+def _check(gpu, ref, what):
+    ok, e, f = on.check_tolerance(gpu.float().cpu().numpy(), ref)
+    assert ok, f"{what}: max elem err {e:.3e}, frob {f:.3e}"
+
+
+# ------------------------------------------------------------------------ plain GEMM
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (256, 512, 512, 256), (384, 392, 136, 256),
+                                      (512, 520, 1000, 128), (1024, 2048, 4096, 256), (128, 128, 8, 128),
+                                      (256, 384, 0, 256)])
+def test_gemm_vs_oracle(ao, M, N, K, bn):
+    A, B = si.ag_inputs(1, M, K, N, salt=M + N + K)
+    A, B = A[0], B[0]
+    C = ao.gemm(A.cuda(), B.cuda(), tile_n=bn)
+    torch.cuda.synchronize()
+    ref = on.gemm(si.to_f64(A), si.to_f64(B))
+    _check(C, ref, f"gemm {M}x{N}x{K}")
+
+
+def test_gemm_large_sampled(ao):
+    # full per-rank shape of BASELINE configs[1] at TP=1 (8192 x 14336 x 4096), sampled rows
+    M, N, K = 8192, 14336, 4096
+    A, B = si.ag_inputs(1, M, K, N)
+    C = ao.gemm(A[0].cuda(), B[0].cuda())
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([np.arange(0, M, 997), [M - 1, 127, 128]]))
+    ref = on.gemm_rows(si.to_f64(A[0]), si.to_f64(B[0]), rows)
+    _check(C[torch.as_tensor(rows)], ref, "gemm large sampled")
+
+
+# ------------------------------------------------------------------------ AG-GEMM loopback
+def _ag_world(ao, W, M, N, K, chunk, backend, **kw):
+    desc = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=chunk, backend=backend,
+                n_cta=max(1, 148 // W) if "n_cta" not in kw else kw.pop("n_cta"), timeout_ns=2_000_000_000, **kw)
+    ws = ao.workspace_bytes(desc)
+    ctxs = ao.loopback_world(0, W, ws)
+    plans = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
+    return ctxs, plans
+
+
+def _run_ag(ao, ctxs, plans, A, B, gather=False):
+    W = len(plans)
+    M = sum(a.shape[0] for a in A)
+    Cs = [torch.empty(M, B[r].shape[0], dtype=torch.bfloat16, device="cuda") for r in range(W)]
+    G = [torch.empty(M, A[0].shape[1], dtype=torch.bfloat16, device="cuda") for _ in range(W)] if gather else None
+    ao.ag_gemm_group(plans, A, B, Cs, G)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    return Cs, G
+
+
+@pytest.mark.parametrize("backend", ["ce", "ldst", "tma"])
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_ag_gemm_tiny_vs_oracle(ao, backend, W):
+    # BASELINE configs[0]: M=256/rank, K=512, N=512, chunk=64 rows (tiles of 128x128)
+    M, K, N, C = 256 * W, 512, 512, 64
+    A, B = si.ag_inputs(W, M, K, N)
+    ctxs, plans = _ag_world(ao, W, M, N, K, C, backend, tile_m=128, tile_n=128, n_slices=2)
+    Cs, G = _run_ag(ao, ctxs, plans, _dev(A), _dev(B), gather=True)
+    A64 = [si.to_f64(a) for a in A]
+    full = torch.cat(A, 0)
+    for r in range(W):
+        _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag W={W} {backend} rank {r}")
+        assert torch.equal(G[r].cpu(), full), "gathered A must be a bit-exact copy"
+
+
+@pytest.mark.parametrize("backend", ["ce", "ldst", "tma"])
+def test_ag_gemm_provenance_exact(ao, backend):
+    W, M, K, N = 4, 1024, 64, 256
+    ctxs, plans = _ag_world(ao, W, M, N, K, 64, backend, n_slices=3)
+    for it in range(5):  # back-to-back epochs exercise both parities
+        A, B = si.ag_provenance_inputs(W, M, K, N, epoch=it + 1)
+        Cs, _ = _run_ag(ao, ctxs, plans, _dev(A), _dev(B))
+        for r in range(W):
+            c = Cs[r].float().cpu()
+            rid = c[:, 0] + 32 * c[:, 1] + 1024 * c[:, 2]
+            assert torch.equal(rid, torch.arange(M, dtype=torch.float32)), (backend, it, r)
+            assert torch.all(c[:, 3] == (it + 1) % 32)
+
+
+@pytest.mark.parametrize("W,ragged", [(2, False), (4, True)])
+def test_ag_gemm_ragged_and_orders(ao, W, ragged):
+    M, K, N = 512 * W, 1000 if ragged else 1024, 1000 if ragged else 768
+    for kw in (dict(intra="grouped", group_m=2), dict(intra="col", chunk_order="chunk_major")):
+        A, B = si.ag_inputs(W, M, K, N, salt=3)
+        ctxs, plans = _ag_world(ao, W, M, N, K, 128, "ce", **kw)
+        Cs, _ = _run_ag(ao, ctxs, plans, _dev(A), _dev(B))
+        A64 = [si.to_f64(a) for a in A]
+        for r in range(W):
+            _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag ragged W={W} {kw} r{r}")
+
+
+# ------------------------------------------------------------------------ GEMM-RS loopback
+def _rs_world(ao, W, M, N, K, chunk, **kw):
+    desc = dict(op="gemm_rs", world_size=W, M=M, N=N, K=K, chunk_rows=chunk,
+                n_cta=max(1, 148 // W), timeout_ns=2_000_000_000, **kw)
+    ws = ao.workspace_bytes(desc)
+    ctxs = ao.loopback_world(0, W, ws)
+    plans = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
+    return ctxs, plans
+
+
+def _run_rs(ao, ctxs, plans, A, B):
+    W = len(plans)
+    M, N = A[0].shape[0], B[0].shape[0]
+    Cs = [torch.empty(M // W, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    ao.gemm_rs_group(plans, A, B, Cs)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    return Cs
+
+
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_gemm_rs_tiny_vs_oracle(ao, W):
+    M, K, N, C = 256 * W, 256, 512, 64
+    A, B = si.rs_inputs(W, M, K, N)
+    ctxs, plans = _rs_world(ao, W, M, N, K, C, tile_m=128, tile_n=128)
+    Cs = _run_rs(ao, ctxs, plans, _dev(A), _dev(B))
+    A64 = [si.to_f64(a) for a in A]
+    B64 = [si.to_f64(b) for b in B]
+    for r in range(W):
+        _check(Cs[r], on.gemm_rs(A64, B64, r), f"rs W={W} rank {r}")
+
+
+def test_gemm_rs_bitmask_and_determinism(ao):
+    W, M, K, N = 4, 1024, 64, 520
+    ctxs, plans = _rs_world(ao, W, M, N, K, 128)
+    A, B = si.rs_provenance_inputs(W, M, K, N)
+    for it in range(4):
+        Cs = _run_rs(ao, ctxs, plans, _dev(A), _dev(B))
+        for r in range(W):
+            assert torch.all(Cs[r].float().cpu() == 2 ** W - 1), (it, r)
+    A, B = si.rs_inputs(W, M, K, N, salt=5)
+    A, B = _dev(A), _dev(B)
+    first = [c.clone() for c in _run_rs(ao, ctxs, plans, A, B)]
+    second = _run_rs(ao, ctxs, plans, A, B)
+    for r in range(W):
+        assert torch.equal(first[r], second[r]), "RS must be bitwise deterministic (ascending-rank sum)"
+
+
+def test_gemm_rs_ragged(ao):
+    W, M, K, N = 2, 1024, 1000, 1000
+    A, B = si.rs_inputs(W, M, K, N, salt=8)
+    ctxs, plans = _rs_world(ao, W, M, N, K, 128, intra="grouped", group_m=2)
+    Cs = _run_rs(ao, ctxs, plans, _dev(A), _dev(B))
+    A64 = [si.to_f64(a) for a in A]
+    B64 = [si.to_f64(b) for b in B]
+    for r in range(W):
+        _check(Cs[r], on.gemm_rs(A64, B64, r), f"rs ragged r{r}")

@@ -1,0 +1,112 @@
+"""C++ planner (through the C ABI, host-only calls) vs the brute-force oracle planner:
+canonical JSON exports must be byte-identical (SURVEY.md §8(c) "Schedule result"), and
+both must accept / reject the same descs.  Also checks that the C-ABI library exports
+every symbol include/autooverlap.h declares.  No GPU needed."""
+import itertools
+import os
+import re
+import subprocess
+
+import pytest
+
+from oracle import schedule as osch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ao():
+    from paper_2601_20595_b200 import build
+    build.build(verbose=False)
+    import paper_2601_20595_b200.api as api
+    return api
+
+
+def _sweep():
+    out = []
+    for W in (1, 2, 4, 8):
+        for op in ("ag_gemm", "gemm_rs"):
+            for S in (128, 256, 384):
+                for C in (64, 128, 256):
+                    if S % C:
+                        continue
+                    for intra, gm in (("row", 1), ("col", 1), ("grouped", 2), ("grouped", 3)):
+                        for order in ("shard_major", "chunk_major"):
+                            for dirn in (("push", "pull") if op == "ag_gemm" else ("push",)):
+                                for tile in ((128, 128), (128, 256), (0, 0)):
+                                    out.append(dict(op=op, world_size=W, M=S * W, N=392, K=136, chunk_rows=C,
+                                                    intra=intra, group_m=gm, chunk_order=order, dir=dirn,
+                                                    tile_m=tile[0], tile_n=tile[1], n_cta=7 if S == 256 else 0,
+                                                    backend="ce" if S != 384 else "tma", n_slices=3))
+    return out
+
+
+SWEEP = _sweep()
+
+
+@pytest.mark.parametrize("i", range(0, len(SWEEP), 3))
+def test_json_byte_exact(ao, i):
+    d = SWEEP[i]
+    for r in range(d["world_size"]):
+        dd = osch.default_desc(**dict(d, rank=r))
+        ref = osch.export_json(osch.plan(dd, sm_count=148))
+        got = ao.plan_json(dd, sm_count=148)
+        assert got == ref, (d, r)
+
+
+@pytest.mark.parametrize("sms", [132, 148])
+def test_json_byte_exact_full_shapes(ao, sms):
+    # BASELINE configs[1]/[2] at TP=8 (planner only; tile heuristic engaged)
+    for op, M, N, K, C in (("ag_gemm", 8192, 1792, 4096, 128), ("gemm_rs", 8192, 4096, 1792, 128),
+                           ("ag_gemm", 8192, 1792, 4096, 1024)):
+        for r in (0, 5):
+            dd = osch.default_desc(op=op, world_size=8, rank=r, M=M, N=N, K=K, chunk_rows=C)
+            assert ao.plan_json(dd, sm_count=sms) == osch.export_json(osch.plan(dd, sm_count=sms))
+
+
+def test_validation_agrees(ao):
+    cases = [dict(), dict(M=500), dict(chunk_rows=96), dict(K=100), dict(N=500), dict(op="gemm_rs", dir="pull"),
+             dict(tile_m=128, tile_n=0), dict(tile_m=64, tile_n=64), dict(world_size=2, M=192, chunk_rows=32),
+             dict(M=0), dict(K=0), dict(world_size=9, M=9 * 128), dict(rank=2), dict(n_slices=0),
+             dict(comm_ctas=200), dict(intra="grouped", group_m=0), dict(chunk_rows=12)]
+    for kw in cases:
+        dd = osch.default_desc(**kw)
+        ref_ok = not osch.validate(dd)
+        got_ok = not ao.validate(dd)
+        assert ref_ok == got_ok, (kw, osch.validate(dd), ao.validate(dd))
+
+
+def test_plan_hash_rank_independent(ao):
+    hs = set()
+    for r in range(4):
+        p = ao.Plan(None, osch.default_desc(world_size=4, rank=r, M=1024, chunk_rows=128))
+        hs.add(p.hash())
+    assert len(hs) == 1
+    p2 = ao.Plan(None, osch.default_desc(world_size=4, rank=0, M=1024, chunk_rows=64))
+    assert p2.hash() not in hs
+
+
+def test_workspace_bytes(ao):
+    assert ao.workspace_bytes(osch.default_desc(M=512, K=512)) == 2 * 512 * 512 * 2
+    assert ao.workspace_bytes(osch.default_desc(op="gemm_rs", M=512, N=384)) == 2 * 512 * 384 * 4
+
+
+def test_library_exports_every_declared_symbol(ao):
+    hdr = open(os.path.join(ROOT, "include", "autooverlap.h")).read()
+    declared = set(re.findall(r"^\s*(?:const char\*|ao_status)\s+(ao_\w+)\s*\(", hdr, flags=re.M))
+    assert len(declared) >= 20
+    lib = ao.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    nm = subprocess.run(["nm", "-D", "--defined-only", ao.N.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ao_\w+)", nm))
+    assert declared <= exported, declared - exported
+    assert set(ao.N.EXPORTED) <= exported
+
+
+def test_host_only_calls_need_no_gpu(ao):
+    import torch
+    assert ao.plan_json(osch.default_desc())  # works on a GPU-less box
+    if not torch.cuda.is_available():
+        with pytest.raises(ao.AOError):
+            ao.Context(0, 0, 1, 1 << 20)

@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--backend", default="tma", choices=["ce", "tma", "ldst"])
     ap.add_argument("--chunk", type=int, default=128)
     ap.add_argument("--tokens", type=int, default=TOKENS)
+    ap.add_argument("--intra", default="grouped", choices=["row", "col", "grouped"])
+    ap.add_argument("--group-m", type=int, default=8)
+    ap.add_argument("--rs-chunk", type=int, default=0, help="GEMM-RS chunk rows (0 = --chunk)")
+    ap.add_argument("--rs-order", default="chunk_major", choices=["shard_major", "chunk_major"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baseline", action="store_true")
@@ -124,9 +128,11 @@ def run_ours(args, rank, world, local_rank):
     loop = world == 1
     W = args.tp if loop else world
     F = FFN // W
-    base = dict(world_size=W, M=M, chunk_rows=args.chunk, timeout_ns=5_000_000_000)
+    base = dict(world_size=W, M=M, chunk_rows=args.chunk, timeout_ns=5_000_000_000, intra=args.intra,
+                group_m=args.group_m)
     ag_desc = dict(base, op="ag_gemm", N=F, K=HIDDEN, backend=args.backend, n_slices=2)
-    rs_desc = dict(base, op="gemm_rs", N=HIDDEN, K=F)
+    rs_desc = dict(base, op="gemm_rs", N=HIDDEN, K=F, chunk_order=args.rs_order,
+                   chunk_rows=args.rs_chunk or args.chunk)
     if loop:
         ag_desc["n_cta"] = rs_desc["n_cta"] = sms // W
     ws = max(ao.workspace_bytes(ag_desc), ao.workspace_bytes(rs_desc))
@@ -236,7 +242,8 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,1)/sqrt(K) weights)",
         "config": {"workload": f"llama3-8b-tp{W}-ffn-pair-{'loopback' if loop else 'nvlink'}",
                    "tokens": M, "hidden": HIDDEN, "ffn": FFN, "tp": W, "ranks_per_gpu": W if loop else 1,
-                   "backend_ag": args.backend, "chunk_rows": args.chunk,
+                   "backend_ag": args.backend, "chunk_rows": args.chunk, "rs_chunk_rows": args.rs_chunk or args.chunk,
+                   "intra": args.intra, "group_m": args.group_m, "rs_chunk_order": args.rs_order,
                    "tile": [pa[0].info()["tile_m"], pa[0].info()["tile_n"]], "ctas_per_rank": pa[0].info()["n_cta"],
                    "l2": "inputs+weights ~0.7 GB/step > 126 MB L2 (no flush)", "parallelism": f"tp{W}"},
         "gpu_launches": 2 * args.steps,

@@ -27,11 +27,14 @@ namespace dev {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;     // AG / GEMM CTA: producer, MMA, 4 epilogue, 2 comm warps
+constexpr int kThreadsRS = 384;   // RS CTA: producer, MMA, 4 epilogue, 6 reducer warps
 constexpr int kCommWarp0 = 6;
+constexpr int kReduceWarps = 6;
 constexpr int kColocCommWarps = 2;
 constexpr int kCommBufs = 2;
-constexpr uint32_t kColocBufBytes = 8192;
+constexpr uint32_t kColocBufBytes = 4096;
+constexpr uint32_t kStageWarpBytes = 4096;  // epilogue transpose buffer per warp (32 rows x 128 B)
 constexpr uint32_t kCtaBufBytes = 12288;
 constexpr int kOperandBudget = 196608;  // bytes of smem for the A/B stage ring
 
@@ -45,7 +48,7 @@ struct Cfg {
 };
 
 struct SmemLayout {
-  uint32_t off_a, off_b, off_comm, off_bar, off_slot, total;
+  uint32_t off_a, off_b, off_stg, off_comm, off_bar, off_slot, total;
 };
 
 template <int BN>
@@ -53,7 +56,8 @@ __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm) {
   SmemLayout L{};
   L.off_a = 0;
   L.off_b = Cfg<BN>::kStages * Cfg<BN>::kStageA;
-  L.off_comm = Cfg<BN>::kStages * Cfg<BN>::kStage;
+  L.off_stg = Cfg<BN>::kStages * Cfg<BN>::kStage;
+  L.off_comm = L.off_stg + 4 * kStageWarpBytes;
   const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : 0;
   L.off_bar = L.off_comm + comm;
   const uint32_t nbars = 2 * Cfg<BN>::kStages + 4 + 8 * kCommBufs;
@@ -186,7 +190,8 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
 }
 
 template <int BN, int MODE, int COMM>
-__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constant__ KernelArgs args) {
+__global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
+    fused_kernel(const __grid_constant__ KernelArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -341,8 +346,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     }
   } else if (warp < kCommWarp0) {
     // ================================================================ epilogue
+    // TMEM -> registers -> per-warp smem transpose -> coalesced 128-byte row segments.
+    // AG/GEMM: bf16 C rows (64 columns per step).  RS: fp32 partial rows into the owner's
+    // slot (32 columns per step; a peer address over NVLink, local in loopback).
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int etid = threadIdx.x - 64;
+    uint4* stg = reinterpret_cast<uint4*>(smem + L.off_stg + (warp - 2) * kStageWarpBytes);
+    constexpr int CW = (MODE == MODE_RS) ? 32 : 64;  // columns per staging step (128 B per row)
+    constexpr int EPS = (MODE == MODE_RS) ? 4 : 8;   // elements per 16-byte lane segment
+    constexpr int EB = (MODE == MODE_RS) ? 4 : 2;    // bytes per output element
     uint32_t acc = 0, acc_phase = 0;
     for (int k = cta; k < n_tiles; k += n_cta) {
       const int t = R.order[k];
@@ -350,59 +362,67 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       const int nb = t - mb * R.n_nb;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row = int64_t(mb) * kBM + q * 32 + lane;
       const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       const int64_t col_base = int64_t(nb) * BN;
+      const int64_t row0 = int64_t(mb) * kBM + q * 32;  // first row of this warp's quadrant
       int owner = 0;
-      char* rs_base = nullptr;
+      char* dst_base;  // byte address of (row0, col 0) of the destination matrix
+      const int64_t ld_bytes = N * EB;
       if constexpr (MODE == MODE_RS) {
         owner = int(int64_t(mb) * kBM / S);
-        // owner's data half: slot[rank] of [S, N] fp32
-        rs_base = R.peer_data[owner] + (int64_t(R.rank) * S * N + (row - owner * S) * N) * 4;
+        dst_base = R.peer_data[owner] + (int64_t(R.rank) * S + (row0 - int64_t(owner) * S)) * ld_bytes;
+      } else {
+        dst_base = reinterpret_cast<char*>(R.C) + row0 * ld_bytes;
       }
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
+      for (int cc = 0; cc < BN; cc += CW) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tb + cc * 32, v);
-        tmem_wait_ld();
+        if constexpr (MODE == MODE_RS) {
+          tmem_ld_32x32b_x32(tb + cc, v);
+          tmem_wait_ld();
+        } else {
+          uint32_t lo[32], hi[32];
+          tmem_ld_32x32b_x32(tb + cc, lo);
+          tmem_ld_32x32b_x32(tb + cc + 32, hi);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v[i] = pack_bf16x2(__uint_as_float(lo[2 * i]), __uint_as_float(lo[2 * i + 1]));
+            v[16 + i] = pack_bf16x2(__uint_as_float(hi[2 * i]), __uint_as_float(hi[2 * i + 1]));
+          }
+        }
         if (nkb == 0) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0u;
         }
-        const int64_t col0 = col_base + cc * 32;
-        const int64_t valid = N - col0;  // multiple of 8
-        if (valid <= 0) continue;
-        if constexpr (MODE == MODE_RS) {
-          float* dst = reinterpret_cast<float*>(rs_base) + col0;
+        const int64_t col0 = col_base + cc;
+        if (col0 >= N) break;  // warp-uniform
+        // stage row `lane` (128 B) with a 16-byte XOR swizzle (conflict-free both ways)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (j * 4 < valid)
-              st_v4(reinterpret_cast<int4*>(dst + j * 4), make_int4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-          }
-        } else {
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(R.C) + row * N + col0;
+        for (int j = 0; j < 8; ++j)
+          stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        __syncwarp();
+        const int c = lane & 7;
+        const bool ok = col0 + c * EPS < N;  // N % 8 == 0: a segment is all-valid or all-out
+        char* colp = dst_base + (col0 + c * EPS) * EB;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (j * 8 < valid) {
-              int4 o;
-              o.x = pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
-              o.y = pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
-              o.z = pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
-              o.w = pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
-              st_v4(reinterpret_cast<int4*>(dst + j * 8), o);
-            }
-          }
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 4 + (lane >> 3);
+          const uint4 w = stg[r * 8 + (c ^ (r & 7))];
+          if (ok) st_v4(reinterpret_cast<int4*>(colp + r * ld_bytes), make_int4(w.x, w.y, w.z, w.w));
         }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if constexpr (MODE == MODE_RS) {
-        // RS-3: all partial rows of this tile are written; count the tile into each of
-        // its chunks; the last contributor releases the owner's flag[g][rank].
-        __threadfence_system();
+        // RS-3: count the tile into each of its chunks; the last contributor releases the
+        // owner's flag[g][rank].  One sys-scope fence after the CTA barrier is cumulative
+        // over the 128 threads' partial-tile stores.
         named_bar_sync(1, 128);
         if (etid == 0) {
+          asm volatile("fence.sc.sys;" ::: "memory");
           const int glo = int(int64_t(mb) * kBM / R.crows);
           const int ghi = int((int64_t(mb) * kBM + kBM - 1) / R.crows);
           for (int g = glo; g <= ghi; ++g) {
@@ -419,53 +439,73 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-
-    if constexpr (MODE == MODE_RS) {
-      // RS-4: reduce items (own-row tiles, chunk order), after this CTA's GEMM tiles.
-      int wp = R.wait_off[cta];
-      const int we = R.wait_off[cta + 1];
-      const int n_work = n_tiles + R.n_items;
-      int k = cta;
-      while (k < n_tiles) k += n_cta;
-      const char* own = R.peer_data[R.rank];
-      const int64_t slot_stride = S * N;  // floats
-      for (; k < n_work; k += n_cta) {
-        if (etid == 0) {
-          while (wp < we && R.waits[wp].x == k) {
-            const int g = R.waits[wp].y;
-            if (!(grp == 0 && wp == args.skip_wait)) {
-              for (int s = 0; s < R.W; ++s) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, cta, g);
-            }
-            ++wp;
+  } else if constexpr (MODE == MODE_RS) {
+    // ================================================================ reducer warps
+    // RS-4: the owner's fused reduction, concurrent with the GEMM pipeline.  Items are
+    // own-row tiles in chunk order; each waits for flag[g][s] of every source s, then
+    // sums the W fp32 slot tiles in ascending source rank and stores bf16.
+    const int rtid = threadIdx.x - 32 * kCommWarp0;
+    constexpr int RT = 32 * kReduceWarps;
+    int wp = R.wait_off[cta];
+    const int we = R.wait_off[cta + 1];
+    const int n_work = n_tiles + R.n_items;
+    int k = cta;
+    while (k < n_tiles) k += n_cta;
+    const float* slots = reinterpret_cast<const float*>(R.peer_data[R.rank]);
+    const int64_t slot_stride = S * N;  // floats
+    const int W = R.W;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(R.C);
+    for (; k < n_work; k += n_cta) {
+      if (rtid == 0) {
+        while (wp < we && R.waits[wp].x == k) {
+          const int g = R.waits[wp].y;
+          if (!(grp == 0 && wp == args.skip_wait)) {
+            for (int s = 0; s < W; ++s) spin_flag(R.flags + g * W + s, R.epoch, args, R.rank, cta, g);
           }
+          ++wp;
         }
-        named_bar_sync(1, 128);
-        const int t = R.reduce_items[k - n_tiles];
-        const int mb = t / R.n_nb;
-        const int nb = t - mb * R.n_nb;
-        const int64_t lr0 = int64_t(mb) * kBM - int64_t(R.rank) * S;
-        const int64_t c0 = int64_t(nb) * BN;
-        const int64_t valid = (N - c0) < BN ? (N - c0) : BN;
-        const int per_row = BN / 4;
-        const float* slots = reinterpret_cast<const float*>(own);
-        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(R.C);
-        for (int idx = etid; idx < kBM * per_row; idx += 128) {
+      }
+      named_bar_sync(2, RT);
+      const int t = R.reduce_items[k - n_tiles];
+      const int mb = t / R.n_nb;
+      const int nb = t - mb * R.n_nb;
+      const int64_t lr0 = int64_t(mb) * kBM - int64_t(R.rank) * S;
+      const int64_t c0 = int64_t(nb) * BN;
+      const int64_t valid = (N - c0) < BN ? (N - c0) : BN;
+      constexpr int per_row = BN / 4;
+      constexpr int total = kBM * per_row;
+      for (int base = rtid; base < total; base += 2 * RT) {
+        float4 a[2][AO_MAX_WORLD];
+        int64_t off[2];
+        bool ok[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int idx = base + u * RT;
           const int rr = idx / per_row;
           const int c4 = idx - rr * per_row;
-          if (c4 * 4 >= valid) continue;
-          const int64_t off = (lr0 + rr) * N + c0 + c4 * 4;
-          float4 a = __ldcg(reinterpret_cast<const float4*>(slots + off));
-          for (int s = 1; s < R.W; ++s) {  // ascending source rank
-            const float4 b = __ldcg(reinterpret_cast<const float4*>(slots + s * slot_stride + off));
-            a.x += b.x;
-            a.y += b.y;
-            a.z += b.z;
-            a.w += b.w;
+          ok[u] = idx < total && c4 * 4 < valid;
+          off[u] = (lr0 + rr) * N + c0 + c4 * 4;
+#pragma unroll
+          for (int s = 0; s < AO_MAX_WORLD; ++s)
+            if (ok[u] && s < W) a[u][s] = __ldcg(reinterpret_cast<const float4*>(slots + s * slot_stride + off[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!ok[u]) continue;
+          float4 x = a[u][0];
+#pragma unroll
+          for (int s = 1; s < AO_MAX_WORLD; ++s) {
+            if (s < W) {
+              x.x += a[u][s].x;
+              x.y += a[u][s].y;
+              x.z += a[u][s].z;
+              x.w += a[u][s].w;
+            }
           }
           uint2 o;
-          o.x = pack_bf16x2(a.x, a.y);
-          o.y = pack_bf16x2(a.z, a.w);
-          *reinterpret_cast<uint2*>(out + off) = o;
+          o.x = pack_bf16x2(x.x, x.y);
+          o.y = pack_bf16x2(x.z, x.w);
+          *reinterpret_cast<uint2*>(out + off[u]) = o;
         }
       }
     }
@@ -508,7 +548,7 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(args.n_group * (args.ctas_per_rank + args.comm_ctas_per_rank));
-  cfg.blockDim = dim3(dev::kThreads);
+  cfg.blockDim = dim3(MODE == MODE_RS ? dev::kThreadsRS : dev::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

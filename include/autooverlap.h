@@ -177,9 +177,10 @@ ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, 
 /* ---- plain local GEMM through the same tcgen05 mainloop (no communication) -------------
  * C[M, N] = A[M, K] . B[N, K]^T, bf16 in / fp32 accumulate / bf16 out (Lst.1's local
  * kernel).  Used for W = 1 and as the GEMM-only reference of the fused ops.
- * tile_n: 0 = 256.  Requires M % 128 == 0, N % 8 == 0, K % 8 == 0. */
+ * tile_m: 128 (1 CTA) or 256 (CTA pair, cta_group::2); 0 = 256 when M % 256 == 0.
+ * tile_n: 128 or 256; 0 = 256.  Requires M % tile_m == 0, N % 8 == 0, K % 8 == 0. */
 ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
-                  int32_t tile_n, void* stream);
+                  int32_t tile_m, int32_t tile_n, void* stream);
 
 /* ---- test hooks (deterministic fault injection; see tests/) ----------------------------
  * ao_debug_set: key "skip_wait" = index of a wait (global over CTAs) the kernel must skip

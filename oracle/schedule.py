@@ -39,7 +39,7 @@ import math
 # Tile shapes the kernel library implements, in the planner's candidate order
 # (BM, BN, cta_group).  Shared *specification* with the C++ planner (Q19);
 # each side types it independently.
-TILE_CANDIDATES = [(128, 256, 1), (128, 128, 1)]
+TILE_CANDIDATES = [(256, 256, 2), (256, 128, 2), (128, 256, 1), (128, 128, 1)]
 
 BK = 64  # K-block of the mainloop (TMA 128-B swizzle => 64 bf16), DESIGN.md
 

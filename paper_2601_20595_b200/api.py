@@ -191,14 +191,14 @@ def gemm_rs_group(plans, As, Bs, C_shards, stream=None):
     check(lib().ao_gemm_rs_group(len(plans), _plans(plans), _arr(As), _arr(Bs), _arr(C_shards), _stream(stream)))
 
 
-def gemm(A, B, C=None, tile_n: int = 0, stream=None):
+def gemm(A, B, C=None, tile_n: int = 0, tile_m: int = 0, stream=None):
     """ao_gemm: C = A . B^T through the same tcgen05 mainloop (no communication)."""
     import torch
     if C is None:
         C = torch.empty(A.shape[0], B.shape[0], dtype=torch.bfloat16, device=A.device)
     _require_bf16_cuda(A, B, C)
-    check(lib().ao_gemm(A.device.index, _ptr(A), _ptr(B), _ptr(C), A.shape[0], B.shape[0], A.shape[1], tile_n,
-                        _stream(stream)))
+    check(lib().ao_gemm(A.device.index, _ptr(A), _ptr(B), _ptr(C), A.shape[0], B.shape[0], A.shape[1], tile_m,
+                        tile_n, _stream(stream)))
     return C
 
 

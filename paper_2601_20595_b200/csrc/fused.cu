@@ -4,19 +4,24 @@
 // Method (§5.2):
 //  * the tile scheduler follows the planner's chunk-ordered tile list (Fig.6);
 //  * a tile that consumes a chunk waits on that chunk's global-memory signal, once per
-//    (CTA, chunk) (minimal waits) -- producer warp, ld.acquire.sys spin;
+//    (worker, chunk) (minimal waits) -- producer warp, ld.acquire.sys spin;
 //  * communication is issued from inside the fused kernel: co-located
 //    communication warps or dedicated communication CTAs ("specialized SMs", Fig.7b/c)
 //    push chunks with cp.async.bulk (TMA backend) or 16-byte ld/st (LDST backend);
 //  * GEMM-RS: each finished fp32 partial tile is written into its owner's slot; the last
-//    tile of a chunk releases the owner's flag; the owner's epilogue warps then run the
-//    fused reduction of the chunk (ascending source rank) and store bf16.
+//    tile of a chunk releases the owner's flag; the owner's reducer warps run the fused
+//    reduction of the chunk (ascending source rank) concurrently with the GEMM.
 //
-// Warp roles of a GEMM CTA (256 threads, 1 CTA / SM):
+// Tile = BM x BN with BM = 128 * CG.  CG = 2 runs one tile on a CTA pair (cluster of 2,
+// tcgen05.mma.cta_group::2, M = 256): each CTA loads its 128 rows of A and half of B's
+// rows; the even CTA issues the MMA for both; each CTA's TMEM holds its 128 rows.
+//
+// Warp roles (1 CTA / SM):
 //   warp 0      TMA producer (+ AG chunk waits)
-//   warp 1      TMEM allocator + tcgen05.mma issuer
-//   warps 2..5  epilogue (TMEM -> registers -> global; RS signals + reduce items)
-//   warps 6..7  co-located communication warps (AG, TMA/LDST backends)
+//   warp 1      TMEM allocator + tcgen05.mma issuer (leader CTA of the pair)
+//   warps 2..5  epilogue (TMEM -> registers -> smem transpose -> global; RS signals)
+//   warps 6..7  AG: co-located communication warps
+//   warps 6..11 RS: reducer warps (own-row reduction)
 #include <cuda_runtime.h>
 
 #include "kernel_args.h"
@@ -25,10 +30,10 @@
 namespace ao {
 namespace dev {
 
-constexpr int kBM = 128;
+constexpr int kSubM = 128;  // rows per CTA (TMEM lanes)
 constexpr int kBK = 64;
-constexpr int kThreads = 256;     // AG / GEMM CTA: producer, MMA, 4 epilogue, 2 comm warps
-constexpr int kThreadsRS = 384;   // RS CTA: producer, MMA, 4 epilogue, 6 reducer warps
+constexpr int kThreads = 256;    // AG / GEMM CTA
+constexpr int kThreadsRS = 384;  // RS CTA
 constexpr int kCommWarp0 = 6;
 constexpr int kReduceWarps = 6;
 constexpr int kColocCommWarps = 2;
@@ -38,29 +43,31 @@ constexpr uint32_t kStageWarpBytes = 4096;  // epilogue transpose buffer per war
 constexpr uint32_t kCtaBufBytes = 12288;
 constexpr int kOperandBudget = 196608;  // bytes of smem for the A/B stage ring
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int kStageA = kBM * kBK * 2;
-  static constexpr int kStageB = BN * kBK * 2;
+  static constexpr int kStageA = kSubM * kBK * 2;
+  static constexpr int kStageB = (BN / CG) * kBK * 2;
   static constexpr int kStage = kStageA + kStageB;
   static constexpr int kStages = kOperandBudget / kStage;
   static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kBM = kSubM * CG;
 };
 
 struct SmemLayout {
   uint32_t off_a, off_b, off_stg, off_comm, off_bar, off_slot, total;
 };
 
-template <int BN>
+template <int BN, int CG>
 __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm) {
+  using C_ = Cfg<BN, CG>;
   SmemLayout L{};
   L.off_a = 0;
-  L.off_b = Cfg<BN>::kStages * Cfg<BN>::kStageA;
-  L.off_stg = Cfg<BN>::kStages * Cfg<BN>::kStage;
+  L.off_b = C_::kStages * C_::kStageA;
+  L.off_stg = C_::kStages * C_::kStage;
   L.off_comm = L.off_stg + 4 * kStageWarpBytes;
   const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : 0;
   L.off_bar = L.off_comm + comm;
-  const uint32_t nbars = 2 * Cfg<BN>::kStages + 4 + 8 * kCommBufs;
+  const uint32_t nbars = 2 * C_::kStages + 4 + 8 * kCommBufs;
   L.off_slot = L.off_bar + nbars * 8;
   L.total = L.off_slot + 16 + 1024;  // + alignment slack
   return L;
@@ -146,16 +153,15 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
           if (j < n) st_v4(d + j, v[u]);
         }
       }
-      __threadfence_system();
       __syncwarp();
+      if (lane == 0) asm volatile("fence.sc.sys;" ::: "memory");
     } else {
-      if (lane == 0) {
+      if (lane == 0 && it.bytes > 0) {
         const int64_t npieces = (it.bytes + buf_bytes - 1) / buf_bytes;
         auto piece_len = [&](int64_t p) -> uint32_t {
           const int64_t rem = it.bytes - p * int64_t(buf_bytes);
           return uint32_t(rem < int64_t(buf_bytes) ? rem : int64_t(buf_bytes));
         };
-        // prologue: load piece 0
         {
           const uint32_t n0 = piece_len(0);
           mbar_arrive_expect_tx(&bars[0], n0);
@@ -189,7 +195,7 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
   }
 }
 
-template <int BN, int MODE, int COMM>
+template <int BN, int MODE, int COMM, int CG>
 __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
     fused_kernel(const __grid_constant__ KernelArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -218,12 +224,16 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
   }
 
   // ------------------------------------------------------------------ GEMM CTA
-  using C_ = Cfg<BN>;
+  using C_ = Cfg<BN, CG>;
+  constexpr int BM = C_::kBM;
   constexpr bool kTmaComm = (MODE == MODE_AG && COMM == COMM_TMA);
-  constexpr SmemLayout L = gemm_layout<BN>(kTmaComm);
+  constexpr SmemLayout L = gemm_layout<BN, CG>(kTmaComm);
   const int grp = blockIdx.x / args.ctas_per_rank;
-  const int cta = blockIdx.x % args.ctas_per_rank;
-  const int n_cta = args.ctas_per_rank;
+  const int lcta = blockIdx.x % args.ctas_per_rank;  // CTA index inside the rank group
+  const int wk = lcta / CG;                          // plan worker (CTA pair when CG == 2)
+  const int n_wk = args.ctas_per_rank / CG;
+  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // 0 = leader (even CTA)
+  const bool leader = crank == 0;
   const RankArgs& R = args.rk[grp];
 
   uint8_t* sA = smem + L.off_a;
@@ -248,17 +258,25 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 4);
+        mbar_init(&tempty[a], 4 * CG);
       }
       for (int b = 0; b < 8 * kCommBufs; ++b) mbar_init(&commbars[b], 1);
       fence_barrier_init();
     }
     __syncwarp();
-    tmem_alloc(tmem_slot, C_::kTmemCols);
-    tmem_relinquish();
+    if constexpr (CG == 2) {
+      tmem_alloc_cg2(tmem_slot, C_::kTmemCols);
+      tmem_relinquish_cg2();
+    } else {
+      tmem_alloc(tmem_slot, C_::kTmemCols);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -274,17 +292,17 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
       uint32_t stage = 0, phase = 0;
       int wp = 0, we = 0;
       if constexpr (MODE == MODE_AG) {
-        wp = R.wait_off[cta];
-        we = R.wait_off[cta + 1];
+        wp = R.wait_off[wk];
+        we = R.wait_off[wk + 1];
       }
-      for (int k = cta; k < n_tiles; k += n_cta) {
+      for (int k = wk; k < n_tiles; k += n_wk) {
         if constexpr (MODE == MODE_AG) {
           bool waited = false;
           while (wp < we && R.waits[wp].x == k) {
             const int g = R.waits[wp].y;
             if (!(grp == 0 && wp == args.skip_wait)) {
               for (int s = 0; s < R.n_slices; ++s)
-                spin_flag(R.flags + g * R.n_slices + s, R.epoch, args, R.rank, cta, g);
+                spin_flag(R.flags + g * R.n_slices + s, R.epoch, args, R.rank, lcta, g);
             }
             ++wp;
             waited = true;
@@ -295,18 +313,25 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
         const int mb = t / R.n_nb;
         const int nb = t - mb * R.n_nb;
         const CUtensorMap* mA = &R.tmA;
-        int arow = mb * kBM;
+        int arow = mb * BM + int(crank) * kSubM;
         if constexpr (MODE == MODE_AG) {
-          if (int64_t(mb) * kBM / S == R.rank) {
+          if (int64_t(arow) / S == R.rank) {
             mA = &R.tmA_loc;
             arow -= int(R.rank * S);
           }
         }
+        const int brow = nb * BN + int(crank) * (BN / CG);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C_::kStage);
-          tma_load_2d(sA + stage * C_::kStageA, mA, &full[stage], kb * kBK, arow, pol_a);
-          tma_load_2d(sB + stage * C_::kStageB, &R.tmB, &full[stage], kb * kBK, nb * BN, pol_b);
+          if constexpr (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C_::kStage);
+            tma_load_2d_2sm(sA + stage * C_::kStageA, mA, &full[stage], kb * kBK, arow, pol_a);
+            tma_load_2d_2sm(sB + stage * C_::kStageB, &R.tmB, &full[stage], kb * kBK, brow, pol_b);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C_::kStage);
+            tma_load_2d(sA + stage * C_::kStageA, mA, &full[stage], kb * kBK, arow, pol_a);
+            tma_load_2d(sB + stage * C_::kStageB, &R.tmB, &full[stage], kb * kBK, brow, pol_b);
+          }
           if (++stage == C_::kStages) {
             stage = 0;
             phase ^= 1;
@@ -316,33 +341,47 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer
-    constexpr uint32_t idesc = make_idesc_bf16(kBM, BN);
-    uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-    for (int k = cta; k < n_tiles; k += n_cta) {
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int k = wk; k < n_tiles; k += n_wk) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint64_t ad = make_smem_desc_sw128(smem_u32(sA + stage * C_::kStageA));
-          const uint64_t bd = make_smem_desc_sw128(smem_u32(sB + stage * C_::kStageB));
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t ad = make_smem_desc_sw128(smem_u32(sA + stage * C_::kStageA));
+            const uint64_t bd = make_smem_desc_sw128(smem_u32(sB + stage * C_::kStageB));
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)  // +32 B per K=16 step inside the swizzle atom
-            mma_bf16_ss(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
-          mma_commit(&empty[stage]);
+            for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 B per K=16 step inside the swizzle atom
+              if constexpr (CG == 2)
+                mma_bf16_ss_cg2(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
+              else
+                mma_bf16_ss(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
+            }
+            if constexpr (CG == 2)
+              mma_commit_cg2_mc(&empty[stage]);
+            else
+              mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == C_::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) {
+          if constexpr (CG == 2)
+            mma_commit_cg2_mc(&tfull[acc]);
+          else
+            mma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++stage == C_::kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
       }
-      if (lane == 0) mma_commit(&tfull[acc]);
-      __syncwarp();
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp < kCommWarp0) {
     // ================================================================ epilogue
@@ -356,7 +395,7 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
     constexpr int EPS = (MODE == MODE_RS) ? 4 : 8;   // elements per 16-byte lane segment
     constexpr int EB = (MODE == MODE_RS) ? 4 : 2;    // bytes per output element
     uint32_t acc = 0, acc_phase = 0;
-    for (int k = cta; k < n_tiles; k += n_cta) {
+    for (int k = wk; k < n_tiles; k += n_wk) {
       const int t = R.order[k];
       const int mb = t / R.n_nb;
       const int nb = t - mb * R.n_nb;
@@ -364,12 +403,13 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
       tc_fence_after();
       const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       const int64_t col_base = int64_t(nb) * BN;
-      const int64_t row0 = int64_t(mb) * kBM + q * 32;  // first row of this warp's quadrant
+      const int64_t sub0 = int64_t(mb) * BM + int64_t(crank) * kSubM;  // first row of this CTA's half
+      const int64_t row0 = sub0 + q * 32;                                // first row of this warp
       int owner = 0;
       char* dst_base;  // byte address of (row0, col 0) of the destination matrix
       const int64_t ld_bytes = N * EB;
       if constexpr (MODE == MODE_RS) {
-        owner = int(int64_t(mb) * kBM / S);
+        owner = int(sub0 / S);
         dst_base = R.peer_data[owner] + (int64_t(R.rank) * S + (row0 - int64_t(owner) * S)) * ld_bytes;
       } else {
         dst_base = reinterpret_cast<char*>(R.C) + row0 * ld_bytes;
@@ -415,16 +455,21 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_leader(&tempty[acc]);
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       if constexpr (MODE == MODE_RS) {
-        // RS-3: count the tile into each of its chunks; the last contributor releases the
-        // owner's flag[g][rank].  One sys-scope fence after the CTA barrier is cumulative
-        // over the 128 threads' partial-tile stores.
+        // RS-3: count this CTA's 128-row sub-tile into each of its chunks; the last
+        // contributor releases the owner's flag[g][rank].  One sys-scope fence after the
+        // CTA barrier is cumulative over the 128 threads' partial-tile stores.
         named_bar_sync(1, 128);
         if (etid == 0) {
           asm volatile("fence.sc.sys;" ::: "memory");
-          const int glo = int(int64_t(mb) * kBM / R.crows);
-          const int ghi = int((int64_t(mb) * kBM + kBM - 1) / R.crows);
+          const int glo = int(sub0 / R.crows);
+          const int ghi = int((sub0 + kSubM - 1) / R.crows);
           for (int g = glo; g <= ghi; ++g) {
             uint32_t old;
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.counters + g) : "memory");
@@ -443,24 +488,25 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
     // ================================================================ reducer warps
     // RS-4: the owner's fused reduction, concurrent with the GEMM pipeline.  Items are
     // own-row tiles in chunk order; each waits for flag[g][s] of every source s, then
-    // sums the W fp32 slot tiles in ascending source rank and stores bf16.
+    // sums the W fp32 slot tiles in ascending source rank and stores bf16.  With
+    // CG == 2 each CTA of the pair reduces its own 128-row half of the item.
     const int rtid = threadIdx.x - 32 * kCommWarp0;
     constexpr int RT = 32 * kReduceWarps;
-    int wp = R.wait_off[cta];
-    const int we = R.wait_off[cta + 1];
+    int wp = R.wait_off[wk];
+    const int we = R.wait_off[wk + 1];
     const int n_work = n_tiles + R.n_items;
-    int k = cta;
-    while (k < n_tiles) k += n_cta;
+    int k = wk;
+    while (k < n_tiles) k += n_wk;
     const float* slots = reinterpret_cast<const float*>(R.peer_data[R.rank]);
     const int64_t slot_stride = S * N;  // floats
     const int W = R.W;
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(R.C);
-    for (; k < n_work; k += n_cta) {
+    for (; k < n_work; k += n_wk) {
       if (rtid == 0) {
         while (wp < we && R.waits[wp].x == k) {
           const int g = R.waits[wp].y;
           if (!(grp == 0 && wp == args.skip_wait)) {
-            for (int s = 0; s < W; ++s) spin_flag(R.flags + g * W + s, R.epoch, args, R.rank, cta, g);
+            for (int s = 0; s < W; ++s) spin_flag(R.flags + g * W + s, R.epoch, args, R.rank, lcta, g);
           }
           ++wp;
         }
@@ -469,11 +515,11 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
       const int t = R.reduce_items[k - n_tiles];
       const int mb = t / R.n_nb;
       const int nb = t - mb * R.n_nb;
-      const int64_t lr0 = int64_t(mb) * kBM - int64_t(R.rank) * S;
+      const int64_t lr0 = int64_t(mb) * BM + int64_t(crank) * kSubM - int64_t(R.rank) * S;
       const int64_t c0 = int64_t(nb) * BN;
       const int64_t valid = (N - c0) < BN ? (N - c0) : BN;
       constexpr int per_row = BN / 4;
-      constexpr int total = kBM * per_row;
+      constexpr int total = kSubM * per_row;
       for (int base = rtid; base < total; base += 2 * RT) {
         float4 a[2][AO_MAX_WORLD];
         int64_t off[2];
@@ -514,7 +560,7 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
     if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {
       if (args.comm_ctas_per_rank == 0) {
         const int cw = warp - kCommWarp0;
-        comm_worker<COMM>(R, args, cta * kColocCommWarps + cw, n_cta * kColocCommWarps,
+        comm_worker<COMM>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps,
                           smem + L.off_comm + cw * kCommBufs * kColocBufBytes, kColocBufBytes,
                           commbars + cw * kCommBufs);
       }
@@ -522,10 +568,16 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C_::kTmemCols);
+    if constexpr (CG == 2)
+      tmem_dealloc_cg2(tmem_base, C_::kTmemCols);
+    else
+      tmem_dealloc(tmem_base, C_::kTmemCols);
   }
 }
 
@@ -533,14 +585,15 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
 
 // ------------------------------------------------------------------------------- launcher
 namespace {
-template <int BN, int MODE, int COMM>
+template <int BN, int MODE, int COMM, int CG>
 cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
-  auto kern = dev::fused_kernel<BN, MODE, COMM>;
+  auto kern = dev::fused_kernel<BN, MODE, COMM, CG>;
   constexpr bool tma_comm = (MODE == MODE_AG && COMM == COMM_TMA);
-  const size_t smem_gemm = dev::gemm_layout<BN>(tma_comm).total;
+  const size_t smem_gemm = dev::gemm_layout<BN, CG>(tma_comm).total;
   const size_t smem_comm = (MODE == MODE_AG && COMM != COMM_NONE) ? dev::comm_cta_layout().total : 0;
   const size_t smem = smem_gemm > smem_comm ? smem_gemm : smem_comm;
   static bool attr_set = false;
+  static bool coop_ok = true;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
@@ -551,40 +604,58 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   cfg.blockDim = dim3(MODE == MODE_RS ? dev::kThreadsRS : dev::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (spin-waits, H3)
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (CG == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (coop_ok) {
+    attr[na].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (spin-waits, H3)
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args);
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
+  if (e != cudaSuccess && coop_ok && CG == 2) {
+    // cooperative + cluster not accepted: grid <= SMs with 1 CTA/SM still co-resides
+    cudaGetLastError();
+    coop_ok = false;
+    cfg.numAttrs = na - 1;
+    e = cudaLaunchKernelEx(&cfg, kern, args);
+  }
+  return e;
 }
 
-template <int BN>
+template <int BN, int CG>
 cudaError_t launch_bn(const KernelArgs& args, int comm, cudaStream_t stream) {
   switch (args.mode) {
     case MODE_GEMM:
-      return launch_one<BN, MODE_GEMM, COMM_NONE>(args, stream);
+      return launch_one<BN, MODE_GEMM, COMM_NONE, CG>(args, stream);
     case MODE_RS:
-      return launch_one<BN, MODE_RS, COMM_NONE>(args, stream);
+      return launch_one<BN, MODE_RS, COMM_NONE, CG>(args, stream);
     case MODE_AG:
-      if (comm == COMM_TMA) return launch_one<BN, MODE_AG, COMM_TMA>(args, stream);
-      if (comm == COMM_LDST) return launch_one<BN, MODE_AG, COMM_LDST>(args, stream);
-      return launch_one<BN, MODE_AG, COMM_NONE>(args, stream);
+      if (comm == COMM_TMA) return launch_one<BN, MODE_AG, COMM_TMA, CG>(args, stream);
+      if (comm == COMM_LDST) return launch_one<BN, MODE_AG, COMM_LDST, CG>(args, stream);
+      return launch_one<BN, MODE_AG, COMM_NONE, CG>(args, stream);
   }
   return cudaErrorInvalidValue;
 }
 }  // namespace
 
-cudaError_t launch_fused(const KernelArgs& args, int bn, int comm, cudaStream_t stream) {
-  if (bn == 256) return launch_bn<256>(args, comm, stream);
-  if (bn == 128) return launch_bn<128>(args, comm, stream);
+cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream) {
+  if (cg == 2) {
+    if (bn == 256) return launch_bn<256, 2>(args, comm, stream);
+    if (bn == 128) return launch_bn<128, 2>(args, comm, stream);
+  } else {
+    if (bn == 256) return launch_bn<256, 1>(args, comm, stream);
+    if (bn == 128) return launch_bn<128, 1>(args, comm, stream);
+  }
   return cudaErrorInvalidValue;
-}
-
-size_t fused_smem_bytes(int bn, int mode, int comm, bool comm_cta) {
-  if (comm_cta) return dev::comm_cta_layout().total;
-  const bool tc = mode == MODE_AG && comm == COMM_TMA;
-  return bn == 256 ? dev::gemm_layout<256>(tc).total : dev::gemm_layout<128>(tc).total;
 }
 
 }  // namespace ao

@@ -38,7 +38,7 @@ struct alignas(64) RankArgs {
   const int* order;            // [n_tiles] tile ids in execution order
   const int* wait_off;         // [n_cta + 1] CSR offsets into waits
   const int2* waits;           // (position k, chunk g)
-  const int* tiles_per_chunk;  // RS [n_chunks]
+  const int* tiles_per_chunk;  // RS [n_chunks]: 128-row sub-tiles (one per CTA) touching chunk g
   const int* reduce_items;     // RS [n_items] tile ids
   const CommItem* comm_items;  // AG in-kernel comm [n_comm_items]
   void* C;                     // AG/GEMM: C [M, N] bf16.  RS: C_shard [S, N] bf16
@@ -56,7 +56,7 @@ struct alignas(64) RankArgs {
 struct KernelArgs {
   RankArgs rk[AO_MAX_WORLD];
   int32_t n_group;
-  int32_t ctas_per_rank;       // GEMM CTAs per rank (== plan n_cta)
+  int32_t ctas_per_rank;       // GEMM CTAs per rank (== plan n_cta * cta_group)
   int32_t comm_ctas_per_rank;  // dedicated comm CTAs per rank
   int32_t mode;                // KernelMode
   uint64_t timeout_ns;
@@ -66,7 +66,7 @@ struct KernelArgs {
 };
 
 // Host-side launcher (fused.cu).
-cudaError_t launch_fused(const KernelArgs& args, int bn, int comm, cudaStream_t stream);
-size_t fused_smem_bytes(int bn, int mode, int comm, bool comm_cta);
+// bn: tile N (128/256); cg: 1 (BM = 128) or 2 (CTA pair, BM = 256); comm: CommKind.
+cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream);
 
 }  // namespace ao

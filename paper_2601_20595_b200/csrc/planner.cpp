@@ -9,7 +9,7 @@
 
 namespace ao {
 
-const TileShape kTileCandidates[] = {{128, 256, 1}, {128, 128, 1}};
+const TileShape kTileCandidates[] = {{256, 256, 2}, {256, 128, 2}, {128, 256, 1}, {128, 128, 1}};
 const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[0]);
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -157,6 +157,13 @@ ao_status upload_tables(ao_plan* p) {
   }
   std::vector<int> items;
   for (auto& it : hp.reduce_items) items.push_back(it[0]);
+  // RS completion counts at 128-row sub-tile granularity (each CTA of a pair signals its
+  // own half): sub-tiles of all column blocks whose rows intersect chunk g.
+  std::vector<int> subtiles(hp.n_chunks, 0);
+  for (int g = 0; g < hp.n_chunks; ++g) {
+    const int64_t r0 = int64_t(g) * hp.C, r1 = r0 + hp.C - 1;
+    subtiles[g] = int(r1 / 128 - r0 / 128 + 1) * hp.n_nb;
+  }
   // in-kernel comm items (AG push, TMA / LDST backends)
   std::vector<ao::CommItem> comm;
   if (hp.is_ag && hp.desc.backend != AO_BACKEND_CE && hp.desc.dir == AO_DIR_PUSH) {
@@ -187,14 +194,14 @@ ao_status upload_tables(ao_plan* p) {
   const size_t o_woff = o_order + al(hp.order.size() * 4 + 4);
   const size_t o_waits = o_woff + al(wait_off.size() * 4);
   const size_t o_tpc = o_waits + al(waits.size() * 8 + 8);
-  const size_t o_items = o_tpc + al(hp.tiles_per_chunk.size() * 4 + 4);
+  const size_t o_items = o_tpc + al(subtiles.size() * 4 + 4);
   const size_t o_comm = o_items + al(items.size() * 4 + 4);
   const size_t total = o_comm + al(comm.size() * sizeof(ao::CommItem) + 16);
   std::vector<char> h(total, 0);
   memcpy(h.data() + o_order, hp.order.data(), hp.order.size() * 4);
   memcpy(h.data() + o_woff, wait_off.data(), wait_off.size() * 4);
   if (!waits.empty()) memcpy(h.data() + o_waits, waits.data(), waits.size() * 8);
-  if (!hp.tiles_per_chunk.empty()) memcpy(h.data() + o_tpc, hp.tiles_per_chunk.data(), hp.tiles_per_chunk.size() * 4);
+  if (!subtiles.empty()) memcpy(h.data() + o_tpc, subtiles.data(), subtiles.size() * 4);
   if (!items.empty()) memcpy(h.data() + o_items, items.data(), items.size() * 4);
   if (!comm.empty()) memcpy(h.data() + o_comm, comm.data(), comm.size() * sizeof(ao::CommItem));
   AO_CUDA(cudaMalloc(&p->d_tables, total));
@@ -296,7 +303,7 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
       s = encode_2d(&R->tmA, A, hp.M, hp.K, 128);
       if (s != AO_OK) return s;
     }
-    s = encode_2d(&R->tmB, B, hp.N, hp.K, bn);
+    s = encode_2d(&R->tmB, B, hp.N, hp.K, bn / hp.tile.cg);
     if (s != AO_OK) return s;
   }
   R->C = C;
@@ -595,7 +602,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
   memset(ka.get(), 0, sizeof(ao::KernelArgs));
   ka->n_group = n;
-  ka->ctas_per_rank = h0.n_cta;
+  ka->ctas_per_rank = h0.n_cta * h0.tile.cg;
   ka->mode = mode;
   ka->timeout_ns = h0.desc.timeout_ns ? h0.desc.timeout_ns : 5000000000ull;
   ka->err = p0->ctx->err_dev;
@@ -636,7 +643,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
       AO_CUDA(cudaEventRecord(c->ev_done, c->side));
     }
   }
-  cudaError_t e = ao::launch_fused(*ka, h0.tile.bn, comm, stream);
+  cudaError_t e = ao::launch_fused(*ka, h0.tile.bn, h0.tile.cg, comm, stream);
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(e));
   if (ce)
     for (int i = 0; i < n; ++i) AO_CUDA(cudaStreamWaitEvent(stream, plans[i]->ctx->ev_done, 0));
@@ -679,12 +686,13 @@ ao_status ao_gemm_rs(ao_plan* plan, const void* A, const void* B, void* C_shard,
 }
 
 // ----------------------------------------------------------------------- plain GEMM entry
-ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int32_t tile_n,
-                  void* stream_v) {
+ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int32_t tile_m,
+                  int32_t tile_n, void* stream_v) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int64_t, int64_t, int64_t, int>, ao_plan*> cache;
-  if (M < 0 || N < 0 || K < 0 || M % 128 != 0 || N % 8 != 0 || K % 8 != 0)
-    return fail(AO_ERR_INVALID_ARG, "ao_gemm needs M %% 128 == 0, N %% 8 == 0, K %% 8 == 0 (M=%lld N=%lld K=%lld)",
+  static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int>, ao_plan*> cache;
+  const int bm = tile_m ? tile_m : (M % 256 == 0 ? 256 : 128);
+  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256) || M % bm != 0 || N % 8 != 0 || K % 8 != 0)
+    return fail(AO_ERR_INVALID_ARG, "ao_gemm needs M %% tile_m == 0, N %% 8 == 0, K %% 8 == 0 (M=%lld N=%lld K=%lld)",
                 (long long)M, (long long)N, (long long)K);
   if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return fail(AO_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
   if (M == 0 || N == 0) return AO_OK;
@@ -693,7 +701,7 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
   ao_plan* p = nullptr;
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(device, M, N, K, bn);
+    auto key = std::make_tuple(device, M, N, K, bm, bn);
     auto it = cache.find(key);
     if (it != cache.end()) {
       p = it->second;
@@ -707,7 +715,7 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
       d.N = N;
       d.K = K;
       d.chunk_rows = int32_t(std::min<int64_t>(M, 1 << 30));
-      d.tile_m = 128;
+      d.tile_m = bm;
       d.tile_n = bn;
       s = ao_plan_create_host(&d, sm, &p);
       if (s != AO_OK) return s;
@@ -723,13 +731,13 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
   std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
   memset(ka.get(), 0, sizeof(ao::KernelArgs));
   ka->n_group = 1;
-  ka->ctas_per_rank = p->hp.n_cta;
+  ka->ctas_per_rank = p->hp.n_cta * p->hp.tile.cg;
   ka->mode = ao::MODE_GEMM;
   ka->timeout_ns = 5000000000ull;
   ka->skip_wait = -1;
   ao_status s = fill_rank(&ka->rk[0], p, 0, A, B, C);
   if (s != AO_OK) return s;
-  cudaError_t e = ao::launch_fused(*ka, bn, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));
+  cudaError_t e = ao::launch_fused(*ka, bn, p->hp.tile.cg, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return AO_OK;
 }

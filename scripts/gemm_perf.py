@@ -29,9 +29,9 @@ for M, N, K in shapes:
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     fl = 2.0 * M * N * K
     res = []
-    for bn in (256, 128):
-        ms = bench(lambda: ao.gemm(A, B, C, tile_n=bn))
-        res.append(f"ao bn={bn}: {fl / ms / 1e9:7.1f} TF/s ({ms:.3f} ms)")
+    for bm, bn in ((256, 256), (256, 128), (128, 256)):
+        ms = bench(lambda: ao.gemm(A, B, C, tile_n=bn, tile_m=bm))
+        res.append(f"ao {bm}x{bn}: {fl / ms / 1e9:7.1f} TF/s")
     ms = bench(lambda: torch.matmul(A, B.t(), out=C))
     res.append(f"cublas: {fl / ms / 1e9:7.1f} TF/s ({ms:.3f} ms)")
     print(f"{M}x{N}x{K}: " + " | ".join(res), flush=True)

@@ -32,13 +32,16 @@ def _check(gpu, ref, what):
 
 
 # ------------------------------------------------------------------------ plain GEMM
-@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (256, 512, 512, 256), (384, 392, 136, 256),
-                                      (512, 520, 1000, 128), (1024, 2048, 4096, 256), (128, 128, 8, 128),
-                                      (256, 384, 0, 256)])
-def test_gemm_vs_oracle(ao, M, N, K, bn):
+@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("M,N,K,bn", [(256, 256, 64, 256), (256, 512, 512, 256), (768, 392, 136, 256),
+                                      (512, 520, 1000, 128), (1024, 2048, 4096, 256), (256, 128, 8, 128),
+                                      (256, 384, 0, 256), (128, 256, 64, 256)])
+def test_gemm_vs_oracle(ao, M, N, K, bn, bm):
+    if M % bm:
+        pytest.skip("M not a multiple of the tile")
     A, B = si.ag_inputs(1, M, K, N, salt=M + N + K)
     A, B = A[0], B[0]
-    C = ao.gemm(A.cuda(), B.cuda(), tile_n=bn)
+    C = ao.gemm(A.cuda(), B.cuda(), tile_n=bn, tile_m=bm)
     torch.cuda.synchronize()
     ref = on.gemm(si.to_f64(A), si.to_f64(B))
     _check(C, ref, f"gemm {M}x{N}x{K}")
@@ -77,13 +80,14 @@ def _run_ag(ao, ctxs, plans, A, B, gather=False):
     return Cs, G
 
 
+@pytest.mark.parametrize("tile", [(128, 128), (256, 128), (256, 256)])
 @pytest.mark.parametrize("backend", ["ce", "ldst", "tma"])
 @pytest.mark.parametrize("W", [1, 2, 4, 8])
-def test_ag_gemm_tiny_vs_oracle(ao, backend, W):
-    # BASELINE configs[0]: M=256/rank, K=512, N=512, chunk=64 rows (tiles of 128x128)
+def test_ag_gemm_tiny_vs_oracle(ao, backend, W, tile):
+    # BASELINE configs[0]: M=256/rank, K=512, N=512, chunk=64 rows
     M, K, N, C = 256 * W, 512, 512, 64
     A, B = si.ag_inputs(W, M, K, N)
-    ctxs, plans = _ag_world(ao, W, M, N, K, C, backend, tile_m=128, tile_n=128, n_slices=2)
+    ctxs, plans = _ag_world(ao, W, M, N, K, C, backend, tile_m=tile[0], tile_n=tile[1], n_slices=2)
     Cs, G = _run_ag(ao, ctxs, plans, _dev(A), _dev(B), gather=True)
     A64 = [si.to_f64(a) for a in A]
     full = torch.cat(A, 0)
@@ -139,11 +143,12 @@ def _run_rs(ao, ctxs, plans, A, B):
     return Cs
 
 
+@pytest.mark.parametrize("tile", [(128, 128), (256, 128), (256, 256)])
 @pytest.mark.parametrize("W", [1, 2, 4, 8])
-def test_gemm_rs_tiny_vs_oracle(ao, W):
+def test_gemm_rs_tiny_vs_oracle(ao, W, tile):
     M, K, N, C = 256 * W, 256, 512, 64
     A, B = si.rs_inputs(W, M, K, N)
-    ctxs, plans = _rs_world(ao, W, M, N, K, C, tile_m=128, tile_n=128)
+    ctxs, plans = _rs_world(ao, W, M, N, K, C, tile_m=tile[0], tile_n=tile[1])
     Cs = _run_rs(ao, ctxs, plans, _dev(A), _dev(B))
     A64 = [si.to_f64(a) for a in A]
     B64 = [si.to_f64(b) for b in B]

@@ -250,16 +250,20 @@ def test_validation_rejects():
 
 
 def test_tile_heuristic_brute_force():
-    # AG@8 per rank on 148 SMs: 448 tiles at 128x256 (util 448/592) vs 896 at 128x128
-    # (util 896/1036): the utilization argmax must be chosen.
+    # AG@8 per rank on 148 SMs (74 CTA pairs): wave-quantization utilization
+    # T / (ceil(T/n) * n) decides; ties go to the larger tile, then larger BN.
     d = _desc(world_size=8, rank=0, M=8192, N=1792, K=4096, chunk_rows=128)
-    bm, bn, cg = osch.pick_tile(d, 148)
-    utils = {}
+    picked = osch.pick_tile(d, 148)
+    best, best_key = None, None
     for a, b, c in osch.TILE_CANDIDATES:
+        n = 148 // c
         T = (8192 // a) * (-(-1792 // b))
-        utils[(a, b)] = T / (-(-T // 148) * 148)
-    best = max(utils.items(), key=lambda kv: (kv[1], kv[0][0] * kv[0][1], kv[0][1]))[0]
-    assert (bm, bn) == best
+        key = (T / (-(-T // n) * n), a * b, b)
+        if best_key is None or key > best_key:
+            best, best_key = (a, b, c), key
+    assert picked == best
+    # 132 SMs (H100 count) changes the answer for the 128-wide shapes
+    assert osch.pick_tile(d, 132) is not None
 
 
 def test_export_is_canonical_and_deterministic():

@@ -41,16 +41,18 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tp", type=int, default=8, help="logical TP ranks in loopback (N=1)")
-    ap.add_argument("--backend", default="tma", choices=["ce", "tma", "ldst"])
-    ap.add_argument("--chunk", type=int, default=128)
+    ap.add_argument("--backend", default="ce", choices=["ce", "tma", "ldst"])
+    ap.add_argument("--chunk", type=int, default=1024)
     ap.add_argument("--tokens", type=int, default=TOKENS)
     ap.add_argument("--intra", default="grouped", choices=["row", "col", "grouped"])
-    ap.add_argument("--group-m", type=int, default=8)
+    ap.add_argument("--group-m", type=int, default=4)
     ap.add_argument("--rs-chunk", type=int, default=0, help="GEMM-RS chunk rows (0 = --chunk)")
-    ap.add_argument("--rs-order", default="chunk_major", choices=["shard_major", "chunk_major"])
+    ap.add_argument("--rs-order", default="shard_major", choices=["shard_major", "chunk_major"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baseline", action="store_true")
+    ap.add_argument("--l2-hint", type=int, default=-1)
+    ap.add_argument("--trace", default="", help="write Chrome traces of one extra step to PREFIX_{ag,rs}.json")
     return ap.parse_args()
 
 
@@ -122,6 +124,8 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if args.l2_hint >= 0:
+        ao.debug_set("l2_hint", args.l2_hint)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     M = args.tokens
@@ -206,6 +210,14 @@ def run_ours(args, rank, world, local_rank):
     flops_ag = 2.0 * M * FFN * HIDDEN  # whole layer, all ranks
     flops_step = 2 * flops_ag
     value = flops_step / (ms * 1e-3) / 1e12
+
+    if args.trace and rank == 0:
+        # three back-to-back steps (launches 0..5: ag, rs, ag, rs, ag, rs) in one trace
+        ctxs[0].trace_enable(1 << 21)
+        for _ in range(3):
+            step()
+        ctxs[0].trace_dump(args.trace + ".json")
+        ctxs[0].trace_enable(0)
 
     # --- sanity vs cuBLAS on sampled rows (not the oracle; parity lives in tests/) ------
     check = None

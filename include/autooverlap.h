@@ -182,6 +182,15 @@ ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, 
 ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                   int32_t tile_m, int32_t tile_n, void* stream);
 
+/* ---- tracing -------------------------------------------------------------
+ * ao_ctx_trace_enable: allocate a device event buffer of `capacity` events (0 = off).  Op
+ *   launches whose first plan belongs to this ctx record %globaltimer-stamped events:
+ *   chunk waits, tile loads, MMA, epilogue, transfers, reductions.
+ * ao_ctx_trace_dump: synchronize, write the recorded events as Chrome-trace JSON to `path`
+ *   (pid = rank, tid = CTA*8 + role), reset the buffer; *n_events = events written. */
+ao_status ao_ctx_trace_enable(ao_ctx* ctx, int64_t capacity);
+ao_status ao_ctx_trace_dump(ao_ctx* ctx, const char* path, int64_t* n_events);
+
 /* ---- test hooks (deterministic fault injection; see tests/) ----------------------------
  * ao_debug_set: key "skip_wait" = index of a wait (global over CTAs) the kernel must skip
  * (-1 = none); "delay_ns" = nanosleep before each transfer/signal (fuzzes arrival order). */

@@ -26,7 +26,10 @@ DESIGN.md, deliberately by enumeration rather than closed forms:
   8. Waits     -- "the minimal set of synchronization points ... a tile that consumes a
                   given chunk cannot start until the corresponding communication operator
                   has completed": one wait per (CTA, chunk) first use.
-  9. Signals   -- "global-memory signals": per-chunk flag words.
+  9. Signals   -- "global-memory signals": per-chunk flag words.  In GEMM-RS the
+                  owner's own-row tiles come last and their epilogue fuses the peer reduction
+                  (north star: "the epilogue of gemm_rs fusing the peer reduction"), so those
+                  tiles wait for the W-1 other sources of their chunks.
 
 Canonical export: JSON, sorted keys, no whitespace, integers only, strings only for
 enum names.  Parity: not applicable (exact).
@@ -196,10 +199,18 @@ def _build_plans(desc, chunks):
                     for g in _shard_chunks(chunks, o):
                         seq.append((o, g))
             else:
+                # chunk-major: round j = chunk j of every peer owner; the own (local
+                # accumulate) op of chunk j is lagged into round j+1, so the owner's fused
+                # reduction of chunk j never waits on the peer tile issued just before it
+                # (reading Q21); the last own chunk closes the list.
                 n_c = len(_shard_chunks(chunks, 0)) if W > 0 else 0
                 for j in range(n_c):
-                    for o in owners:
+                    for o in owners[:-1]:
                         seq.append((o, _shard_chunks(chunks, o)[j]))
+                    if j >= 1:
+                        seq.append((q, _shard_chunks(chunks, q)[j - 1]))
+                if n_c:
+                    seq.append((q, _shard_chunks(chunks, q)[n_c - 1]))
             for o, g in seq:
                 row0, rows, _ = chunks[g]
                 ops.append({"accumulate": 1, "deps": [], "direction": "push", "dst_chunk": [row0, rows],
@@ -287,32 +298,23 @@ def plan(desc, sm_count=148):
     keyed.sort(key=lambda x: x[0])
     order = [t for _, t in keyed]
 
-    reduce_items = []
     tiles_per_chunk = []
     if not is_ag:
         tiles_per_chunk = [sum(1 for t in range(T) if g in tile_chunks[t]) for g in range(len(chunks))]
-        own = []
-        for t in range(T):
-            mb, nb = divmod(t, n_nb)
-            if (mb * bm) // S == r:
-                latest_j = max(_shard_chunks(chunks, r).index(g) for g in tile_chunks[t])
-                own.append(((latest_j,) + _intra_key(desc, mb, nb), t))
-        own.sort(key=lambda x: x[0])
-        reduce_items = [[t, tile_chunks[t][0], tile_chunks[t][-1]] for _, t in own]
 
-    # CTA assignment: position k -> CTA k mod n_cta; reduce items continue the stride.
-    work = [("tile", t) for t in order] + [("reduce", it[0]) for it in reduce_items]
+    # CTA assignment: position k -> CTA k mod n_cta.  Waits: AG tiles wait for their
+    # remote chunks; RS own-row tiles (whose epilogue fuses the peer reduction) wait for
+    # the other sources' contributions to their chunks.
     waits = []
     for c in range(n_cta):
         seen = set()
         lst = []
-        for k in range(c, len(work), n_cta):
-            kind, t = work[k]
-            need = []
-            if is_ag and kind == "tile":
+        for k in range(c, len(order), n_cta):
+            t = order[k]
+            if is_ag:
                 need = [g for g in tile_chunks[t] if chunks[g][2] != r]
-            elif (not is_ag) and kind == "reduce":
-                need = list(tile_chunks[t])
+            else:
+                need = [g for g in tile_chunks[t] if chunks[g][2] == r] if W > 1 else []
             for g in need:
                 if g not in seen:
                     seen.add(g)
@@ -323,7 +325,7 @@ def plan(desc, sm_count=148):
         contrib = [0 if chunks[g][2] == r else (1 if desc["backend"] == "ce" else desc["n_slices"])
                    for g in range(len(chunks))]
     else:
-        contrib = [W if chunks[g][2] == r else 0 for g in range(len(chunks))]
+        contrib = [W - 1 if chunks[g][2] == r else 0 for g in range(len(chunks))]
 
     if is_ag:
         tensors = {"A": {"elem_bytes": 2, "shape": [M, K]}, "C": {"elem_bytes": 2, "shape": [M, N]}}
@@ -344,7 +346,6 @@ def plan(desc, sm_count=148):
     }
     if not is_ag:
         out["tiles_per_chunk"] = tiles_per_chunk
-        out["reduce_items"] = reduce_items
     return out
 
 

@@ -91,6 +91,8 @@ _SIGS = {
     "ao_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
     "ao_debug_set": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64]),
+    "ao_ctx_trace_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
+    "ao_ctx_trace_dump": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
 }
 
 EXPORTED = sorted(_SIGS)

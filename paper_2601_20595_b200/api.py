@@ -127,6 +127,14 @@ class Context:
             ctypes.memmove(arr[i].bytes, raw, N.AO_HANDLE_BYTES)
         check(lib().ao_ctx_import_handles(self.handle, arr))
 
+    def trace_enable(self, capacity: int = 1 << 20):
+        check(lib().ao_ctx_trace_enable(self.handle, int(capacity)))
+
+    def trace_dump(self, path: str) -> int:
+        n = ctypes.c_int64(0)
+        check(lib().ao_ctx_trace_dump(self.handle, path.encode(), ctypes.byref(n)))
+        return n.value
+
     def check_async(self):
         check(lib().ao_ctx_check_async(self.handle))
 

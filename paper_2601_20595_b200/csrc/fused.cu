@@ -9,8 +9,10 @@
 //    communication warps or dedicated communication CTAs ("specialized SMs", Fig.7b/c)
 //    push chunks with cp.async.bulk (TMA backend) or 16-byte ld/st (LDST backend);
 //  * GEMM-RS: each finished fp32 partial tile is written into its owner's slot; the last
-//    tile of a chunk releases the owner's flag; the owner's reducer warps run the fused
-//    reduction of the chunk (ascending source rank) concurrently with the GEMM.
+//    tile of a chunk releases the owner's flag.  The owner computes its own rows last; the
+//    epilogue of an own tile waits for the other sources' flags of its chunks, adds their
+//    partials to its TMEM accumulator in ascending source rank and stores bf16 --
+//    the peer reduction fused into the epilogue (north star).
 //
 // Tile = BM x BN with BM = 128 * CG.  CG = 2 runs one tile on a CTA pair (cluster of 2,
 // tcgen05.mma.cta_group::2, M = 256): each CTA loads its 128 rows of A and half of B's
@@ -21,7 +23,6 @@
 //   warp 1      TMEM allocator + tcgen05.mma issuer (leader CTA of the pair)
 //   warps 2..5  epilogue (TMEM -> registers -> smem transpose -> global; RS signals)
 //   warps 6..7  AG: co-located communication warps
-//   warps 6..11 RS: reducer warps (own-row reduction)
 #include <cuda_runtime.h>
 
 #include "kernel_args.h"
@@ -32,10 +33,8 @@ namespace dev {
 
 constexpr int kSubM = 128;  // rows per CTA (TMEM lanes)
 constexpr int kBK = 64;
-constexpr int kThreads = 256;    // AG / GEMM CTA
-constexpr int kThreadsRS = 384;  // RS CTA
+constexpr int kThreads = 256;
 constexpr int kCommWarp0 = 6;
-constexpr int kReduceWarps = 6;
 constexpr int kColocCommWarps = 2;
 constexpr int kCommBufs = 2;
 constexpr uint32_t kColocBufBytes = 4096;
@@ -112,6 +111,21 @@ __device__ __noinline__ void spin_flag(const uint32_t* p, uint32_t target, const
   }
 }
 
+__device__ __forceinline__ void trace_event(const KernelArgs& A, uint32_t kind, int rank, int cta, int id, uint64_t t0) {
+  if (A.trace == nullptr) return;
+  const uint32_t i = atomicAdd(A.trace_cursor, 1u);
+  if (i < A.trace_cap) {
+    TraceEvent e;
+    e.t0 = t0;
+    e.t1 = globaltimer();
+    e.kind = kind | (A.trace_seq << 8);
+    e.rank = uint32_t(rank);
+    e.cta = uint32_t(cta);
+    e.id = uint32_t(id);
+    A.trace[i] = e;
+  }
+}
+
 __device__ __forceinline__ int4 ld_nc_v4(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -132,6 +146,7 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
   const int lane = lane_id();
   uint32_t phase_bits = 0;
   for (int i = worker; i < R.n_comm_items; i += n_workers) {
+    const uint64_t t_item = A.trace ? globaltimer() : 0;
     const CommItem it = R.comm_items[i];
     const char* src = R.A_shard + it.src_off;
     char* dst = R.peer_data[it.peer] + it.dst_off;
@@ -190,14 +205,14 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
     if (lane == 0) {
       if (A.delay_ns) __nanosleep((uint32_t(i) * 2654435761u) % A.delay_ns);
       st_release_sys(R.peer_flags[it.peer] + it.g * R.n_slices + it.slice, R.epoch);
+      trace_event(A, TR_COMM, R.rank, worker, i, t_item);
     }
     __syncwarp();
   }
 }
 
 template <int BN, int MODE, int COMM, int CG>
-__global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
-    fused_kernel(const __grid_constant__ KernelArgs args) {
+__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constant__ KernelArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -287,8 +302,10 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
   if (warp == 0) {
     // ================================================================ TMA producer
     if (lane == 0) {
-      const uint64_t pol_b = policy_evict_last();
-      const uint64_t pol_a = policy_evict_first();
+      // L2 policy follows the tile order: with grouped / column orders an A row block is
+      // reused across every column tile of its group, B tiles only by neighbours in time.
+      const uint64_t pol_b = args.l2_hint ? policy_evict_first() : policy_evict_last();
+      const uint64_t pol_a = args.l2_hint ? policy_evict_last() : policy_evict_first();
       uint32_t stage = 0, phase = 0;
       int wp = 0, we = 0;
       if constexpr (MODE == MODE_AG) {
@@ -300,15 +317,18 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
           bool waited = false;
           while (wp < we && R.waits[wp].x == k) {
             const int g = R.waits[wp].y;
+            const uint64_t tw = args.trace ? globaltimer() : 0;
             if (!(grp == 0 && wp == args.skip_wait)) {
               for (int s = 0; s < R.n_slices; ++s)
                 spin_flag(R.flags + g * R.n_slices + s, R.epoch, args, R.rank, lcta, g);
             }
+            trace_event(args, TR_WAIT, R.rank, lcta, g, tw);
             ++wp;
             waited = true;
           }
           if (waited) fence_proxy_async_global();  // generic-proxy arrivals -> TMA reads
         }
+        const uint64_t t_load = args.trace ? globaltimer() : 0;
         const int t = R.order[k];
         const int mb = t / R.n_nb;
         const int nb = t - mb * R.n_nb;
@@ -337,6 +357,7 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
             phase ^= 1;
           }
         }
+        trace_event(args, TR_LOAD, R.rank, lcta, t, t_load);
       }
     }
   } else if (warp == 1) {
@@ -345,6 +366,7 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
       constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       for (int k = wk; k < n_tiles; k += n_wk) {
+        const uint64_t t_mma = args.trace ? globaltimer() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -377,6 +399,7 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
             mma_commit_cg2_mc(&tfull[acc]);
           else
             mma_commit(&tfull[acc]);
+          trace_event(args, TR_MMA, R.rank, lcta, R.order[k], t_mma);
         }
         __syncwarp();
         acc ^= 1;
@@ -395,25 +418,126 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
     constexpr int EPS = (MODE == MODE_RS) ? 4 : 8;   // elements per 16-byte lane segment
     constexpr int EB = (MODE == MODE_RS) ? 4 : 2;    // bytes per output element
     uint32_t acc = 0, acc_phase = 0;
+    int wp = 0, we = 0;  // RS: this worker's wait list (own tiles)
+    if constexpr (MODE == MODE_RS) {
+      wp = R.wait_off[wk];
+      we = R.wait_off[wk + 1];
+    }
     for (int k = wk; k < n_tiles; k += n_wk) {
       const int t = R.order[k];
       const int mb = t / R.n_nb;
       const int nb = t - mb * R.n_nb;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      const uint64_t t_epi = args.trace ? globaltimer() : 0;
       const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       const int64_t col_base = int64_t(nb) * BN;
       const int64_t sub0 = int64_t(mb) * BM + int64_t(crank) * kSubM;  // first row of this CTA's half
       const int64_t row0 = sub0 + q * 32;                                // first row of this warp
       int owner = 0;
+      bool own_tile = false;
       char* dst_base;  // byte address of (row0, col 0) of the destination matrix
       const int64_t ld_bytes = N * EB;
       if constexpr (MODE == MODE_RS) {
         owner = int(sub0 / S);
+        own_tile = owner == R.rank;
         dst_base = R.peer_data[owner] + (int64_t(R.rank) * S + (row0 - int64_t(owner) * S)) * ld_bytes;
       } else {
         dst_base = reinterpret_cast<char*>(R.C) + row0 * ld_bytes;
       }
+      if constexpr (MODE == MODE_RS) {
+        if (own_tile) {
+          // RS-4 fused reduction: wait for the other sources' partials of this tile's chunks
+          if (etid == 0) {
+            while (wp < we && R.waits[wp].x == k) {
+              const int g = R.waits[wp].y;
+              const uint64_t tw = args.trace ? globaltimer() : 0;
+              if (!(grp == 0 && wp == args.skip_wait)) {
+                for (int s = 0; s < R.W; ++s)
+                  if (s != R.rank) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, lcta, g);
+              }
+              trace_event(args, TR_REDWAIT, R.rank, lcta, g, tw);
+              ++wp;
+            }
+          }
+          named_bar_sync(1, 128);
+          // Coalesced layout: stage the own accumulator (thread = row) through smem, then
+          // lane l handles rows (i*4 + l/8), columns 4*(l%8)..+3 for i = 0..7, so every
+          // peer-slot load and the bf16 store are 8 lanes x 16 B along one row.
+          const int64_t lrow0 = row0 - int64_t(R.rank) * S;  // first row of this warp in C_shard
+          const float* slots = reinterpret_cast<const float*>(R.peer_data[R.rank]);
+          const int64_t slot_stride = S * N;  // floats
+          __nv_bfloat16* cout = reinterpret_cast<__nv_bfloat16*>(R.C);
+          const int c = lane & 7;
+#pragma unroll 1
+          for (int cc = 0; cc < BN; cc += 32) {
+            const int64_t col0 = col_base + cc;
+            if (col0 >= N) break;  // warp-uniform
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tb + cc, v);
+            tmem_wait_ld();
+            if (nkb == 0) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            __syncwarp();
+            const bool ok = col0 + 4 * c < N;
+            float4 own[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = i * 4 + (lane >> 3);
+              const uint4 w = stg[r * 8 + (c ^ (r & 7))];
+              own[i] = make_float4(__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z), __uint_as_float(w.w));
+            }
+            __syncwarp();
+            float4 acc[8];
+            const int64_t base_off = (lrow0 + (lane >> 3)) * N + col0 + 4 * c;  // row i*4 + lane/8 adds i*4*N
+            // ascending source rank; own contribution at s == rank; two slots in flight
+            for (int s0 = 0; s0 < R.W; s0 += 2) {
+              float4 ld[2][8];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int s = s0 + u;
+                if (s < R.W && s != R.rank && ok) {
+                  const float* src = slots + s * slot_stride + base_off;
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) ld[u][i] = __ldcg(reinterpret_cast<const float4*>(src + int64_t(i) * 4 * N));
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int s = s0 + u;
+                if (s >= R.W) break;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float4 x = (s == R.rank) ? own[i] : ld[u][i];
+                  if (s == 0) {
+                    acc[i] = x;
+                  } else {
+                    acc[i].x += x.x;
+                    acc[i].y += x.y;
+                    acc[i].z += x.z;
+                    acc[i].w += x.w;
+                  }
+                }
+              }
+            }
+            if (ok) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                uint2 o;
+                o.x = pack_bf16x2(acc[i].x, acc[i].y);
+                o.y = pack_bf16x2(acc[i].z, acc[i].w);
+                *reinterpret_cast<uint2*>(cout + base_off + int64_t(i) * 4 * N) = o;
+              }
+            }
+          }
+        }
+      }
+      if (!own_tile) {
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += CW) {
         uint32_t v[32];
@@ -453,6 +577,7 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
         }
         __syncwarp();
       }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -461,7 +586,7 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
         else
           mbar_arrive(&tempty[acc]);
       }
-      if constexpr (MODE == MODE_RS) {
+      if (MODE == MODE_RS && !own_tile) {
         // RS-3: count this CTA's 128-row sub-tile into each of its chunks; the last
         // contributor releases the owner's flag[g][rank].  One sys-scope fence after the
         // CTA barrier is cumulative over the 128 threads' partial-tile stores.
@@ -481,79 +606,9 @@ __global__ void __launch_bounds__(MODE == MODE_RS ? kThreadsRS : kThreads, 1)
           }
         }
       }
+      if (etid == 0) trace_event(args, TR_EPI, R.rank, lcta, t, t_epi);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
-  } else if constexpr (MODE == MODE_RS) {
-    // ================================================================ reducer warps
-    // RS-4: the owner's fused reduction, concurrent with the GEMM pipeline.  Items are
-    // own-row tiles in chunk order; each waits for flag[g][s] of every source s, then
-    // sums the W fp32 slot tiles in ascending source rank and stores bf16.  With
-    // CG == 2 each CTA of the pair reduces its own 128-row half of the item.
-    const int rtid = threadIdx.x - 32 * kCommWarp0;
-    constexpr int RT = 32 * kReduceWarps;
-    int wp = R.wait_off[wk];
-    const int we = R.wait_off[wk + 1];
-    const int n_work = n_tiles + R.n_items;
-    int k = wk;
-    while (k < n_tiles) k += n_wk;
-    const float* slots = reinterpret_cast<const float*>(R.peer_data[R.rank]);
-    const int64_t slot_stride = S * N;  // floats
-    const int W = R.W;
-    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(R.C);
-    for (; k < n_work; k += n_wk) {
-      if (rtid == 0) {
-        while (wp < we && R.waits[wp].x == k) {
-          const int g = R.waits[wp].y;
-          if (!(grp == 0 && wp == args.skip_wait)) {
-            for (int s = 0; s < W; ++s) spin_flag(R.flags + g * W + s, R.epoch, args, R.rank, lcta, g);
-          }
-          ++wp;
-        }
-      }
-      named_bar_sync(2, RT);
-      const int t = R.reduce_items[k - n_tiles];
-      const int mb = t / R.n_nb;
-      const int nb = t - mb * R.n_nb;
-      const int64_t lr0 = int64_t(mb) * BM + int64_t(crank) * kSubM - int64_t(R.rank) * S;
-      const int64_t c0 = int64_t(nb) * BN;
-      const int64_t valid = (N - c0) < BN ? (N - c0) : BN;
-      constexpr int per_row = BN / 4;
-      constexpr int total = kSubM * per_row;
-      for (int base = rtid; base < total; base += 2 * RT) {
-        float4 a[2][AO_MAX_WORLD];
-        int64_t off[2];
-        bool ok[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int idx = base + u * RT;
-          const int rr = idx / per_row;
-          const int c4 = idx - rr * per_row;
-          ok[u] = idx < total && c4 * 4 < valid;
-          off[u] = (lr0 + rr) * N + c0 + c4 * 4;
-#pragma unroll
-          for (int s = 0; s < AO_MAX_WORLD; ++s)
-            if (ok[u] && s < W) a[u][s] = __ldcg(reinterpret_cast<const float4*>(slots + s * slot_stride + off[u]));
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (!ok[u]) continue;
-          float4 x = a[u][0];
-#pragma unroll
-          for (int s = 1; s < AO_MAX_WORLD; ++s) {
-            if (s < W) {
-              x.x += a[u][s].x;
-              x.y += a[u][s].y;
-              x.z += a[u][s].z;
-              x.w += a[u][s].w;
-            }
-          }
-          uint2 o;
-          o.x = pack_bf16x2(x.x, x.y);
-          o.y = pack_bf16x2(x.z, x.w);
-          *reinterpret_cast<uint2*>(out + off[u]) = o;
-        }
-      }
     }
   } else {
     // ================================================================ co-located comm warps
@@ -601,7 +656,7 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(args.n_group * (args.ctas_per_rank + args.comm_ctas_per_rank));
-  cfg.blockDim = dim3(MODE == MODE_RS ? dev::kThreadsRS : dev::kThreads);
+  cfg.blockDim = dim3(dev::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -613,21 +668,17 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (coop_ok) {
-    attr[na].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (spin-waits, H3)
+  if (CG == 1 && coop_ok) {
+    // all CTAs co-resident (spin-waits, H3).  Cluster launches (CG == 2) rely on
+    // grid <= SMs with one CTA per SM instead: ncu cannot replay cooperative cluster
+    // launches, and the 2-CTA grid never exceeds the SM count.
+    attr[na].id = cudaLaunchAttributeCooperative;
     attr[na].val.cooperative = 1;
     ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
-  if (e != cudaSuccess && coop_ok && CG == 2) {
-    // cooperative + cluster not accepted: grid <= SMs with 1 CTA/SM still co-resides
-    cudaGetLastError();
-    coop_ok = false;
-    cfg.numAttrs = na - 1;
-    e = cudaLaunchKernelEx(&cfg, kern, args);
-  }
   return e;
 }
 

@@ -53,6 +53,13 @@ struct alignas(64) RankArgs {
   int32_t pad;
 };
 
+// In-kernel trace event (AO tracing): 32 bytes, %globaltimer nanoseconds.
+enum TraceKind : uint32_t { TR_WAIT = 1, TR_LOAD = 2, TR_MMA = 3, TR_EPI = 4, TR_COMM = 5, TR_RED = 6, TR_REDWAIT = 7 };
+struct TraceEvent {
+  uint64_t t0, t1;
+  uint32_t kind, rank, cta, id;
+};
+
 struct KernelArgs {
   RankArgs rk[AO_MAX_WORLD];
   int32_t n_group;
@@ -63,6 +70,11 @@ struct KernelArgs {
   ErrorInfo* err;              // host-mapped
   int32_t skip_wait;           // debug: CSR index of a wait of rank group 0 to skip (-1 none)
   uint32_t delay_ns;           // debug: sleep before each comm signal
+  TraceEvent* trace;           // null = tracing off
+  uint32_t* trace_cursor;
+  uint32_t trace_cap;
+  uint32_t trace_seq;          // launch sequence number stamped into events (kind >> 8)
+  int32_t l2_hint;             // 0: A evict_first / B evict_last (row order); 1: A evict_last / B evict_first
 };
 
 // Host-side launcher (fused.cu).

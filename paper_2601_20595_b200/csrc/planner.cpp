@@ -227,8 +227,12 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
         for (int e = 0; e < W; ++e)
           for (int j = 0; j < n_c; ++j) emit(e, j);
       } else {
-        for (int j = 0; j < n_c; ++j)
-          for (int e = 0; e < W; ++e) emit(e, j);
+        // chunk-major with the own chunk lagged by one round (Q21)
+        for (int j = 0; j < n_c; ++j) {
+          for (int e = 0; e < W - 1; ++e) emit(e, j);
+          if (j >= 1) emit(W - 1, j - 1);
+        }
+        if (n_c > 0) emit(W - 1, n_c - 1);
       }
     }
   }
@@ -247,7 +251,13 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
     } else {
       const int dd = (src - r + W) % W;
       const int e = dd == 0 ? W - 1 : dd - 1;
-      pos = d.chunk_order == AO_CHUNK_SHARD_MAJOR ? e * n_c + j : j * W + e;
+      if (d.chunk_order == AO_CHUNK_SHARD_MAJOR) {
+        pos = e * n_c + j;
+      } else if (e < W - 1) {
+        pos = j == 0 ? e : j * W - 1 + e;  // round 0 has W-1 ops, later rounds W
+      } else {
+        pos = j < n_c - 1 ? (j + 2) * W - 2 : n_c * W - 1;  // own chunk j lagged into round j+1
+      }
     }
     P.chunks[g] = {g, int(int64_t(g) * P.C), P.C, src, pos};
   }
@@ -280,7 +290,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
     return std::make_tuple(P.deps[a][3], intra_key(a)) < std::make_tuple(P.deps[b][3], intra_key(b));
   });
 
-  // RS: tiles_per_chunk and reduce items (own-row tiles by (latest j, intra key)).
+  // RS: tiles_per_chunk (tiles contributing to chunk g at a source rank).
   if (!P.is_ag) {
     P.tiles_per_chunk.assign(P.n_chunks, 0);
     for (int g = 0; g < P.n_chunks; ++g) {
@@ -288,37 +298,19 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
       const int mb_lo = int(r0 / BM), mb_hi = int(r1 / BM);
       P.tiles_per_chunk[g] = (mb_hi - mb_lo + 1) * P.n_nb;
     }
-    std::vector<int> own;
-    for (int t = 0; t < P.n_tiles; ++t)
-      if ((int64_t(t / P.n_nb) * BM) / P.S == r) own.push_back(t);
-    std::stable_sort(own.begin(), own.end(), [&](int a, int b) {
-      return std::make_tuple(j_of(ghi_of[a]), intra_key(a)) < std::make_tuple(j_of(ghi_of[b]), intra_key(b));
-    });
-    for (int t : own) P.reduce_items.push_back({t, glo_of[t], ghi_of[t]});
   }
 
-  // Rules 7/8: CTA k mod n_cta; one wait per (CTA, chunk) first use.
-  const int n_work = P.n_tiles + int(P.reduce_items.size());
+  // Rules 7/8: CTA k mod n_cta; one wait per (CTA, chunk) first use.  AG tiles wait for
+  // remote chunks; RS own-row tiles (fused peer reduction in their epilogue) wait for the
+  // other sources' contributions.
   P.waits.assign(P.n_cta, {});
   std::vector<int> seen(P.n_chunks, -1);
   for (int c = 0; c < P.n_cta; ++c) {
-    for (int k = c; k < n_work; k += P.n_cta) {
-      int glo, ghi;
-      bool need;
-      if (k < P.n_tiles) {
-        const int t = P.order[k];
-        glo = glo_of[t];
-        ghi = ghi_of[t];
-        need = P.is_ag;
-      } else {
-        const auto& it = P.reduce_items[k - P.n_tiles];
-        glo = it[1];
-        ghi = it[2];
-        need = true;
-      }
-      if (!need) continue;
-      for (int g = glo; g <= ghi; ++g) {
-        if (P.is_ag && P.chunks[g][3] == r) continue;
+    for (int k = c; k < P.n_tiles; k += P.n_cta) {
+      const int t = P.order[k];
+      for (int g = glo_of[t]; g <= ghi_of[t]; ++g) {
+        const bool own = P.chunks[g][3] == r;
+        if (P.is_ag ? own : (!own || W == 1)) continue;
         if (seen[g] == c) continue;
         seen[g] = c;
         P.waits[c].push_back({k, g});
@@ -331,7 +323,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
   const int ns = d.backend == AO_BACKEND_CE ? 1 : d.n_slices;
   for (int g = 0; g < P.n_chunks; ++g) {
     const bool own = P.chunks[g][3] == r;
-    P.contrib[g] = P.is_ag ? (own ? 0 : ns) : (own ? W : 0);
+    P.contrib[g] = P.is_ag ? (own ? 0 : ns) : (own ? W - 1 : 0);
   }
 
   // ---- canonical export ---------------------------------------------------------------
@@ -421,10 +413,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
     o.put("waits", s + "]");
   }
   o.put("contrib", int_list(P.contrib));
-  if (!P.is_ag) {
-    o.put("tiles_per_chunk", int_list(P.tiles_per_chunk));
-    o.put("reduce_items", list_of(P.reduce_items));
-  }
+  if (!P.is_ag) o.put("tiles_per_chunk", int_list(P.tiles_per_chunk));
   P.json = o.str();
   P.hash = fnv1a64(rank_independent_key(P));
   return {};

@@ -54,7 +54,6 @@ struct HostPlan {
   std::vector<std::vector<std::array<int, 2>>> waits;  // per CTA: (k, g)
   std::vector<int> contrib;
   std::vector<int> tiles_per_chunk;                // RS
-  std::vector<std::array<int, 3>> reduce_items;    // RS: t, g_lo, g_hi
   std::string json;
   uint64_t hash = 0;
 };

@@ -103,6 +103,7 @@ static_assert(sizeof(Blob) <= AO_HANDLE_BYTES, "blob too large");
 struct DebugKnobs {
   int64_t skip_wait = -1;
   int64_t delay_ns = 0;
+  int64_t l2_hint = -1;  // -1: follow the plan's tile order
 };
 DebugKnobs g_debug;
 
@@ -121,6 +122,11 @@ struct ao_ctx {
   char* peer_base[AO_MAX_WORLD] = {};
   bool peer_opened[AO_MAX_WORLD] = {};
   uint32_t epoch = 0;
+  uint32_t* epoch_cell = nullptr;   // device word holding the current epoch (CE flag source)
+  ao::TraceEvent* trace = nullptr;  // device ring (AO tracing)
+  uint32_t* trace_cursor = nullptr;
+  uint32_t trace_cap = 0;
+  uint32_t trace_seq = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
 
@@ -143,6 +149,8 @@ struct ao_plan {
   const ao::CommItem* d_comm = nullptr;
   int n_comm = 0;
   int comm_kind = ao::COMM_NONE;
+  // CE backend: instantiated copy-chain graphs keyed by (parity, group plans, A pointers)
+  std::map<std::vector<uintptr_t>, cudaGraphExec_t> ce_graphs;
 };
 
 namespace {
@@ -155,8 +163,7 @@ ao_status upload_tables(ao_plan* p) {
     for (auto& w : hp.waits[c]) waits.push_back(make_int2(w[0], w[1]));
     wait_off[c + 1] = int(waits.size());
   }
-  std::vector<int> items;
-  for (auto& it : hp.reduce_items) items.push_back(it[0]);
+  std::vector<int> items;  // (no separate reduce items: the own-tile epilogue reduces)
   // RS completion counts at 128-row sub-tile granularity (each CTA of a pair signals its
   // own half): sub-tiles of all column blocks whose rows intersect chunk g.
   std::vector<int> subtiles(hp.n_chunks, 0);
@@ -277,7 +284,7 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
   R->crows = hp.C;
   R->n_chunks = hp.n_chunks;
   R->n_tiles = hp.n_tiles;
-  R->n_items = int(hp.reduce_items.size());
+  R->n_items = 0;
   R->n_nb = hp.n_nb;
   R->n_slices = hp.desc.backend == AO_BACKEND_CE ? 1 : hp.desc.n_slices;
   R->n_cta = hp.n_cta;
@@ -341,6 +348,7 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   if (!key) return fail(AO_ERR_INVALID_ARG, "null key");
   if (!strcmp(key, "skip_wait")) g_debug.skip_wait = value;
   else if (!strcmp(key, "delay_ns")) g_debug.delay_ns = value;
+  else if (!strcmp(key, "l2_hint")) g_debug.l2_hint = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
   return AO_OK;
 }
@@ -432,6 +440,7 @@ ao_status ao_plan_destroy(ao_plan* p) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(p->device);
+    for (auto& kv : p->ce_graphs) cudaGraphExecDestroy(kv.second);
     cudaFree(p->d_tables);
     cudaSetDevice(cur);
   }
@@ -458,6 +467,8 @@ ao_status ao_ctx_create(int device, int rank, int world_size, size_t workspace_b
   cudaError_t e = cudaMalloc(&c->base, c->total);
   if (e != cudaSuccess) return fail(AO_ERR_OOM, "cudaMalloc(%zu): %s", c->total, cudaGetErrorString(e));
   AO_CUDA(cudaMemset(c->base + 2 * c->data_half, 0, 2 * kFlagWordsPerParity * 4));
+  AO_CUDA(cudaMalloc(&c->epoch_cell, 64));
+  AO_CUDA(cudaMemset(c->epoch_cell, 0, 64));
   AO_CUDA(cudaMalloc(&c->counters, kCounterWords * 4));
   AO_CUDA(cudaMemset(c->counters, 0, kCounterWords * 4));
   AO_CUDA(cudaHostAlloc(&c->err_host, sizeof(ao::ErrorInfo), cudaHostAllocMapped));
@@ -539,11 +550,64 @@ ao_status ao_ctx_destroy(ao_ctx* c) {
     if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
   if (c->base) cudaFree(c->base);
   if (c->counters) cudaFree(c->counters);
+  if (c->epoch_cell) cudaFree(c->epoch_cell);
   if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->trace) cudaFree(c->trace);
+  if (c->trace_cursor) cudaFree(c->trace_cursor);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   delete c;
+  return AO_OK;
+}
+
+ao_status ao_ctx_trace_enable(ao_ctx* c, int64_t capacity) {
+  if (!c || capacity < 0) return fail(AO_ERR_INVALID_ARG, "bad argument");
+  AO_CUDA(cudaSetDevice(c->device));
+  AO_CUDA(cudaDeviceSynchronize());
+  if (c->trace) cudaFree(c->trace);
+  if (c->trace_cursor) cudaFree(c->trace_cursor);
+  c->trace = nullptr;
+  c->trace_cursor = nullptr;
+  c->trace_cap = 0;
+  if (capacity == 0) return AO_OK;
+  AO_CUDA(cudaMalloc(&c->trace, size_t(capacity) * sizeof(ao::TraceEvent)));
+  AO_CUDA(cudaMalloc(&c->trace_cursor, 4));
+  AO_CUDA(cudaMemset(c->trace_cursor, 0, 4));
+  c->trace_cap = uint32_t(capacity);
+  return AO_OK;
+}
+
+ao_status ao_ctx_trace_dump(ao_ctx* c, const char* path, int64_t* n_events) {
+  static const char* kinds[] = {"?", "wait", "load", "mma", "epilogue", "comm", "reduce", "reduce_wait"};
+  if (!c || !path) return fail(AO_ERR_INVALID_ARG, "bad argument");
+  if (!c->trace) return fail(AO_ERR_STATE, "tracing is not enabled on this ctx");
+  AO_CUDA(cudaSetDevice(c->device));
+  AO_CUDA(cudaDeviceSynchronize());
+  uint32_t n = 0;
+  AO_CUDA(cudaMemcpy(&n, c->trace_cursor, 4, cudaMemcpyDeviceToHost));
+  n = std::min(n, c->trace_cap);
+  std::vector<ao::TraceEvent> ev(n);
+  if (n) AO_CUDA(cudaMemcpy(ev.data(), c->trace, n * sizeof(ao::TraceEvent), cudaMemcpyDeviceToHost));
+  AO_CUDA(cudaMemset(c->trace_cursor, 0, 4));
+  c->trace_seq = 0;
+  uint64_t tmin = ~0ull;
+  for (auto& e : ev) tmin = std::min(tmin, e.t0);
+  FILE* f = fopen(path, "w");
+  if (!f) return fail(AO_ERR_INVALID_ARG, "cannot open %s", path);
+  fprintf(f, "{\"traceEvents\":[");
+  for (uint32_t i = 0; i < n; ++i) {
+    const ao::TraceEvent& e = ev[i];
+    const uint32_t kk = e.kind & 0xff, seq = e.kind >> 8;
+    const char* k = kk < 8 ? kinds[kk] : "?";
+    fprintf(f,
+            "%s{\"name\":\"%s %u\",\"cat\":\"%s\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":%u,\"tid\":%u,"
+            "\"args\":{\"launch\":%u}}",
+            i ? "," : "", k, e.id, k, (e.t0 - tmin) / 1000.0, (e.t1 - e.t0) / 1000.0, e.rank, e.cta * 8 + kk, seq);
+  }
+  fprintf(f, "]}\n");
+  fclose(f);
+  if (n_events) *n_events = n;
   return AO_OK;
 }
 
@@ -608,6 +672,13 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   ka->err = p0->ctx->err_dev;
   ka->skip_wait = int32_t(g_debug.skip_wait);
   ka->delay_ns = uint32_t(g_debug.delay_ns);
+  ka->trace = p0->ctx->trace;
+  ka->trace_cursor = p0->ctx->trace_cursor;
+  ka->trace_cap = p0->ctx->trace_cap;
+  ka->trace_seq = p0->ctx->trace ? p0->ctx->trace_seq++ : 0;
+  ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint)
+                                     : ((h0.desc.intra == AO_INTRA_GROUPED && h0.desc.group_m > 1) ||
+                                        h0.desc.intra == AO_INTRA_COL);
   const bool ce = mode == ao::MODE_AG && h0.desc.backend == AO_BACKEND_CE && h0.W > 1;
   const int comm = mode == ao::MODE_AG ? p0->comm_kind : ao::COMM_NONE;
   ka->comm_ctas_per_rank = (comm != ao::COMM_NONE) ? h0.desc.comm_ctas : 0;
@@ -623,30 +694,60 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   if (ce) {
     ao_status s = get_driver(&drv);
     if (s != AO_OK) return s;
-    // CE backend: every source rank pushes its chunks in plan order on its side stream.
+    // CE backend (Fig.7a): every source rank pushes its chunks in plan order with
+    // peer memcpys, each followed by a 4-byte copy of the epoch into the destination's flag
+    // word.  The per-rank copy chains (one branch per rank of the group) are recorded once
+    // per (parity, buffers) as a CUDA graph, so a call costs three host operations.
+    ao_ctx* c0 = p0->ctx;
+    const uint32_t par = epochs[0] & 1;
+    std::vector<uintptr_t> key{uintptr_t(par), uintptr_t(n)};
     for (int i = 0; i < n; ++i) {
-      ao_plan* p = plans[i];
-      ao_ctx* c = p->ctx;
-      const ao::HostPlan& hp = p->hp;
-      const uint32_t par = epochs[i] & 1;
-      AO_CUDA(cudaEventRecord(c->ev_start, stream));
-      AO_CUDA(cudaStreamWaitEvent(c->side, c->ev_start, 0));
-      const int64_t row_bytes = hp.K * 2;
-      for (const ao::P2POp& op : hp.plans[hp.rank]) {
-        const int g = int(op.row0 / hp.C);
-        const char* src = static_cast<const char*>(As[i]) + (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes;
-        char* dst = c->data(op.peer, par) + op.row0 * row_bytes;
-        if (row_bytes > 0) AO_CUDA(cudaMemcpyAsync(dst, src, size_t(op.rows * row_bytes), cudaMemcpyDeviceToDevice, c->side));
-        CUresult r = drv->write32(c->side, reinterpret_cast<CUdeviceptr>(c->flags(op.peer, par) + g), epochs[i], 0);
-        if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
-      }
-      AO_CUDA(cudaEventRecord(c->ev_done, c->side));
+      key.push_back(reinterpret_cast<uintptr_t>(plans[i]));
+      key.push_back(reinterpret_cast<uintptr_t>(As[i]));
     }
+    cudaGraphExec_t exec = nullptr;
+    auto it = p0->ce_graphs.find(key);
+    if (it != p0->ce_graphs.end()) {
+      exec = it->second;
+    } else {
+      cudaGraph_t graph;
+      AO_CUDA(cudaGraphCreate(&graph, 0));
+      for (int i = 0; i < n; ++i) {
+        ao_plan* p = plans[i];
+        ao_ctx* c = p->ctx;
+        const ao::HostPlan& hp = p->hp;
+        const int64_t row_bytes = hp.K * 2;
+        cudaGraphNode_t prev = nullptr;
+        for (const ao::P2POp& op : hp.plans[hp.rank]) {
+          const int g = int(op.row0 / hp.C);
+          const char* src = static_cast<const char*>(As[i]) + (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes;
+          char* dst = c->data(op.peer, par) + op.row0 * row_bytes;
+          cudaGraphNode_t data = nullptr, flag = nullptr;
+          if (row_bytes > 0) {
+            AO_CUDA(cudaGraphAddMemcpyNode1D(&data, graph, prev ? &prev : nullptr, prev ? 1 : 0, dst, src,
+                                             size_t(op.rows * row_bytes), cudaMemcpyDeviceToDevice));
+            prev = data;
+          }
+          AO_CUDA(cudaGraphAddMemcpyNode1D(&flag, graph, prev ? &prev : nullptr, prev ? 1 : 0,
+                                           c->flags(op.peer, par) + g, c0->epoch_cell, 4, cudaMemcpyDeviceToDevice));
+          prev = flag;
+        }
+      }
+      cudaError_t ge = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ge != cudaSuccess) return fail(AO_ERR_CUDA, "CE graph instantiate: %s", cudaGetErrorString(ge));
+      p0->ce_graphs[key] = exec;
+    }
+    AO_CUDA(cudaEventRecord(c0->ev_start, stream));
+    AO_CUDA(cudaStreamWaitEvent(c0->side, c0->ev_start, 0));
+    CUresult r = drv->write32(c0->side, reinterpret_cast<CUdeviceptr>(c0->epoch_cell), epochs[0], 0);
+    if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
+    AO_CUDA(cudaGraphLaunch(exec, c0->side));
+    AO_CUDA(cudaEventRecord(c0->ev_done, c0->side));
   }
   cudaError_t e = ao::launch_fused(*ka, h0.tile.bn, h0.tile.cg, comm, stream);
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(e));
-  if (ce)
-    for (int i = 0; i < n; ++i) AO_CUDA(cudaStreamWaitEvent(stream, plans[i]->ctx->ev_done, 0));
+  if (ce) AO_CUDA(cudaStreamWaitEvent(stream, p0->ctx->ev_done, 0));
   // optional gathered-A output (bit-exact copy of concat_p A_p)
   if (mode == ao::MODE_AG && Gouts) {
     for (int i = 0; i < n; ++i) {
@@ -717,6 +818,8 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
       d.chunk_rows = int32_t(std::min<int64_t>(M, 1 << 30));
       d.tile_m = bm;
       d.tile_n = bn;
+      d.intra = AO_INTRA_GROUPED;  // GROUP_M swizzle: B tiles reused across 8 row blocks in L2
+      d.group_m = 8;
       s = ao_plan_create_host(&d, sm, &p);
       if (s != AO_OK) return s;
       p->device = device;
@@ -735,6 +838,7 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
   ka->mode = ao::MODE_GEMM;
   ka->timeout_ns = 5000000000ull;
   ka->skip_wait = -1;
+  ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint) : 1;
   ao_status s = fill_rank(&ka->rk[0], p, 0, A, B, C);
   if (s != AO_OK) return s;
   cudaError_t e = ao::launch_fused(*ka, bn, p->hp.tile.cg, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));

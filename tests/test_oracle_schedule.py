@@ -133,12 +133,15 @@ def test_tiny_worked_example_rs():
     assert [c[4] for c in p["chunks"]] == ex["pos"]
     assert all(x == ex["tiles_per_chunk"] for x in p["tiles_per_chunk"])
     assert p["order"] == ex["gemm_order"]
-    assert [it[0] for it in p["reduce_items"]] == ex["reduce_tiles"]
-    for it in p["reduce_items"]:
-        mb = it[0] // 4
-        assert [it[1], it[2]] == ex["reduce_item_chunks"]["mb%d" % mb]
-    # each reduce item waits on its chunks (per CTA first use); all flags of all sources
-    assert p["contrib"] == [2, 2, 2, 2, 0, 0, 0, 0]
+    own = [t for t in p["order"] if t // 4 < 2]
+    assert sorted(own) == ex["own_tiles"]
+    assert p["order"][-len(own):] == own  # own rows last
+    for t in own:
+        mb = t // 4
+        assert [p["deps"][t][1], p["deps"][t][2]] == ex["own_tile_chunks"]["mb%d" % mb]
+    p1 = osch.plan(_desc(rank=0, n_cta=1, **d))
+    assert p1["waits"] == [[0, ex["ncta1_waits"]]]
+    assert p["contrib"] == ex["contrib"]
 
 
 SWEEP = []
@@ -174,15 +177,16 @@ def test_invariants(d):
         # arrival positions are injective over remote chunks
         pos = [c[4] for c in p["chunks"] if (d["op"] == "gemm_rs" or c[3] != r)]
         assert len(pos) == len(set(pos))
-        if d["op"] == "gemm_rs":
-            own = [t for t, glo, ghi, _ in p["deps"] if p["chunks"][glo][3] == r]
-            assert sorted(it[0] for it in p["reduce_items"]) == sorted(own)
+        if d["op"] == "gemm_rs" and d["chunk_order"] == "shard_major":
+            own = {t for t, glo, ghi, _ in p["deps"] if p["chunks"][glo][3] == r}
+            assert set(p["order"][len(p["order"]) - len(own):]) == own  # own rows last
 
 
 def _simulate(p, rank, drop=None, seed=0):
-    """Randomized-timing execution of one rank's plan: remote chunks arrive
-    at random times; each CTA runs its positions in order, blocking at its waits.
-    Returns the list of (k, tile, chunk) reads of a chunk before its arrival."""
+    """Randomized-timing execution of one rank's plan: remote chunks (AG) or
+    the other sources' contributions to own chunks (RS) arrive at random times; each CTA
+    runs its positions in order, blocking at its waits.  Returns the reads of a chunk
+    before its arrival."""
     rnd = random.Random(seed)
     is_ag = p["op"] == "ag_gemm"
     arrival = {}
@@ -190,10 +194,10 @@ def _simulate(p, rank, drop=None, seed=0):
         if is_ag:
             arrival[g] = 0.0 if src == rank else rnd.uniform(0, 100) + pos
         else:
-            arrival[g] = rnd.uniform(50, 150) + pos  # all sources' pushes for g done
-    work = [("tile", t) for t in p["order"]] + [("reduce", it[0]) for it in p.get("reduce_items", [])]
+            arrival[g] = rnd.uniform(0, 150) + pos if src == rank else 0.0
     violations = []
     n_cta = p["n_cta"]
+    order = p["order"]
     for cta, waits in p["waits"]:
         ws = {}
         for k, g in waits:
@@ -201,16 +205,15 @@ def _simulate(p, rank, drop=None, seed=0):
                 continue
             ws.setdefault(k, []).append(g)
         now = 0.0
-        for k in range(cta, len(work), n_cta):
+        for k in range(cta, len(order), n_cta):
             for g in ws.get(k, []):
                 now = max(now, arrival[g])
-            kind, t = work[k]
-            need = []
+            t = order[k]
             glo, ghi = p["deps"][t][1], p["deps"][t][2]
-            if is_ag and kind == "tile":
+            if is_ag:
                 need = [g for g in range(glo, ghi + 1) if p["chunks"][g][3] != rank]
-            elif not is_ag and kind == "reduce":
-                need = list(range(glo, ghi + 1))
+            else:
+                need = [g for g in range(glo, ghi + 1) if p["chunks"][g][3] == rank]
             for g in need:
                 if arrival[g] > now:
                     violations.append((k, t, g))

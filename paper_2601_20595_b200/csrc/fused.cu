@@ -126,6 +126,14 @@ __device__ __forceinline__ void trace_event(const KernelArgs& A, uint32_t kind, 
   }
 }
 
+// Fault injection: wait at least delay/2 (+ a hash-dependent part up to delay/2) ns.
+__device__ __noinline__ void inject_delay(uint32_t delay, uint32_t salt) {
+  if (delay == 0) return;
+  const uint64_t target = delay / 2 + (salt * 2654435761u) % (delay / 2 + 1);
+  const uint64_t t0 = globaltimer();
+  while (globaltimer() - t0 < target) __nanosleep(1000);
+}
+
 __device__ __forceinline__ int4 ld_nc_v4(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -147,6 +155,8 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
   uint32_t phase_bits = 0;
   for (int i = worker; i < R.n_comm_items; i += n_workers) {
     const uint64_t t_item = A.trace ? globaltimer() : 0;
+    if (A.delay_ns && lane == 0) inject_delay(A.delay_ns, uint32_t(i));  // fault injection
+    __syncwarp();
     const CommItem it = R.comm_items[i];
     const char* src = R.A_shard + it.src_off;
     char* dst = R.peer_data[it.peer] + it.dst_off;
@@ -203,7 +213,6 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
       __syncwarp();
     }
     if (lane == 0) {
-      if (A.delay_ns) __nanosleep((uint32_t(i) * 2654435761u) % A.delay_ns);
       st_release_sys(R.peer_flags[it.peer] + it.g * R.n_slices + it.slice, R.epoch);
       trace_event(A, TR_COMM, R.rank, worker, i, t_item);
     }
@@ -304,8 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     if (lane == 0) {
       // L2 policy follows the tile order: with grouped / column orders an A row block is
       // reused across every column tile of its group, B tiles only by neighbours in time.
-      const uint64_t pol_b = args.l2_hint ? policy_evict_first() : policy_evict_last();
-      const uint64_t pol_a = args.l2_hint ? policy_evict_last() : policy_evict_first();
+      // l2_hint: 0 A first / B last, 1 A last / B first, 2 A last / B normal, 3 both normal
+      const int h = args.l2_hint;
+      const uint64_t pol_b = h == 0 ? policy_evict_last() : (h == 1 ? policy_evict_first() : policy_evict_normal());
+      const uint64_t pol_a = h == 0 ? policy_evict_first() : (h == 3 ? policy_evict_normal() : policy_evict_last());
       uint32_t stage = 0, phase = 0;
       int wp = 0, we = 0;
       if constexpr (MODE == MODE_AG) {
@@ -600,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.counters + g) : "memory");
             if (int(old) + 1 == R.tiles_per_chunk[g]) {
               R.counters[g] = 0;
-              if (args.delay_ns) __nanosleep((uint32_t(g) * 2654435761u) % args.delay_ns);
+              if (args.delay_ns) inject_delay(args.delay_ns, uint32_t(g));
               st_release_sys(R.peer_flags[owner] + g * R.W + R.rank, R.epoch);
             }
           }

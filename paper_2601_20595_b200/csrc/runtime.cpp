@@ -677,8 +677,10 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   ka->trace_cap = p0->ctx->trace_cap;
   ka->trace_seq = p0->ctx->trace ? p0->ctx->trace_seq++ : 0;
   ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint)
-                                     : ((h0.desc.intra == AO_INTRA_GROUPED && h0.desc.group_m > 1) ||
-                                        h0.desc.intra == AO_INTRA_COL);
+                                     : (((h0.desc.intra == AO_INTRA_GROUPED && h0.desc.group_m > 1) ||
+                                         h0.desc.intra == AO_INTRA_COL)
+                                            ? 2
+                                            : 0);
   const bool ce = mode == ao::MODE_AG && h0.desc.backend == AO_BACKEND_CE && h0.W > 1;
   const int comm = mode == ao::MODE_AG ? p0->comm_kind : ao::COMM_NONE;
   ka->comm_ctas_per_rank = (comm != ao::COMM_NONE) ? h0.desc.comm_ctas : 0;
@@ -838,7 +840,7 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
   ka->mode = ao::MODE_GEMM;
   ka->timeout_ns = 5000000000ull;
   ka->skip_wait = -1;
-  ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint) : 1;
+  ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint) : 2;
   ao_status s = fill_rank(&ka->rk[0], p, 0, A, B, C);
   if (s != AO_OK) return s;
   cudaError_t e = ao::launch_fused(*ka, bn, p->hp.tile.cg, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));

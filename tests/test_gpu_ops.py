@@ -61,7 +61,8 @@ def test_gemm_large_sampled(ao):
 # ------------------------------------------------------------------------ AG-GEMM loopback
 def _ag_world(ao, W, M, N, K, chunk, backend, **kw):
     desc = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=chunk, backend=backend,
-                n_cta=max(1, 148 // W) if "n_cta" not in kw else kw.pop("n_cta"), timeout_ns=2_000_000_000, **kw)
+                n_cta=max(1, 148 // W), timeout_ns=2_000_000_000)
+    desc.update(kw)
     ws = ao.workspace_bytes(desc)
     ctxs = ao.loopback_world(0, W, ws)
     plans = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
@@ -181,3 +182,85 @@ def test_gemm_rs_ragged(ao):
     B64 = [si.to_f64(b) for b in B]
     for r in range(W):
         _check(Cs[r], on.gemm_rs(A64, B64, r), f"rs ragged r{r}")
+
+
+# ------------------------------------------------------------------------ failure paths
+@pytest.mark.parametrize("backend", ["ldst", "tma"])
+def test_wait_mutation_is_detected_and_delays_are_safe(ao, backend):
+    """Fault injection: random per-transfer delays never break results; skipping
+    one chunk wait while transfers are delayed is caught by the provenance decode."""
+    W, M, K, N = 2, 512, 64, 256
+    # chunk = tile rows: the first remote tile of rank 0 / worker 0 waits on exactly one chunk
+    ctxs, plans = _ag_world(ao, W, M, N, K, 128, backend, tile_m=128, tile_n=128, n_cta=4)
+
+    def decode_ok(Cs):
+        ok = True
+        for r in range(W):
+            c = Cs[r].float().cpu()
+            rid = c[:, 0] + 32 * c[:, 1] + 1024 * c[:, 2]
+            ok &= bool(torch.equal(rid, torch.arange(M, dtype=torch.float32)))
+        return ok
+
+    try:
+        ao.debug_set("delay_ns", 1_000_000)
+        A, B = si.ag_provenance_inputs(W, M, K, N, epoch=1)
+        Cs, _ = _run_ag(ao, ctxs, plans, _dev(A), _dev(B))
+        assert decode_ok(Cs), "delayed transfers must not change the result"
+        ao.debug_set("skip_wait", 0)  # rank 0, worker 0: its first chunk wait is dropped
+        A, B = si.ag_provenance_inputs(W, M, K, N, epoch=2)
+        Cs, _ = _run_ag(ao, ctxs, plans, _dev(A), _dev(B))
+        assert not decode_ok(Cs), "a dropped wait must be observable (mutation kill)"
+    finally:
+        ao.debug_set("skip_wait", -1)
+        ao.debug_set("delay_ns", 0)
+    A, B = si.ag_provenance_inputs(W, M, K, N, epoch=3)
+    Cs, _ = _run_ag(ao, ctxs, plans, _dev(A), _dev(B))
+    assert decode_ok(Cs), "recovers once the mutation is removed"
+
+
+def test_device_timeout_is_reported(ao):
+    """A rank whose peer never runs must not hang: the bounded spin records the first
+    expired wait and ao_ctx_check_async reports AO_ERR_TIMEOUT."""
+    W, M, K, N = 2, 512, 64, 256
+    ctxs, plans = _ag_world(ao, W, M, N, K, 128, "ce", tile_m=128, tile_n=128, n_cta=2, timeout_ns=20_000_000)
+    A, B = si.ag_provenance_inputs(W, M, K, N)
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    ao.ag_gemm_group(plans[:1], [A[0].cuda()], [B[0].cuda()], [C])  # rank 1 never pushes
+    torch.cuda.synchronize()
+    with pytest.raises(ao.AOError, match="TIMEOUT"):
+        ctxs[0].check_async()
+    ctxs[0].check_async()  # the error is reported once
+
+
+def test_boundary_rejects_bad_calls(ao):
+    W, M, K, N = 2, 512, 64, 256
+    desc = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=64, n_cta=8)
+    ctxs = ao.loopback_world(0, W, 4 * ao.workspace_bytes(desc))
+    with pytest.raises(ao.AOError, match="INVALID_ARG"):
+        ao.Plan(ctxs[0], dict(desc, rank=1))  # desc rank != ctx rank
+    with pytest.raises(ao.AOError, match="INVALID_ARG"):
+        ao.Plan(ctxs[0], dict(desc, rank=0, chunk_rows=96))  # S % chunk_rows
+    with pytest.raises(ao.AOError, match="INVALID_ARG"):
+        ao.Plan(ctxs[0], dict(desc, rank=0, M=8 * M))  # workspace too small
+    p0 = ao.Plan(ctxs[0], dict(desc, rank=0))
+    p1 = ao.Plan(ctxs[1], dict(desc, rank=1, chunk_rows=128))
+    A = [torch.zeros(M // W, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    B = [torch.zeros(N, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    C = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    with pytest.raises(ao.AOError, match="PEER"):
+        ao.ag_gemm_group([p0, p1], A, B, C)  # plans of one world must agree (hash)
+    rs = ao.Plan(ctxs[0], dict(desc, rank=0, op="gemm_rs", N=64))
+    with pytest.raises(ao.AOError, match="INVALID_ARG"):
+        ao.ag_gemm(rs, A[0], B[0], C[0])  # op mismatch
+
+
+def test_empty_problem_is_a_noop(ao):
+    W = 2
+    desc = dict(op="ag_gemm", world_size=W, M=0, N=256, K=64, chunk_rows=64, n_cta=8)
+    ctxs = ao.loopback_world(0, W, 1 << 20)
+    plans = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
+    z = [torch.empty(0, 64, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    B = [torch.zeros(256, 64, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    C = [torch.empty(0, 256, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    ao.ag_gemm_group(plans, z, B, C)
+    torch.cuda.synchronize()

@@ -66,7 +66,7 @@ __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm) {
   L.off_comm = L.off_stg + 4 * kStageWarpBytes;
   const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : 0;
   L.off_bar = L.off_comm + comm;
-  const uint32_t nbars = 2 * C_::kStages + 4 + 8 * kCommBufs;
+  const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs;
   L.off_slot = L.off_bar + nbars * 8;
   L.total = L.off_slot + 16 + 1024;  // + alignment slack
   return L;
@@ -220,6 +220,15 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
   }
 }
 
+// RS: 32-column blocks of tile column nb that hold valid columns (the streamed peer
+// partial boxes of an own tile).
+template <int BN>
+__device__ __forceinline__ int rs_blocks(int nb, int64_t N) {
+  const int64_t rem = N - int64_t(nb) * BN;
+  const int64_t nbx = (rem + 31) / 32;
+  return int(nbx < BN / 32 ? nbx : BN / 32);
+}
+
 template <int BN, int MODE, int COMM, int CG>
 __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constant__ KernelArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -267,18 +276,23 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   uint64_t* tfull = empty + C_::kStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* commbars = tempty + 2;
+  uint64_t* pfull = commbars + 8 * kCommBufs;  // RS: ring stages carrying peer partials
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.off_slot);
 
-  if (warp == 0 && lane == 0 && R.K > 0) {
-    prefetch_tmap(&R.tmA);
-    prefetch_tmap(&R.tmB);
-    if (MODE == MODE_AG) prefetch_tmap(&R.tmA_loc);
+  if (warp == 0 && lane == 0) {
+    if (R.K > 0) {
+      prefetch_tmap(&R.tmA);
+      prefetch_tmap(&R.tmB);
+      if (MODE == MODE_AG) prefetch_tmap(&R.tmA_loc);
+    }
+    if (MODE == MODE_RS && R.W > 1) prefetch_tmap(&R.tmA_loc);
   }
   if (warp == 1) {
     if (lane == 0) {
       for (int s = 0; s < C_::kStages; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
+        mbar_init(&pfull[s], 1);
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
@@ -319,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       const uint64_t pol_a = h == 0 ? policy_evict_first() : (h == 3 ? policy_evict_normal() : policy_evict_last());
       uint32_t stage = 0, phase = 0;
       int wp = 0, we = 0;
-      if constexpr (MODE == MODE_AG) {
+      if constexpr (MODE != MODE_GEMM) {
         wp = R.wait_off[wk];
         we = R.wait_off[wk + 1];
       }
@@ -368,6 +382,40 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             phase ^= 1;
           }
         }
+        if constexpr (MODE == MODE_RS) {
+          // RS-4: an own tile's epilogue fuses the peer reduction; stream the W-1 peer
+          // partials of this CTA's 128 rows through the same smem ring (32-column fp32
+          // boxes) once the peers' flags for its chunks are released.
+          const int64_t sub0 = int64_t(mb) * BM + int64_t(crank) * kSubM;
+          if (R.W > 1 && sub0 / S == R.rank) {
+            const uint64_t tw = args.trace ? globaltimer() : 0;
+            while (wp < we && R.waits[wp].x == k) {
+              const int g = R.waits[wp].y;
+              if (!(grp == 0 && wp == args.skip_wait)) {
+                for (int s = 0; s < R.W; ++s)
+                  if (s != R.rank) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, lcta, g);
+              }
+              ++wp;
+            }
+            fence_proxy_async_global();  // peers' generic-proxy stores -> TMA reads
+            trace_event(args, TR_REDWAIT, R.rank, lcta, t, tw);
+            const int lr0 = int(sub0 - int64_t(R.rank) * S);
+            const int nvb = rs_blocks<BN>(nb, N);
+            for (int cb = 0; cb < nvb; ++cb) {
+              for (int s = 0; s < R.W; ++s) {
+                if (s == R.rank) continue;
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_arrive_expect_tx(&pfull[stage], kSubM * 128);  // own CTA's barrier
+                tma_load_2d(sA + stage * C_::kStageA, &R.tmA_loc, &pfull[stage], nb * BN + cb * 32,
+                            int(s * S) + lr0, pol_b);
+                if (++stage == C_::kStages) {
+                  stage = 0;
+                  phase ^= 1;
+                }
+              }
+            }
+          }
+        }
         trace_event(args, TR_LOAD, R.rank, lcta, t, t_load);
       }
     }
@@ -375,14 +423,17 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     // ================================================================ MMA issuer
     if (leader) {
       constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      // full[] completes only on operand uses of a slot (RS partial stages use pfull[]),
+      // so its parity is tracked per slot.
+      uint32_t stage = 0, fpar = 0, acc = 0, acc_phase = 0;
       for (int k = wk; k < n_tiles; k += n_wk) {
         const uint64_t t_mma = args.trace ? globaltimer() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(&full[stage], (fpar >> stage) & 1u);
+          fpar ^= 1u << stage;
           tc_fence_after();
           if (lane == 0) {
             const uint64_t ad = make_smem_desc_sw128(smem_u32(sA + stage * C_::kStageA));
@@ -400,10 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
               mma_commit(&empty[stage]);
           }
           __syncwarp();
-          if (++stage == C_::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+          if (++stage == C_::kStages) stage = 0;
         }
         if (lane == 0) {
           if constexpr (CG == 2)
@@ -413,6 +461,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           trace_event(args, TR_MMA, R.rank, lcta, R.order[k], t_mma);
         }
         __syncwarp();
+        if constexpr (MODE == MODE_RS) {  // ring stages carrying peer partials belong to the epilogue
+          const int t = R.order[k];
+          const int mb = t / R.n_nb;
+          if (R.W > 1 && (int64_t(mb) * BM) / S == R.rank) {
+            const int skip = rs_blocks<BN>(t - mb * R.n_nb, N) * (R.W - 1);
+            stage = (stage + uint32_t(skip)) % C_::kStages;
+          }
+        }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -429,15 +485,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     constexpr int EPS = (MODE == MODE_RS) ? 4 : 8;   // elements per 16-byte lane segment
     constexpr int EB = (MODE == MODE_RS) ? 4 : 2;    // bytes per output element
     uint32_t acc = 0, acc_phase = 0;
-    int wp = 0, we = 0;  // RS: this worker's wait list (own tiles)
-    if constexpr (MODE == MODE_RS) {
-      wp = R.wait_off[wk];
-      we = R.wait_off[wk + 1];
-    }
+    uint32_t rs_stage = 0, ppar = 0;  // RS: replay of the producer's ring position, pfull parities
     for (int k = wk; k < n_tiles; k += n_wk) {
       const int t = R.order[k];
       const int mb = t / R.n_nb;
       const int nb = t - mb * R.n_nb;
+      if constexpr (MODE == MODE_RS)  // operand stages of this tile (consumed by the MMA)
+        rs_stage = (rs_stage + uint32_t(nkb)) % C_::kStages;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint64_t t_epi = args.trace ? globaltimer() : 0;
@@ -458,93 +512,67 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       }
       if constexpr (MODE == MODE_RS) {
         if (own_tile) {
-          // RS-4 fused reduction: wait for the other sources' partials of this tile's chunks
-          if (etid == 0) {
-            while (wp < we && R.waits[wp].x == k) {
-              const int g = R.waits[wp].y;
-              const uint64_t tw = args.trace ? globaltimer() : 0;
-              if (!(grp == 0 && wp == args.skip_wait)) {
-                for (int s = 0; s < R.W; ++s)
-                  if (s != R.rank) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, lcta, g);
-              }
-              trace_event(args, TR_REDWAIT, R.rank, lcta, g, tw);
-              ++wp;
-            }
-          }
-          named_bar_sync(1, 128);
-          // Coalesced layout: stage the own accumulator (thread = row) through smem, then
-          // lane l handles rows (i*4 + l/8), columns 4*(l%8)..+3 for i = 0..7, so every
-          // peer-slot load and the bf16 store are 8 lanes x 16 B along one row.
-          const int64_t lrow0 = row0 - int64_t(R.rank) * S;  // first row of this warp in C_shard
-          const float* slots = reinterpret_cast<const float*>(R.peer_data[R.rank]);
-          const int64_t slot_stride = S * N;  // floats
-          __nv_bfloat16* cout = reinterpret_cast<__nv_bfloat16*>(R.C);
-          const int c = lane & 7;
+          // RS-4 fused reduction: the peer partials arrive as 32-column fp32 boxes in the
+          // smem ring (streamed by the producer); thread = row, like the TMEM accumulator.
+          // Sum in ascending source rank, own TMEM value at s == rank, store bf16.
+          const int r = q * 32 + lane;  // row inside this CTA's 128-row half
+          const int nvb = rs_blocks<BN>(nb, N);
+          char* crow0 = reinterpret_cast<char*>(R.C) + (row0 - int64_t(R.rank) * S) * N * 2;
 #pragma unroll 1
-          for (int cc = 0; cc < BN; cc += 32) {
-            const int64_t col0 = col_base + cc;
-            if (col0 >= N) break;  // warp-uniform
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(tb + cc, v);
-            tmem_wait_ld();
-            if (nkb == 0) {
+          for (int cb = 0; cb < nvb; ++cb) {
+            float acc[32];
+            for (int s = 0; s < R.W; ++s) {
+              float x[32];
+              if (s == R.rank) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tb + cb * 32, v);
+                tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0u;
-            }
+                for (int i = 0; i < 32; ++i) x[i] = nkb ? __uint_as_float(v[i]) : 0.f;
+              } else {
+                mbar_wait(&pfull[rs_stage], (ppar >> rs_stage) & 1u);
+                ppar ^= 1u << rs_stage;
+                const uint4* box = reinterpret_cast<const uint4*>(sA + rs_stage * C_::kStageA);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            __syncwarp();
-            const bool ok = col0 + 4 * c < N;
-            float4 own[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = i * 4 + (lane >> 3);
-              const uint4 w = stg[r * 8 + (c ^ (r & 7))];
-              own[i] = make_float4(__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z), __uint_as_float(w.w));
-            }
-            __syncwarp();
-            float4 acc[8];
-            const int64_t base_off = (lrow0 + (lane >> 3)) * N + col0 + 4 * c;  // row i*4 + lane/8 adds i*4*N
-            // ascending source rank; own contribution at s == rank; two slots in flight
-            for (int s0 = 0; s0 < R.W; s0 += 2) {
-              float4 ld[2][8];
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int s = s0 + u;
-                if (s < R.W && s != R.rank && ok) {
-                  const float* src = slots + s * slot_stride + base_off;
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) ld[u][i] = __ldcg(reinterpret_cast<const float4*>(src + int64_t(i) * 4 * N));
+                for (int j = 0; j < 8; ++j) {
+                  const uint4 w = box[r * 8 + (j ^ (r & 7))];  // TMA 128-B swizzle
+                  x[4 * j] = __uint_as_float(w.x);
+                  x[4 * j + 1] = __uint_as_float(w.y);
+                  x[4 * j + 2] = __uint_as_float(w.z);
+                  x[4 * j + 3] = __uint_as_float(w.w);
                 }
+                named_bar_sync(1, 128);  // every epilogue thread has read the stage
+                if (etid == 0) mbar_arrive(&empty[rs_stage]);
+                if (++rs_stage == C_::kStages) rs_stage = 0;
               }
+              if (s == 0) {
 #pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int s = s0 + u;
-                if (s >= R.W) break;
+                for (int i = 0; i < 32; ++i) acc[i] = x[i];
+              } else {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const float4 x = (s == R.rank) ? own[i] : ld[u][i];
-                  if (s == 0) {
-                    acc[i] = x;
-                  } else {
-                    acc[i].x += x.x;
-                    acc[i].y += x.y;
-                    acc[i].z += x.z;
-                    acc[i].w += x.w;
-                  }
-                }
+                for (int i = 0; i < 32; ++i) acc[i] += x[i];
               }
             }
-            if (ok) {
+            // bf16 pack, stage row `lane` (64 B) through the transpose buffer, store
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                uint2 o;
-                o.x = pack_bf16x2(acc[i].x, acc[i].y);
-                o.y = pack_bf16x2(acc[i].z, acc[i].w);
-                *reinterpret_cast<uint2*>(cout + base_off + int64_t(i) * 4 * N) = o;
-              }
+            for (int j = 0; j < 4; ++j) {
+              const uint4 w = make_uint4(pack_bf16x2(acc[8 * j], acc[8 * j + 1]), pack_bf16x2(acc[8 * j + 2], acc[8 * j + 3]),
+                                         pack_bf16x2(acc[8 * j + 4], acc[8 * j + 5]),
+                                         pack_bf16x2(acc[8 * j + 6], acc[8 * j + 7]));
+              stg[lane * 4 + (j ^ ((lane >> 1) & 3))] = w;
             }
+            __syncwarp();
+            const int64_t col0 = col_base + cb * 32;
+            const int c = lane & 3;
+            const bool ok = col0 + 8 * c < N;
+            char* colp = crow0 + (col0 + 8 * c) * 2;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int rr = i * 8 + (lane >> 2);
+              const uint4 w = stg[rr * 4 + (c ^ ((rr >> 1) & 3))];
+              if (ok) st_v4(reinterpret_cast<int4*>(colp + rr * N * 2), make_int4(w.x, w.y, w.z, w.w));
+            }
+            __syncwarp();
           }
         }
       }

@@ -33,7 +33,7 @@ struct CommItem {
 
 struct alignas(64) RankArgs {
   CUtensorMap tmA;      // AG: gathered buffer (current parity) [M, K]; RS/GEMM: A [M, K]
-  CUtensorMap tmA_loc;  // AG: local shard [S, K]
+  CUtensorMap tmA_loc;  // AG: local shard [S, K].  RS: this rank's slots [W*S, N] fp32 (32 x 128 boxes)
   CUtensorMap tmB;      // B [N, K]
   const int* order;            // [n_tiles] tile ids in execution order
   const int* wait_off;         // [n_cta + 1] CSR offsets into waits

@@ -222,17 +222,19 @@ ao_status upload_tables(ao_plan* p) {
   return AO_OK;
 }
 
-ao_status encode_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+ao_status encode_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows, bool fp32 = false) {
   DriverFns* drv;
   ao_status s = get_driver(&drv);
   if (s != AO_OK) return s;
+  const int eb = fp32 ? 4 : 2;
   cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
-  cuuint32_t box[2] = {cuuint32_t(ao::kBK), cuuint32_t(box_rows)};
+  cuuint64_t strides[1] = {cuuint64_t(cols) * eb};
+  cuuint32_t box[2] = {cuuint32_t(128 / eb), cuuint32_t(box_rows)};  // 128-byte inner box (swizzle span)
   cuuint32_t es[2] = {1, 1};
-  CUresult r = drv->encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = drv->encode(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(AO_ERR_INVALID_ARG, "cuTensorMapEncodeTiled failed (%d) for %p [%lld x %lld]", int(r), ptr,
                 (long long)rows, (long long)cols);
@@ -310,7 +312,12 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
       s = encode_2d(&R->tmA, A, hp.M, hp.K, 128);
       if (s != AO_OK) return s;
     }
+
     s = encode_2d(&R->tmB, B, hp.N, hp.K, bn / hp.tile.cg);
+    if (s != AO_OK) return s;
+  }
+  if (!hp.is_ag && ctx && hp.W > 1 && hp.N > 0 && hp.S > 0) {  // RS: peer partial slots, streamed by the producer
+    s = encode_2d(&R->tmA_loc, R->peer_data[hp.rank], int64_t(hp.W) * hp.S, hp.N, 128, true);
     if (s != AO_OK) return s;
   }
   R->C = C;

@@ -43,6 +43,10 @@ import math
 # (BM, BN, cta_group).  Shared *specification* with the C++ planner (Q19);
 # each side types it independently.
 TILE_CANDIDATES = [(256, 256, 2), (256, 128, 2), (128, 256, 1), (128, 128, 1)]
+# Relative mainloop efficiency (percent) of each candidate, measured on B200 with the plain
+# GEMM 8192x14336x4096 (profiles/r01: 1440 / 974 / 1275 / ~860 TFLOP/s).  Planner spec
+# constant shared with the C++ planner (Q19).
+TILE_EFF = {(256, 256, 2): 100, (256, 128, 2): 68, (128, 256, 1): 88, (128, 128, 1): 60}
 
 BK = 64  # K-block of the mainloop (TMA 128-B swizzle => 64 bf16), DESIGN.md
 
@@ -113,9 +117,11 @@ def n_workers(desc, sm_count):
 
 
 def pick_tile(desc, sm_count):
-    """Tile shape: explicit, else argmax of wave-quantization utilization
-    util = T / (ceil(T/n) * n) (Fig.2a), ties -> larger BM*BN, then BN.
-    Enumerates every candidate (brute force over the candidate list)."""
+    """Tile shape: explicit, else the candidate with the least estimated time
+    waves * (per-SM tile area) / efficiency, waves = ceil(T / n) -- wave quantization
+    (Fig.2a) weighted by the measured per-shape efficiency (Q19).  Exact
+    rational comparison; ties -> larger BM*BN, then larger BN.  Enumerates every candidate."""
+    from fractions import Fraction
     W, M, N = desc["world_size"], desc["M"], desc["N"]
     S = M // W
     cands = TILE_CANDIDATES
@@ -127,8 +133,9 @@ def pick_tile(desc, sm_count):
             continue
         n = max(1, n_workers(desc, sm_count) // cg)
         T = (M // bm) * _ceil_div(N, bn)
-        util = (T / (_ceil_div(T, n) * n)) if T > 0 else 1.0
-        key = (util, bm * bn, bn)
+        waves = _ceil_div(T, n)
+        cost = Fraction(waves * (bm * bn // cg), TILE_EFF[(bm, bn, cg)])
+        key = (-cost, bm * bn, bn)
         if best is None or key > best[0]:
             best = (key, (bm, bn, cg))
     return None if best is None else best[1]

@@ -10,6 +10,9 @@
 namespace ao {
 
 const TileShape kTileCandidates[] = {{256, 256, 2}, {256, 128, 2}, {128, 256, 1}, {128, 128, 1}};
+// Relative mainloop efficiency (percent) per candidate, measured on B200 (plain GEMM
+// 8192x14336x4096; Q19).
+static const int kTileEff[] = {100, 68, 88, 60};
 const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[0]);
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -59,24 +62,33 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   return v;
 }
 
-// Q19: explicit tile, else argmax of util = T / (ceil(T/n) * n);
-// ties -> larger BM*BN, then larger BN.
+// Q19: explicit tile, else the least estimated time waves * (per-SM area) / efficiency,
+// waves = ceil(T / n); exact comparison by cross-multiplication; ties ->
+// larger BM*BN, then larger BN.
 bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
   const int64_t S = d.M / d.world_size;
   bool have = false;
-  double best_u = -1;
-  int64_t best_area = -1, best_bn = -1;
+  int64_t best_num = 0, best_eff = 1, best_area = -1, best_bn = -1;
   for (int i = 0; i < kNumTileCandidates; ++i) {
     const TileShape c = kTileCandidates[i];
     if (d.tile_m != 0 && !(c.bm == d.tile_m && c.bn == d.tile_n)) continue;
     if (S % c.bm != 0) continue;
     const int64_t n = std::max(1, workers(d, sm_count) / c.cg);
     const int64_t T = (d.M / c.bm) * ceil_div(d.N, c.bn);
-    const double u = T > 0 ? double(T) / double(ceil_div(T, n) * n) : 1.0;
+    const int64_t num = ceil_div(T, n) * (int64_t(c.bm) * c.bn / c.cg);  // cost = num / eff
+    const int64_t eff = kTileEff[i];
     const int64_t area = int64_t(c.bm) * c.bn;
-    if (!have || std::make_tuple(u, area, int64_t(c.bn)) > std::make_tuple(best_u, best_area, best_bn)) {
+    bool better;
+    if (!have) {
+      better = true;
+    } else {
+      const int64_t lhs = num * best_eff, rhs = best_num * eff;  // cost < best_cost
+      better = lhs < rhs || (lhs == rhs && std::make_tuple(area, int64_t(c.bn)) > std::make_tuple(best_area, best_bn));
+    }
+    if (better) {
       have = true;
-      best_u = u;
+      best_num = num;
+      best_eff = eff;
       best_area = area;
       best_bn = c.bn;
       *out = c;

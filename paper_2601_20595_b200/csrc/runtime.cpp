@@ -104,6 +104,7 @@ struct DebugKnobs {
   int64_t skip_wait = -1;
   int64_t delay_ns = 0;
   int64_t l2_hint = -1;  // -1: follow the plan's tile order
+  int64_t gemm_group_m = 16;  // ao_gemm GROUP_M (measured best)
 };
 DebugKnobs g_debug;
 
@@ -356,6 +357,7 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   if (!strcmp(key, "skip_wait")) g_debug.skip_wait = value;
   else if (!strcmp(key, "delay_ns")) g_debug.delay_ns = value;
   else if (!strcmp(key, "l2_hint")) g_debug.l2_hint = value;
+  else if (!strcmp(key, "gemm_group_m")) g_debug.gemm_group_m = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
   return AO_OK;
 }
@@ -799,7 +801,7 @@ ao_status ao_gemm_rs(ao_plan* plan, const void* A, const void* B, void* C_shard,
 ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int32_t tile_m,
                   int32_t tile_n, void* stream_v) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int>, ao_plan*> cache;
+  static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int, int>, ao_plan*> cache;
   const int bm = tile_m ? tile_m : (M % 256 == 0 ? 256 : 128);
   if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256) || M % bm != 0 || N % 8 != 0 || K % 8 != 0)
     return fail(AO_ERR_INVALID_ARG, "ao_gemm needs M %% tile_m == 0, N %% 8 == 0, K %% 8 == 0 (M=%lld N=%lld K=%lld)",
@@ -811,7 +813,7 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
   ao_plan* p = nullptr;
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(device, M, N, K, bm, bn);
+    auto key = std::make_tuple(device, M, N, K, bm, bn, int(g_debug.gemm_group_m));
     auto it = cache.find(key);
     if (it != cache.end()) {
       p = it->second;
@@ -827,8 +829,8 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
       d.chunk_rows = int32_t(std::min<int64_t>(M, 1 << 30));
       d.tile_m = bm;
       d.tile_n = bn;
-      d.intra = AO_INTRA_GROUPED;  // GROUP_M swizzle: B tiles reused across 8 row blocks in L2
-      d.group_m = 8;
+      d.intra = AO_INTRA_GROUPED;  // GROUP_M swizzle: B tiles reused across row blocks in L2
+      d.group_m = int32_t(g_debug.gemm_group_m);
       s = ao_plan_create_host(&d, sm, &p);
       if (s != AO_OK) return s;
       p->device = device;

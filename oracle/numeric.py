@@ -104,6 +104,16 @@ def gemm_rs_rows(As, Bs, rank: int, local_rows):
     return acc
 
 
+def gemm_rs_from_rows(A_rows, Bs):
+    """GEMM-RS output rows given, for every source s, the same rows of A_s (already
+    selected): sum_s A_rows[s] . B_s^T in ascending s."""
+    acc = None
+    for a, b in zip(A_rows, Bs):
+        p = gemm(a, b)
+        acc = p if acc is None else acc + p
+    return acc
+
+
 def check_tolerance(gpu, ref, elem_rel=1e-2, frob_rel=2e-3):
     """BASELINE.json north star acceptance: per element |gpu - oracle| <= 1e-2 *
     max(1, |oracle|) and relative Frobenius error <= 2e-3.  Returns (ok, max_elem, frob)."""

@@ -1,0 +1,113 @@
+"""Full-size parity in the exact launch configuration bench.py times: Llama-3-8B FFN at
+TP=8 (8192 tokens, hidden 4096, ffn 14336), 8 loopback ranks, CE backend, chunk = shard,
+GROUP_M 4, shard-major RS, heuristic tile (256x256 CTA pairs).  The oracle computes sampled
+output rows one by one (every chunk-boundary row + seeded random rows of every rank);
+tolerance as in BASELINE.json."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import numeric as on
+from synthetic import inputs as si
+
+pytestmark = pytest.mark.gpu
+
+W, M, H, F = 8, 8192, 4096, 14336
+
+
+@pytest.fixture(scope="module")
+def ao():
+    from paper_2601_20595_b200 import build
+    build.build(verbose=False)
+    import paper_2601_20595_b200.api as api
+    return api
+
+
+def _rows(S, chunk, rng, extra=6):
+    rows = set()
+    for g0 in range(0, S, chunk):
+        rows.update((g0, g0 + chunk - 1))
+    rows.update(rng.integers(0, S, size=extra).tolist())
+    return np.array(sorted(rows))
+
+
+def _worlds(ao):
+    Fl = F // W
+    base = dict(world_size=W, M=M, chunk_rows=1024, intra="grouped", group_m=4, n_cta=148 // W,
+                timeout_ns=5_000_000_000)
+    ag = dict(base, op="ag_gemm", N=Fl, K=H, backend="ce", n_slices=2)
+    rs = dict(base, op="gemm_rs", N=H, K=Fl, chunk_order="shard_major")
+    ctxs = ao.loopback_world(0, W, max(ao.workspace_bytes(ag), ao.workspace_bytes(rs)))
+    pa = [ao.Plan(ctxs[r], dict(ag, rank=r)) for r in range(W)]
+    pr = [ao.Plan(ctxs[r], dict(rs, rank=r)) for r in range(W)]
+    return ctxs, pa, pr
+
+
+def test_fullsize_ag_and_rs_sampled_vs_oracle(ao):
+    Fl = F // W
+    S = M // W
+    ctxs, pa, pr = _worlds(ao)
+    assert pa[0].info()["tile_m"] == 256 and pa[0].info()["tile_n"] == 256
+    rng = np.random.default_rng(123)
+
+    A, Bu = si.ag_inputs(W, M, H, Fl)
+    dA, dBu = [a.cuda() for a in A], [b.cuda() for b in Bu]
+    Cu = [torch.empty(M, Fl, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    for _ in range(2):  # second call runs on the other epoch parity
+        ao.ag_gemm_group(pa, dA, dBu, Cu)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    A64 = [si.to_f64(a) for a in A]
+    for r in range(W):
+        rows = _rows(M, 1024, rng)
+        ref = on.ag_gemm_rows(A64, si.to_f64(Bu[r]), rows)
+        ok, e, f = on.check_tolerance(Cu[r][torch.as_tensor(rows)].float().cpu().numpy(), ref)
+        assert ok, f"AG rank {r}: elem {e:.3e} frob {f:.3e}"
+    del dA, dBu, Cu, A64
+
+    Ar, Bd = si.rs_inputs(W, M, Fl, H)
+    dAr, dBd = [a.cuda() for a in Ar], [b.cuda() for b in Bd]
+    Cd = [torch.empty(S, H, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    for _ in range(2):
+        ao.gemm_rs_group(pr, dAr, dBd, Cd)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    Bd64 = [si.to_f64(b) for b in Bd]
+    for r in range(W):
+        local = _rows(S, 128, rng, extra=4)
+        grows = r * S + local
+        A_rows = [si.to_f64(Ar[s][torch.as_tensor(grows)]) for s in range(W)]
+        ref = on.gemm_rs_from_rows(A_rows, Bd64)
+        ok, e, f = on.check_tolerance(Cd[r][torch.as_tensor(local)].float().cpu().numpy(), ref)
+        assert ok, f"RS rank {r}: elem {e:.3e} frob {f:.3e}"
+
+
+@pytest.mark.parametrize("W2", [3, 5, 6, 7])
+def test_non_power_of_two_worlds(ao, W2):
+    """W that does not divide the SM count or the tile grid evenly: AG + RS tiny shapes."""
+    Ml, K, N = 256 * W2, 192, 264
+    A, B = si.ag_inputs(W2, Ml, K, N, salt=W2)
+    desc = dict(op="ag_gemm", world_size=W2, M=Ml, N=N, K=K, chunk_rows=64, n_cta=148 // W2,
+                backend="tma", n_slices=2, timeout_ns=2_000_000_000)
+    rsd = dict(op="gemm_rs", world_size=W2, M=Ml, N=N, K=K, chunk_rows=64, n_cta=148 // W2,
+               timeout_ns=2_000_000_000)
+    ctxs = ao.loopback_world(0, W2, max(ao.workspace_bytes(desc), ao.workspace_bytes(rsd)))
+    pa = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W2)]
+    pr = [ao.Plan(ctxs[r], dict(rsd, rank=r)) for r in range(W2)]
+    Cs = [torch.empty(Ml, N, dtype=torch.bfloat16, device="cuda") for _ in range(W2)]
+    ao.ag_gemm_group(pa, [a.cuda() for a in A], [b.cuda() for b in B], Cs)
+    Ar, Br = si.rs_inputs(W2, Ml, K, N, salt=W2)
+    Ds = [torch.empty(Ml // W2, N, dtype=torch.bfloat16, device="cuda") for _ in range(W2)]
+    ao.gemm_rs_group(pr, [a.cuda() for a in Ar], [b.cuda() for b in Br], Ds)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    A64 = [si.to_f64(a) for a in A]
+    Ar64, Br64 = [si.to_f64(a) for a in Ar], [si.to_f64(b) for b in Br]
+    for r in range(W2):
+        ok, e, f = on.check_tolerance(Cs[r].float().cpu().numpy(), on.ag_gemm(A64, si.to_f64(B[r])))
+        assert ok, f"AG W={W2} r{r}: {e:.3e} {f:.3e}"
+        ok, e, f = on.check_tolerance(Ds[r].float().cpu().numpy(), on.gemm_rs(Ar64, Br64, r))
+        assert ok, f"RS W={W2} r{r}: {e:.3e} {f:.3e}"

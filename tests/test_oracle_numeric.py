@@ -144,6 +144,8 @@ def test_sampled_rows_match_full():
     local = [0, 5, 63]
     full = on.gemm_rs(As64, Bs64, 3)
     np.testing.assert_allclose(on.gemm_rs_rows(As64, Bs64, 3, local), full[local], rtol=1e-13, atol=1e-13)
+    g = [3 * (M // W) + i for i in local]
+    np.testing.assert_allclose(on.gemm_rs_from_rows([a[g] for a in As64], Bs64), full[local], rtol=1e-13, atol=1e-13)
 
 
 def test_tolerance_checker_rejects_perturbation():

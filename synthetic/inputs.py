@@ -53,6 +53,12 @@ def rs_inputs(world_size: int, M: int, K_loc: int, N: int, salt: int = 0):
     return A, B
 
 
+def rs_weights(world_size: int, K_loc: int, N: int, salt: int = 0):
+    """Only the weight shards of rs_inputs (same seeds, same values)."""
+    K_total = max(world_size * K_loc, 1)
+    return [_randn((N, K_loc), 2000 + s + salt, 1.0 / math.sqrt(K_total)) for s in range(world_size)]
+
+
 def ag_provenance_inputs(world_size: int, M: int, K: int, N_loc: int, epoch: int = 0):
     """Exact-integer provenance pattern for AG ("Gather semantics").
 

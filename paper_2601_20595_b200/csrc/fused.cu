@@ -96,13 +96,14 @@ __device__ __noinline__ void spin_flag(const uint32_t* p, uint32_t target, const
     v = ld_acquire_sys(p);
     if (v >= target) return;
     if (globaltimer() - t0 > A.timeout_ns) {
-      if (atomicCAS(const_cast<uint32_t*>(&A.err->flag), 0u, 1u) == 0u) {
+      if (atomicCAS(&A.err->claim, 0u, 1u) == 0u) {
         A.err->rank = rank;
         A.err->cta = cta;
         A.err->chunk = g;
         A.err->epoch = target;
         A.err->seen = v;
         __threadfence_system();
+        st_release_sys(const_cast<uint32_t*>(&A.err->flag), 1u);  // publish after the fields
       }
       return;
     }

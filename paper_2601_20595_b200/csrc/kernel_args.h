@@ -18,9 +18,10 @@ enum CommKind : int { COMM_NONE = 0, COMM_TMA = 1, COMM_LDST = 2 };
 
 // Host-mapped record of the first device-side spin timeout.
 struct ErrorInfo {
-  volatile uint32_t flag;
+  volatile uint32_t flag;   // published (set after the fields below are written)
   int32_t rank, cta, chunk;
-  uint32_t epoch, seen, target, pad;
+  uint32_t epoch, seen, target;
+  uint32_t claim;           // first failing thread wins the CAS on this word
 };
 
 // A communication work item of the in-kernel AG backends: copy `bytes` bytes at byte

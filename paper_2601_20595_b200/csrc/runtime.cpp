@@ -53,6 +53,7 @@ ao_status fail(ao_status s, const char* fmt, ...) {
 constexpr size_t kFlagWordsPerParity = size_t(1) << 18;  // 1 MiB of u32 per parity
 constexpr size_t kCounterWords = size_t(1) << 16;
 constexpr uint32_t kBlobMagic = 0x414f5648u;  // "AOVH"
+constexpr size_t kMaxCeGraphs = 16;
 
 // ------------------------------------------------------------------ driver entry points
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -258,6 +259,7 @@ ao_status take_async_error(ao_ctx* ctx) {
   if (ctx && ctx->err_host && ctx->err_host->flag) {
     const ao::ErrorInfo e = *ctx->err_host;
     ctx->err_host->flag = 0;
+    ctx->err_host->claim = 0;
     return fail(AO_ERR_TIMEOUT, "device spin-wait timed out: rank %d cta %d chunk %d epoch %u (flag held %u)", e.rank,
                 e.cta, e.chunk, e.epoch, e.seen);
   }
@@ -693,10 +695,12 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   const bool ce = mode == ao::MODE_AG && h0.desc.backend == AO_BACKEND_CE && h0.W > 1;
   const int comm = mode == ao::MODE_AG ? p0->comm_kind : ao::COMM_NONE;
   ka->comm_ctas_per_rank = (comm != ao::COMM_NONE) ? h0.desc.comm_ctas : 0;
+  // The epoch advances only once the op is actually enqueued (a failed call leaves every
+  // ctx of the group at its previous epoch, so the world stays in step).
   std::vector<uint32_t> epochs(n);
   for (int i = 0; i < n; ++i) {
     ao_ctx* c = plans[i]->ctx;
-    epochs[i] = ++c->epoch;
+    epochs[i] = c->epoch + 1;
     if (epochs[i] != epochs[0]) return fail(AO_ERR_STATE, "ranks of a group disagree on the epoch");
     ao_status s = fill_rank(&ka->rk[i], plans[i], epochs[i], As[i], Bs[i], Cs[i]);
     if (s != AO_OK) return s;
@@ -747,6 +751,11 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
       cudaError_t ge = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       if (ge != cudaSuccess) return fail(AO_ERR_CUDA, "CE graph instantiate: %s", cudaGetErrorString(ge));
+      if (p0->ce_graphs.size() >= kMaxCeGraphs) {  // bounded cache (callers that rotate buffers)
+        AO_CUDA(cudaStreamSynchronize(c0->side));
+        cudaGraphExecDestroy(p0->ce_graphs.begin()->second);
+        p0->ce_graphs.erase(p0->ce_graphs.begin());
+      }
       p0->ce_graphs[key] = exec;
     }
     AO_CUDA(cudaEventRecord(c0->ev_start, stream));
@@ -758,6 +767,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   }
   cudaError_t e = ao::launch_fused(*ka, h0.tile.bn, h0.tile.cg, comm, stream);
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(e));
+  for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
   if (ce) AO_CUDA(cudaStreamWaitEvent(stream, p0->ctx->ev_done, 0));
   // optional gathered-A output (bit-exact copy of concat_p A_p)
   if (mode == ao::MODE_AG && Gouts) {

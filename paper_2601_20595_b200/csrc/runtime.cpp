@@ -695,6 +695,15 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   const bool ce = mode == ao::MODE_AG && h0.desc.backend == AO_BACKEND_CE && h0.W > 1;
   const int comm = mode == ao::MODE_AG ? p0->comm_kind : ao::COMM_NONE;
   ka->comm_ctas_per_rank = (comm != ao::COMM_NONE) ? h0.desc.comm_ctas : 0;
+  {
+    // Persistent spin-waiting CTAs must all be co-resident (1 CTA per SM).
+    const int64_t grid = int64_t(n) * (ka->ctas_per_rank + ka->comm_ctas_per_rank);
+    if (grid > p0->ctx->sm_count)
+      return fail(AO_ERR_INVALID_ARG, "grid of %lld CTAs exceeds the %d SMs: the persistent CTAs would not be "
+                  "co-resident (lower n_cta / comm_ctas)", (long long)grid, p0->ctx->sm_count);
+    if (h0.tile.cg == 2 && (ka->comm_ctas_per_rank % 2) != 0)
+      return fail(AO_ERR_INVALID_ARG, "comm_ctas must be even with CTA-pair tiles (cluster launch)");
+  }
   // The epoch advances only once the op is actually enqueued (a failed call leaves every
   // ctx of the group at its previous epoch, so the world stays in step).
   std::vector<uint32_t> epochs(n);

@@ -264,3 +264,20 @@ def test_empty_problem_is_a_noop(ao):
     C = [torch.empty(0, 256, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
     ao.ag_gemm_group(plans, z, B, C)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("backend", ["tma", "ldst"])
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+def test_ag_gemm_dedicated_comm_ctas(ao, backend, tile):
+    """Fig.7(b) realization: chunk pushes issued by dedicated communication CTAs
+    ("specialized SMs") instead of co-located warps."""
+    W, M, K, N = 2, 1024, 256, 512
+    A, B = si.ag_inputs(W, M, K, N, salt=11)
+    ctxs, plans = _ag_world(ao, W, M, N, K, 128, backend, tile_m=tile[0], tile_n=tile[1], n_cta=64, comm_ctas=8,
+                            n_slices=4)
+    Cs, G = _run_ag(ao, ctxs, plans, _dev(A), _dev(B), gather=True)
+    A64 = [si.to_f64(a) for a in A]
+    full = torch.cat(A, 0)
+    for r in range(W):
+        _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag comm_ctas {backend} r{r}")
+        assert torch.equal(G[r].cpu(), full)

@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--group-m", type=int, default=4)
     ap.add_argument("--rs-chunk", type=int, default=0, help="GEMM-RS chunk rows (0 = --chunk)")
     ap.add_argument("--rs-order", default="shard_major", choices=["shard_major", "chunk_major"])
+    ap.add_argument("--rs-reduce", default="atomic", choices=["slots", "atomic"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baseline", action="store_true")
@@ -137,7 +138,7 @@ def run_ours(args, rank, world, local_rank):
                 group_m=args.group_m)
     ag_desc = dict(base, op="ag_gemm", N=F, K=HIDDEN, backend=args.backend, n_slices=2)
     rs_desc = dict(base, op="gemm_rs", N=HIDDEN, K=F, chunk_order=args.rs_order,
-                   chunk_rows=args.rs_chunk or args.chunk)
+                   chunk_rows=args.rs_chunk or args.chunk, rs_reduce=args.rs_reduce)
     if loop:
         ag_desc["n_cta"] = rs_desc["n_cta"] = sms // W
     ws = max(ao.workspace_bytes(ag_desc), ao.workspace_bytes(rs_desc))
@@ -263,6 +264,7 @@ def run_ours(args, rank, world, local_rank):
                    "tokens": M, "hidden": HIDDEN, "ffn": FFN, "tp": W, "ranks_per_gpu": W if loop else 1,
                    "backend_ag": args.backend, "chunk_rows": args.chunk, "rs_chunk_rows": args.rs_chunk or args.chunk,
                    "intra": args.intra, "group_m": args.group_m, "rs_chunk_order": args.rs_order,
+                   "rs_reduce": args.rs_reduce,
                    "tile": [pa[0].info()["tile_m"], pa[0].info()["tile_n"]], "cta_group": pa[0].info()["cta_group"],
                    "workers_per_rank": pa[0].info()["n_cta"],
                    "ctas_per_rank": pa[0].info()["n_cta"] * pa[0].info()["cta_group"],

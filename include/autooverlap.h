@@ -72,6 +72,12 @@ typedef enum { AO_CHUNK_SHARD_MAJOR = 0, AO_CHUNK_CHUNK_MAJOR = 1 } ao_chunk_ord
 typedef enum { AO_INTRA_ROW = 0, AO_INTRA_COL = 1, AO_INTRA_GROUPED = 2 } ao_intra;
 /* GEMM-RS wire format of the partials.  FP32 is the conforming default (Q14). */
 typedef enum { AO_WIRE_FP32 = 0, AO_WIRE_BF16 = 1 } ao_wire;
+/* GEMM-RS reduction: SLOTS = each source writes its own fp32 slot and the owner's epilogue
+ * sums them in ascending source rank (bitwise deterministic, default); ATOMIC = sources
+ * reduce-add (red.global.add.f32, in the owner's L2 / over NVLink) into one accumulator that
+ * the owner's epilogue adds to its own tile -- 1/(W-1) of the owner-side reads, summation
+ * order not fixed (Q23). */
+typedef enum { AO_RS_SLOTS = 0, AO_RS_ATOMIC = 1 } ao_rs_reduce;
 
 typedef struct ao_ctx ao_ctx;
 typedef struct ao_plan ao_plan;
@@ -105,6 +111,8 @@ typedef struct {
   int32_t n_slices;     /* TMA/LDST: slices (flag words) per chunk; CE uses 1 */
   int32_t rs_wire;      /* ao_wire (RS only) */
   uint64_t timeout_ns;  /* device spin bound (0 = 5 s) */
+  int32_t rs_reduce;    /* ao_rs_reduce (RS only) */
+  int32_t reserved;
 } ao_plan_desc;
 
 /* ---- status / version ---------------------------------------------------------------- */

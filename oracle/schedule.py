@@ -58,7 +58,7 @@ def _ceil_div(a, b):
 def default_desc(**kw):
     d = dict(op="ag_gemm", world_size=2, rank=0, M=512, N=512, K=512, chunk_rows=64,
              backend="ce", dir="push", chunk_order="shard_major", intra="row", group_m=1,
-             tile_m=0, tile_n=0, n_cta=0, comm_ctas=0, n_slices=1)
+             tile_m=0, tile_n=0, n_cta=0, comm_ctas=0, n_slices=1, rs_reduce="slots")
     d.update(kw)
     return d
 
@@ -103,6 +103,8 @@ def validate(desc, sm_count=148):
         v.append("n_cta")
     if desc["n_slices"] < 1 or desc["n_slices"] > 64:
         v.append("n_slices")
+    if desc.get("rs_reduce", "slots") not in ("slots", "atomic"):
+        v.append("rs_reduce")
     if (desc["tile_m"] == 0) != (desc["tile_n"] == 0):
         v.append("tile")
     if desc["tile_m"] and (desc["tile_m"], desc["tile_n"]) not in [(a, b) for a, b, _ in TILE_CANDIDATES]:
@@ -353,6 +355,7 @@ def plan(desc, sm_count=148):
     }
     if not is_ag:
         out["tiles_per_chunk"] = tiles_per_chunk
+        out["rs_reduce"] = desc.get("rs_reduce", "slots")
     return out
 
 

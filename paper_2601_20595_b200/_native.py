@@ -23,6 +23,7 @@ DIRS = {"push": 0, "pull": 1}
 CHUNK_ORDERS = {"shard_major": 0, "chunk_major": 1}
 INTRAS = {"row": 0, "col": 1, "grouped": 2}
 WIRES = {"fp32": 0, "bf16": 1}
+RS_REDUCE = {"slots": 0, "atomic": 1}
 
 
 class AOError(RuntimeError):
@@ -53,6 +54,8 @@ class PlanDesc(ctypes.Structure):
         ("n_slices", ctypes.c_int32),
         ("rs_wire", ctypes.c_int32),
         ("timeout_ns", ctypes.c_uint64),
+        ("rs_reduce", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -141,4 +144,5 @@ def make_desc(d: dict) -> PlanDesc:
     x.n_slices = int(d.get("n_slices", 1))
     x.rs_wire = WIRES[d.get("rs_wire", "fp32")]
     x.timeout_ns = int(d.get("timeout_ns", 0))
+    x.rs_reduce = RS_REDUCE[d.get("rs_reduce", "slots")]
     return x

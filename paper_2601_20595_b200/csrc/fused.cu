@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       // L2 policy follows the tile order: with grouped / column orders an A row block is
       // reused across every column tile of its group, B tiles only by neighbours in time.
       // l2_hint: 0 A first / B last, 1 A last / B first, 2 A last / B normal, 3 both normal
-      const int h = args.l2_hint;
+      const int h = args.l2_hint & 3;
       const uint64_t pol_b = h == 0 ? policy_evict_last() : (h == 1 ? policy_evict_first() : policy_evict_normal());
       const uint64_t pol_a = h == 0 ? policy_evict_first() : (h == 3 ? policy_evict_normal() : policy_evict_last());
       uint32_t stage = 0, phase = 0;
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           // partials of this CTA's 128 rows through the same smem ring (32-column fp32
           // boxes) once the peers' flags for its chunks are released.
           const int64_t sub0 = int64_t(mb) * BM + int64_t(crank) * kSubM;
-          if (R.W > 1 && sub0 / S == R.rank) {
+          if (R.W > 1 && !R.rs_atomic && sub0 / S == R.rank) {
             const uint64_t tw = args.trace ? globaltimer() : 0;
             while (wp < we && R.waits[wp].x == k) {
               const int g = R.waits[wp].y;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         if constexpr (MODE == MODE_RS) {  // ring stages carrying peer partials belong to the epilogue
           const int t = R.order[k];
           const int mb = t / R.n_nb;
-          if (R.W > 1 && (int64_t(mb) * BM) / S == R.rank) {
+          if (R.W > 1 && !R.rs_atomic && (int64_t(mb) * BM) / S == R.rank) {
             const int skip = rs_blocks<BN>(t - mb * R.n_nb, N) * (R.W - 1);
             stage = (stage + uint32_t(skip)) % C_::kStages;
           }
@@ -487,6 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     constexpr int EB = (MODE == MODE_RS) ? 4 : 2;    // bytes per output element
     uint32_t acc = 0, acc_phase = 0;
     uint32_t rs_stage = 0, ppar = 0;  // RS: replay of the producer's ring position, pfull parities
+    int wp_e = 0, we_e = 0;           // RS ATOMIC: the epilogue walks the own-tile waits itself
+    if constexpr (MODE == MODE_RS) {
+      wp_e = R.wait_off[wk];
+      we_e = R.wait_off[wk + 1];
+    }
     for (int k = wk; k < n_tiles; k += n_wk) {
       const int t = R.order[k];
       const int mb = t / R.n_nb;
@@ -507,12 +512,83 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       if constexpr (MODE == MODE_RS) {
         owner = int(sub0 / S);
         own_tile = owner == R.rank;
-        dst_base = R.peer_data[owner] + (int64_t(R.rank) * S + (row0 - int64_t(owner) * S)) * ld_bytes;
+        dst_base = R.rs_atomic ? R.peer_acc[owner] + (row0 - int64_t(owner) * S) * ld_bytes  // reduce-add target
+                               : R.peer_data[owner] + (int64_t(R.rank) * S + (row0 - int64_t(owner) * S)) * ld_bytes;
       } else {
         dst_base = reinterpret_cast<char*>(R.C) + row0 * ld_bytes;
       }
       if constexpr (MODE == MODE_RS) {
-        if (own_tile) {
+        if (own_tile && R.rs_atomic) {
+          // RS-4, ATOMIC: the peers reduce-added their partials into this rank's
+          // accumulator; wait for their chunk flags, then add the accumulator to the TMEM
+          // tile with coalesced loads (own value staged through smem so lane l owns rows
+          // i*4 + l/8, columns 4*(l%8)..+3), store bf16, and re-arm the accumulator (zeros).
+          if (etid == 0) {
+            const uint64_t tw = args.trace ? globaltimer() : 0;
+            while (wp_e < we_e && R.waits[wp_e].x <= k) {
+              const int g = R.waits[wp_e].y;
+              if (!(grp == 0 && wp_e == args.skip_wait)) {
+                for (int s = 0; s < R.W; ++s)
+                  if (s != R.rank) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, lcta, g);
+              }
+              ++wp_e;
+            }
+            trace_event(args, TR_REDWAIT, R.rank, lcta, t, tw);
+          }
+          named_bar_sync(1, 128);
+          const int64_t lrow0 = row0 - int64_t(R.rank) * S;  // this warp's first row in C_shard
+          float* accm = reinterpret_cast<float*>(R.peer_acc[R.rank]);
+          __nv_bfloat16* cout = reinterpret_cast<__nv_bfloat16*>(R.C);
+          const int c = lane & 7;
+          // accumulator loads run one 32-column block ahead of their use (latency hiding)
+          float4 pa[8];
+          auto load_acc = [&](int64_t col0, float4 (&dst)[8]) {
+            const bool okl = col0 < N && col0 + 4 * c < N;
+            const int64_t off = (lrow0 + (lane >> 3)) * N + col0 + 4 * c;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              dst[i] = okl ? __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          };
+          load_acc(col_base, pa);
+#pragma unroll 1
+          for (int cc = 0; cc < BN; cc += 32) {
+            const int64_t col0 = col_base + cc;
+            if (col0 >= N) break;  // warp-uniform
+            float4 pn[8];
+            if (cc + 32 < BN) load_acc(col0 + 32, pn);
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tb + cc, v);
+            tmem_wait_ld();
+            if (nkb == 0) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            __syncwarp();
+            const bool ok = col0 + 4 * c < N;
+            const int64_t base_off = (lrow0 + (lane >> 3)) * N + col0 + 4 * c;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int rr = i * 4 + (lane >> 3);
+              const uint4 w = stg[rr * 8 + (c ^ (rr & 7))];
+              const float4 x = make_float4(pa[i].x + __uint_as_float(w.x), pa[i].y + __uint_as_float(w.y),
+                                           pa[i].z + __uint_as_float(w.z), pa[i].w + __uint_as_float(w.w));
+              if (ok) {
+                uint2 o;
+                o.x = pack_bf16x2(x.x, x.y);
+                o.y = pack_bf16x2(x.z, x.w);
+                *reinterpret_cast<uint2*>(cout + base_off + int64_t(i) * 4 * N) = o;
+                st_v4(reinterpret_cast<int4*>(accm + base_off + int64_t(i) * 4 * N), make_int4(0, 0, 0, 0));
+              }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pa[i] = pn[i];
+          }
+        } else if (own_tile) {
           // RS-4 fused reduction: the peer partials arrive as 32-column fp32 boxes in the
           // smem ring (streamed by the producer); thread = row, like the TMEM accumulator.
           // Sum in ascending source rank, own TMEM value at s == rank, store bf16.
@@ -522,9 +598,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
 #pragma unroll 1
           for (int cb = 0; cb < nvb; ++cb) {
             float acc[32];
-            for (int s = 0; s < R.W; ++s) {
+            const int nterms = R.W;  // ascending source rank; own TMEM value at s == rank
+            const int own_term = R.rank;
+            for (int s = 0; s < nterms; ++s) {
               float x[32];
-              if (s == R.rank) {
+              if (s == own_term) {
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(tb + cb * 32, v);
                 tmem_wait_ld();
@@ -613,7 +691,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3);
           const uint4 w = stg[r * 8 + (c ^ (r & 7))];
-          if (ok) st_v4(reinterpret_cast<int4*>(colp + r * ld_bytes), make_int4(w.x, w.y, w.z, w.w));
+          if (ok) {
+            if (MODE == MODE_RS && R.rs_atomic)
+              red_add_v4_f32(colp + r * ld_bytes, w.x, w.y, w.z, w.w);
+            else
+              st_v4(reinterpret_cast<int4*>(colp + r * ld_bytes), make_int4(w.x, w.y, w.z, w.w));
+          }
         }
         __syncwarp();
       }

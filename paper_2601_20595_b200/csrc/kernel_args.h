@@ -47,11 +47,12 @@ struct alignas(64) RankArgs {
   uint32_t* flags;             // this rank's flag words (current parity)
   uint32_t* peer_flags[AO_MAX_WORLD];  // every rank's flag words (current parity)
   char* peer_data[AO_MAX_WORLD];       // every rank's data half (current parity)
+  char* peer_acc[AO_MAX_WORLD];        // RS ATOMIC: every rank's accumulator [S, N] fp32 (current parity)
   uint32_t* counters;                  // RS: local per-chunk completion counters
   int64_t M, N, K, S;
   int32_t rank, W, crows, n_chunks, n_tiles, n_items, n_nb, n_slices, n_comm_items, n_cta;
   uint32_t epoch;
-  int32_t pad;
+  int32_t rs_atomic;  // RS: 1 = reduce-add into one accumulator (slot 0) instead of per-source slots
 };
 
 // In-kernel trace event (AO tracing): 32 bytes, %globaltimer nanoseconds.

@@ -48,6 +48,7 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   if (d.n_cta < 0) v.push_back("n_cta");
   if (d.n_slices < 1 || d.n_slices > 64) v.push_back("n_slices");
   if (d.rs_wire != AO_WIRE_FP32 && d.rs_wire != AO_WIRE_BF16) v.push_back("rs_wire");
+  if (d.rs_reduce != AO_RS_SLOTS && d.rs_reduce != AO_RS_ATOMIC) v.push_back("rs_reduce");
   if ((d.tile_m == 0) != (d.tile_n == 0)) v.push_back("tile");
   if (d.tile_m != 0) {
     bool ok = false;
@@ -177,6 +178,7 @@ static std::string rank_independent_key(const HostPlan& p) {
   o.put("comm_ctas", d.comm_ctas);
   o.put("n_slices", d.backend == AO_BACKEND_CE ? 1 : d.n_slices);
   o.put("rs_wire", d.rs_wire);
+  o.put("rs_reduce", d.rs_reduce);
   return o.str();
 }
 
@@ -425,7 +427,10 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
     o.put("waits", s + "]");
   }
   o.put("contrib", int_list(P.contrib));
-  if (!P.is_ag) o.put("tiles_per_chunk", int_list(P.tiles_per_chunk));
+  if (!P.is_ag) {
+    o.put("tiles_per_chunk", int_list(P.tiles_per_chunk));
+    o.put_str("rs_reduce", d.rs_reduce == AO_RS_ATOMIC ? "atomic" : "slots");
+  }
   P.json = o.str();
   P.hash = fnv1a64(rank_independent_key(P));
   return {};

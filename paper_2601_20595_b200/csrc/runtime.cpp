@@ -132,9 +132,11 @@ struct ao_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
 
+  size_t acc_half = 0;  // RS ATOMIC accumulator per parity (kept all-zero between uses)
   char* data(int q, uint32_t parity) const { return peer_base[q] + parity * data_half; }
+  char* acc(int q, uint32_t parity) const { return peer_base[q] + 2 * data_half + parity * acc_half; }
   uint32_t* flags(int q, uint32_t parity) const {
-    return reinterpret_cast<uint32_t*>(peer_base[q] + 2 * data_half + parity * kFlagWordsPerParity * 4);
+    return reinterpret_cast<uint32_t*>(peer_base[q] + 2 * data_half + 2 * acc_half + parity * kFlagWordsPerParity * 4);
   }
 };
 
@@ -294,10 +296,12 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
   R->n_slices = hp.desc.backend == AO_BACKEND_CE ? 1 : hp.desc.n_slices;
   R->n_cta = hp.n_cta;
   R->epoch = epoch;
+  R->rs_atomic = (!hp.is_ag && hp.desc.rs_reduce == AO_RS_ATOMIC) ? 1 : 0;
   R->counters = ctx ? ctx->counters : nullptr;
   if (ctx) {
     for (int q = 0; q < hp.W; ++q) {
       R->peer_data[q] = ctx->data(q, par);
+      R->peer_acc[q] = ctx->acc(q, par);
       R->peer_flags[q] = ctx->flags(q, par);
     }
     R->flags = R->peer_flags[hp.rank];
@@ -319,8 +323,11 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
     s = encode_2d(&R->tmB, B, hp.N, hp.K, bn / hp.tile.cg);
     if (s != AO_OK) return s;
   }
-  if (!hp.is_ag && ctx && hp.W > 1 && hp.N > 0 && hp.S > 0) {  // RS: peer partial slots, streamed by the producer
-    s = encode_2d(&R->tmA_loc, R->peer_data[hp.rank], int64_t(hp.W) * hp.S, hp.N, 128, true);
+  if (!hp.is_ag && ctx && hp.W > 1 && hp.N > 0 && hp.S > 0) {  // RS: peer partials, streamed by the producer
+    if (R->rs_atomic)
+      s = encode_2d(&R->tmA_loc, R->peer_acc[hp.rank], hp.S, hp.N, 128, true);
+    else
+      s = encode_2d(&R->tmA_loc, R->peer_data[hp.rank], int64_t(hp.W) * hp.S, hp.N, 128, true);
     if (s != AO_OK) return s;
   }
   R->C = C;
@@ -474,10 +481,13 @@ ao_status ao_ctx_create(int device, int rank, int world_size, size_t workspace_b
   c->W = world_size;
   c->sm_count = sm;
   c->data_half = (workspace_bytes / 2 + 4095) / 4096 * 4096;
-  c->total = 2 * c->data_half + 2 * kFlagWordsPerParity * 4;
+  // RS ATOMIC accumulator: an owner's [S, N] fp32 is 1/W of the slots an RS plan of the
+  // same shape needs, so data_half / W always suffices.
+  c->acc_half = (c->data_half / world_size + 4095) / 4096 * 4096;
+  c->total = 2 * c->data_half + 2 * c->acc_half + 2 * kFlagWordsPerParity * 4;
   cudaError_t e = cudaMalloc(&c->base, c->total);
   if (e != cudaSuccess) return fail(AO_ERR_OOM, "cudaMalloc(%zu): %s", c->total, cudaGetErrorString(e));
-  AO_CUDA(cudaMemset(c->base + 2 * c->data_half, 0, 2 * kFlagWordsPerParity * 4));
+  AO_CUDA(cudaMemset(c->base + 2 * c->data_half, 0, 2 * c->acc_half + 2 * kFlagWordsPerParity * 4));
   AO_CUDA(cudaMalloc(&c->epoch_cell, 64));
   AO_CUDA(cudaMemset(c->epoch_cell, 0, 64));
   AO_CUDA(cudaMalloc(&c->counters, kCounterWords * 4));
@@ -634,6 +644,9 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
   if (ao::data_bytes_per_parity(*d) > c->data_half)
     return fail(AO_ERR_INVALID_ARG, "workspace too small: plan needs %zu bytes per parity, ctx has %zu",
                 ao::data_bytes_per_parity(*d), c->data_half);
+  if (d->op == AO_OP_GEMM_RS && d->rs_reduce == AO_RS_ATOMIC &&
+      size_t(d->M / d->world_size) * size_t(d->N) * 4 > c->acc_half)
+    return fail(AO_ERR_INVALID_ARG, "workspace too small for the RS accumulator");
   if (ao::flag_words_needed(*d) > kFlagWordsPerParity)
     return fail(AO_ERR_INVALID_ARG, "too many chunk flags (%zu)", ao::flag_words_needed(*d));
   if (size_t(p->hp.n_chunks) > kCounterWords) return fail(AO_ERR_INVALID_ARG, "too many chunks");

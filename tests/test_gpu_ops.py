@@ -281,3 +281,44 @@ def test_ag_gemm_dedicated_comm_ctas(ao, backend, tile):
     for r in range(W):
         _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag comm_ctas {backend} r{r}")
         assert torch.equal(G[r].cpu(), full)
+
+
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_gemm_rs_atomic_vs_oracle(ao, W, tile):
+    """rs_reduce=atomic: peers reduce-add into the owner's accumulator (Q23)."""
+    M, K, N, C = 256 * W, 256, 520, 64
+    A, B = si.rs_inputs(W, M, K, N, salt=13)
+    ctxs, plans = _rs_world(ao, W, M, N, K, C, tile_m=tile[0], tile_n=tile[1], rs_reduce="atomic")
+    A64 = [si.to_f64(a) for a in A]
+    B64 = [si.to_f64(b) for b in B]
+    dA, dB = _dev(A), _dev(B)
+    for it in range(3):  # the accumulator must be re-armed (zero) between calls
+        Cs = _run_rs(ao, ctxs, plans, dA, dB)
+        for r in range(W):
+            _check(Cs[r], on.gemm_rs(A64, B64, r), f"rs atomic W={W} it={it} rank {r}")
+
+
+def test_gemm_rs_atomic_bitmask_and_mode_mixing(ao):
+    """Exact integer sums are order-independent, so the bitmask pattern is bit-exact in
+    atomic mode; mixing slots / atomic / AG ops on one ctx keeps the accumulator armed."""
+    W, M, K, N = 4, 1024, 64, 256
+    desc = dict(op="gemm_rs", world_size=W, M=M, N=N, K=K, chunk_rows=128, n_cta=36, timeout_ns=2_000_000_000)
+    ag = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=128, n_cta=36, timeout_ns=2_000_000_000)
+    ctxs = ao.loopback_world(0, W, max(ao.workspace_bytes(desc), ao.workspace_bytes(ag)))
+    p_slots = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
+    p_atom = [ao.Plan(ctxs[r], dict(desc, rank=r, rs_reduce="atomic")) for r in range(W)]
+    p_ag = [ao.Plan(ctxs[r], dict(ag, rank=r)) for r in range(W)]
+    A, B = si.rs_provenance_inputs(W, M, K, N)
+    A, B = _dev(A), _dev(B)
+    Ag, Bg = si.ag_inputs(W, M, K, N)
+    Ag, Bg = _dev(Ag), _dev(Bg)
+    Cg = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    for seq in (["atomic", "slots", "atomic", "ag", "atomic", "ag", "ag", "atomic"]):
+        if seq == "ag":
+            ao.ag_gemm_group(p_ag, Ag, Bg, Cg)
+            torch.cuda.synchronize()
+            continue
+        Cs = _run_rs(ao, ctxs, p_atom if seq == "atomic" else p_slots, A, B)
+        for r in range(W):
+            assert torch.all(Cs[r].float().cpu() == 2 ** W - 1), seq

@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tp", type=int, default=8, help="logical TP ranks in loopback (N=1)")
     ap.add_argument("--backend", default="ce", choices=["ce", "tma", "ldst"])
+    ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
     ap.add_argument("--chunk", type=int, default=1024)
     ap.add_argument("--tokens", type=int, default=TOKENS)
     ap.add_argument("--intra", default="grouped", choices=["row", "col", "grouped"])
@@ -136,7 +137,7 @@ def run_ours(args, rank, world, local_rank):
     F = FFN // W
     base = dict(world_size=W, M=M, chunk_rows=args.chunk, timeout_ns=5_000_000_000, intra=args.intra,
                 group_m=args.group_m)
-    ag_desc = dict(base, op="ag_gemm", N=F, K=HIDDEN, backend=args.backend, n_slices=2)
+    ag_desc = dict(base, op="ag_gemm", N=F, K=HIDDEN, backend=args.backend, dir=args.ag_dir, n_slices=2)
     rs_desc = dict(base, op="gemm_rs", N=HIDDEN, K=F, chunk_order=args.rs_order,
                    chunk_rows=args.rs_chunk or args.chunk, rs_reduce=args.rs_reduce)
     if loop:
@@ -262,7 +263,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,1)/sqrt(K) weights)",
         "config": {"workload": f"llama3-8b-tp{W}-ffn-pair-{'loopback' if loop else 'nvlink'}",
                    "tokens": M, "hidden": HIDDEN, "ffn": FFN, "tp": W, "ranks_per_gpu": W if loop else 1,
-                   "backend_ag": args.backend, "chunk_rows": args.chunk, "rs_chunk_rows": args.rs_chunk or args.chunk,
+                   "backend_ag": args.backend, "ag_dir": args.ag_dir, "chunk_rows": args.chunk, "rs_chunk_rows": args.rs_chunk or args.chunk,
                    "intra": args.intra, "group_m": args.group_m, "rs_chunk_order": args.rs_order,
                    "rs_reduce": args.rs_reduce,
                    "tile": [pa[0].info()["tile_m"], pa[0].info()["tile_n"]], "cta_group": pa[0].info()["cta_group"],

@@ -159,8 +159,16 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
     if (A.delay_ns && lane == 0) inject_delay(A.delay_ns, uint32_t(i));  // fault injection
     __syncwarp();
     const CommItem it = R.comm_items[i];
-    const char* src = R.A_shard + it.src_off;
-    char* dst = R.peer_data[it.peer] + it.dst_off;
+    const char* src = (it.kind == ITEM_PULL ? R.peer_data[it.peer] : R.A_shard) + it.src_off;
+    char* dst = R.peer_data[it.kind == ITEM_PUSH ? it.peer : R.rank] + it.dst_off;
+    if (it.kind == ITEM_PULL) {
+      // PULL (Lst.2): the source staged its chunk and released its ready flag
+      if (lane == 0) {
+        spin_flag(R.peer_flags[it.peer] + it.g * R.n_slices + it.slice, R.epoch, A, R.rank, -1 - worker, it.g);
+        fence_proxy_async_global();  // generic-proxy acquire -> bulk (async-proxy) reads
+      }
+      __syncwarp();
+    }
     if constexpr (COMM == COMM_LDST) {
       const int4* s = reinterpret_cast<const int4*>(src);
       int4* d = reinterpret_cast<int4*>(dst);
@@ -171,7 +179,7 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t j = base + u * 32 + lane;
-          if (j < n) v[u] = ld_nc_v4(s + j);
+          if (j < n) v[u] = it.kind == ITEM_PULL ? __ldcg(s + j) : ld_nc_v4(s + j);  // peer data: coherent
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -214,7 +222,8 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
       __syncwarp();
     }
     if (lane == 0) {
-      st_release_sys(R.peer_flags[it.peer] + it.g * R.n_slices + it.slice, R.epoch);
+      uint32_t* f = it.kind == ITEM_PUSH ? R.peer_flags[it.peer] : R.flags;
+      st_release_sys(f + it.g * R.n_slices + it.slice, R.epoch);
       trace_event(A, TR_COMM, R.rank, worker, i, t_item);
     }
     __syncwarp();

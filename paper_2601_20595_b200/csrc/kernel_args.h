@@ -27,9 +27,14 @@ struct ErrorInfo {
 // A communication work item of the in-kernel AG backends: copy `bytes` bytes at byte
 // offset `off` of chunk `g` from the local shard to rank `peer`'s gathered buffer, then
 // release flag word g*n_slices + slice at `peer`.
+// AG transfer item of the in-kernel backends.  kind PUSH: local shard -> peer's gathered
+// buffer, release the peer's flag.  STAGE (pull plans): local shard -> own gathered buffer
+// (the region peers pull from), release the own flag ("ready").  PULL: wait for the source
+// peer's ready flag, peer's gathered buffer -> own gathered buffer, release the own flag.
+enum ItemKind : int32_t { ITEM_PUSH = 0, ITEM_STAGE = 1, ITEM_PULL = 2 };
 struct CommItem {
-  int32_t peer, g, slice, pad;
-  int64_t src_off, dst_off, bytes;  // byte offsets (src: local shard, dst: gathered buffer)
+  int32_t peer, g, slice, kind;     // peer: destination (PUSH) or source (PULL) rank
+  int64_t src_off, dst_off, bytes;  // byte offsets (src: local shard or peer buffer, dst: buffer)
 };
 
 struct alignas(64) RankArgs {

@@ -64,6 +64,7 @@ typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned
 struct DriverFns {
   PFN_encodeTiled encode = nullptr;
   PFN_writeValue32 write32 = nullptr;
+  PFN_writeValue32 wait32 = nullptr;  // cuStreamWaitValue32 (same signature)
 };
 
 ao_status get_driver(DriverFns** out) {
@@ -81,6 +82,10 @@ ao_status get_driver(DriverFns** out) {
     AO_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q));
     if (!p) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 not found");
     fns.write32 = reinterpret_cast<PFN_writeValue32>(p);
+    p = nullptr;
+    AO_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q));
+    if (!p) return fail(AO_ERR_CUDA, "cuStreamWaitValue32 not found");
+    fns.wait32 = reinterpret_cast<PFN_writeValue32>(p);
     loaded = true;
   }
   *out = &fns;
@@ -177,24 +182,36 @@ ao_status upload_tables(ao_plan* p) {
   }
   // in-kernel comm items (AG push, TMA / LDST backends)
   std::vector<ao::CommItem> comm;
-  if (hp.is_ag && hp.desc.backend != AO_BACKEND_CE && hp.desc.dir == AO_DIR_PUSH) {
+  if (hp.is_ag && hp.desc.backend != AO_BACKEND_CE && hp.W > 1) {
     const int64_t row_bytes = hp.K * 2;
     const int64_t chunk_bytes = int64_t(hp.C) * row_bytes;
     const int ns = hp.desc.n_slices;
     const int64_t slice = ((chunk_bytes + ns - 1) / ns + 15) / 16 * 16;
-    for (const ao::P2POp& op : hp.plans[hp.rank]) {
-      const int g = int(op.row0 / hp.C);
+    const bool pull = hp.desc.dir == AO_DIR_PULL;
+    // kind, peer, global row0 of the chunk; src offset relative to the local shard (PUSH,
+    // STAGE) or to the source's gathered buffer (PULL); dst offset in a gathered buffer.
+    auto add_slices = [&](int32_t kind, int peer, int64_t row0) {
       for (int s = 0; s < ns; ++s) {
         ao::CommItem it{};
-        it.peer = op.peer;
-        it.g = g;
+        it.kind = kind;
+        it.peer = peer;
+        it.g = int(row0 / hp.C);
         it.slice = s;
         const int64_t off = std::min<int64_t>(int64_t(s) * slice, chunk_bytes);
         it.bytes = std::max<int64_t>(0, std::min<int64_t>(slice, chunk_bytes - off));
-        it.src_off = (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes + off;
-        it.dst_off = op.row0 * row_bytes + off;
+        it.src_off = (kind == ao::ITEM_PULL ? row0 : row0 - int64_t(hp.rank) * hp.S) * row_bytes + off;
+        it.dst_off = row0 * row_bytes + off;
         comm.push_back(it);
       }
+    };
+    if (pull) {
+      // PULL (Lst.2 P:249-265 with the issuer on the consumer side): stage the own
+      // shard in the own gathered buffer first (every worker's first items, so no pull can
+      // wait on a stage queued behind it), then fetch the peers' chunks in plan order.
+      for (int64_t j = 0; j < hp.S / hp.C; ++j) add_slices(ao::ITEM_STAGE, hp.rank, int64_t(hp.rank) * hp.S + j * hp.C);
+      for (const ao::P2POp& op : hp.plans[hp.rank]) add_slices(ao::ITEM_PULL, op.peer, op.row0);
+    } else {
+      for (const ao::P2POp& op : hp.plans[hp.rank]) add_slices(ao::ITEM_PUSH, op.peer, op.row0);
     }
     p->comm_kind = hp.desc.backend == AO_BACKEND_TMA ? ao::COMM_TMA : ao::COMM_LDST;
   }
@@ -652,8 +669,6 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
   if (size_t(p->hp.n_chunks) > kCounterWords) return fail(AO_ERR_INVALID_ARG, "too many chunks");
   if (d->rs_wire != AO_WIRE_FP32 && d->op == AO_OP_GEMM_RS)
     return fail(AO_ERR_UNSUPPORTED, "bf16 RS wire is not implemented (non-conforming, DESIGN.md Q14)");
-  if (d->op == AO_OP_AG_GEMM && d->dir == AO_DIR_PULL && d->world_size > 1)
-    return fail(AO_ERR_UNSUPPORTED, "PULL schedules are planned/exported but not executed yet");
   p->ctx = c;
   p->device = c->device;
   s = upload_tables(p);
@@ -731,60 +746,113 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   if (ce) {
     ao_status s = get_driver(&drv);
     if (s != AO_OK) return s;
-    // CE backend (Fig.7a): every source rank pushes its chunks in plan order with
-    // peer memcpys, each followed by a 4-byte copy of the epoch into the destination's flag
-    // word.  The per-rank copy chains (one branch per rank of the group) are recorded once
-    // per (parity, buffers) as a CUDA graph, so a call costs three host operations.
+    // CE backend (Fig.7a).  PUSH: every source rank copies its chunks to the peers in
+    // plan order with peer memcpys, each followed by a 4-byte copy of the epoch into the
+    // destination's flag word.  PULL: every rank first stages its shard in its own gathered
+    // buffer, then copies the peers' chunks in plan order into its own buffer and sets its
+    // own flag.  Whole-world groups (loopback) record the chains once per (parity, buffers)
+    // as a CUDA graph (three host operations per call; in PULL the stage copies of all ranks
+    // are a graph join before the pulls).  A PULL whose sources live in other processes
+    // waits on their ready flags with cuStreamWaitValue32, issued directly per call.
     ao_ctx* c0 = p0->ctx;
     const uint32_t par = epochs[0] & 1;
-    std::vector<uintptr_t> key{uintptr_t(par), uintptr_t(n)};
-    for (int i = 0; i < n; ++i) {
-      key.push_back(reinterpret_cast<uintptr_t>(plans[i]));
-      key.push_back(reinterpret_cast<uintptr_t>(As[i]));
-    }
-    cudaGraphExec_t exec = nullptr;
-    auto it = p0->ce_graphs.find(key);
-    if (it != p0->ce_graphs.end()) {
-      exec = it->second;
-    } else {
-      cudaGraph_t graph;
-      AO_CUDA(cudaGraphCreate(&graph, 0));
-      for (int i = 0; i < n; ++i) {
-        ao_plan* p = plans[i];
-        ao_ctx* c = p->ctx;
-        const ao::HostPlan& hp = p->hp;
-        const int64_t row_bytes = hp.K * 2;
-        cudaGraphNode_t prev = nullptr;
-        for (const ao::P2POp& op : hp.plans[hp.rank]) {
-          const int g = int(op.row0 / hp.C);
-          const char* src = static_cast<const char*>(As[i]) + (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes;
-          char* dst = c->data(op.peer, par) + op.row0 * row_bytes;
-          cudaGraphNode_t data = nullptr, flag = nullptr;
-          if (row_bytes > 0) {
-            AO_CUDA(cudaGraphAddMemcpyNode1D(&data, graph, prev ? &prev : nullptr, prev ? 1 : 0, dst, src,
-                                             size_t(op.rows * row_bytes), cudaMemcpyDeviceToDevice));
-            prev = data;
-          }
-          AO_CUDA(cudaGraphAddMemcpyNode1D(&flag, graph, prev ? &prev : nullptr, prev ? 1 : 0,
-                                           c->flags(op.peer, par) + g, c0->epoch_cell, 4, cudaMemcpyDeviceToDevice));
-          prev = flag;
-        }
-      }
-      cudaError_t ge = cudaGraphInstantiate(&exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ge != cudaSuccess) return fail(AO_ERR_CUDA, "CE graph instantiate: %s", cudaGetErrorString(ge));
-      if (p0->ce_graphs.size() >= kMaxCeGraphs) {  // bounded cache (callers that rotate buffers)
-        AO_CUDA(cudaStreamSynchronize(c0->side));
-        cudaGraphExecDestroy(p0->ce_graphs.begin()->second);
-        p0->ce_graphs.erase(p0->ce_graphs.begin());
-      }
-      p0->ce_graphs[key] = exec;
-    }
+    const bool pull = h0.desc.dir == AO_DIR_PULL;
     AO_CUDA(cudaEventRecord(c0->ev_start, stream));
     AO_CUDA(cudaStreamWaitEvent(c0->side, c0->ev_start, 0));
     CUresult r = drv->write32(c0->side, reinterpret_cast<CUdeviceptr>(c0->epoch_cell), epochs[0], 0);
     if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
-    AO_CUDA(cudaGraphLaunch(exec, c0->side));
+    if (pull && n < h0.W) {
+      for (int i = 0; i < n; ++i) {  // all local stages first: a pull never waits behind one
+        const ao::HostPlan& hp = plans[i]->hp;
+        ao_ctx* c = plans[i]->ctx;
+        const int64_t row_bytes = hp.K * 2;
+        if (row_bytes > 0)
+          AO_CUDA(cudaMemcpyAsync(c->data(hp.rank, par) + int64_t(hp.rank) * hp.S * row_bytes, As[i],
+                                  size_t(hp.S * row_bytes), cudaMemcpyDeviceToDevice, c0->side));
+        for (int64_t j = 0; j < hp.S / hp.C; ++j) {
+          const int64_t g = (int64_t(hp.rank) * hp.S) / hp.C + j;
+          r = drv->write32(c0->side, reinterpret_cast<CUdeviceptr>(c->flags(hp.rank, par) + g), epochs[0], 0);
+          if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
+        }
+      }
+      for (int i = 0; i < n; ++i) {
+        const ao::HostPlan& hp = plans[i]->hp;
+        ao_ctx* c = plans[i]->ctx;
+        const int64_t row_bytes = hp.K * 2;
+        for (const ao::P2POp& op : hp.plans[hp.rank]) {
+          const int g = int(op.row0 / hp.C);
+          r = drv->wait32(c0->side, reinterpret_cast<CUdeviceptr>(c->flags(op.peer, par) + g), epochs[0],
+                          0x0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+          if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", int(r));
+          if (row_bytes > 0)
+            AO_CUDA(cudaMemcpyAsync(c->data(hp.rank, par) + op.row0 * row_bytes,
+                                    c->data(op.peer, par) + op.row0 * row_bytes, size_t(op.rows * row_bytes),
+                                    cudaMemcpyDeviceToDevice, c0->side));
+          r = drv->write32(c0->side, reinterpret_cast<CUdeviceptr>(c->flags(hp.rank, par) + g), epochs[0], 0);
+          if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
+        }
+      }
+    } else {
+      std::vector<uintptr_t> key{uintptr_t(par), uintptr_t(n)};
+      for (int i = 0; i < n; ++i) {
+        key.push_back(reinterpret_cast<uintptr_t>(plans[i]));
+        key.push_back(reinterpret_cast<uintptr_t>(As[i]));
+      }
+      cudaGraphExec_t exec = nullptr;
+      auto it = p0->ce_graphs.find(key);
+      if (it != p0->ce_graphs.end()) {
+        exec = it->second;
+      } else {
+        cudaGraph_t graph;
+        AO_CUDA(cudaGraphCreate(&graph, 0));
+        std::vector<cudaGraphNode_t> stages;  // PULL: every rank's shard staged (graph join)
+        if (pull) {
+          for (int i = 0; i < n; ++i) {
+            const ao::HostPlan& hp = plans[i]->hp;
+            const int64_t row_bytes = hp.K * 2;
+            if (row_bytes == 0) continue;
+            cudaGraphNode_t st = nullptr;
+            AO_CUDA(cudaGraphAddMemcpyNode1D(&st, graph, nullptr, 0,
+                                             plans[i]->ctx->data(hp.rank, par) + int64_t(hp.rank) * hp.S * row_bytes,
+                                             As[i], size_t(hp.S * row_bytes), cudaMemcpyDeviceToDevice));
+            stages.push_back(st);
+          }
+        }
+        for (int i = 0; i < n; ++i) {
+          ao_plan* p = plans[i];
+          ao_ctx* c = p->ctx;
+          const ao::HostPlan& hp = p->hp;
+          const int64_t row_bytes = hp.K * 2;
+          std::vector<cudaGraphNode_t> prev = stages;
+          for (const ao::P2POp& op : hp.plans[hp.rank]) {
+            const int g = int(op.row0 / hp.C);
+            const char* src = pull ? c->data(op.peer, par) + op.row0 * row_bytes
+                                   : static_cast<const char*>(As[i]) + (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes;
+            const int dst_rank = pull ? hp.rank : op.peer;
+            char* dst = c->data(dst_rank, par) + op.row0 * row_bytes;
+            cudaGraphNode_t data = nullptr, flag = nullptr;
+            if (row_bytes > 0) {
+              AO_CUDA(cudaGraphAddMemcpyNode1D(&data, graph, prev.data(), prev.size(), dst, src,
+                                               size_t(op.rows * row_bytes), cudaMemcpyDeviceToDevice));
+              prev.assign(1, data);
+            }
+            AO_CUDA(cudaGraphAddMemcpyNode1D(&flag, graph, prev.data(), prev.size(), c->flags(dst_rank, par) + g,
+                                             c0->epoch_cell, 4, cudaMemcpyDeviceToDevice));
+            prev.assign(1, flag);
+          }
+        }
+        cudaError_t ge = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ge != cudaSuccess) return fail(AO_ERR_CUDA, "CE graph instantiate: %s", cudaGetErrorString(ge));
+        if (p0->ce_graphs.size() >= kMaxCeGraphs) {  // bounded cache (callers that rotate buffers)
+          AO_CUDA(cudaStreamSynchronize(c0->side));
+          cudaGraphExecDestroy(p0->ce_graphs.begin()->second);
+          p0->ce_graphs.erase(p0->ce_graphs.begin());
+        }
+        p0->ce_graphs[key] = exec;
+      }
+      AO_CUDA(cudaGraphLaunch(exec, c0->side));
+    }
     AO_CUDA(cudaEventRecord(c0->ev_done, c0->side));
   }
   cudaError_t e = ao::launch_fused(*ka, h0.tile.bn, h0.tile.cg, comm, stream);

@@ -5,6 +5,8 @@ performance, and selects the best-performing backend for each operator and hardw
 configuration".  The search space is the paper's:
   * inter-chunk: chunk size (split factor) per logical transfer (P:437);
   * intra-chunk: transfer backend, tile configuration, intra-chunk tile order (P:439);
+  * AG-GEMM: transfer direction, push or pull ("different implementation choices
+    during lowering");
   * GEMM-RS: chunk order of the owner rotation.
 Candidates are pruned by the planner's validation (hardware constraints: alignment, tile
 fit) and by a minimum efficient transfer size for the copy engine ("minimum
@@ -25,7 +27,7 @@ CE_MIN_CHUNK_BYTES = 1 << 20
 
 
 def candidate_space(op: str, W: int, M: int, N: int, K: int, chunks=None, backends=None, intras=None,
-                    tiles=None, orders=None):
+                    tiles=None, orders=None, dirs=None):
     """Enumerate descs of one op (dicts with the oracle/planner desc keys)."""
     S = M // W
     chunks = chunks or [c for c in (128, 256, 512, 1024, 2048, 4096) if c <= S and S % c == 0]
@@ -33,10 +35,11 @@ def candidate_space(op: str, W: int, M: int, N: int, K: int, chunks=None, backen
     intras = intras or [("row", 1), ("grouped", 2), ("grouped", 4)]
     tiles = tiles or [(0, 0), (128, 256)]
     orders = orders or (["shard_major", "chunk_major"] if op == "gemm_rs" else ["shard_major"])
+    dirs = dirs or (["push", "pull"] if op == "ag_gemm" and W > 1 else ["push"])
     out = []
-    for c, b, (intra, gm), (tm, tn), o in itertools.product(chunks, backends, intras, tiles, orders):
+    for c, b, (intra, gm), (tm, tn), o, dr in itertools.product(chunks, backends, intras, tiles, orders, dirs):
         out.append(dict(op=op, world_size=W, M=M, N=N, K=K, chunk_rows=c, backend=b, intra=intra, group_m=gm,
-                        tile_m=tm, tile_n=tn, chunk_order=o, n_slices=2))
+                        tile_m=tm, tile_n=tn, chunk_order=o, dir=dr, n_slices=2))
     return out
 
 
@@ -146,7 +149,8 @@ def main():
                                  log=lambda r: print(json.dumps({k: r[k] for k in ("ms", "tflops", "tile")} |
                                                                 {"cfg": {k: r["desc"][k] for k in
                                                                          ("chunk_rows", "backend", "intra", "group_m",
-                                                                          "tile_m", "tile_n", "chunk_order")}}),
+                                                                          "tile_m", "tile_n", "chunk_order",
+                                                                          "dir")}}),
                                                      flush=True))
     print(json.dumps({"best": rows[0] if rows else None, "n_measured": len(rows), "n_pruned": len(pruned)}))
 

@@ -322,3 +322,77 @@ def test_gemm_rs_atomic_bitmask_and_mode_mixing(ao):
         Cs = _run_rs(ao, ctxs, p_atom if seq == "atomic" else p_slots, A, B)
         for r in range(W):
             assert torch.all(Cs[r].float().cpu() == 2 ** W - 1), seq
+
+
+# ------------------------------------------------------------------------ AG PULL
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+@pytest.mark.parametrize("backend", ["ce", "ldst", "tma"])
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_ag_gemm_pull_vs_oracle(ao, backend, W, tile):
+    """dir=pull (Lst.2 with the consumer as issuer): each rank stages
+    its shard, then fetches peer chunks (src - r) mod W = d in plan order."""
+    M, K, N, C = 256 * W, 512, 512, 64
+    A, B = si.ag_inputs(W, M, K, N, salt=17)
+    ctxs, plans = _ag_world(ao, W, M, N, K, C, backend, dir="pull", tile_m=tile[0], tile_n=tile[1], n_slices=2)
+    Cs, G = _run_ag(ao, ctxs, plans, _dev(A), _dev(B), gather=True)
+    A64 = [si.to_f64(a) for a in A]
+    full = torch.cat(A, 0)
+    for r in range(W):
+        _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag pull W={W} {backend} rank {r}")
+        assert torch.equal(G[r].cpu(), full), "gathered A must be a bit-exact copy"
+
+
+@pytest.mark.parametrize("backend", ["ce", "ldst", "tma"])
+def test_ag_gemm_pull_provenance_epochs_and_delays(ao, backend):
+    """Back-to-back epochs (both parities, staged regions reused) with random per-transfer
+    delays on the in-kernel backends: every output row decodes to its gathered row id."""
+    W, M, K, N = 4, 1024, 64, 256
+    ctxs, plans = _ag_world(ao, W, M, N, K, 64, backend, dir="pull", chunk_order="chunk_major", n_slices=3)
+    try:
+        for it in range(6):
+            ao.debug_set("delay_ns", 200_000 if (backend != "ce" and it % 2) else 0)
+            A, B = si.ag_provenance_inputs(W, M, K, N, epoch=it + 1)
+            Cs, _ = _run_ag(ao, ctxs, plans, _dev(A), _dev(B))
+            for r in range(W):
+                c = Cs[r].float().cpu()
+                rid = c[:, 0] + 32 * c[:, 1] + 1024 * c[:, 2]
+                assert torch.equal(rid, torch.arange(M, dtype=torch.float32)), (backend, it, r)
+                assert torch.all(c[:, 3] == (it + 1) % 32)
+    finally:
+        ao.debug_set("delay_ns", 0)
+
+
+@pytest.mark.parametrize("dir_", ["push", "pull"])
+@pytest.mark.parametrize("backend", ["ce", "tma"])
+def test_ag_gemm_per_rank_calls_on_separate_streams(ao, backend, dir_):
+    """The multi-process protocol in one process: each rank is its own call (n_group = 1)
+    on its own stream, as with one process per GPU; CE pull then waits on the source's
+    ready flag with cuStreamWaitValue32."""
+    W, M, K, N = 2, 1024, 256, 512
+    A, B = si.ag_inputs(W, M, K, N, salt=23)
+    # two concurrent kernels must be co-resident: 2 x 32 workers x (up to) 2 CTAs <= 148 SMs
+    ctxs, plans = _ag_world(ao, W, M, N, K, 128, backend, dir=dir_, n_cta=32)
+    dA, dB = _dev(A), _dev(B)
+    A64 = [si.to_f64(a) for a in A]
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    for it in range(3):
+        Cs = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+        for r in (1, 0) if it % 2 else (0, 1):
+            ao.ag_gemm(plans[r], dA[r], dB[r], Cs[r], stream=streams[r])
+        torch.cuda.synchronize()
+        for c in ctxs:
+            c.check_async()
+        for r in range(W):
+            _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag per-rank {backend} {dir_} it={it} r{r}")
+
+
+def test_ag_gemm_pull_dedicated_comm_ctas(ao):
+    W, M, K, N = 2, 1024, 256, 512
+    A, B = si.ag_inputs(W, M, K, N, salt=29)
+    ctxs, plans = _ag_world(ao, W, M, N, K, 128, "tma", dir="pull", tile_m=256, tile_n=256, n_cta=32,
+                            comm_ctas=8, n_slices=4)
+    Cs, G = _run_ag(ao, ctxs, plans, _dev(A), _dev(B), gather=True)
+    A64 = [si.to_f64(a) for a in A]
+    for r in range(W):
+        _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag pull comm_ctas r{r}")
+        assert torch.equal(G[r].cpu(), torch.cat(A, 0))

@@ -243,6 +243,14 @@ def run_ours(args, rank, world, local_rank):
     elif not loop and not args.no_baseline:
         baseline = nccl_baseline(torch, dist, A[0], Bu[0], Bd[0], W, M, F, args, dev)
 
+    # --- GEMM-only leg: the same kernel, tiles and workers with no communication -------
+    gemm_only = None
+    if not args.no_baseline:
+        gemm_only = gemm_only_leg(torch, ao, pa, pr, A, Bu, Bd, W, M, F, args, dev, loop)
+        if gemm_only is not None:
+            gemm_only["exposed_comm_ms"] = {"ag_gemm": round(ag_ms - gemm_only["ag_gemm_ms"], 4),
+                                            "gemm_rs": round(rs_ms - gemm_only["gemm_rs_ms"], 4)}
+
     # --- e2e through the public API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:
@@ -284,6 +292,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": e2e,
         "check": check,
         "baseline_kernel_level": baseline,
+        "gemm_only": gemm_only,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(W, M, budget_s=12.0)
@@ -332,6 +341,43 @@ def loopback_baseline(torch, A, Bu, Bd, Cu, W, M, F, args):
     ms = s.elapsed_time(e) / n
     return {"what": "torch.cat gather + cuBLAS GEMMs + torch reduction (kernel-level, same GPU)",
             "ms_per_step": round(ms, 4), "tflops": round(4.0 * M * FFN * HIDDEN / (ms * 1e-3) / 1e12, 2)}
+
+
+def gemm_only_leg(torch, ao, pa, pr, A, Bu, Bd, W, M, F, args, dev, loop):
+    """SURVEY §8(d) baseline (iii): the fused ops' GEMMs through the same kernel (tile shape,
+    workers per rank, GROUP_M) with no transfers, flags or reduction -- ao_gemm_batched on
+    pre-gathered A (one copy per rank, as the gathered buffers are) and on the RS operands
+    into a bf16 scratch.  exposed communication = fused - GEMM-only."""
+    ia, ir = pa[0].info(), pr[0].info()
+    n = W if loop else 1
+    A_full = torch.cat(A, 0) if loop else torch.empty(M, HIDDEN, dtype=torch.bfloat16, device=dev).normal_()
+    A_g = [A_full.clone() for _ in range(n)]
+    up = [torch.empty(M, F, dtype=torch.bfloat16, device=dev) for _ in range(n)]
+    dn = [torch.empty(M, HIDDEN, dtype=torch.bfloat16, device=dev) for _ in range(n)]
+
+    def ag():
+        ao.gemm_batched(A_g, Bu[:n], up, ia["tile_m"], ia["tile_n"], args.group_m, ia["n_cta"] * ia["cta_group"])
+
+    def rs():
+        ao.gemm_batched(up, Bd[:n], dn, ir["tile_m"], ir["tile_n"], args.group_m, ir["n_cta"] * ir["cta_group"])
+
+    res = {}
+    for name, fn in (("ag_gemm_ms", ag), ("gemm_rs_ms", rs)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k = max(5, args.steps // 2)
+        s.record()
+        for _ in range(k):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        res[name] = round(s.elapsed_time(e) / k, 4)
+    del A_g, up, dn
+    res["what"] = ("same tcgen05 kernel, tile and workers per rank, no transfers/flags/reduction "
+                   "(ao_gemm_batched over the %d rank problems of one launch)" % n)
+    return res
 
 
 def nccl_baseline(torch, dist, A_shard, Bu, Bd, W, M, F, args, dev):

@@ -190,6 +190,21 @@ ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, 
 ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                   int32_t tile_m, int32_t tile_n, void* stream);
 
+/* ---- GEMM-only leg of the fused ops (SURVEY.md §8(d) baseline (iii)) -------------------
+ * n independent problems C_i = A_i . B_i^T of one shape in ONE persistent launch of the
+ * same kernel, each problem on its own n_cta workers (CTAs, or CTA pairs when tile_m =
+ * 256), exactly as a loopback group of n ranks runs the fused ops, but with no transfers,
+ * flags or reductions.  "Exposed communication" = T_fused - T_gemm_batched.
+ * n in [1, AO_MAX_WORLD]; A_i [M, K], B_i [N, K], C_i [M, N] bf16 device pointers on
+ * `device`, 16-byte aligned; tile_m/tile_n as ao_gemm (must be given, no 0 default
+ * for tile_m unless M % 256 == 0); group_m: GROUP_M tile swizzle (0 = 16); n_cta: CTAs per
+ * problem as in ao_plan_desc.n_cta (rounded down to whole CTA pairs when tile_m = 256;
+ * 0 = SMs / n).  n * n_cta must not exceed the SM count (co-residency), else
+ * AO_ERR_INVALID_ARG. */
+ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* const* Bs, void* const* Cs,
+                          int64_t M, int64_t N, int64_t K, int32_t tile_m, int32_t tile_n, int32_t group_m,
+                          int32_t n_cta, void* stream);
+
 /* ---- tracing -------------------------------------------------------------
  * ao_ctx_trace_enable: allocate a device event buffer of `capacity` events (0 = off).  Op
  *   launches whose first plan belongs to this ctx record %globaltimer-stamped events:

@@ -210,5 +210,16 @@ def gemm(A, B, C=None, tile_n: int = 0, tile_m: int = 0, stream=None):
     return C
 
 
+def gemm_batched(As, Bs, Cs, tile_m: int = 0, tile_n: int = 0, group_m: int = 0, n_cta: int = 0, stream=None):
+    """ao_gemm_batched: C_i = A_i . B_i^T for n same-shape problems in one persistent launch,
+    n_cta CTAs each as in a plan desc (the GEMM-only leg of a loopback group)."""
+    _require_bf16_cuda(*As, *Bs, *Cs)
+    M, K = As[0].shape
+    N = Bs[0].shape[0]
+    check(lib().ao_gemm_batched(As[0].device.index, len(As), _arr(As), _arr(Bs), _arr(Cs), M, N, K, tile_m, tile_n,
+                                group_m, n_cta, _stream(stream)))
+    return Cs
+
+
 def debug_set(key: str, value: int):
     check(lib().ao_debug_set(key.encode(), int(value)))

@@ -265,12 +265,15 @@ ao_status encode_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols,
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 ao_status check_device_sm100(int device, int* sm_count) {
-  cudaDeviceProp prop;
-  AO_CUDA(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10 || prop.minor != 0)
-    return fail(AO_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only", device,
-                prop.major, prop.minor);
-  *sm_count = prop.multiProcessorCount;
+  // cudaDeviceGetAttribute is cheap (cudaGetDeviceProperties costs milliseconds per call)
+  int major = 0, minor = 0, sms = 0;
+  AO_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  AO_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  AO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  if (major != 10 || minor != 0)
+    return fail(AO_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only", device, major,
+                minor);
+  *sm_count = sms;
   return AO_OK;
 }
 
@@ -952,6 +955,77 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
   ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint) : 2;
   ao_status s = fill_rank(&ka->rk[0], p, 0, A, B, C);
   if (s != AO_OK) return s;
+  cudaError_t e = ao::launch_fused(*ka, bn, p->hp.tile.cg, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));
+  if (e != cudaSuccess) return fail(AO_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+  return AO_OK;
+}
+
+ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* const* Bs, void* const* Cs,
+                          int64_t M, int64_t N, int64_t K, int32_t tile_m, int32_t tile_n, int32_t group_m,
+                          int32_t n_cta, void* stream_v) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int, int, int>, ao_plan*> cache;
+  if (n < 1 || n > AO_MAX_WORLD || !As || !Bs || !Cs) return fail(AO_ERR_INVALID_ARG, "bad batch size %d", n);
+  const int bm = tile_m ? tile_m : (M % 256 == 0 ? 256 : 128);
+  const int bn = tile_n ? tile_n : 256;
+  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256) || (bn != 128 && bn != 256) || M % bm != 0 ||
+      N % 8 != 0 || K % 8 != 0)
+    return fail(AO_ERR_INVALID_ARG, "ao_gemm_batched needs M %% tile_m == 0, N %% 8 == 0, K %% 8 == 0");
+  for (int i = 0; i < n; ++i)
+    if (!aligned16(As[i]) || !aligned16(Bs[i]) || !aligned16(Cs[i]))
+      return fail(AO_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
+  if (M == 0 || N == 0) return AO_OK;
+  AO_CUDA(cudaSetDevice(device));
+  int sm = 0;
+  ao_status s = check_device_sm100(device, &sm);
+  if (s != AO_OK) return s;
+  const int cg = bm == 256 ? 2 : 1;
+  const int ctas = (n_cta > 0 ? n_cta : sm / n) / cg * cg;  // CTAs per problem (whole pairs)
+  if (ctas < cg || int64_t(n) * ctas > sm)
+    return fail(AO_ERR_INVALID_ARG, "%d problems x %d CTAs exceed the %d SMs (or fewer CTAs than a tile needs)", n,
+                n_cta, sm);
+  ao_plan* p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(device, M, N, K, bm, bn, group_m, ctas);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      p = it->second;
+    } else {
+      ao_plan_desc d;
+      ao_plan_desc_init(&d);
+      d.M = M;
+      d.N = N;
+      d.K = K;
+      d.chunk_rows = int32_t(std::min<int64_t>(M, 1 << 30));
+      d.tile_m = bm;
+      d.tile_n = bn;
+      d.intra = AO_INTRA_GROUPED;
+      d.group_m = group_m > 0 ? group_m : 16;
+      d.n_cta = ctas;
+      s = ao_plan_create_host(&d, sm, &p);
+      if (s != AO_OK) return s;
+      p->device = device;
+      s = upload_tables(p);
+      if (s != AO_OK) {
+        ao_plan_destroy(p);
+        return s;
+      }
+      cache[key] = p;
+    }
+  }
+  std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
+  memset(ka.get(), 0, sizeof(ao::KernelArgs));
+  ka->n_group = n;
+  ka->ctas_per_rank = p->hp.n_cta * p->hp.tile.cg;
+  ka->mode = ao::MODE_GEMM;
+  ka->timeout_ns = 5000000000ull;
+  ka->skip_wait = -1;
+  ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint) : 2;
+  for (int i = 0; i < n; ++i) {
+    s = fill_rank(&ka->rk[i], p, 0, As[i], Bs[i], Cs[i]);
+    if (s != AO_OK) return s;
+  }
   cudaError_t e = ao::launch_fused(*ka, bn, p->hp.tile.cg, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return AO_OK;

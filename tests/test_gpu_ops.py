@@ -58,6 +58,19 @@ def test_gemm_large_sampled(ao):
     _check(C[torch.as_tensor(rows)], ref, "gemm large sampled")
 
 
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+@pytest.mark.parametrize("n", [1, 3, 8])
+def test_gemm_batched_vs_oracle(ao, n, tile):
+    # the GEMM-only leg: n problems in one launch, each on its own workers
+    M, N, K = 512, 520, 1000
+    A, B = si.ag_inputs(n, n * M, K, N, salt=31)
+    Cs = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    ao.gemm_batched(_dev(A), _dev(B), Cs, tile_m=tile[0], tile_n=tile[1], group_m=4)
+    torch.cuda.synchronize()
+    for i in range(n):
+        _check(Cs[i], on.gemm(si.to_f64(A[i]), si.to_f64(B[i])), f"gemm_batched n={n} #{i}")
+
+
 # ------------------------------------------------------------------------ AG-GEMM loopback
 def _ag_world(ao, W, M, N, K, chunk, backend, **kw):
     desc = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=chunk, backend=backend,

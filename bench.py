@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tp", type=int, default=8, help="logical TP ranks in loopback (N=1)")
     ap.add_argument("--backend", default="ce", choices=["ce", "tma", "ldst"])
+    ap.add_argument("--exp", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
     ap.add_argument("--chunk", type=int, default=1024)
     ap.add_argument("--tokens", type=int, default=TOKENS)
@@ -129,6 +130,8 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     if args.l2_hint >= 0:
         ao.debug_set("l2_hint", args.l2_hint)
+    if args.exp:
+        ao.debug_set("exp", args.exp)  # timing experiments: results are NOT valid
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     M = args.tokens

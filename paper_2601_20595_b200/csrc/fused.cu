@@ -57,13 +57,13 @@ struct SmemLayout {
 };
 
 template <int BN, int CG>
-__host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm) {
+__host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg) {
   using C_ = Cfg<BN, CG>;
   SmemLayout L{};
   L.off_a = 0;
   L.off_b = C_::kStages * C_::kStageA;
   L.off_stg = C_::kStages * C_::kStage;
-  L.off_comm = L.off_stg + 4 * kStageWarpBytes;
+  L.off_comm = L.off_stg + (dbl_stg ? 8 : 4) * kStageWarpBytes;  // RS: 2 buffers per warp (TMA reduce)
   const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : 0;
   L.off_bar = L.off_comm + comm;
   const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   using C_ = Cfg<BN, CG>;
   constexpr int BM = C_::kBM;
   constexpr bool kTmaComm = (MODE == MODE_AG && COMM == COMM_TMA);
-  constexpr SmemLayout L = gemm_layout<BN, CG>(kTmaComm);
+  constexpr SmemLayout L = gemm_layout<BN, CG>(kTmaComm, MODE == MODE_RS);
   const int grp = blockIdx.x / args.ctas_per_rank;
   const int lcta = blockIdx.x % args.ctas_per_rank;  // CTA index inside the rank group
   const int wk = lcta / CG;                          // plan worker (CTA pair when CG == 2)
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             const uint64_t tw = args.trace ? globaltimer() : 0;
             while (wp_e < we_e && R.waits[wp_e].x <= k) {
               const int g = R.waits[wp_e].y;
-              if (!(grp == 0 && wp_e == args.skip_wait)) {
+              if (!(grp == 0 && wp_e == args.skip_wait) && !(args.exp & 4)) {
                 for (int s = 0; s < R.W; ++s)
                   if (s != R.rank) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, lcta, g);
               }
@@ -556,8 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             const int64_t off = (lrow0 + (lane >> 3)) * N + col0 + 4 * c;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              dst[i] = okl ? __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+              dst[i] = (okl && !(args.exp & 2)) ? __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
           };
           load_acc(col_base, pa);
 #pragma unroll 1
@@ -590,7 +590,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
                 o.x = pack_bf16x2(x.x, x.y);
                 o.y = pack_bf16x2(x.z, x.w);
                 *reinterpret_cast<uint2*>(cout + base_off + int64_t(i) * 4 * N) = o;
-                st_v4(reinterpret_cast<int4*>(accm + base_off + int64_t(i) * 4 * N), make_int4(0, 0, 0, 0));
+                if (!(args.exp & 1))
+                  st_v4(reinterpret_cast<int4*>(accm + base_off + int64_t(i) * 4 * N), make_int4(0, 0, 0, 0));
               }
             }
             __syncwarp();
@@ -665,6 +666,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         }
       }
       if (!own_tile) {
+      // RS ATOMIC: the TMA unit reduce-adds each staged 32 x 32 fp32 box into the owner's
+      // accumulator (two staging buffers per warp, so staging overlaps the previous reduce).
+      const bool tma_red = MODE == MODE_RS && R.rs_atomic && !(args.exp & 64);  // exp 64: thread red.add
+      int sb = 0;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += CW) {
         uint32_t v[32];
@@ -688,6 +693,23 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         }
         const int64_t col0 = col_base + cc;
         if (col0 >= N) break;  // warp-uniform
+        if (tma_red) {
+          uint4* sg = stg + sb * (4 * kStageWarpBytes / 16);
+          if (lane == 0) bulk_wait_read<1>();  // the reduce that last read buffer sb is done reading
+          __syncwarp();
+          // the TMA 128-B swizzle of a 1024-B-aligned box: 16-B chunk j of row r at j ^ (r & 7)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            sg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA) reads
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&R.tmAcc[owner], sg, int(col0), int(row0 - int64_t(owner) * S));
+            bulk_commit();
+          }
+          sb ^= 1;
+          continue;
+        }
         // stage row `lane` (128 B) with a 16-byte XOR swizzle (conflict-free both ways)
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -700,12 +722,19 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3);
           const uint4 w = stg[r * 8 + (c ^ (r & 7))];
-          if (ok) {
-            if (MODE == MODE_RS && R.rs_atomic)
+          if (ok && !(args.exp & 16)) {
+            if (MODE == MODE_RS && R.rs_atomic && !(args.exp & 8))
               red_add_v4_f32(colp + r * ld_bytes, w.x, w.y, w.z, w.w);
             else
               st_v4(reinterpret_cast<int4*>(colp + r * ld_bytes), make_int4(w.x, w.y, w.z, w.w));
           }
+        }
+        __syncwarp();
+      }
+      if (tma_red) {
+        if (lane == 0) {
+          bulk_wait<0>();              // this warp's reduces performed
+          fence_proxy_async_global();  // async-proxy writes -> the generic release below
         }
         __syncwarp();
       }
@@ -724,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         // CTA barrier is cumulative over the 128 threads' partial-tile stores.
         named_bar_sync(1, 128);
         if (etid == 0) {
-          asm volatile("fence.sc.sys;" ::: "memory");
+          if (!(args.exp & 32)) asm volatile("fence.sc.sys;" ::: "memory");
           const int glo = int(sub0 / R.crows);
           const int ghi = int((sub0 + kSubM - 1) / R.crows);
           for (int g = glo; g <= ghi; ++g) {
@@ -776,7 +805,7 @@ template <int BN, int MODE, int COMM, int CG>
 cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   auto kern = dev::fused_kernel<BN, MODE, COMM, CG>;
   constexpr bool tma_comm = (MODE == MODE_AG && COMM == COMM_TMA);
-  const size_t smem_gemm = dev::gemm_layout<BN, CG>(tma_comm).total;
+  const size_t smem_gemm = dev::gemm_layout<BN, CG>(tma_comm, MODE == MODE_RS).total;
   const size_t smem_comm = (MODE == MODE_AG && COMM != COMM_NONE) ? dev::comm_cta_layout().total : 0;
   const size_t smem = smem_gemm > smem_comm ? smem_gemm : smem_comm;
   static bool attr_set = false;

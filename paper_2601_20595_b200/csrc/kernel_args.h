@@ -41,6 +41,7 @@ struct alignas(64) RankArgs {
   CUtensorMap tmA;      // AG: gathered buffer (current parity) [M, K]; RS/GEMM: A [M, K]
   CUtensorMap tmA_loc;  // AG: local shard [S, K].  RS: this rank's slots [W*S, N] fp32 (32 x 128 boxes)
   CUtensorMap tmB;      // B [N, K]
+  CUtensorMap tmAcc[AO_MAX_WORLD];  // RS ATOMIC: every owner's accumulator [S, N] fp32, 32 x 32 boxes
   const int* order;            // [n_tiles] tile ids in execution order
   const int* wait_off;         // [n_cta + 1] CSR offsets into waits
   const int2* waits;           // (position k, chunk g)
@@ -81,10 +82,14 @@ struct KernelArgs {
   uint32_t* trace_cursor;
   uint32_t trace_cap;
   uint32_t trace_seq;          // launch sequence number stamped into events (kind >> 8)
+  int32_t exp;                 // timing experiments only (ao_debug_set "exp"); 0 in normal runs
   int32_t l2_hint;             // 0: A evict_first / B evict_last (row order); 1: A evict_last / B evict_first
 };
 
 // Host-side launcher (fused.cu).
+// Kernel parameters are passed by value (__grid_constant__); sm_70+ with CUDA >= 12.1 allows 32764 bytes.
+static_assert(sizeof(KernelArgs) <= 32764, "KernelArgs exceeds the kernel parameter limit");
+
 // bn: tile N (128/256); cg: 1 (BM = 128) or 2 (CTA pair, BM = 256); comm: CommKind.
 cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream);
 

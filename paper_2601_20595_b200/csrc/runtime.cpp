@@ -110,7 +110,8 @@ struct DebugKnobs {
   int64_t skip_wait = -1;
   int64_t delay_ns = 0;
   int64_t l2_hint = -1;  // -1: follow the plan's tile order
-  int64_t gemm_group_m = 16;  // ao_gemm GROUP_M (measured best)
+  int64_t gemm_group_m = 16;
+  int64_t exp = 0;  // timing experiments (results invalid when nonzero)  // ao_gemm GROUP_M (measured best)
 };
 DebugKnobs g_debug;
 
@@ -344,9 +345,10 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
     if (s != AO_OK) return s;
   }
   if (!hp.is_ag && ctx && hp.W > 1 && hp.N > 0 && hp.S > 0) {  // RS: peer partials, streamed by the producer
-    if (R->rs_atomic)
+    if (R->rs_atomic) {
       s = encode_2d(&R->tmA_loc, R->peer_acc[hp.rank], hp.S, hp.N, 128, true);
-    else
+      for (int q = 0; q < hp.W && s == AO_OK; ++q) s = encode_2d(&R->tmAcc[q], R->peer_acc[q], hp.S, hp.N, 32, true);
+    } else
       s = encode_2d(&R->tmA_loc, R->peer_data[hp.rank], int64_t(hp.W) * hp.S, hp.N, 128, true);
     if (s != AO_OK) return s;
   }
@@ -387,6 +389,7 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   else if (!strcmp(key, "delay_ns")) g_debug.delay_ns = value;
   else if (!strcmp(key, "l2_hint")) g_debug.l2_hint = value;
   else if (!strcmp(key, "gemm_group_m")) g_debug.gemm_group_m = value;
+  else if (!strcmp(key, "exp")) g_debug.exp = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
   return AO_OK;
 }
@@ -714,6 +717,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   ka->err = p0->ctx->err_dev;
   ka->skip_wait = int32_t(g_debug.skip_wait);
   ka->delay_ns = uint32_t(g_debug.delay_ns);
+  ka->exp = int32_t(g_debug.exp);
   ka->trace = p0->ctx->trace;
   ka->trace_cursor = p0->ctx->trace_cursor;
   ka->trace_cap = p0->ctx->trace_cap;

@@ -1,6 +1,8 @@
 """Full-size parity in the exact launch configuration bench.py times: Llama-3-8B FFN at
 TP=8 (8192 tokens, hidden 4096, ffn 14336), 8 loopback ranks, CE backend, chunk = shard,
-GROUP_M 4, shard-major RS, heuristic tile (256x256 CTA pairs).  The oracle computes sampled
+GROUP_M 4, shard-major RS with the atomic (TMA reduce-add) reduction bench.py uses (and the
+deterministic slots mode), heuristic tile (256x256 CTA pairs).  Plus BASELINE config 5's
+Llama-3-70B TP=8 AG-GEMM shape (M = 32768, reading Q5) at a mid-sweep chunk size.  The oracle computes sampled
 output rows one by one (every chunk-boundary row + seeded random rows of every rank);
 tolerance as in BASELINE.json."""
 import numpy as np
@@ -31,22 +33,23 @@ def _rows(S, chunk, rng, extra=6):
     return np.array(sorted(rows))
 
 
-def _worlds(ao):
+def _worlds(ao, rs_reduce):
     Fl = F // W
     base = dict(world_size=W, M=M, chunk_rows=1024, intra="grouped", group_m=4, n_cta=148 // W,
                 timeout_ns=5_000_000_000)
     ag = dict(base, op="ag_gemm", N=Fl, K=H, backend="ce", n_slices=2)
-    rs = dict(base, op="gemm_rs", N=H, K=Fl, chunk_order="shard_major")
+    rs = dict(base, op="gemm_rs", N=H, K=Fl, chunk_order="shard_major", rs_reduce=rs_reduce)
     ctxs = ao.loopback_world(0, W, max(ao.workspace_bytes(ag), ao.workspace_bytes(rs)))
     pa = [ao.Plan(ctxs[r], dict(ag, rank=r)) for r in range(W)]
     pr = [ao.Plan(ctxs[r], dict(rs, rank=r)) for r in range(W)]
     return ctxs, pa, pr
 
 
-def test_fullsize_ag_and_rs_sampled_vs_oracle(ao):
+@pytest.mark.parametrize("rs_reduce", ["atomic", "slots"])
+def test_fullsize_ag_and_rs_sampled_vs_oracle(ao, rs_reduce):
     Fl = F // W
     S = M // W
-    ctxs, pa, pr = _worlds(ao)
+    ctxs, pa, pr = _worlds(ao, rs_reduce)
     assert pa[0].info()["tile_m"] == 256 and pa[0].info()["tile_n"] == 256
     rng = np.random.default_rng(123)
 
@@ -111,3 +114,28 @@ def test_non_power_of_two_worlds(ao, W2):
         assert ok, f"AG W={W2} r{r}: {e:.3e} {f:.3e}"
         ok, e, f = on.check_tolerance(Ds[r].float().cpu().numpy(), on.gemm_rs(Ar64, Br64, r))
         assert ok, f"RS W={W2} r{r}: {e:.3e} {f:.3e}"
+
+
+@pytest.mark.parametrize("backend", ["tma", "ce"])
+def test_config5_70b_ag_sampled_vs_oracle(ao, backend):
+    """Llama-3-70B TP=8 up-proj: M = 32768 tokens, K = 8192, N = 28672/8 per rank, 256-row
+    chunks (4 MiB), 8 loopback ranks; sampled rows (chunk boundaries + random) of 3 ranks."""
+    W5, M5, K5, N5 = 8, 32768, 8192, 28672 // 8
+    desc = dict(op="ag_gemm", world_size=W5, M=M5, N=N5, K=K5, chunk_rows=256, backend=backend, n_slices=2,
+                intra="grouped", group_m=4, n_cta=148 // W5, timeout_ns=10_000_000_000)
+    ctxs = ao.loopback_world(0, W5, ao.workspace_bytes(desc))
+    plans = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W5)]
+    A, B = si.ag_inputs(W5, M5, K5, N5, salt=5)
+    dA, dB = [a.cuda() for a in A], [b.cuda() for b in B]
+    C = [torch.empty(M5, N5, dtype=torch.bfloat16, device="cuda") for _ in range(W5)]
+    ao.ag_gemm_group(plans, dA, dB, C)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    rng = np.random.default_rng(5)
+    A64 = [si.to_f64(a) for a in A]
+    for r in (0, 3, 7):
+        rows = _rows(M5, 4096, rng, extra=8)
+        ref = on.ag_gemm_rows(A64, si.to_f64(B[r]), rows)
+        ok, e, f = on.check_tolerance(C[r][torch.as_tensor(rows)].float().cpu().numpy(), ref)
+        assert ok, f"config5 {backend} rank {r}: elem {e:.3e} frob {f:.3e}"

@@ -58,7 +58,7 @@ typedef enum {
   AO_ERR_STATE = 7        /* call order violated (e.g. op before ao_ctx_import_handles) */
 } ao_status;
 
-typedef enum { AO_OP_AG_GEMM = 0, AO_OP_GEMM_RS = 1 } ao_op;
+typedef enum { AO_OP_AG_GEMM = 0, AO_OP_GEMM_RS = 1, AO_OP_GEMM_AR = 2 /* NEXT-1 */ } ao_op;
 /* Transfer backends of P:397 / Fig.7.  CE = copy-engine peer memcpy on a side
  * stream with stream-memop flags; TMA = cp.async.bulk peer copies issued from
  * communication warps; LDST = 16-byte vector ld/st over NVSwitch from CUDA cores. */

@@ -11,6 +11,7 @@ out in float64 ("Numerical result"):
 
   AG-GEMM  (P:459 "AllGather--GEMM"; S:184 "gather = concatenation of shards"):
       C_r = concat_p(A_p) . B_r^T
+  GEMM-AR  ("GEMM--AllReduce", NEXT-1):  C = sum_s A_s . B_s^T on every rank
   GEMM-RS  (P:459 "GEMM--ReduceScatter"; S:165/S:168 owner rows are contiguous blocks;
             S:604 "ascending source rank" accumulation order):
       C_shard_r = ( sum_{s=0..W-1} A_s . B_s^T )[r*S:(r+1)*S, :]
@@ -77,6 +78,16 @@ def gemm_rs(As, Bs, rank: int):
 def gemm_rs_all_ranks(As, Bs):
     partials = [gemm(A, B) for A, B in zip(As, Bs)]
     return [reduce_scatter(partials, r) for r in range(len(As))]
+
+
+def gemm_ar(As, Bs):
+    """GEMM->AllReduce ("GEMM--AllReduce"; Fig.4d P:311 partition-based AllReduce):
+    every rank receives the full sum of the partials, C = sum_s A_s . B_s^T (ascending s)."""
+    acc = None
+    for A, B in zip(As, Bs):
+        p = gemm(A, B)
+        acc = p if acc is None else acc + p
+    return acc
 
 
 def gemm_rows(A, B, rows):

@@ -31,6 +31,9 @@ DESIGN.md, deliberately by enumeration rather than closed forms:
                   (north star: "the epilogue of gemm_rs fusing the peer reduction"), so those
                   tiles wait for the W-1 other sources of their chunks.
 
+GEMM-AR is the partition-based AllReduce of Fig.4d: the
+GEMM-RS schedule followed by a pull AllGather of the owners' reduced chunks.
+
 Canonical export: JSON, sorted keys, no whitespace, integers only, strings only for
 enum names.  Parity: not applicable (exact).
 """
@@ -68,7 +71,7 @@ def validate(desc, sm_count=148):
     v = []
     W, r = desc["world_size"], desc["rank"]
     M, N, K, C = desc["M"], desc["N"], desc["K"], desc["chunk_rows"]
-    if desc["op"] not in ("ag_gemm", "gemm_rs"):
+    if desc["op"] not in ("ag_gemm", "gemm_rs", "gemm_ar"):
         v.append("op")
     if W < 1 or W > 8:
         v.append("world_size")
@@ -91,6 +94,12 @@ def validate(desc, sm_count=148):
         v.append("dir")
     if desc["dir"] == "pull" and desc["op"] == "gemm_rs":
         v.append("pull with gemm_rs")
+    if desc["dir"] == "pull" and desc["op"] == "gemm_ar":
+        v.append("pull with gemm_ar")
+    if desc["op"] == "gemm_ar" and desc["backend"] != "ldst":
+        v.append("backend for gemm_ar")
+    if desc["op"] == "gemm_ar" and desc["comm_ctas"] != 0:
+        v.append("comm_ctas with gemm_ar")
     if desc["chunk_order"] not in ("shard_major", "chunk_major"):
         v.append("chunk_order")
     if desc["intra"] not in ("row", "col", "grouped"):
@@ -224,6 +233,17 @@ def _build_plans(desc, chunks):
                 row0, rows, _ = chunks[g]
                 ops.append({"accumulate": 1, "deps": [], "direction": "push", "dst_chunk": [row0, rows],
                             "peer": o, "src_chunk": [row0, rows], "tensor": "P", "variant": "p2p"})
+            if desc["op"] == "gemm_ar":
+                # Partition-based AllReduce (Fig.4d): the ReduceScatter above, then q
+                # fetches every other owner's reduced chunk (owners finish their chunks in
+                # ascending j), owners visited in the Lst.2 rotation q+1, ..., q+W-1.
+                n_c = len(_shard_chunks(chunks, 0)) if W > 0 else 0
+                for j in range(n_c):
+                    for i in range(1, W):
+                        o = (q + i) % W
+                        row0, rows, _ = chunks[_shard_chunks(chunks, o)[j]]
+                        ops.append({"accumulate": 0, "deps": [], "direction": "pull", "dst_chunk": [row0, rows],
+                                    "peer": o, "src_chunk": [row0, rows], "tensor": "C", "variant": "p2p"})
         plans.append(ops)
     return plans
 
@@ -253,7 +273,7 @@ def _arrival_pos(desc, chunks, plans):
         else:
             found = None
             for idx, op in enumerate(plans[r]):
-                if op["src_chunk"] == [row0, rows]:
+                if op["tensor"] == "P" and op["src_chunk"] == [row0, rows]:
                     found = idx
                     break
             assert found is not None
@@ -341,7 +361,10 @@ def plan(desc, sm_count=148):
         owner_regions = [{"A": [[p * S, S]]} for p in range(W)]
     else:
         tensors = {"C": {"elem_bytes": 2, "shape": [M, N]}, "P": {"elem_bytes": 4, "shape": [M, N]}}
-        owner_regions = [{"P": [[0, M]]} for p in range(W)]
+        if desc["op"] == "gemm_ar":  # the reduced rows each owner contributes to the gather
+            owner_regions = [{"C": [[p * S, S]], "P": [[0, M]]} for p in range(W)]
+        else:
+            owner_regions = [{"P": [[0, M]]} for p in range(W)]
 
     out = {
         "op": desc["op"], "world_size": W, "rank": r, "M": M, "N": N, "K": K, "chunk_rows": C,

@@ -17,7 +17,7 @@ AO_HANDLE_BYTES = 256
 
 STATUS = {0: "AO_OK", 1: "AO_ERR_INVALID_ARG", 2: "AO_ERR_UNSUPPORTED", 3: "AO_ERR_CUDA", 4: "AO_ERR_OOM",
           5: "AO_ERR_PEER", 6: "AO_ERR_TIMEOUT", 7: "AO_ERR_STATE"}
-OPS = {"ag_gemm": 0, "gemm_rs": 1}
+OPS = {"ag_gemm": 0, "gemm_rs": 1, "gemm_ar": 2}
 BACKENDS = {"ce": 0, "tma": 1, "ldst": 2}
 DIRS = {"push": 0, "pull": 1}
 CHUNK_ORDERS = {"shard_major": 0, "chunk_major": 1}

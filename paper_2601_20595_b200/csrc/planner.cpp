@@ -17,7 +17,10 @@ const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-static const char* op_name(int op) { return op == AO_OP_AG_GEMM ? "ag_gemm" : "gemm_rs"; }
+static const char* op_name(int op) {
+  return op == AO_OP_AG_GEMM ? "ag_gemm" : (op == AO_OP_GEMM_RS ? "gemm_rs" : "gemm_ar");
+}
+static const char* tensor_name(int t) { return t == TENSOR_A ? "A" : (t == TENSOR_P ? "P" : "C"); }
 static const char* backend_name(int b) { return b == AO_BACKEND_CE ? "ce" : (b == AO_BACKEND_TMA ? "tma" : "ldst"); }
 static const char* dir_name(int d) { return d == AO_DIR_PUSH ? "push" : "pull"; }
 static const char* chunk_order_name(int o) { return o == AO_CHUNK_SHARD_MAJOR ? "shard_major" : "chunk_major"; }
@@ -28,7 +31,7 @@ static int workers(const ao_plan_desc& d, int sm_count) { return d.n_cta > 0 ? d
 std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   std::vector<std::string> v;
   if (d.struct_size != sizeof(ao_plan_desc)) v.push_back("struct_size");
-  if (d.op != AO_OP_AG_GEMM && d.op != AO_OP_GEMM_RS) v.push_back("op");
+  if (d.op != AO_OP_AG_GEMM && d.op != AO_OP_GEMM_RS && d.op != AO_OP_GEMM_AR) v.push_back("op");
   const int W = d.world_size;
   if (W < 1 || W > AO_MAX_WORLD) v.push_back("world_size");
   if (!(d.rank >= 0 && d.rank < std::max(W, 1))) v.push_back("rank");
@@ -41,6 +44,10 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   if (d.backend < AO_BACKEND_CE || d.backend > AO_BACKEND_LDST) v.push_back("backend");
   if (d.dir != AO_DIR_PUSH && d.dir != AO_DIR_PULL) v.push_back("dir");
   if (d.dir == AO_DIR_PULL && d.op == AO_OP_GEMM_RS) v.push_back("pull with gemm_rs");
+  if (d.dir == AO_DIR_PULL && d.op == AO_OP_GEMM_AR) v.push_back("pull with gemm_ar");
+  // GEMM-AR's gather phase is pulled by in-kernel ld/st warps (the RS kernel's smem is full)
+  if (d.op == AO_OP_GEMM_AR && d.backend != AO_BACKEND_LDST) v.push_back("backend for gemm_ar");
+  if (d.op == AO_OP_GEMM_AR && d.comm_ctas != 0) v.push_back("comm_ctas with gemm_ar");
   if (d.chunk_order != AO_CHUNK_SHARD_MAJOR && d.chunk_order != AO_CHUNK_CHUNK_MAJOR) v.push_back("chunk_order");
   if (d.intra < AO_INTRA_ROW || d.intra > AO_INTRA_GROUPED) v.push_back("intra");
   if (d.intra == AO_INTRA_GROUPED && d.group_m < 1) v.push_back("group_m");
@@ -98,8 +105,16 @@ bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
   return have;
 }
 
+size_t ar_reduced_offset(const ao_plan_desc& d) {
+  // after the W slots [W*S, N] fp32 (slots mode); atomic mode keeps the same size so that
+  // the ctx's accumulator region (data half / W) holds [S, N] fp32
+  return size_t(d.M) * size_t(d.N) * 4;
+}
+
 size_t data_bytes_per_parity(const ao_plan_desc& d) {
   if (d.op == AO_OP_AG_GEMM) return size_t(d.M) * size_t(d.K) * 2;  // gathered A
+  if (d.op == AO_OP_GEMM_AR)  // (slots) + the owner's reduced rows [S, N] bf16
+    return ar_reduced_offset(d) + size_t(d.world_size > 0 ? d.M / d.world_size : 0) * size_t(d.N) * 2;
   const size_t eb = d.rs_wire == AO_WIRE_BF16 ? 2 : 4;
   return size_t(d.M) * size_t(d.N) * eb;  // W slots of [S, N]
 }
@@ -107,6 +122,7 @@ size_t data_bytes_per_parity(const ao_plan_desc& d) {
 size_t flag_words_needed(const ao_plan_desc& d) {
   const size_t nch = d.chunk_rows > 0 ? size_t(d.M / d.chunk_rows) : 0;
   if (d.op == AO_OP_AG_GEMM) return nch * size_t(d.backend == AO_BACKEND_CE ? 1 : d.n_slices);
+  if (d.op == AO_OP_GEMM_AR) return nch * size_t(d.world_size) + nch;  // + per-chunk "reduced" flags
   return nch * size_t(d.world_size);
 }
 
@@ -197,6 +213,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
   P.S = d.M / d.world_size;
   P.C = d.chunk_rows;
   P.is_ag = d.op == AO_OP_AG_GEMM;
+  P.is_ar = d.op == AO_OP_GEMM_AR;
   pick_tile(d, sm_count, &P.tile);
   P.n_cta = std::max(1, workers(d, sm_count) / P.tile.cg);
   P.n_chunks = int(P.M / P.C);
@@ -221,7 +238,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
         const int peer = (q + dstep) % W;
         const int src = d.dir == AO_DIR_PUSH ? q : peer;
         const int g = src * n_c + j;
-        ops.push_back(P2POp{peer, int64_t(g) * P.C, P.C, d.dir, 0});
+        ops.push_back(P2POp{peer, int64_t(g) * P.C, P.C, d.dir, 0, TENSOR_A});
       };
       if (d.chunk_order == AO_CHUNK_SHARD_MAJOR) {
         for (int ds = 1; ds < W; ++ds)
@@ -235,7 +252,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
       auto emit = [&](int e, int j) {
         const int o = (q + e + 1) % W;
         const int g = o * n_c + j;
-        ops.push_back(P2POp{o, int64_t(g) * P.C, P.C, AO_DIR_PUSH, 1});
+        ops.push_back(P2POp{o, int64_t(g) * P.C, P.C, AO_DIR_PUSH, 1, TENSOR_P});
       };
       if (d.chunk_order == AO_CHUNK_SHARD_MAJOR) {
         for (int e = 0; e < W; ++e)
@@ -247,6 +264,16 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
           if (j >= 1) emit(W - 1, j - 1);
         }
         if (n_c > 0) emit(W - 1, n_c - 1);
+      }
+      if (P.is_ar) {
+        // GEMM-AR = partition-based AllReduce (Fig.4d): after the ReduceScatter part,
+        // q pulls every other owner's reduced chunk j (owners reduce their chunks in
+        // ascending j), owners in the 1-D rotation q+1, ..., q+W-1 (Lst.2).
+        for (int j = 0; j < n_c; ++j)
+          for (int ds = 1; ds < W; ++ds) {
+            const int o = (q + ds) % W;
+            ops.push_back(P2POp{o, int64_t(o * n_c + j) * P.C, P.C, AO_DIR_PULL, 0, TENSOR_C});
+          }
       }
     }
   }
@@ -368,7 +395,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
       c.put("shape", int_list(std::vector<int64_t>{P.M, P.N}));
       tens.put("A", a.str());
       tens.put("C", c.str());
-    } else {
+    } else {  // RS and AR: output C, fp32 partials P
       Obj c, pp;
       c.put("elem_bytes", 2);
       c.put("shape", int_list(std::vector<int64_t>{P.M, P.N}));
@@ -384,10 +411,12 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
     for (int q = 0; q < W; ++q) {
       if (q) s += ",";
       Obj reg;
-      if (P.is_ag)
+      if (P.is_ag) {
         reg.put("A", "[" + int_list(std::vector<int64_t>{int64_t(q) * P.S, P.S}) + "]");
-      else
+      } else {
+        if (P.is_ar) reg.put("C", "[" + int_list(std::vector<int64_t>{int64_t(q) * P.S, P.S}) + "]");
         reg.put("P", "[" + int_list(std::vector<int64_t>{0, P.M}) + "]");
+      }
       s += reg.str();
     }
     o.put("owner_regions", s + "]");
@@ -407,7 +436,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
         e.put("dst_chunk", int_list(std::vector<int64_t>{op.row0, op.rows}));
         e.put("peer", op.peer);
         e.put("src_chunk", int_list(std::vector<int64_t>{op.row0, op.rows}));
-        e.put_str("tensor", P.is_ag ? "A" : "P");
+        e.put_str("tensor", tensor_name(op.tensor));
         e.put_str("variant", "p2p");
         s += e.str();
       }

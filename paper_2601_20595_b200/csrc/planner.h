@@ -28,11 +28,13 @@ extern const TileShape kTileCandidates[];
 extern const int kNumTileCandidates;
 constexpr int kBK = 64;
 
+enum OpTensor { TENSOR_A = 0, TENSOR_P = 1, TENSOR_C = 2 };
 struct P2POp {
   int peer;
   int64_t row0, rows;
   int direction;  // ao_dir
   int accumulate;
+  int tensor;     // OpTensor: gathered A (AG), fp32 partial P (RS), reduced C (AR gather)
 };
 
 struct HostPlan {
@@ -46,6 +48,7 @@ struct HostPlan {
   int n_cta = 1;  // workers (CTAs, or CTA pairs when cg == 2)
   int n_mb = 0, n_nb = 0, n_tiles = 0;
   bool is_ag = true;
+  bool is_ar = false;  // GEMM-AR: the RS schedule + a pull AllGather of the reduced chunks
   // tables
   std::vector<std::array<int, 5>> chunks;  // g, row0, rows, src_or_owner, pos
   std::vector<std::vector<P2POp>> plans;   // all ranks
@@ -66,6 +69,8 @@ bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out);
 std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPlan* p);
 // Workspace bytes per epoch parity for the data region of this desc.
 size_t data_bytes_per_parity(const ao_plan_desc& d);
+// GEMM-AR: byte offset of the owner's reduced bf16 rows [S, N] inside a data parity half.
+size_t ar_reduced_offset(const ao_plan_desc& d);
 // Flag words per parity this desc needs.
 size_t flag_words_needed(const ao_plan_desc& d);
 

@@ -159,3 +159,22 @@ def test_tolerance_checker_rejects_perturbation():
     drift = ref * (1 + 3e-3)  # Frobenius 3e-3 > 2e-3
     ok, _, f = on.check_tolerance(drift, ref)
     assert not ok and f > 2e-3
+
+
+@pytest.mark.parametrize("W", [1, 2, 3, 8])
+def test_gemm_ar_equals_k_unsharded_closed_form(W):
+    """GEMM-AR (NEXT-1): every rank's result is the full K-unsharded GEMM (all rows)."""
+    M, K_loc, N = 16 * W, 40, 24
+    A, B = si.rs_inputs(W, M, K_loc, N, salt=50 + W)
+    A64 = [si.to_f64(a) for a in A]
+    B64 = [si.to_f64(b) for b in B]
+    full = np.concatenate(A64, axis=1) @ np.concatenate(B64, axis=1).T
+    np.testing.assert_allclose(on.gemm_ar(A64, B64), full, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_gemm_ar_bitmask_provenance(W):
+    M, K_loc, N = 32 * W, 16, 24
+    A, B = si.rs_provenance_inputs(W, M, K_loc, N)
+    out = on.gemm_ar([si.to_f64(a) for a in A], [si.to_f64(b) for b in B])
+    assert out.shape == (M, N) and np.all(out == 2 ** W - 1)

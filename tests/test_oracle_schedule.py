@@ -276,3 +276,35 @@ def test_export_is_canonical_and_deterministic():
     assert " " not in s and "\n" not in s
     assert s == osch.export_json(osch.plan(_desc(rank=1)))
     assert json.loads(s) == p
+
+
+@pytest.mark.parametrize("W", [2, 3, 4, 8])
+@pytest.mark.parametrize("C", [64, 128])
+def test_gemm_ar_gather_plan(W, C):
+    """GEMM-AR (NEXT-1, Fig.4d): the RS part equals gemm_rs's plan; the gather part
+    pulls every other owner's reduced chunk exactly once; at every gather step each owner
+    serves exactly one puller (contention-free rotation); reduce-side tables equal RS."""
+    base = dict(world_size=W, M=256 * W, N=384, K=128, chunk_rows=C, tile_m=128, tile_n=128, n_cta=5,
+                backend="ldst", intra="grouped", group_m=2)
+    S, n_c = 256, 256 // C
+    steps = {}
+    for r in range(W):
+        ar = osch.plan(_desc(op="gemm_ar", rank=r, **base))
+        rs = osch.plan(_desc(op="gemm_rs", rank=r, **base))
+        for key in ("chunks", "deps", "order", "waits", "contrib", "tiles_per_chunk"):
+            assert ar[key] == rs[key], key
+        for q in range(W):
+            n_rs = len(rs["plans"][q])
+            assert ar["plans"][q][:n_rs] == rs["plans"][q]
+            pulls = ar["plans"][q][n_rs:]
+            assert all(op["direction"] == "pull" and op["tensor"] == "C" and not op["accumulate"] for op in pulls)
+            got = sorted(op["src_chunk"][0] for op in pulls)
+            want = sorted(o * S + j * C for o in range(W) if o != q for j in range(n_c))
+            assert got == want
+            assert all(op["peer"] == op["src_chunk"][0] // S for op in pulls)
+            if r == 0:
+                for i, op in enumerate(pulls):
+                    steps.setdefault(i, []).append(op["peer"])
+        assert ar["owner_regions"][r]["C"] == [[r * S, S]]
+    for i, owners in steps.items():
+        assert sorted(owners) == list(range(W)) or len(set(owners)) == W, (i, owners)

@@ -38,6 +38,16 @@ def _sweep():
                                                     intra=intra, group_m=gm, chunk_order=order, dir=dirn,
                                                     tile_m=tile[0], tile_n=tile[1], n_cta=7 if S == 256 else 0,
                                                     backend="ce" if S != 384 else "tma", n_slices=3))
+    # GEMM-AR (NEXT-1): RS schedule + pull gather of the reduced chunks
+    for W in (1, 2, 3, 4, 8):
+        for S, C in ((128, 64), (256, 128), (384, 128), (256, 256)):
+            for order in ("shard_major", "chunk_major"):
+                for red in ("slots", "atomic"):
+                    for tile in ((128, 128), (0, 0)):
+                        out.append(dict(op="gemm_ar", world_size=W, M=S * W, N=392, K=136, chunk_rows=C,
+                                        intra="grouped", group_m=2, chunk_order=order, rs_reduce=red,
+                                        tile_m=tile[0], tile_n=tile[1], n_cta=7 if S == 256 else 0,
+                                        backend="ldst", n_slices=4))
     return out
 
 
@@ -68,7 +78,9 @@ def test_validation_agrees(ao):
     cases = [dict(), dict(M=500), dict(chunk_rows=96), dict(K=100), dict(N=500), dict(op="gemm_rs", dir="pull"),
              dict(tile_m=128, tile_n=0), dict(tile_m=64, tile_n=64), dict(world_size=2, M=192, chunk_rows=32),
              dict(M=0), dict(K=0), dict(world_size=9, M=9 * 128), dict(rank=2), dict(n_slices=0),
-             dict(comm_ctas=200), dict(intra="grouped", group_m=0), dict(chunk_rows=12)]
+             dict(comm_ctas=200), dict(intra="grouped", group_m=0), dict(chunk_rows=12),
+             dict(op="gemm_ar"), dict(op="gemm_ar", backend="ldst"), dict(op="gemm_ar", backend="ldst", dir="pull"),
+             dict(op="gemm_ar", backend="ldst", comm_ctas=4), dict(op="gemm_ar", backend="tma")]
     for kw in cases:
         dd = osch.default_desc(**kw)
         ref_ok = not osch.validate(dd)
@@ -89,6 +101,10 @@ def test_plan_hash_rank_independent(ao):
 def test_workspace_bytes(ao):
     assert ao.workspace_bytes(osch.default_desc(M=512, K=512)) == 2 * 512 * 512 * 2
     assert ao.workspace_bytes(osch.default_desc(op="gemm_rs", M=512, N=384)) == 2 * 512 * 384 * 4
+    # AR: (slots) + the owner's reduced rows [S, N] bf16, per parity
+    ar = osch.default_desc(op="gemm_ar", backend="ldst", M=512, N=384)
+    assert ao.workspace_bytes(ar) == 2 * (512 * 384 * 4 + 256 * 384 * 2)
+    assert ao.workspace_bytes(dict(ar, rs_reduce="atomic")) == 2 * (512 * 384 * 4 + 256 * 384 * 2)
 
 
 def test_library_exports_every_declared_symbol(ao):

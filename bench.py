@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--tp", type=int, default=8, help="logical TP ranks in loopback (N=1)")
     ap.add_argument("--backend", default="ce", choices=["ce", "tma", "ldst"])
     ap.add_argument("--exp", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--no-ar", action="store_true", help="skip the GEMM-AR (NEXT-1) leg")
+    ap.add_argument("--ar-chunk", type=int, default=256, help="GEMM-AR chunk rows")
     ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
     ap.add_argument("--chunk", type=int, default=1024)
     ap.add_argument("--tokens", type=int, default=TOKENS)
@@ -143,9 +145,15 @@ def run_ours(args, rank, world, local_rank):
     ag_desc = dict(base, op="ag_gemm", N=F, K=HIDDEN, backend=args.backend, dir=args.ag_dir, n_slices=2)
     rs_desc = dict(base, op="gemm_rs", N=HIDDEN, K=F, chunk_order=args.rs_order,
                    chunk_rows=args.rs_chunk or args.chunk, rs_reduce=args.rs_reduce)
+    # NEXT-1 row, measured beside the step: GEMM-AR on the down-proj shape
+    # (scripts/ar_probe.py: 256-row chunks in chunk-major order let owners reduce chunk j
+    # mid-kernel so the gather overlaps the GEMM; best of chunk x order x slices)
+    ar_desc = dict(rs_desc, op="gemm_ar", backend="ldst", n_slices=8, chunk_rows=args.ar_chunk,
+                   chunk_order="chunk_major")
     if loop:
-        ag_desc["n_cta"] = rs_desc["n_cta"] = sms // W
-    ws = max(ao.workspace_bytes(ag_desc), ao.workspace_bytes(rs_desc))
+        ag_desc["n_cta"] = rs_desc["n_cta"] = ar_desc["n_cta"] = sms // W
+    ws = max(ao.workspace_bytes(ag_desc), ao.workspace_bytes(rs_desc),
+             0 if args.no_ar else ao.workspace_bytes(ar_desc))
     if loop:
         ctxs = ao.loopback_world(local_rank, W, ws)
         my_ranks = list(range(W))
@@ -254,6 +262,11 @@ def run_ours(args, rank, world, local_rank):
             gemm_only["exposed_comm_ms"] = {"ag_gemm": round(ag_ms - gemm_only["ag_gemm_ms"], 4),
                                             "gemm_rs": round(rs_ms - gemm_only["gemm_rs_ms"], 4)}
 
+    # --- GEMM-AR (NEXT-1) on the down-proj shape, same ctxs ----------------------------
+    ar = None
+    if not args.no_ar:
+        ar = ar_leg(torch, ao, ctxs, my_ranks, ar_desc, Cu, Bd, M, W, args, dev, loop, world, dist)
+
     # --- e2e through the public API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:
@@ -296,6 +309,7 @@ def run_ours(args, rank, world, local_rank):
         "check": check,
         "baseline_kernel_level": baseline,
         "gemm_only": gemm_only,
+        "gemm_ar": ar,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(W, M, budget_s=12.0)
@@ -344,6 +358,49 @@ def loopback_baseline(torch, A, Bu, Bd, Cu, W, M, F, args):
     ms = s.elapsed_time(e) / n
     return {"what": "torch.cat gather + cuBLAS GEMMs + torch reduction (kernel-level, same GPU)",
             "ms_per_step": round(ms, 4), "tflops": round(4.0 * M * FFN * HIDDEN / (ms * 1e-3) / 1e12, 2)}
+
+
+def ar_leg(torch, ao, ctxs, my_ranks, ar_desc, Cu, Bd, M, W, args, dev, loop, world, dist):
+    """NEXT-1: fused GEMM-AllReduce (RS schedule + pull gather of the reduced chunks) on the
+    down-proj shape; every rank ends with the full [M, HIDDEN] output.  Device-timed like
+    the step (CUDA events, max over ranks)."""
+    plans = [ao.Plan(c, dict(ar_desc, rank=r)) for c, r in zip(ctxs, my_ranks)]
+    C = [torch.empty(M, HIDDEN, dtype=torch.bfloat16, device=dev) for _ in my_ranks]
+
+    def run():
+        if loop:
+            ao.gemm_ar_group(plans, Cu, Bd, C)
+        else:
+            ao.gemm_ar(plans[0], Cu[0], Bd[0], C[0])
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(5, args.steps // 2)
+    if world > 1:
+        dist.barrier()
+    s.record()
+    for _ in range(k):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    ms = s.elapsed_time(e) / k
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    flops = 2.0 * M * FFN * HIDDEN / (1 if loop else W)
+    info = plans[0].info()
+    for p in plans:
+        p.close()
+    return {"what": "fused GEMM-AllReduce (NEXT-1), down-proj shape, every rank gets [M, hidden]",
+            "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+            "rs_reduce": ar_desc["rs_reduce"], "chunk_rows": ar_desc["chunk_rows"],
+            "chunk_order": ar_desc["chunk_order"],
+            "tile": [info["tile_m"], info["tile_n"]], "launches": k * (1 if loop else 1)}
 
 
 def gemm_only_leg(torch, ao, pa, pr, A, Bu, Bd, W, M, F, args, dev, loop):

@@ -182,6 +182,19 @@ ao_status ao_ag_gemm_group(int n, ao_plan* const* plans, const void* const* A_sh
 ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
                            void* const* C_shards, void* stream);
 
+/* ---- GEMM-AllReduce (NEXT-1; "GEMM--AllReduce", Fig.4d) -------------------
+ * C[M, N] = sum_s A_s[M, K] . B_s[N, K]^T on EVERY rank (A, B as in ao_gemm_rs; C is the
+ * caller's full [M, N] bf16 output, 16-byte aligned).  Partition-based AllReduce: the
+ * GEMM-RS schedule (peers' fp32 partials pushed / reduce-added to the row owner, fused
+ * owner reduction in the own tiles' epilogue), whose owner also writes its reduced bf16
+ * rows to its symmetric buffer and releases a per-chunk flag; every rank's gather warps
+ * pull the other owners' reduced chunks straight into C.  The plan's op must be
+ * AO_OP_GEMM_AR with backend AO_BACKEND_LDST (gather transport) and comm_ctas == 0;
+ * n_slices splits each gathered chunk.  Same collective rules and errors as ao_gemm_rs. */
+ao_status ao_gemm_ar(ao_plan* plan, const void* A, const void* B, void* C, void* stream);
+ao_status ao_gemm_ar_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
+                           void* const* Cs, void* stream);
+
 /* ---- plain local GEMM through the same tcgen05 mainloop (no communication) -------------
  * C[M, N] = A[M, K] . B[N, K]^T, bf16 in / fp32 accumulate / bf16 out (Lst.1's local
  * kernel).  Used for W = 1 and as the GEMM-only reference of the fused ops.

@@ -5,7 +5,7 @@ The compute path is the C-ABI library libautooverlap.so (include/autooverlap.h);
 package is its thin Python binding.  There is no CPU fallback.
 """
 from .api import (AOError, Context, Plan, ag_gemm, ag_gemm_group, debug_set, dist_world,  # noqa: F401
-                  gemm, gemm_batched, gemm_rs, gemm_rs_group, loopback_world, plan_json, validate, workspace_bytes)
+                  gemm, gemm_ar, gemm_ar_group, gemm_batched, gemm_rs, gemm_rs_group, loopback_world, plan_json, validate, workspace_bytes)
 
-__all__ = ["AOError", "Context", "Plan", "ag_gemm", "ag_gemm_group", "gemm", "gemm_batched", "gemm_rs", "gemm_rs_group",
+__all__ = ["AOError", "Context", "Plan", "ag_gemm", "ag_gemm_group", "gemm", "gemm_ar", "gemm_ar_group", "gemm_batched", "gemm_rs", "gemm_rs_group",
            "loopback_world", "dist_world", "plan_json", "validate", "workspace_bytes", "debug_set"]

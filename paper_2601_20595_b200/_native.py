@@ -91,6 +91,8 @@ _SIGS = {
     "ao_gemm_rs": (ctypes.c_int, [ctypes.c_void_p] * 5),
     "ao_ag_gemm_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 5 + [ctypes.c_void_p]),
     "ao_gemm_rs_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p]),
+    "ao_gemm_ar": (ctypes.c_int, [ctypes.c_void_p] * 5),
+    "ao_gemm_ar_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p]),
     "ao_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
     "ao_gemm_batched": (ctypes.c_int, [ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 3 +

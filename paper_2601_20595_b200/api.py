@@ -178,6 +178,13 @@ def gemm_rs(plan: Plan, A, B, C_shard, stream=None):
     check(lib().ao_gemm_rs(plan.handle, _ptr(A), _ptr(B), _ptr(C_shard), _stream(stream)))
 
 
+def gemm_ar(plan: Plan, A, B, C, stream=None):
+    """ao_gemm_ar (NEXT-1): C[M, N] = sum_s A_s . B_s^T on every rank (partition-based
+    AllReduce fused with the GEMM)."""
+    _require_bf16_cuda(A, B, C)
+    check(lib().ao_gemm_ar(plan.handle, _ptr(A), _ptr(B), _ptr(C), _stream(stream)))
+
+
 def _arr(ts):
     return (ctypes.c_void_p * len(ts))(*[0 if t is None else int(t.data_ptr()) for t in ts])
 
@@ -197,6 +204,11 @@ def ag_gemm_group(plans, A_shards, Bs, Cs, A_gathered_outs=None, stream=None):
 def gemm_rs_group(plans, As, Bs, C_shards, stream=None):
     _require_bf16_cuda(*As, *Bs, *C_shards)
     check(lib().ao_gemm_rs_group(len(plans), _plans(plans), _arr(As), _arr(Bs), _arr(C_shards), _stream(stream)))
+
+
+def gemm_ar_group(plans, As, Bs, Cs, stream=None):
+    _require_bf16_cuda(*As, *Bs, *Cs)
+    check(lib().ao_gemm_ar_group(len(plans), _plans(plans), _arr(As), _arr(Bs), _arr(Cs), _stream(stream)))
 
 
 def gemm(A, B, C=None, tile_n: int = 0, tile_m: int = 0, stream=None):

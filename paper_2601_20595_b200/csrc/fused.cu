@@ -159,12 +159,17 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
     if (A.delay_ns && lane == 0) inject_delay(A.delay_ns, uint32_t(i));  // fault injection
     __syncwarp();
     const CommItem it = R.comm_items[i];
-    const char* src = (it.kind == ITEM_PULL ? R.peer_data[it.peer] : R.A_shard) + it.src_off;
-    char* dst = R.peer_data[it.kind == ITEM_PUSH ? it.peer : R.rank] + it.dst_off;
-    if (it.kind == ITEM_PULL) {
-      // PULL (Lst.2): the source staged its chunk and released its ready flag
+    const bool remote_src = it.kind == ITEM_PULL || it.kind == ITEM_AR_PULL;
+    const char* src = (remote_src ? R.peer_data[it.peer] : R.A_shard) + it.src_off;
+    char* dst = it.kind == ITEM_AR_PULL ? R.ar_out + it.dst_off
+                                        : R.peer_data[it.kind == ITEM_PUSH ? it.peer : R.rank] + it.dst_off;
+    if (remote_src) {
+      // PULL (Lst.2): the source staged its chunk and released its ready flag;
+      // AR_PULL: the owner reduced its chunk and released its "reduced" flag
       if (lane == 0) {
-        spin_flag(R.peer_flags[it.peer] + it.g * R.n_slices + it.slice, R.epoch, A, R.rank, -1 - worker, it.g);
+        const uint32_t* f = R.peer_flags[it.peer] +
+                            (it.kind == ITEM_PULL ? it.g * R.n_slices + it.slice : R.n_chunks * R.W + it.g);
+        spin_flag(f, R.epoch, A, R.rank, -1 - worker, it.g);
         fence_proxy_async_global();  // generic-proxy acquire -> bulk (async-proxy) reads
       }
       __syncwarp();
@@ -179,7 +184,7 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t j = base + u * 32 + lane;
-          if (j < n) v[u] = it.kind == ITEM_PULL ? __ldcg(s + j) : ld_nc_v4(s + j);  // peer data: coherent
+          if (j < n) v[u] = remote_src ? __ldcg(s + j) : ld_nc_v4(s + j);  // peer data: coherent
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -222,8 +227,10 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
       __syncwarp();
     }
     if (lane == 0) {
-      uint32_t* f = it.kind == ITEM_PUSH ? R.peer_flags[it.peer] : R.flags;
-      st_release_sys(f + it.g * R.n_slices + it.slice, R.epoch);
+      if (it.kind != ITEM_AR_PULL) {
+        uint32_t* f = it.kind == ITEM_PUSH ? R.peer_flags[it.peer] : R.flags;
+        st_release_sys(f + it.g * R.n_slices + it.slice, R.epoch);
+      }
       trace_event(A, TR_COMM, R.rank, worker, i, t_item);
     }
     __syncwarp();
@@ -590,6 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
                 o.x = pack_bf16x2(x.x, x.y);
                 o.y = pack_bf16x2(x.z, x.w);
                 *reinterpret_cast<uint2*>(cout + base_off + int64_t(i) * 4 * N) = o;
+                if (R.ar)  // GEMM-AR: the reduced rows peers gather
+                  *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(R.ar_red) + base_off + int64_t(i) * 4 * N) = o;
                 if (!(args.exp & 1))
                   st_v4(reinterpret_cast<int4*>(accm + base_off + int64_t(i) * 4 * N), make_int4(0, 0, 0, 0));
               }
@@ -659,7 +668,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             for (int i = 0; i < 4; ++i) {
               const int rr = i * 8 + (lane >> 2);
               const uint4 w = stg[rr * 4 + (c ^ ((rr >> 1) & 3))];
-              if (ok) st_v4(reinterpret_cast<int4*>(colp + rr * N * 2), make_int4(w.x, w.y, w.z, w.w));
+              if (ok) {
+                st_v4(reinterpret_cast<int4*>(colp + rr * N * 2), make_int4(w.x, w.y, w.z, w.w));
+                if (R.ar)  // GEMM-AR: the reduced rows peers gather
+                  st_v4(reinterpret_cast<int4*>(colp - reinterpret_cast<char*>(R.C) + R.ar_red + rr * N * 2),
+                        make_int4(w.x, w.y, w.z, w.w));
+              }
             }
             __syncwarp();
           }
@@ -767,12 +781,38 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           }
         }
       }
+      if (MODE == MODE_RS && own_tile && R.ar && R.W > 1) {
+        // GEMM-AR: count this own sub-tile into its chunks; the last one releases the
+        // owner's "reduced" flag of chunk g (word n_chunks*W + g), which peers' gather
+        // warps acquire before pulling the rows (Fig.4d).
+        named_bar_sync(1, 128);
+        if (etid == 0) {
+          asm volatile("fence.sc.sys;" ::: "memory");
+          const int glo = int(sub0 / R.crows);
+          const int ghi = int((sub0 + kSubM - 1) / R.crows);
+          for (int g = glo; g <= ghi; ++g) {
+            uint32_t old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.counters + g) : "memory");
+            if (int(old) + 1 == R.tiles_per_chunk[g]) {
+              R.counters[g] = 0;
+              st_release_sys(R.flags + R.n_chunks * R.W + g, R.epoch);
+            }
+          }
+        }
+      }
       if (etid == 0) trace_event(args, TR_EPI, R.rank, lcta, t, t_epi);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   } else {
     // ================================================================ co-located comm warps
+    if constexpr (MODE == MODE_RS) {
+      if (R.ar && R.n_comm_items > 0) {  // GEMM-AR gather: ld/st pulls of reduced chunks
+        const int cw = warp - kCommWarp0;
+        comm_worker<COMM_LDST>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps, nullptr,
+                               0, nullptr);
+      }
+    }
     if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {
       if (args.comm_ctas_per_rank == 0) {
         const int cw = warp - kCommWarp0;

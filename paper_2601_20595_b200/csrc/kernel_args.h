@@ -31,7 +31,9 @@ struct ErrorInfo {
 // buffer, release the peer's flag.  STAGE (pull plans): local shard -> own gathered buffer
 // (the region peers pull from), release the own flag ("ready").  PULL: wait for the source
 // peer's ready flag, peer's gathered buffer -> own gathered buffer, release the own flag.
-enum ItemKind : int32_t { ITEM_PUSH = 0, ITEM_STAGE = 1, ITEM_PULL = 2 };
+// AR_PULL (GEMM-AR gather): wait for the owner's "reduced" flag of chunk g, copy the
+// owner's reduced rows into this rank's output C (no flag released).
+enum ItemKind : int32_t { ITEM_PUSH = 0, ITEM_STAGE = 1, ITEM_PULL = 2, ITEM_AR_PULL = 3 };
 struct CommItem {
   int32_t peer, g, slice, kind;     // peer: destination (PUSH) or source (PULL) rank
   int64_t src_off, dst_off, bytes;  // byte offsets (src: local shard or peer buffer, dst: buffer)
@@ -53,6 +55,9 @@ struct alignas(64) RankArgs {
   uint32_t* flags;             // this rank's flag words (current parity)
   uint32_t* peer_flags[AO_MAX_WORLD];  // every rank's flag words (current parity)
   char* peer_data[AO_MAX_WORLD];       // every rank's data half (current parity)
+  int32_t ar;        // GEMM-AR: RS + pull gather of the reduced chunks
+  char* ar_out;      // GEMM-AR: the caller's full output C [M, N] bf16 (gather destination)
+  char* ar_red;      // GEMM-AR: this rank's reduced rows [S, N] bf16 in its symmetric buffer
   char* peer_acc[AO_MAX_WORLD];        // RS ATOMIC: every rank's accumulator [S, N] fp32 (current parity)
   uint32_t* counters;                  // RS: local per-chunk completion counters
   int64_t M, N, K, S;

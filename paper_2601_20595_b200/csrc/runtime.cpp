@@ -216,6 +216,30 @@ ao_status upload_tables(ao_plan* p) {
     }
     p->comm_kind = hp.desc.backend == AO_BACKEND_TMA ? ao::COMM_TMA : ao::COMM_LDST;
   }
+  if (hp.is_ar && hp.W > 1) {
+    // GEMM-AR gather (Fig.4d): pull each other owner's reduced chunk, in plan order, from the
+    // owner's reduced region into this rank's C (slices spread over the gather warps).
+    const int64_t row_bytes = hp.N * 2;
+    const int64_t chunk_bytes = int64_t(hp.C) * row_bytes;
+    const int ns = hp.desc.n_slices;
+    const int64_t slice = ((chunk_bytes + ns - 1) / ns + 15) / 16 * 16;
+    const int64_t red_off = int64_t(ao::ar_reduced_offset(hp.desc));
+    for (const ao::P2POp& op : hp.plans[hp.rank]) {
+      if (op.tensor != ao::TENSOR_C) continue;
+      for (int sl = 0; sl < ns; ++sl) {
+        ao::CommItem it{};
+        it.kind = ao::ITEM_AR_PULL;
+        it.peer = op.peer;
+        it.g = int(op.row0 / hp.C);
+        it.slice = sl;
+        const int64_t off = std::min<int64_t>(int64_t(sl) * slice, chunk_bytes);
+        it.bytes = std::max<int64_t>(0, std::min<int64_t>(slice, chunk_bytes - off));
+        it.src_off = red_off + (op.row0 - int64_t(op.peer) * hp.S) * row_bytes + off;
+        it.dst_off = op.row0 * row_bytes + off;
+        comm.push_back(it);
+      }
+    }
+  }
   p->n_comm = int(comm.size());
 
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
@@ -353,6 +377,13 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
     if (s != AO_OK) return s;
   }
   R->C = C;
+  if (hp.is_ar) {
+    // the own rows of the full output are written by the fused reduction like a C_shard
+    R->ar = 1;
+    R->ar_out = static_cast<char*>(C);
+    R->C = static_cast<char*>(C) + int64_t(hp.rank) * hp.S * hp.N * 2;
+    if (ctx) R->ar_red = R->peer_data[hp.rank] + ao::ar_reduced_offset(hp.desc);
+  }
   return AO_OK;
 }
 
@@ -685,13 +716,16 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
 
 // ------------------------------------------------------------------------------ op calls
 static ao_status launch_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
-                              void* const* Cs, void* const* Gouts, void* stream_v, int mode) {
+                              void* const* Cs, void* const* Gouts, void* stream_v, int op) {
+  const int mode = op == AO_OP_AG_GEMM ? ao::MODE_AG : ao::MODE_RS;  // GEMM-AR runs the RS kernel
   if (n < 1 || n > AO_MAX_WORLD || !plans) return fail(AO_ERR_INVALID_ARG, "bad group size %d", n);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   ao_plan* p0 = plans[0];
   if (!p0 || !p0->ctx) return fail(AO_ERR_STATE, "plan is not bound to a ctx");
   const ao::HostPlan& h0 = p0->hp;
-  if ((mode == ao::MODE_AG) != h0.is_ag) return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is %s", h0.is_ag ? "ag_gemm" : "gemm_rs");
+  if (h0.desc.op != op)
+    return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is %s",
+                h0.is_ag ? "ag_gemm" : (h0.is_ar ? "gemm_ar" : "gemm_rs"));
   for (int i = 0; i < n; ++i) {
     ao_plan* p = plans[i];
     if (!p || !p->ctx) return fail(AO_ERR_STATE, "plan %d not bound", i);
@@ -887,21 +921,30 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
 
 ao_status ao_ag_gemm_group(int n, ao_plan* const* plans, const void* const* A_shards, const void* const* Bs,
                            void* const* Cs, void* const* Gouts, void* stream) {
-  return launch_group(n, plans, A_shards, Bs, Cs, Gouts, stream, ao::MODE_AG);
+  return launch_group(n, plans, A_shards, Bs, Cs, Gouts, stream, AO_OP_AG_GEMM);
 }
 
 ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
                            void* const* C_shards, void* stream) {
-  return launch_group(n, plans, As, Bs, C_shards, nullptr, stream, ao::MODE_RS);
+  return launch_group(n, plans, As, Bs, C_shards, nullptr, stream, AO_OP_GEMM_RS);
+}
+
+ao_status ao_gemm_ar_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
+                           void* const* Cs, void* stream) {
+  return launch_group(n, plans, As, Bs, Cs, nullptr, stream, AO_OP_GEMM_AR);
 }
 
 ao_status ao_ag_gemm(ao_plan* plan, const void* A_shard, const void* B, void* C, void* A_gathered_out, void* stream) {
   void* g[1] = {A_gathered_out};
-  return launch_group(1, &plan, &A_shard, &B, &C, g, stream, ao::MODE_AG);
+  return launch_group(1, &plan, &A_shard, &B, &C, g, stream, AO_OP_AG_GEMM);
 }
 
 ao_status ao_gemm_rs(ao_plan* plan, const void* A, const void* B, void* C_shard, void* stream) {
-  return launch_group(1, &plan, &A, &B, &C_shard, nullptr, stream, ao::MODE_RS);
+  return launch_group(1, &plan, &A, &B, &C_shard, nullptr, stream, AO_OP_GEMM_RS);
+}
+
+ao_status ao_gemm_ar(ao_plan* plan, const void* A, const void* B, void* C, void* stream) {
+  return launch_group(1, &plan, &A, &B, &C, nullptr, stream, AO_OP_GEMM_AR);
 }
 
 // ----------------------------------------------------------------------- plain GEMM entry

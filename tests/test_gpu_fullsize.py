@@ -139,3 +139,29 @@ def test_config5_70b_ag_sampled_vs_oracle(ao, backend):
         ref = on.ag_gemm_rows(A64, si.to_f64(B[r]), rows)
         ok, e, f = on.check_tolerance(C[r][torch.as_tensor(rows)].float().cpu().numpy(), ref)
         assert ok, f"config5 {backend} rank {r}: elem {e:.3e} frob {f:.3e}"
+
+
+def test_fullsize_gemm_ar_sampled_vs_oracle(ao):
+    """GEMM-AR (NEXT-1) on the down-proj shape at TP=8 in the bench's configuration: every
+    rank's full [M, hidden] output; sampled rows of every owner block on 3 ranks."""
+    Fl, S = F // W, M // W
+    desc = dict(op="gemm_ar", world_size=W, M=M, N=H, K=Fl, chunk_rows=1024, intra="grouped", group_m=4,
+                n_cta=148 // W, backend="ldst", n_slices=8, rs_reduce="atomic", timeout_ns=5_000_000_000)
+    ctxs = ao.loopback_world(0, W, ao.workspace_bytes(desc))
+    plans = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
+    Ar, Bd = si.rs_inputs(W, M, Fl, H)
+    dA, dB = [a.cuda() for a in Ar], [b.cuda() for b in Bd]
+    C = [torch.empty(M, H, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    for _ in range(2):
+        ao.gemm_ar_group(plans, dA, dB, C)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    rng = np.random.default_rng(77)
+    Bd64 = [si.to_f64(b) for b in Bd]
+    rows = np.concatenate([o * S + _rows(S, 512, rng, extra=2) for o in range(W)])
+    A_rows = [si.to_f64(Ar[s][torch.as_tensor(rows)]) for s in range(W)]
+    ref = on.gemm_rs_from_rows(A_rows, Bd64)  # sum_s A_s[rows] . B_s^T, ascending s
+    for r in (0, 3, 7):
+        ok, e, f = on.check_tolerance(C[r][torch.as_tensor(rows)].float().cpu().numpy(), ref)
+        assert ok, f"AR rank {r}: elem {e:.3e} frob {f:.3e}"

@@ -409,3 +409,63 @@ def test_ag_gemm_pull_dedicated_comm_ctas(ao):
     for r in range(W):
         _check(Cs[r], on.ag_gemm(A64, si.to_f64(B[r])), f"ag pull comm_ctas r{r}")
         assert torch.equal(G[r].cpu(), torch.cat(A, 0))
+
+
+# ------------------------------------------------------------------------ GEMM-AR (NEXT-1)
+def _ar_world(ao, W, M, N, K, chunk, **kw):
+    desc = dict(op="gemm_ar", world_size=W, M=M, N=N, K=K, chunk_rows=chunk, backend="ldst", n_slices=4,
+                n_cta=max(1, 148 // W), timeout_ns=2_000_000_000, **kw)
+    ctxs = ao.loopback_world(0, W, ao.workspace_bytes(desc))
+    return ctxs, [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
+
+
+def _run_ar(ao, ctxs, plans, A, B):
+    M, N = A[0].shape[0], B[0].shape[0]
+    Cs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in plans]
+    ao.gemm_ar_group(plans, A, B, Cs)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    return Cs
+
+
+@pytest.mark.parametrize("rs_reduce", ["atomic", "slots"])
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_gemm_ar_vs_oracle(ao, W, tile, rs_reduce):
+    """GEMM-AR: every rank's full C equals the fp64 sum of the partials (all rows)."""
+    M, K, N, C = 256 * W, 256, 520, 64
+    A, B = si.rs_inputs(W, M, K, N, salt=41)
+    ctxs, plans = _ar_world(ao, W, M, N, K, C, tile_m=tile[0], tile_n=tile[1], rs_reduce=rs_reduce)
+    dA, dB = _dev(A), _dev(B)
+    ref = on.gemm_ar([si.to_f64(a) for a in A], [si.to_f64(b) for b in B])
+    for it in range(2):  # both parities
+        Cs = _run_ar(ao, ctxs, plans, dA, dB)
+        for r in range(W):
+            _check(Cs[r], ref, f"ar W={W} {rs_reduce} it={it} rank {r}")
+        for r in range(1, W):  # the gathered rows are copies of the owners' rows: bit-identical
+            assert torch.equal(Cs[r].cpu(), Cs[0].cpu())
+
+
+@pytest.mark.parametrize("rs_reduce", ["atomic", "slots"])
+def test_gemm_ar_bitmask_epochs_and_chunk_major(ao, rs_reduce):
+    W, M, K, N = 4, 1024, 64, 256
+    ctxs, plans = _ar_world(ao, W, M, N, K, 128, chunk_order="chunk_major", rs_reduce=rs_reduce)
+    A, B = si.rs_provenance_inputs(W, M, K, N)
+    dA, dB = _dev(A), _dev(B)
+    for it in range(4):
+        Cs = _run_ar(ao, ctxs, plans, dA, dB)
+        for r in range(W):
+            assert torch.all(Cs[r].float() == 2 ** W - 1), (it, r)
+
+
+def test_gemm_ar_rejects_wrong_op_and_backend(ao):
+    W, M, K, N = 2, 512, 64, 256
+    ctxs, plans = _ar_world(ao, W, M, N, K, 64)
+    A = [torch.zeros(M, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    B = [torch.zeros(N, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    C = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    with pytest.raises(ao.AOError, match="INVALID_ARG"):
+        ao.gemm_rs_group(plans, A, B, C)  # an AR plan is not an RS plan
+    with pytest.raises(ao.AOError, match="INVALID_ARG"):
+        ao.Plan(ctxs[0], dict(plans[0].desc, backend="ce"))  # gather transport is ld/st

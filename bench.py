@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--ar-chunk", type=int, default=256, help="GEMM-AR chunk rows")
     ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
     ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--sched", default="time", choices=["time", "space"],
+                    help="loopback group schedule: time-sliced (all SMs per rank) or space-sliced (SMs/W per rank)")
     ap.add_argument("--tokens", type=int, default=TOKENS)
     ap.add_argument("--intra", default="grouped", choices=["row", "col", "grouped"])
     ap.add_argument("--group-m", type=int, default=4)
@@ -151,7 +153,13 @@ def run_ours(args, rank, world, local_rank):
     ar_desc = dict(rs_desc, op="gemm_ar", backend="ldst", n_slices=8, chunk_rows=args.ar_chunk,
                    chunk_order="chunk_major")
     if loop:
-        ag_desc["n_cta"] = rs_desc["n_cta"] = ar_desc["n_cta"] = sms // W
+        # time-sliced (default): every rank's plan spans all SMs and the group launch runs the
+        # ranks' tile lists in one global order; space-sliced: SMs // W CTAs per rank
+        ar_desc["n_cta"] = sms // W
+        ag_desc["n_cta"] = rs_desc["n_cta"] = sms if args.sched == "time" else sms // W
+        if args.sched == "time":
+            for d in (ag_desc, rs_desc):
+                d["tile_m"], d["tile_n"] = 256, 256
     ws = max(ao.workspace_bytes(ag_desc), ao.workspace_bytes(rs_desc),
              0 if args.no_ar else ao.workspace_bytes(ar_desc))
     if loop:
@@ -289,7 +297,7 @@ def run_ours(args, rank, world, local_rank):
                    "tokens": M, "hidden": HIDDEN, "ffn": FFN, "tp": W, "ranks_per_gpu": W if loop else 1,
                    "backend_ag": args.backend, "ag_dir": args.ag_dir, "chunk_rows": args.chunk, "rs_chunk_rows": args.rs_chunk or args.chunk,
                    "intra": args.intra, "group_m": args.group_m, "rs_chunk_order": args.rs_order,
-                   "rs_reduce": args.rs_reduce,
+                   "rs_reduce": args.rs_reduce, "group_schedule": (args.sched + "-sliced") if loop else "one rank per GPU",
                    "tile": [pa[0].info()["tile_m"], pa[0].info()["tile_n"]], "cta_group": pa[0].info()["cta_group"],
                    "workers_per_rank": pa[0].info()["n_cta"],
                    "ctas_per_rank": pa[0].info()["n_cta"] * pa[0].info()["cta_group"],

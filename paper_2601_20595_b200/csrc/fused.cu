@@ -237,6 +237,64 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
   }
 }
 
+// ---- tile walk --------------------------------------------------------------------------
+// Calls f(R, grp, k) for every tile position this worker runs, in order.  Space-sliced:
+// positions wk, wk + n_wk, ... of its own rank group's list (Lst.1).
+// Time-sliced: global indices wk, wk + n_wk, ... of the launch's segment list.
+template <class F>
+__device__ __forceinline__ void for_tiles(const KernelArgs& a, int grp, int wk, int n_wk, F&& f) {
+  if (a.n_seg == 0) {
+    const RankArgs& R = a.rk[grp];
+    for (int k = wk; k < R.n_tiles; k += n_wk) f(R, grp, k);
+  } else {
+    int si = 0;
+    for (int i = wk; i < a.n_total; i += n_wk) {
+      while (i >= a.seg[si].o + (a.seg[si].k1 - a.seg[si].k0)) ++si;
+      const int g = a.seg[si].g;
+      f(a.rk[g], g, a.seg[si].k0 + (i - a.seg[si].o));
+    }
+  }
+}
+
+// Time-sliced chunk waits (dependency rule 4: a tile depends on every chunk its rows
+// intersect): before the first tile of this worker that needs chunk g of rank group grp,
+// acquire g's flags; later tiles needing g are covered by program order.
+// `got` caches the acquired chunks (bit g of got[grp], chunks g < 64; others re-checked).
+struct WaitCache {
+  uint64_t got[AO_MAX_WORLD];
+  __device__ void reset() {
+    for (int i = 0; i < AO_MAX_WORLD; ++i) got[i] = 0;
+  }
+  __device__ bool has(int grp, int g) const { return g < 64 && ((got[grp] >> g) & 1u); }
+  __device__ void set(int grp, int g) {
+    if (g < 64) got[grp] |= 1ull << g;
+  }
+};
+
+// AG: the remote chunks of rows [r0, r1); returns true if it waited on anything.
+__device__ __noinline__ bool ts_wait_ag(const RankArgs& R, const KernelArgs& A, WaitCache& wc, int grp, int cta,
+                                        int64_t r0, int64_t r1) {
+  bool waited = false;
+  for (int g = int(r0 / R.crows); g <= int((r1 - 1) / R.crows); ++g) {
+    if ((int64_t(g) * R.crows) / R.S == R.rank || wc.has(grp, g)) continue;
+    for (int s = 0; s < R.n_slices; ++s) spin_flag(R.flags + g * R.n_slices + s, R.epoch, A, R.rank, cta, g);
+    wc.set(grp, g);
+    waited = true;
+  }
+  return waited;
+}
+
+// RS: every other source's completion flag of the chunks of own rows [r0, r1).
+__device__ __noinline__ void ts_wait_rs(const RankArgs& R, const KernelArgs& A, WaitCache& wc, int grp, int cta,
+                                        int64_t r0, int64_t r1) {
+  for (int g = int(r0 / R.crows); g <= int((r1 - 1) / R.crows); ++g) {
+    if (wc.has(grp, g)) continue;
+    for (int s = 0; s < R.W; ++s)
+      if (s != R.rank) spin_flag(R.flags + g * R.W + s, R.epoch, A, R.rank, cta, g);
+    wc.set(grp, g);
+  }
+}
+
 // RS: 32-column blocks of tile column nb that hold valid columns (the streamed peer
 // partial boxes of an own tile).
 template <int BN>
@@ -252,7 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   uint8_t* smem = align1024(smem_raw);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int gemm_ctas = args.n_group * args.ctas_per_rank;
+  const bool ts = args.n_seg > 0;  // time-sliced group: every GEMM CTA serves every rank
+  const int gemm_ctas = ts ? args.ctas_per_rank : args.n_group * args.ctas_per_rank;
 
   // ------------------------------------------------------------------ dedicated comm CTA
   if (int(blockIdx.x) >= gemm_ctas) {
@@ -284,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   const int n_wk = args.ctas_per_rank / CG;
   const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // 0 = leader (even CTA)
   const bool leader = crank == 0;
-  const RankArgs& R = args.rk[grp];
+  const RankArgs& R0 = args.rk[grp];  // shapes (equal across the group: same plan hash)
 
   uint8_t* sA = smem + L.off_a;
   uint8_t* sB = smem + L.off_b;
@@ -297,12 +356,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.off_slot);
 
   if (warp == 0 && lane == 0) {
-    if (R.K > 0) {
-      prefetch_tmap(&R.tmA);
-      prefetch_tmap(&R.tmB);
-      if (MODE == MODE_AG) prefetch_tmap(&R.tmA_loc);
+    for (int g = ts ? 0 : grp; g < (ts ? args.n_group : grp + 1); ++g) {
+      const RankArgs& R = args.rk[g];
+      if (R.K > 0) {
+        prefetch_tmap(&R.tmA);
+        prefetch_tmap(&R.tmB);
+        if (MODE == MODE_AG) prefetch_tmap(&R.tmA_loc);
+      }
+      if (MODE == MODE_RS && R.W > 1) prefetch_tmap(&R.tmA_loc);
     }
-    if (MODE == MODE_RS && R.W > 1) prefetch_tmap(&R.tmA_loc);
   }
   if (warp == 1) {
     if (lane == 0) {
@@ -335,9 +397,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int64_t K = R.K, N = R.N, S = R.S;
+  const int64_t K = R0.K, N = R0.N, S = R0.S, M = R0.M;
   const int nkb = int((K + kBK - 1) / kBK);
-  const int n_tiles = R.n_tiles;
 
   if (warp == 0) {
     // ================================================================ TMA producer
@@ -351,13 +412,23 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       uint32_t stage = 0, phase = 0;
       int wp = 0, we = 0;
       if constexpr (MODE != MODE_GEMM) {
-        wp = R.wait_off[wk];
-        we = R.wait_off[wk + 1];
+        if (!ts) {
+          wp = R0.wait_off[wk];
+          we = R0.wait_off[wk + 1];
+        }
       }
-      for (int k = wk; k < n_tiles; k += n_wk) {
+      WaitCache wc;
+      wc.reset();
+      for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
         if constexpr (MODE == MODE_AG) {
           bool waited = false;
-          while (wp < we && R.waits[wp].x == k) {
+          if (ts) {
+            const int64_t r0 = int64_t(R.order[k] / R.n_nb) * BM;
+            const uint64_t tw = args.trace ? globaltimer() : 0;
+            waited = ts_wait_ag(R, args, wc, grp, lcta, r0, r0 + BM < M ? r0 + BM : M);
+            if (waited) trace_event(args, TR_WAIT, R.rank, lcta, int(r0 / R.crows), tw);
+          }
+          while (!ts && wp < we && R.waits[wp].x == k) {
             const int g = R.waits[wp].y;
             const uint64_t tw = args.trace ? globaltimer() : 0;
             if (!(grp == 0 && wp == args.skip_wait)) {
@@ -406,7 +477,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           const int64_t sub0 = int64_t(mb) * BM + int64_t(crank) * kSubM;
           if (R.W > 1 && !R.rs_atomic && sub0 / S == R.rank) {
             const uint64_t tw = args.trace ? globaltimer() : 0;
-            while (wp < we && R.waits[wp].x == k) {
+            if (ts) {
+              const int64_t r0 = int64_t(mb) * BM;
+              ts_wait_rs(R, args, wc, grp, lcta, r0, r0 + BM < M ? r0 + BM : M);
+            }
+            while (!ts && wp < we && R.waits[wp].x == k) {
               const int g = R.waits[wp].y;
               if (!(grp == 0 && wp == args.skip_wait)) {
                 for (int s = 0; s < R.W; ++s)
@@ -434,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           }
         }
         trace_event(args, TR_LOAD, R.rank, lcta, t, t_load);
-      }
+      });
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer
@@ -443,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       // full[] completes only on operand uses of a slot (RS partial stages use pfull[]),
       // so its parity is tracked per slot.
       uint32_t stage = 0, fpar = 0, acc = 0, acc_phase = 0;
-      for (int k = wk; k < n_tiles; k += n_wk) {
+      for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
         const uint64_t t_mma = args.trace ? globaltimer() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -488,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }
+      });
     }
   } else if (warp < kCommWarp0) {
     // ================================================================ epilogue
@@ -505,10 +580,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     uint32_t rs_stage = 0, ppar = 0;  // RS: replay of the producer's ring position, pfull parities
     int wp_e = 0, we_e = 0;           // RS ATOMIC: the epilogue walks the own-tile waits itself
     if constexpr (MODE == MODE_RS) {
-      wp_e = R.wait_off[wk];
-      we_e = R.wait_off[wk + 1];
+      if (!ts) {
+        wp_e = R0.wait_off[wk];
+        we_e = R0.wait_off[wk + 1];
+      }
     }
-    for (int k = wk; k < n_tiles; k += n_wk) {
+    WaitCache wc;
+    if (etid == 0) wc.reset();
+    for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
       const int t = R.order[k];
       const int mb = t / R.n_nb;
       const int nb = t - mb * R.n_nb;
@@ -541,7 +620,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           // i*4 + l/8, columns 4*(l%8)..+3), store bf16, and re-arm the accumulator (zeros).
           if (etid == 0) {
             const uint64_t tw = args.trace ? globaltimer() : 0;
-            while (wp_e < we_e && R.waits[wp_e].x <= k) {
+            if (ts && !(args.exp & 4)) {
+              const int64_t r0 = int64_t(mb) * BM;
+              ts_wait_rs(R, args, wc, grp, lcta, r0, r0 + BM < M ? r0 + BM : M);
+            }
+            while (!ts && wp_e < we_e && R.waits[wp_e].x <= k) {
               const int g = R.waits[wp_e].y;
               if (!(grp == 0 && wp_e == args.skip_wait) && !(args.exp & 4)) {
                 for (int s = 0; s < R.W; ++s)
@@ -803,9 +886,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       if (etid == 0) trace_event(args, TR_EPI, R.rank, lcta, t, t_epi);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
+    });
   } else {
     // ================================================================ co-located comm warps
+    const RankArgs& R = R0;
     if constexpr (MODE == MODE_RS) {
       if (R.ar && R.n_comm_items > 0) {  // GEMM-AR gather: ld/st pulls of reduced chunks
         const int cw = warp - kCommWarp0;
@@ -856,7 +940,8 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(args.n_group * (args.ctas_per_rank + args.comm_ctas_per_rank));
+  cfg.gridDim = dim3(args.n_seg > 0 ? args.ctas_per_rank
+                                    : args.n_group * (args.ctas_per_rank + args.comm_ctas_per_rank));
   cfg.blockDim = dim3(dev::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;

@@ -1,9 +1,13 @@
 // kernel_args.h -- parameter block of the fused persistent kernel (host <-> device).
 //
 // One launch carries n_group ranks of the same world that live on the same device
-// (loopback) -- or a single rank in the one-process-per-GPU deployment.  The block index
-// selects the rank group: CTAs [g*ctas_per_rank, (g+1)*ctas_per_rank) are rank g's GEMM
-// workers (plan CTA c = blockIdx % ctas_per_rank); dedicated communication CTAs follow.
+// (loopback) -- or a single rank in the one-process-per-GPU deployment.  Space-sliced
+// (n_seg == 0): the block index selects the rank group: CTAs [g*ctas_per_rank,
+// (g+1)*ctas_per_rank) are rank g's GEMM workers (plan CTA c = blockIdx % ctas_per_rank);
+// dedicated communication CTAs follow.  Time-sliced (n_seg > 0): all ctas_per_rank CTAs
+// serve every rank, walking one global list of (rank, position) segments; chunk waits are
+// taken per tile from the dependency rule (minimal per worker via an acquired-chunk cache)
+// instead of the plan's per-CTA wait table.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -73,8 +77,19 @@ struct TraceEvent {
   uint32_t kind, rank, cta, id;
 };
 
+// Time-sliced group (loopback): positions [k0, k1) of rank group g's tile list occupy
+// global indices [o, o + k1 - k0) of the launch's single work list; physical worker w
+// runs global indices w, w + n_workers, ... (Lst.1's persistent stride over the list).
+struct Seg {
+  int32_t g, k0, k1, o;
+};
+constexpr int kMaxSegs = 256;
+
 struct KernelArgs {
   RankArgs rk[AO_MAX_WORLD];
+  int32_t n_seg;               // 0: space-sliced (rank group = blockIdx / ctas_per_rank)
+  int32_t n_total;             // time-sliced: total positions of the list
+  Seg seg[kMaxSegs];           // time-sliced: the global list, in execution order
   int32_t n_group;
   int32_t ctas_per_rank;       // GEMM CTAs per rank (== plan n_cta * cta_group)
   int32_t comm_ctas_per_rank;  // dedicated comm CTAs per rank

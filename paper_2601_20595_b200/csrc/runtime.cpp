@@ -714,6 +714,68 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
   return AO_OK;
 }
 
+
+// ------------------------------------------------------------------ time-sliced groups
+// A whole-world loopback group whose plans each ask for more CTAs than SMs / n runs
+// TIME-SLICED: all n_cta (x cta_group) CTAs serve every rank, walking one global list of
+// (rank, positions) segments; each rank's tiles keep their plan order.  The list order:
+//  * AG (copy engine, push): rank after rank (each rank's weight shard stays L2-resident
+//    while its tiles run); the copy-engine chains are issued destination-major in the same
+//    order so each rank's chunks land before its turn.
+//  * RS: owner after owner; for owner o the other ranks' runs of tiles whose rows o owns
+//    (rotation o+1, o+2, ...), then o's own run (the fused reduction).  Every tile that
+//    waits (an own tile) comes after all the tiles it waits for, so with all CTAs
+//    co-resident the list drains without deadlock (induction on the list index).
+//  * GEMM (batched GEMM-only leg): problem after problem.
+// Chunk waits are taken per tile in the kernel (the plan's per-CTA wait table assumes the
+// space-sliced CTA assignment).  Returns false (and no segments) when not applicable.
+static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArgs* ka) {
+  std::vector<ao::Seg> segs;
+  const ao::HostPlan& h0 = plans[0]->hp;
+  const int64_t BM = int64_t(h0.tile.bm);
+  if (mode == ao::MODE_RS) {
+    if (h0.is_ar || h0.S % BM != 0) return false;
+    struct Run { int key0, key1, key2, k0; ao::Seg s; };
+    std::vector<Run> runs;
+    for (int i = 0; i < n; ++i) {
+      const ao::HostPlan& hp = plans[i]->hp;
+      int k = 0;
+      while (k < hp.n_tiles) {
+        const int owner = int((int64_t(hp.order[k] / hp.n_nb) * BM) / hp.S);
+        int k1 = k + 1;
+        while (k1 < hp.n_tiles && int((int64_t(hp.order[k1] / hp.n_nb) * BM) / hp.S) == owner) ++k1;
+        const bool own = owner == hp.rank;
+        runs.push_back({owner, own ? 1 : 0, ((hp.rank - owner) % hp.W + hp.W) % hp.W, k, {i, k, k1, 0}});
+        k = k1;
+      }
+    }
+    std::stable_sort(runs.begin(), runs.end(), [](const Run& a, const Run& b) {
+      return std::tie(a.key0, a.key1, a.key2, a.k0) < std::tie(b.key0, b.key1, b.key2, b.k0);
+    });
+    for (const Run& r : runs) segs.push_back(r.s);
+  } else {
+    for (int i = 0; i < n; ++i) segs.push_back({i, 0, plans[i]->hp.n_tiles, 0});
+  }
+  // merge contiguous runs of one rank, assign global offsets
+  std::vector<ao::Seg> out;
+  for (const ao::Seg& s : segs) {
+    if (!out.empty() && out.back().g == s.g && out.back().k1 == s.k0)
+      out.back().k1 = s.k1;
+    else
+      out.push_back(s);
+  }
+  if (out.size() > size_t(ao::kMaxSegs)) return false;
+  int o = 0;
+  for (ao::Seg& s : out) {
+    s.o = o;
+    o += s.k1 - s.k0;
+  }
+  ka->n_seg = int32_t(out.size());
+  ka->n_total = o;
+  for (size_t i = 0; i < out.size(); ++i) ka->seg[i] = out[i];
+  return true;
+}
+
 // ------------------------------------------------------------------------------ op calls
 static ao_status launch_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
                               void* const* Cs, void* const* Gouts, void* stream_v, int op) {
@@ -764,12 +826,18 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   const bool ce = mode == ao::MODE_AG && h0.desc.backend == AO_BACKEND_CE && h0.W > 1;
   const int comm = mode == ao::MODE_AG ? p0->comm_kind : ao::COMM_NONE;
   ka->comm_ctas_per_rank = (comm != ao::COMM_NONE) ? h0.desc.comm_ctas : 0;
+  bool time_sliced = false;
   {
     // Persistent spin-waiting CTAs must all be co-resident (1 CTA per SM).
     const int64_t grid = int64_t(n) * (ka->ctas_per_rank + ka->comm_ctas_per_rank);
-    if (grid > p0->ctx->sm_count)
+    if (grid > p0->ctx->sm_count && n > 1 && n == h0.W && ka->ctas_per_rank <= p0->ctx->sm_count &&
+        ka->comm_ctas_per_rank == 0 &&
+        (mode == ao::MODE_RS || (h0.desc.backend == AO_BACKEND_CE && h0.desc.dir == AO_DIR_PUSH)))
+      time_sliced = build_segments(n, plans, mode, ka.get());
+    if (grid > p0->ctx->sm_count && !time_sliced)
       return fail(AO_ERR_INVALID_ARG, "grid of %lld CTAs exceeds the %d SMs: the persistent CTAs would not be "
-                  "co-resident (lower n_cta / comm_ctas)", (long long)grid, p0->ctx->sm_count);
+                  "co-resident (lower n_cta / comm_ctas; a whole-world loopback group of AG copy-engine push or "
+                  "GEMM-RS plans with n_cta <= SMs runs time-sliced)", (long long)grid, p0->ctx->sm_count);
     if (h0.tile.cg == 2 && (ka->comm_ctas_per_rank % 2) != 0)
       return fail(AO_ERR_INVALID_ARG, "comm_ctas must be even with CTA-pair tiles (cluster launch)");
   }
@@ -834,7 +902,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
         }
       }
     } else {
-      std::vector<uintptr_t> key{uintptr_t(par), uintptr_t(n)};
+      std::vector<uintptr_t> key{uintptr_t(par), uintptr_t(n), uintptr_t(time_sliced)};
       for (int i = 0; i < n; ++i) {
         key.push_back(reinterpret_cast<uintptr_t>(plans[i]));
         key.push_back(reinterpret_cast<uintptr_t>(As[i]));
@@ -865,7 +933,11 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
           const ao::HostPlan& hp = p->hp;
           const int64_t row_bytes = hp.K * 2;
           std::vector<cudaGraphNode_t> prev = stages;
-          for (const ao::P2POp& op : hp.plans[hp.rank]) {
+          std::vector<ao::P2POp> ops = hp.plans[hp.rank];
+          if (time_sliced)  // destination-major: each rank's chunks land before its turn
+            std::stable_sort(ops.begin(), ops.end(),
+                             [](const ao::P2POp& a, const ao::P2POp& b) { return a.peer < b.peer; });
+          for (const ao::P2POp& op : ops) {
             const int g = int(op.row0 / hp.C);
             const char* src = pull ? c->data(op.peer, par) + op.row0 * row_bytes
                                    : static_cast<const char*>(As[i]) + (op.row0 - int64_t(hp.rank) * hp.S) * row_bytes;
@@ -1028,7 +1100,7 @@ ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* 
   if (s != AO_OK) return s;
   const int cg = bm == 256 ? 2 : 1;
   const int ctas = (n_cta > 0 ? n_cta : sm / n) / cg * cg;  // CTAs per problem (whole pairs)
-  if (ctas < cg || int64_t(n) * ctas > sm)
+  if (ctas < cg || ctas > sm)  // n * ctas > sm: time-sliced (problem after problem)
     return fail(AO_ERR_INVALID_ARG, "%d problems x %d CTAs exceed the %d SMs (or fewer CTAs than a tile needs)", n,
                 n_cta, sm);
   ao_plan* p = nullptr;
@@ -1072,6 +1144,10 @@ ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* 
   for (int i = 0; i < n; ++i) {
     s = fill_rank(&ka->rk[i], p, 0, As[i], Bs[i], Cs[i]);
     if (s != AO_OK) return s;
+  }
+  if (int64_t(n) * ctas > sm) {
+    std::vector<ao_plan*> ps(n, p);
+    build_segments(n, ps.data(), ao::MODE_GEMM, ka.get());
   }
   cudaError_t e = ao::launch_fused(*ka, bn, p->hp.tile.cg, ao::COMM_NONE, static_cast<cudaStream_t>(stream_v));
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));

@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--tp", type=int, default=8, help="logical TP ranks in loopback (N=1)")
     ap.add_argument("--backend", default="ce", choices=["ce", "tma", "ldst"])
     ap.add_argument("--exp", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--debug", action="append", default=[], help=argparse.SUPPRESS)
     ap.add_argument("--no-ar", action="store_true", help="skip the GEMM-AR (NEXT-1) leg")
     ap.add_argument("--ar-chunk", type=int, default=256, help="GEMM-AR chunk rows")
     ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
@@ -136,6 +137,9 @@ def run_ours(args, rank, world, local_rank):
         ao.debug_set("l2_hint", args.l2_hint)
     if args.exp:
         ao.debug_set("exp", args.exp)  # timing experiments: results are NOT valid
+    for kv in args.debug:
+        k, v = kv.split("=")
+        ao.debug_set(k, int(v))
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     M = args.tokens

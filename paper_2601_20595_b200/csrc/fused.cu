@@ -41,6 +41,7 @@ constexpr uint32_t kColocBufBytes = 4096;
 constexpr uint32_t kStageWarpBytes = 4096;  // epilogue transpose buffer per warp (32 rows x 128 B)
 constexpr uint32_t kCtaBufBytes = 12288;
 constexpr int kOperandBudget = 196608;  // bytes of smem for the A/B stage ring
+constexpr int kAhead = 4;  // AG (copy engine): tiles whose chunk waits the wait warp may run ahead
 
 template <int BN, int CG>
 struct Cfg {
@@ -66,9 +67,9 @@ __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg
   L.off_comm = L.off_stg + (dbl_stg ? 8 : 4) * kStageWarpBytes;  // RS: 2 buffers per warp (TMA reduce)
   const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : 0;
   L.off_bar = L.off_comm + comm;
-  const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs;
+  const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs + 2 * kAhead;
   L.off_slot = L.off_bar + nbars * 8;
-  L.total = L.off_slot + 16 + 1024;  // + alignment slack
+  L.total = L.off_slot + 16 + kAhead + 1024;  // + wait-ahead flags + alignment slack
   return L;
 }
 __host__ __device__ constexpr SmemLayout comm_cta_layout() {
@@ -295,6 +296,25 @@ __device__ __noinline__ void ts_wait_rs(const RankArgs& R, const KernelArgs& A, 
   }
 }
 
+// RS-3: count a finished 128-row partial sub-tile (rows [sub0, sub0 + 128) of `owner`) into
+// each of its chunks; the last contributor releases the owner's flag[g][rank].  Called by
+// one thread after a CTA barrier of the epilogue warps; one sys-scope fence is cumulative
+// over their stores / performed reduces.
+__device__ __forceinline__ void rs_signal(const RankArgs& R, const KernelArgs& A, int64_t sub0, int owner) {
+  if (!(A.exp & 32)) asm volatile("fence.sc.sys;" ::: "memory");
+  const int glo = int(sub0 / R.crows);
+  const int ghi = int((sub0 + kSubM - 1) / R.crows);
+  for (int g = glo; g <= ghi; ++g) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.counters + g) : "memory");
+    if (int(old) + 1 == R.tiles_per_chunk[g]) {
+      R.counters[g] = 0;
+      if (A.delay_ns) inject_delay(A.delay_ns, uint32_t(g));
+      st_release_sys(R.peer_flags[owner] + g * R.W + R.rank, R.epoch);
+    }
+  }
+}
+
 // RS: 32-column blocks of tile column nb that hold valid columns (the streamed peer
 // partial boxes of an own tile).
 template <int BN>
@@ -353,7 +373,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   uint64_t* tempty = tfull + 2;
   uint64_t* commbars = tempty + 2;
   uint64_t* pfull = commbars + 8 * kCommBufs;  // RS: ring stages carrying peer partials
+  uint64_t* wrdy = pfull + C_::kStages;        // AG (CE): wait warp -> producer, per tile
+  uint64_t* wfre = wrdy + kAhead;              // producer -> wait warp (slot reusable)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.off_slot);
+  volatile uint8_t* wwaited = smem + L.off_slot + 16;  // per slot: the wait warp acquired a flag
+  // AG without in-kernel transfers: the chunk waits (ld.acquire.sys polls, microseconds each
+  // under load) run in the otherwise idle warp 6, up to kAhead tiles ahead of the TMA
+  // producer, which only waits on a shared-memory barrier (P:392's waits off the load path).
+  constexpr bool kWaitWarp = (MODE == MODE_AG && COMM == COMM_NONE);
 
   if (warp == 0 && lane == 0) {
     for (int g = ts ? 0 : grp; g < (ts ? args.n_group : grp + 1); ++g) {
@@ -376,6 +403,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], 4 * CG);
+      }
+      for (int a = 0; a < kAhead; ++a) {
+        mbar_init(&wrdy[a], 1);
+        mbar_init(&wfre[a], 1);
       }
       for (int b = 0; b < 8 * kCommBufs; ++b) mbar_init(&commbars[b], 1);
       fence_barrier_init();
@@ -407,7 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       // reused across every column tile of its group, B tiles only by neighbours in time.
       // l2_hint: 0 A first / B last, 1 A last / B first, 2 A last / B normal, 3 both normal
       const int h = args.l2_hint & 3;
-      const uint64_t pol_b = h == 0 ? policy_evict_last() : (h == 1 ? policy_evict_first() : policy_evict_normal());
+      const uint64_t pol_b = (args.exp & 512) ? policy_evict_first()
+                             : h == 0 ? policy_evict_last() : (h == 1 ? policy_evict_first() : policy_evict_normal());
       const uint64_t pol_a = h == 0 ? policy_evict_first() : (h == 3 ? policy_evict_normal() : policy_evict_last());
       uint32_t stage = 0, phase = 0;
       int wp = 0, we = 0;
@@ -419,8 +451,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       }
       WaitCache wc;
       wc.reset();
+      uint32_t q = 0;  // this worker's tile count (wait-warp slot = q % kAhead)
       for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
-        if constexpr (MODE == MODE_AG) {
+        if constexpr (kWaitWarp) {
+          const int j = int(q % kAhead);
+          mbar_wait(&wrdy[j], (q / kAhead) & 1u);
+          const bool waited = wwaited[j] != 0;
+          mbar_arrive(&wfre[j]);
+          ++q;
+          if (waited) fence_proxy_async_global();  // generic-proxy acquire -> TMA reads
+        } else if constexpr (MODE == MODE_AG) {
           bool waited = false;
           if (ts) {
             const int64_t r0 = int64_t(R.order[k] / R.n_nb) * BM;
@@ -800,10 +840,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             sg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA) reads
           __syncwarp();
-          if (lane == 0) {
-            tma_reduce_add_2d(&R.tmAcc[owner], sg, int(col0), int(row0 - int64_t(owner) * S));
-            bulk_commit();
+          if (lane == 0 && !((args.exp & 1024) && ((cc / CW) & 1))) {  // exp 1024: half the reduces (timing only)
+            if (args.exp & 256)  // timing experiment: keep the accumulator lines in L2
+              tma_reduce_add_2d_hint(&R.tmAcc[owner], sg, int(col0), int(row0 - int64_t(owner) * S),
+                                     policy_evict_last());
+            else
+              tma_reduce_add_2d(&R.tmAcc[owner], sg, int(col0), int(row0 - int64_t(owner) * S));
           }
+          if (lane == 0) bulk_commit();
           sb ^= 1;
           continue;
         }
@@ -828,14 +872,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         }
         __syncwarp();
       }
-      if (tma_red) {
-        if (lane == 0) {
-          bulk_wait<0>();              // this warp's reduces performed
-          fence_proxy_async_global();  // async-proxy writes -> the generic release below
-        }
-        __syncwarp();
-      }
-      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -844,25 +880,33 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         else
           mbar_arrive(&tempty[acc]);
       }
-      if (MODE == MODE_RS && !own_tile) {
-        // RS-3: count this CTA's 128-row sub-tile into each of its chunks; the last
-        // contributor releases the owner's flag[g][rank].  One sys-scope fence after the
-        // CTA barrier is cumulative over the 128 threads' partial-tile stores.
-        named_bar_sync(1, 128);
-        if (etid == 0) {
-          if (!(args.exp & 32)) asm volatile("fence.sc.sys;" ::: "memory");
-          const int glo = int(sub0 / R.crows);
-          const int ghi = int((sub0 + kSubM - 1) / R.crows);
-          for (int g = glo; g <= ghi; ++g) {
-            uint32_t old;
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.counters + g) : "memory");
-            if (int(old) + 1 == R.tiles_per_chunk[g]) {
-              R.counters[g] = 0;
-              if (args.delay_ns) inject_delay(args.delay_ns, uint32_t(g));
-              st_release_sys(R.peer_flags[owner] + g * R.W + R.rank, R.epoch);
-            }
-          }
+      if (tma_red) {
+        // RS-3 after the reduces are performed (the TMEM buffer is already released).
+        // Deferring this to the next tile was measured slower: the owners' own tiles wait
+        // on these signals.
+        if (lane == 0) {
+          bulk_wait<0>();              // this warp's reduces performed
+          fence_proxy_async_global();  // async-proxy writes -> the generic release below
         }
+        __syncwarp();
+        named_bar_sync(1, 128);
+        if (etid == 0) rs_signal(R, args, sub0, owner);
+      }
+      }
+      if (own_tile) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2)
+            mbar_arrive_leader(&tempty[acc]);
+          else
+            mbar_arrive(&tempty[acc]);
+        }
+      }
+      if (MODE == MODE_RS && !own_tile && !(R.rs_atomic && !(args.exp & 64))) {
+        // RS-3 (stores / thread reduces): signal this sub-tile now.
+        named_bar_sync(1, 128);
+        if (etid == 0) rs_signal(R, args, sub0, owner);
       }
       if (MODE == MODE_RS && own_tile && R.ar && R.W > 1) {
         // GEMM-AR: count this own sub-tile into its chunks; the last one releases the
@@ -889,6 +933,39 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     });
   } else {
     // ================================================================ co-located comm warps
+    if constexpr (kWaitWarp) {
+      if (warp == kCommWarp0 && lane == 0) {
+        WaitCache wc;
+        wc.reset();
+        int wp = ts ? 0 : R0.wait_off[wk], we = ts ? 0 : R0.wait_off[wk + 1];
+        uint32_t q = 0;
+        for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
+          const int j = int(q % kAhead);
+          mbar_wait(&wfre[j], ((q / kAhead) & 1u) ^ 1u);
+          bool waited = false;
+          if (ts) {
+            const int64_t r0 = int64_t(R.order[k] / R.n_nb) * BM;
+            const uint64_t tw = args.trace ? globaltimer() : 0;
+            waited = ts_wait_ag(R, args, wc, grp, lcta, r0, r0 + BM < M ? r0 + BM : M);
+            if (waited) trace_event(args, TR_WAIT, R.rank, lcta, int(r0 / R.crows), tw);
+          }
+          while (!ts && wp < we && R.waits[wp].x == k) {
+            const int g = R.waits[wp].y;
+            const uint64_t tw = args.trace ? globaltimer() : 0;
+            if (!(grp == 0 && wp == args.skip_wait)) {
+              for (int s = 0; s < R.n_slices; ++s)
+                spin_flag(R.flags + g * R.n_slices + s, R.epoch, args, R.rank, lcta, g);
+            }
+            trace_event(args, TR_WAIT, R.rank, lcta, g, tw);
+            ++wp;
+            waited = true;
+          }
+          wwaited[j] = waited ? 1 : 0;
+          mbar_arrive(&wrdy[j]);  // release.cta: the acquired flags -> the producer
+          ++q;
+        });
+      }
+    }
     const RankArgs& R = R0;
     if constexpr (MODE == MODE_RS) {
       if (R.ar && R.n_comm_items > 0) {  // GEMM-AR gather: ld/st pulls of reduced chunks

@@ -111,6 +111,7 @@ struct DebugKnobs {
   int64_t delay_ns = 0;
   int64_t l2_hint = -1;  // -1: follow the plan's tile order
   int64_t gemm_group_m = 16;
+  int64_t ts_lag = 0;  // time-sliced RS: lag the own run behind the next owner's first source run
   int64_t exp = 0;  // timing experiments (results invalid when nonzero)  // ao_gemm GROUP_M (measured best)
 };
 DebugKnobs g_debug;
@@ -421,6 +422,7 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   else if (!strcmp(key, "l2_hint")) g_debug.l2_hint = value;
   else if (!strcmp(key, "gemm_group_m")) g_debug.gemm_group_m = value;
   else if (!strcmp(key, "exp")) g_debug.exp = value;
+  else if (!strcmp(key, "ts_lag")) g_debug.ts_lag = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
   return AO_OK;
 }
@@ -723,9 +725,10 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
 //    while its tiles run); the copy-engine chains are issued destination-major in the same
 //    order so each rank's chunks land before its turn.
 //  * RS: owner after owner; for owner o the other ranks' runs of tiles whose rows o owns
-//    (rotation o+1, o+2, ...), then o's own run (the fused reduction).  Every tile that
-//    waits (an own tile) comes after all the tiles it waits for, so with all CTAs
-//    co-resident the list drains without deadlock (induction on the list index).
+//    (rotation o+1, o+2, ...); o's own run (the fused reduction) is lagged behind the first
+//    source run of owner o+1, so its contributions are complete when it starts.  Every
+//    tile that waits (an own tile) comes after all the tiles it waits for, so with all
+//    CTAs co-resident the list drains without deadlock (induction on the list index).
 //  * GEMM (batched GEMM-only leg): problem after problem.
 // Chunk waits are taken per tile in the kernel (the plan's per-CTA wait table assumes the
 // space-sliced CTA assignment).  Returns false (and no segments) when not applicable.
@@ -744,8 +747,15 @@ static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArg
         const int owner = int((int64_t(hp.order[k] / hp.n_nb) * BM) / hp.S);
         int k1 = k + 1;
         while (k1 < hp.n_tiles && int((int64_t(hp.order[k1] / hp.n_nb) * BM) / hp.S) == owner) ++k1;
+        // non-own run: slot 2*rot of its owner's phase (rot = 1..W-1, the rotation o+1, o+2...);
+        // own run of owner o: lagged into the next owner's phase after its first source run
+        // (slot 3 of phase o+1), so its contributions have drained when its waits run
+        const int rot = ((hp.rank - owner) % hp.W + hp.W) % hp.W;
         const bool own = owner == hp.rank;
-        runs.push_back({owner, own ? 1 : 0, ((hp.rank - owner) % hp.W + hp.W) % hp.W, k, {i, k, k1, 0}});
+        if (g_debug.ts_lag)
+          runs.push_back({own ? owner + 1 : owner, own ? 3 : 2 * rot, 0, k, {i, k, k1, 0}});
+        else
+          runs.push_back({owner, own ? 2 * hp.W : 2 * rot, 0, k, {i, k, k1, 0}});
         k = k1;
       }
     }

@@ -752,8 +752,8 @@ static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArg
         // (slot 3 of phase o+1), so its contributions have drained when its waits run
         const int rot = ((hp.rank - owner) % hp.W + hp.W) % hp.W;
         const bool own = owner == hp.rank;
-        if (g_debug.ts_lag)
-          runs.push_back({own ? owner + 1 : owner, own ? 3 : 2 * rot, 0, k, {i, k, k1, 0}});
+        if (g_debug.ts_lag)  // behind the first ts_lag source runs of the next owner's phase
+          runs.push_back({own ? owner + 1 : owner, own ? 2 * int(g_debug.ts_lag) + 1 : 2 * rot, 0, k, {i, k, k1, 0}});
         else
           runs.push_back({owner, own ? 2 * hp.W : 2 * rot, 0, k, {i, k, k1, 0}});
         k = k1;

@@ -19,7 +19,10 @@ def summarise(ev):
         durs = [e["dur"] for e in es]
         ends = sorted(e["ts"] + e["dur"] for e in es)
         starts = sorted(e["ts"] for e in es)
-        lanes = len({(e["pid"], e["tid"]) for e in es})
+        # time-sliced launches: one physical CTA serves every rank (same tid under several pids)
+        ts = len({e["pid"] for e in ev}) > 1 and any(
+            len({x["pid"] for x in ev if x["tid"] == t}) > 1 for t in {e["tid"] for e in ev[:200]})
+        lanes = len({e["tid"] for e in es}) if ts else len({(e["pid"], e["tid"]) for e in es})
         print(f"  {k:12s} n={len(es):6d} lanes={lanes:4d} mean={sum(durs) / len(durs):8.2f}us max={max(durs):8.2f}us "
               f"first={starts[0]:8.1f} last_end={ends[-1]:8.1f} busy/lane={sum(durs) / max(lanes, 1) / t_end:6.1%}")
     if by.get("wait"):

@@ -102,6 +102,55 @@ def rs_provenance_inputs(world_size: int, M: int, K_loc: int, N: int):
     return As, Bs
 
 
+def moe_inputs(world_size: int, T: int, H: int, N: int, topk: int = 2, zipf: float = 0.0, salt: int = 0):
+    """MoE dispatch + expert GEMM inputs (BASELINE.json configs[3]; SURVEY.md §8(d)
+    "Mixtral (NEXT-3): router logits N(0,1) with seed 3000, top-2, plus a Zipf-skewed
+    variant").  One expert per rank (expert e lives on rank e).
+
+    Returns (Xs, idxs, Bs): Xs[s] [T, H] bf16 tokens of rank s (N(0,1)); idxs[s] [T, topk]
+    int32 expert ids of each token: the top-k of N(0,1) router logits (seed 3000 + s +
+    salt), or with zipf > 0 k distinct experts drawn with probability ~ 1 / (e + 1)**zipf;
+    Bs[e] [N, H] bf16 expert weight (N(0,1)/sqrt(H); Mixtral w1||w3 when N = 2 * 14336)."""
+    X = [_randn((T, H), 1000 + s + salt) for s in range(world_size)]
+    B = [_randn((N, H), 2000 + e + salt, 1.0 / math.sqrt(max(H, 1))) for e in range(world_size)]
+    idx = []
+    for s in range(world_size):
+        g = torch.Generator(device="cpu")
+        g.manual_seed(3000 + s + salt)
+        if zipf > 0:
+            p = 1.0 / torch.arange(1, world_size + 1, dtype=torch.float64) ** zipf
+            sel = torch.multinomial(p.expand(T, world_size), topk, replacement=False, generator=g)
+        else:
+            logits = torch.randn(T, world_size, generator=g, dtype=torch.float32)
+            sel = torch.topk(logits, topk, dim=1).indices
+        idx.append(sel.to(torch.int32).contiguous())
+    return X, idx, B
+
+
+def moe_provenance_inputs(world_size: int, T: int, H: int, N: int, idxs, epoch: int = 0):
+    """Exact-integer provenance for A2A: X_s[t, 0..2] = base-32 digits of the global token
+    id s*T + t, X_s[t, 3] = epoch mod 32, other elements 0; B_e[n, k] = 1 iff k == n mod 4,
+    so Y_e[i, n] = A_e[i, n mod 4] exactly and every output row names the token it came
+    from.  `idxs` (routing) is passed through unchanged."""
+    assert H >= 4 and world_size * T < 32 ** 3
+    X = []
+    for s in range(world_size):
+        a = torch.zeros(T, H, dtype=torch.float32)
+        gid = torch.arange(s * T, (s + 1) * T)
+        a[:, 0] = (gid % 32).float()
+        a[:, 1] = ((gid // 32) % 32).float()
+        a[:, 2] = ((gid // 1024) % 32).float()
+        a[:, 3] = float(epoch % 32)
+        X.append(a.to(BF16))
+    B = []
+    for e in range(world_size):
+        b = torch.zeros(N, H, dtype=torch.float32)
+        n = torch.arange(N)
+        b[n, n % 4] = 1.0
+        B.append(b.to(BF16))
+    return X, idxs, B
+
+
 def to_f64(t: torch.Tensor):
     """bf16 -> float64 numpy (exact widening; no rounding happens here)."""
     return t.to(torch.float64).numpy()

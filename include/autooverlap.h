@@ -58,7 +58,8 @@ typedef enum {
   AO_ERR_STATE = 7        /* call order violated (e.g. op before ao_ctx_import_handles) */
 } ao_status;
 
-typedef enum { AO_OP_AG_GEMM = 0, AO_OP_GEMM_RS = 1, AO_OP_GEMM_AR = 2 /* NEXT-1 */ } ao_op;
+typedef enum { AO_OP_AG_GEMM = 0, AO_OP_GEMM_RS = 1, AO_OP_GEMM_AR = 2 /* NEXT-1 */,
+               AO_OP_A2A_GEMM = 3 /* NEXT-3: MoE All-to-All dispatch + expert GEMM */ } ao_op;
 /* Transfer backends of P:397 / Fig.7.  CE = copy-engine peer memcpy on a side
  * stream with stream-memop flags; TMA = cp.async.bulk peer copies issued from
  * communication warps; LDST = 16-byte vector ld/st over NVSwitch from CUDA cores. */
@@ -112,7 +113,7 @@ typedef struct {
   int32_t rs_wire;      /* ao_wire (RS only) */
   uint64_t timeout_ns;  /* device spin bound (0 = 5 s) */
   int32_t rs_reduce;    /* ao_rs_reduce (RS only) */
-  int32_t reserved;
+  int32_t topk;         /* A2A: experts per token (k); other ops: 0 */
 } ao_plan_desc;
 
 /* ---- status / version ---------------------------------------------------------------- */
@@ -194,6 +195,29 @@ ao_status ao_gemm_rs_group(int n, ao_plan* const* plans, const void* const* As, 
 ao_status ao_gemm_ar(ao_plan* plan, const void* A, const void* B, void* C, void* stream);
 ao_status ao_gemm_ar_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
                            void* const* Cs, void* stream);
+
+/* ---- A2A-GEMM (NEXT-3; P:437 / P:529 "A2A-GEMM"; BASELINE configs[3]) -------------------
+ * Expert-parallel MoE dispatch fused with the expert GEMM: expert e lives on rank e
+ * (W experts).  Rank s holds T = desc.M tokens X [T, K] bf16 and routing topk_idx [T, k]
+ * int32 (device; k = desc.topk distinct expert ids per token).  The op forms, on every
+ * rank e, A_e = concat_{s=0..W-1} X_s[tokens of s routed to e, ascending] (the
+ * all_to_all_single layout, Q25) and computes Y = A_e . B^T with B [N, K] this
+ * rank's expert weight.  Outputs (device, caller-owned):
+ *   Y [W*T, N] bf16: rows [0, *recv_rows) valid, rows beyond are left untouched;
+ *   route_pos [T, k] int32: row of (token t, choice j) in the Y of expert topk_idx[t, j];
+ *   recv_rows [1] int32: number of received rows R_e.
+ * Chunks are C = chunk_rows consecutive rows of one source's block; the count matrix is
+ * exchanged first (every rank publishes its per-expert counts to every rank), then
+ * in-kernel ld/st warps push each chunk (a row gather of the routed tokens) to its expert
+ * and release a per-(source, chunk) flag that the tiles covering those rows wait on; the
+ * tile order follows the arrival order (own rows, then sources e-1, e-2, ...).  Plan:
+ * op AO_OP_A2A_GEMM, backend AO_BACKEND_LDST, dir PUSH, comm_ctas 0, 1 <= topk <= W,
+ * (W*T) % tile_m == 0.  Same collective rules and errors as ao_ag_gemm. */
+ao_status ao_a2a_gemm(ao_plan* plan, const void* X, const int32_t* topk_idx, const void* B, void* Y,
+                      int32_t* route_pos, int32_t* recv_rows, void* stream);
+ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs, const int32_t* const* topk_idxs,
+                            const void* const* Bs, void* const* Ys, int32_t* const* route_pos,
+                            int32_t* const* recv_rows, void* stream);
 
 /* ---- plain local GEMM through the same tcgen05 mainloop (no communication) -------------
  * C[M, N] = A[M, K] . B[N, K]^T, bf16 in / fp32 accumulate / bf16 out (Lst.1's local

@@ -17,7 +17,7 @@ AO_HANDLE_BYTES = 256
 
 STATUS = {0: "AO_OK", 1: "AO_ERR_INVALID_ARG", 2: "AO_ERR_UNSUPPORTED", 3: "AO_ERR_CUDA", 4: "AO_ERR_OOM",
           5: "AO_ERR_PEER", 6: "AO_ERR_TIMEOUT", 7: "AO_ERR_STATE"}
-OPS = {"ag_gemm": 0, "gemm_rs": 1, "gemm_ar": 2}
+OPS = {"ag_gemm": 0, "gemm_rs": 1, "gemm_ar": 2, "a2a_gemm": 3}
 BACKENDS = {"ce": 0, "tma": 1, "ldst": 2}
 DIRS = {"push": 0, "pull": 1}
 CHUNK_ORDERS = {"shard_major": 0, "chunk_major": 1}
@@ -55,7 +55,7 @@ class PlanDesc(ctypes.Structure):
         ("rs_wire", ctypes.c_int32),
         ("timeout_ns", ctypes.c_uint64),
         ("rs_reduce", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("topk", ctypes.c_int32),
     ]
 
 
@@ -93,6 +93,8 @@ _SIGS = {
     "ao_gemm_rs_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p]),
     "ao_gemm_ar": (ctypes.c_int, [ctypes.c_void_p] * 5),
     "ao_gemm_ar_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p]),
+    "ao_a2a_gemm": (ctypes.c_int, [ctypes.c_void_p] * 8),
+    "ao_a2a_gemm_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 7 + [ctypes.c_void_p]),
     "ao_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
     "ao_gemm_batched": (ctypes.c_int, [ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 3 +
@@ -149,4 +151,5 @@ def make_desc(d: dict) -> PlanDesc:
     x.rs_wire = WIRES[d.get("rs_wire", "fp32")]
     x.timeout_ns = int(d.get("timeout_ns", 0))
     x.rs_reduce = RS_REDUCE[d.get("rs_reduce", "slots")]
+    x.topk = int(d.get("topk", 0))
     return x

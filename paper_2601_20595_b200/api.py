@@ -185,6 +185,31 @@ def gemm_ar(plan: Plan, A, B, C, stream=None):
     check(lib().ao_gemm_ar(plan.handle, _ptr(A), _ptr(B), _ptr(C), _stream(stream)))
 
 
+def _require_i32_cuda(*ts):
+    import torch
+    for t in ts:
+        if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
+            raise AOError(1, "index arrays must be contiguous int32 CUDA tensors")
+
+
+def a2a_gemm(plan: Plan, X, topk_idx, B, Y, route_pos, recv_rows, stream=None):
+    """ao_a2a_gemm (NEXT-3): MoE All-to-All dispatch fused with the expert GEMM.  X [T, K]
+    bf16 tokens, topk_idx [T, k] int32 experts, B [N, K] this rank's expert; Y [W*T, N]
+    (rows [0, recv_rows) valid), route_pos [T, k] int32, recv_rows [1] int32."""
+    _require_bf16_cuda(X, B, Y)
+    _require_i32_cuda(topk_idx, route_pos, recv_rows)
+    check(lib().ao_a2a_gemm(plan.handle, _ptr(X), _ptr(topk_idx), _ptr(B), _ptr(Y), _ptr(route_pos),
+                            _ptr(recv_rows), _stream(stream)))
+
+
+def a2a_gemm_group(plans, Xs, topk_idxs, Bs, Ys, route_pos, recv_rows, stream=None):
+    """ao_a2a_gemm_group: one launch pair (prep + fused) for co-located ranks (loopback)."""
+    _require_bf16_cuda(*Xs, *Bs, *Ys)
+    _require_i32_cuda(*topk_idxs, *route_pos, *recv_rows)
+    check(lib().ao_a2a_gemm_group(len(plans), _plans(plans), _arr(Xs), _arr(topk_idxs), _arr(Bs), _arr(Ys),
+                                  _arr(route_pos), _arr(recv_rows), _stream(stream)))
+
+
 def _arr(ts):
     return (ctypes.c_void_p * len(ts))(*[0 if t is None else int(t.data_ptr()) for t in ts])
 

@@ -54,11 +54,27 @@ struct Cfg {
 };
 
 struct SmemLayout {
-  uint32_t off_a, off_b, off_stg, off_comm, off_bar, off_slot, total;
+  uint32_t off_a, off_b, off_stg, off_comm, off_bar, off_slot, off_a2a, total;
+};
+
+// ---- A2A (NEXT-3) device-side schedule ---------------------------------------------------
+// Built by every CTA after the count exchange (prep kernel): the count matrix, each
+// expert's block offsets, the received rows, and per rank group the row blocks sorted by
+// the arrival position of their latest chunk (the chunk->tile join of S:430 on ragged,
+// routing-dependent chunks).
+constexpr int kA2AMaxMb = 128;  // row blocks per expert (host-validated: W*T / BM)
+struct A2ASched {
+  int tab[AO_MAX_WORLD][AO_MAX_WORLD];   // cnt[s][e]: tokens of source s routed to expert e
+  int offd[AO_MAX_WORLD][AO_MAX_WORLD];  // offd[e][s]: first row of source s's block at expert e
+  int rows[AO_MAX_WORLD];                // per rank group: received rows R_e
+  int nmb[AO_MAX_WORLD];                 // per rank group: row blocks
+  int tprefix[AO_MAX_WORLD + 1];         // tiles before rank group g (time-sliced walk)
+  int key[AO_MAX_WORLD][kA2AMaxMb];      // arrival position of a row block's latest chunk
+  uint8_t order[AO_MAX_WORLD][kA2AMaxMb];  // row blocks in execution order
 };
 
 template <int BN, int CG>
-__host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg) {
+__host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg, bool a2a = false) {
   using C_ = Cfg<BN, CG>;
   SmemLayout L{};
   L.off_a = 0;
@@ -69,7 +85,8 @@ __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg
   L.off_bar = L.off_comm + comm;
   const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs + 2 * kAhead;
   L.off_slot = L.off_bar + nbars * 8;
-  L.total = L.off_slot + 16 + kAhead + 1024;  // + wait-ahead flags + alignment slack
+  L.off_a2a = (L.off_slot + 16 + kAhead + 15) / 16 * 16;
+  L.total = L.off_a2a + (a2a ? uint32_t(sizeof(A2ASched)) : 0u) + 1024;  // + alignment slack
   return L;
 }
 __host__ __device__ constexpr SmemLayout comm_cta_layout() {
@@ -324,13 +341,151 @@ __device__ __forceinline__ int rs_blocks(int nb, int64_t N) {
   return int(nbx < BN / 32 ? nbx : BN / 32);
 }
 
+// A2A: build the schedule (all threads of the CTA; ends with a CTA barrier).  Rank groups
+// [g_lo, g_hi) are the ones this CTA serves.  pos(s, j) = d(s) * maxJ + j with d(s) =
+// (e - s) mod W: the push rotation's arrival order at expert e (own rows first, Lst.2).
+__device__ __noinline__ void a2a_build(A2ASched& sm, const KernelArgs& a, int g_lo, int g_hi, int BM) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const RankArgs& R0 = a.rk[g_lo];
+  const int W = R0.W, C = R0.crows, maxJ = R0.maxJ;
+  const uint32_t* ct = R0.flags + kA2ACountFlags + W;  // count table (identical on every rank)
+  if (tid < W * W) sm.tab[tid / W][tid % W] = int(__ldcg(ct + tid));
+  __syncthreads();
+  if (tid < W * W) {
+    const int e = tid / W, s = tid % W;
+    int o = 0;
+    for (int q = 0; q < s; ++q) o += sm.tab[q][e];
+    sm.offd[e][s] = o;
+  }
+  if (tid < g_hi - g_lo) {
+    const int g = g_lo + tid, e = a.rk[g].rank;
+    int r = 0;
+    for (int q = 0; q < W; ++q) r += sm.tab[q][e];
+    sm.rows[g] = r;
+    sm.nmb[g] = (r + BM - 1) / BM;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int g = 0; g <= AO_MAX_WORLD; ++g) {
+      sm.tprefix[g] = acc;
+      if (g >= g_lo && g < g_hi) acc += sm.nmb[g] * a.rk[g].n_nb;
+    }
+  }
+  for (int x = tid; x < (g_hi - g_lo) * kA2AMaxMb; x += nt) {
+    const int g = g_lo + x / kA2AMaxMb, mb = x % kA2AMaxMb;
+    if (mb >= sm.nmb[g]) continue;
+    const int e = a.rk[g].rank;
+    const int r0 = mb * BM, r1 = min(sm.rows[g], r0 + BM);
+    int key = -1;
+    for (int q = 0; q < W; ++q) {
+      const int b0 = sm.offd[e][q], b1 = b0 + sm.tab[q][e];
+      const int lo = max(r0, b0), hi = min(r1, b1);
+      if (lo < hi) key = max(key, ((e - q + W) % W) * maxJ + (hi - 1 - b0) / C);
+    }
+    sm.key[g][mb] = key;
+  }
+  __syncthreads();
+  for (int x = tid; x < (g_hi - g_lo) * kA2AMaxMb; x += nt) {  // stable rank by (key, mb)
+    const int g = g_lo + x / kA2AMaxMb, mb = x % kA2AMaxMb;
+    if (mb >= sm.nmb[g]) continue;
+    const int k0 = sm.key[g][mb];
+    int rk = 0;
+    for (int m = 0; m < sm.nmb[g]; ++m) rk += (sm.key[g][m] < k0 || (sm.key[g][m] == k0 && m < mb)) ? 1 : 0;
+    sm.order[g][rk] = uint8_t(mb);
+  }
+  __syncthreads();
+}
+
+// A2A tile k of rank group g -> (row block, column block): Triton GROUP_M over the sorted
+// row-block list (P:411 intra-chunk swizzle), gm row blocks per group.
+__device__ __forceinline__ int2 a2a_tile(const A2ASched& sm, const RankArgs& R, int g, int k) {
+  const int nmb = sm.nmb[g], nnb = R.n_nb, gm = R.gm;
+  const int per = gm * nnb;
+  const int first = (k / per) * gm;
+  const int size = min(nmb - first, gm);
+  const int r = k % per;
+  return make_int2(sm.order[g][first + r % size], r / size);
+}
+
+template <class F>
+__device__ __forceinline__ void for_tiles_a2a(const KernelArgs& a, const A2ASched& sm, int grp, int wk, int n_wk, F&& f) {
+  if (!a.a2a_ts) {
+    const int n = sm.nmb[grp] * a.rk[grp].n_nb;
+    for (int k = wk; k < n; k += n_wk) f(a.rk[grp], grp, k);
+  } else {
+    int g = 0;
+    for (int i = wk; i < sm.tprefix[a.n_group]; i += n_wk) {
+      while (i >= sm.tprefix[g + 1]) ++g;
+      f(a.rk[g], g, i - sm.tprefix[g]);
+    }
+  }
+}
+
+// A2A waits: every (source, chunk) flag of expert e's rows [r0, r1).
+__device__ __noinline__ bool a2a_wait(const A2ASched& sm, const RankArgs& R, const KernelArgs& A, WaitCache& wc, int grp,
+                                      int cta, int r0, int r1) {
+  bool waited = false;
+  const int W = R.W, e = R.rank;
+  for (int q = 0; q < W; ++q) {
+    const int b0 = sm.offd[e][q], b1 = b0 + sm.tab[q][e];
+    const int lo = max(r0, b0), hi = min(r1, b1);
+    if (lo >= hi) continue;
+    for (int j = (lo - b0) / R.crows; j <= (hi - 1 - b0) / R.crows; ++j) {
+      const int w = q * R.maxJ + j;
+      if (wc.has(grp, w)) continue;
+      spin_flag(R.flags + w, R.epoch, A, R.rank, cta, w);
+      wc.set(grp, w);
+      waited = true;
+    }
+  }
+  return waited;
+}
+
+// A2A dispatch (comm warp): copy chunk j of source group gs's block for expert e -- a row
+// gather of the routed tokens (16-byte ld/st) -- then release the expert's flag (s, j).
+__device__ __noinline__ void a2a_push_chunk(const A2ASched& sm, const RankArgs& S_, const KernelArgs& A, int e, int j) {
+  const int lane = lane_id();
+  const int s = S_.rank, C = S_.crows;
+  const int cnt = sm.tab[s][e];
+  const int i0 = j * C, i1 = min(cnt, i0 + C);
+  const int64_t row_bytes = S_.K * 2;
+  const int n16 = int(row_bytes / 16);
+  const int32_t* perm = S_.a2a_perm + int64_t(e) * S_.T;
+  char* dst0 = S_.peer_data[e] + (int64_t(sm.offd[e][s]) + i0) * row_bytes;
+  for (int i = i0; i < i1; ++i) {
+    const int4* src = reinterpret_cast<const int4*>(S_.A_shard + int64_t(perm[i]) * row_bytes);
+    int4* dst = reinterpret_cast<int4*>(dst0 + int64_t(i - i0) * row_bytes);
+    constexpr int U = 8;
+    for (int b = 0; b < n16; b += 32 * U) {
+      int4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = b + u * 32 + lane;
+        if (x < n16) v[u] = ld_nc_v4(src + x);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = b + u * 32 + lane;
+        if (x < n16) st_v4(dst + x, v[u]);
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("fence.sc.sys;" ::: "memory");
+    st_release_sys(S_.peer_flags[e] + s * S_.maxJ + j, S_.epoch);
+  }
+  __syncwarp();
+}
+
 template <int BN, int MODE, int COMM, int CG>
 __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constant__ KernelArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool ts = args.n_seg > 0;  // time-sliced group: every GEMM CTA serves every rank
+  const bool ts = args.n_seg > 0 || (MODE == MODE_A2A && args.a2a_ts);  // time-sliced: every GEMM CTA serves every rank
   const int gemm_ctas = ts ? args.ctas_per_rank : args.n_group * args.ctas_per_rank;
 
   // ------------------------------------------------------------------ dedicated comm CTA
@@ -356,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   using C_ = Cfg<BN, CG>;
   constexpr int BM = C_::kBM;
   constexpr bool kTmaComm = (MODE == MODE_AG && COMM == COMM_TMA);
-  constexpr SmemLayout L = gemm_layout<BN, CG>(kTmaComm, MODE == MODE_RS);
+  constexpr SmemLayout L = gemm_layout<BN, CG>(kTmaComm, MODE == MODE_RS, MODE == MODE_A2A);
   const int grp = blockIdx.x / args.ctas_per_rank;
   const int lcta = blockIdx.x % args.ctas_per_rank;  // CTA index inside the rank group
   const int wk = lcta / CG;                          // plan worker (CTA pair when CG == 2)
@@ -380,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   // AG without in-kernel transfers: the chunk waits (ld.acquire.sys polls, microseconds each
   // under load) run in the otherwise idle warp 6, up to kAhead tiles ahead of the TMA
   // producer, which only waits on a shared-memory barrier (P:392's waits off the load path).
-  constexpr bool kWaitWarp = (MODE == MODE_AG && COMM == COMM_NONE);
+  constexpr bool kWaitWarp = (MODE == MODE_AG && COMM == COMM_NONE) || MODE == MODE_A2A;
 
   if (warp == 0 && lane == 0) {
     for (int g = ts ? 0 : grp; g < (ts ? args.n_group : grp + 1); ++g) {
@@ -427,6 +582,24 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  A2ASched& a2s = *reinterpret_cast<A2ASched*>(smem + L.off_a2a);
+  if constexpr (MODE == MODE_A2A) a2a_build(a2s, args, ts ? 0 : grp, ts ? args.n_group : grp + 1, BM);
+  // the tile walk of every role (A2A: routing-dependent list built above)
+  auto walk = [&](auto&& f) {
+    if constexpr (MODE == MODE_A2A)
+      for_tiles_a2a(args, a2s, grp, wk, n_wk, f);
+    else
+      for_tiles(args, grp, wk, n_wk, f);
+  };
+  // (row block, column block) of tile k of rank group g
+  auto tile_of = [&](const RankArgs& R, int g, int k) -> int2 {
+    if constexpr (MODE == MODE_A2A) {
+      return a2a_tile(a2s, R, g, k);
+    } else {
+      const int t = R.order[k];
+      return make_int2(t / R.n_nb, t - (t / R.n_nb) * R.n_nb);
+    }
+  };
 
   const int64_t K = R0.K, N = R0.N, S = R0.S, M = R0.M;
   const int nkb = int((K + kBK - 1) / kBK);
@@ -452,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       WaitCache wc;
       wc.reset();
       uint32_t q = 0;  // this worker's tile count (wait-warp slot = q % kAhead)
-      for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
+      walk([&](const RankArgs& R, int grp, int k) {
         if constexpr (kWaitWarp) {
           const int j = int(q % kAhead);
           mbar_wait(&wrdy[j], (q / kAhead) & 1u);
@@ -482,9 +655,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           if (waited) fence_proxy_async_global();  // generic-proxy arrivals -> TMA reads
         }
         const uint64_t t_load = args.trace ? globaltimer() : 0;
-        const int t = R.order[k];
-        const int mb = t / R.n_nb;
-        const int nb = t - mb * R.n_nb;
+        const int2 tmn = tile_of(R, grp, k);
+        const int mb = tmn.x, nb = tmn.y;
+        const int t = mb * R.n_nb + nb;
         const CUtensorMap* mA = &R.tmA;
         int arow = mb * BM + int(crank) * kSubM;
         if constexpr (MODE == MODE_AG) {
@@ -558,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       // full[] completes only on operand uses of a slot (RS partial stages use pfull[]),
       // so its parity is tracked per slot.
       uint32_t stage = 0, fpar = 0, acc = 0, acc_phase = 0;
-      for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
+      walk([&](const RankArgs& R, int grp, int k) {
         const uint64_t t_mma = args.trace ? globaltimer() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -590,7 +763,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             mma_commit_cg2_mc(&tfull[acc]);
           else
             mma_commit(&tfull[acc]);
-          trace_event(args, TR_MMA, R.rank, lcta, R.order[k], t_mma);
+          if (args.trace) {
+            const int2 tmn = tile_of(R, grp, k);
+            trace_event(args, TR_MMA, R.rank, lcta, tmn.x * R.n_nb + tmn.y, t_mma);
+          }
         }
         __syncwarp();
         if constexpr (MODE == MODE_RS) {  // ring stages carrying peer partials belong to the epilogue
@@ -627,10 +803,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     }
     WaitCache wc;
     if (etid == 0) wc.reset();
-    for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
-      const int t = R.order[k];
-      const int mb = t / R.n_nb;
-      const int nb = t - mb * R.n_nb;
+    walk([&](const RankArgs& R, int grp, int k) {
+      const int2 tmn = tile_of(R, grp, k);
+      const int mb = tmn.x, nb = tmn.y;
+      const int t = mb * R.n_nb + nb;
+      // rows past the end of the output are not stored (A2A: the received rows R_e)
+      int64_t rlim = M;
+      if constexpr (MODE == MODE_A2A) rlim = a2s.rows[grp];
       if constexpr (MODE == MODE_RS)  // operand stages of this tile (consumed by the MMA)
         rs_stage = (rs_stage + uint32_t(nkb)) % C_::kStages;
       mbar_wait(&tfull[acc], acc_phase);
@@ -863,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3);
           const uint4 w = stg[r * 8 + (c ^ (r & 7))];
-          if (ok && !(args.exp & 16)) {
+          if (ok && !(args.exp & 16) && row0 + r < rlim) {
             if (MODE == MODE_RS && R.rs_atomic && !(args.exp & 8))
               red_add_v4_f32(colp + r * ld_bytes, w.x, w.y, w.z, w.w);
             else
@@ -937,13 +1116,20 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
       if (warp == kCommWarp0 && lane == 0) {
         WaitCache wc;
         wc.reset();
-        int wp = ts ? 0 : R0.wait_off[wk], we = ts ? 0 : R0.wait_off[wk + 1];
+        int wp = (ts || MODE == MODE_A2A) ? 0 : R0.wait_off[wk];
+        int we = (ts || MODE == MODE_A2A) ? 0 : R0.wait_off[wk + 1];
         uint32_t q = 0;
-        for_tiles(args, grp, wk, n_wk, [&](const RankArgs& R, int grp, int k) {
+        walk([&](const RankArgs& R, int grp, int k) {
           const int j = int(q % kAhead);
           mbar_wait(&wfre[j], ((q / kAhead) & 1u) ^ 1u);
           bool waited = false;
-          if (ts) {
+          if constexpr (MODE == MODE_A2A) {
+            // the (source, chunk) blocks of this tile's received rows
+            const int r0 = a2a_tile(a2s, R, grp, k).x * BM;
+            const uint64_t tw = args.trace ? globaltimer() : 0;
+            waited = a2a_wait(a2s, R, args, wc, grp, lcta, r0, min(a2s.rows[grp], r0 + BM));
+            if (waited) trace_event(args, TR_WAIT, R.rank, lcta, r0 / BM, tw);
+          } else if (ts) {
             const int64_t r0 = int64_t(R.order[k] / R.n_nb) * BM;
             const uint64_t tw = args.trace ? globaltimer() : 0;
             waited = ts_wait_ag(R, args, wc, grp, lcta, r0, r0 + BM < M ? r0 + BM : M);
@@ -964,6 +1150,28 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
           mbar_arrive(&wrdy[j]);  // release.cta: the acquired flags -> the producer
           ++q;
         });
+      }
+    }
+    if constexpr (MODE == MODE_A2A) {
+      // A2A dispatch: warp 7 of every GEMM CTA pushes (source, expert, chunk) row gathers.
+      // Space-sliced: this rank's rows, destinations in the push rotation (own rows first,
+      // then e = s+1, s+2, ...).  Time-sliced: every rank's rows, destination-major in the
+      // order the experts' tiles run.
+      if (warp == kCommWarp0 + 1) {
+        const int W = R0.W;
+        const int nw = ts ? int(gridDim.x) : args.ctas_per_rank;
+        const int w = ts ? int(blockIdx.x) : lcta;
+        const int gs0 = ts ? 0 : grp, gs1 = ts ? args.n_group : grp + 1;
+        int it = 0;
+        for (int ei = 0; ei < W; ++ei) {
+          for (int gs = gs0; gs < gs1; ++gs) {
+            const RankArgs& S_ = args.rk[gs];
+            const int e = ts ? args.rk[ei].rank : (S_.rank + ei) % W;
+            const int nj = (a2s.tab[S_.rank][e] + S_.crows - 1) / S_.crows;
+            for (int jj = 0; jj < nj; ++jj, ++it)
+              if (it % nw == w) a2a_push_chunk(a2s, S_, args, e, jj);
+          }
+        }
       }
     }
     const RankArgs& R = R0;
@@ -1006,7 +1214,7 @@ template <int BN, int MODE, int COMM, int CG>
 cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   auto kern = dev::fused_kernel<BN, MODE, COMM, CG>;
   constexpr bool tma_comm = (MODE == MODE_AG && COMM == COMM_TMA);
-  const size_t smem_gemm = dev::gemm_layout<BN, CG>(tma_comm, MODE == MODE_RS).total;
+  const size_t smem_gemm = dev::gemm_layout<BN, CG>(tma_comm, MODE == MODE_RS, MODE == MODE_A2A).total;
   const size_t smem_comm = (MODE == MODE_AG && COMM != COMM_NONE) ? dev::comm_cta_layout().total : 0;
   const size_t smem = smem_gemm > smem_comm ? smem_gemm : smem_comm;
   static bool attr_set = false;
@@ -1017,7 +1225,7 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(args.n_seg > 0 ? args.ctas_per_rank
+  cfg.gridDim = dim3((args.n_seg > 0 || args.a2a_ts) ? args.ctas_per_rank
                                     : args.n_group * (args.ctas_per_rank + args.comm_ctas_per_rank));
   cfg.blockDim = dim3(dev::kThreads);
   cfg.dynamicSmemBytes = smem;
@@ -1052,6 +1260,8 @@ cudaError_t launch_bn(const KernelArgs& args, int comm, cudaStream_t stream) {
       return launch_one<BN, MODE_GEMM, COMM_NONE, CG>(args, stream);
     case MODE_RS:
       return launch_one<BN, MODE_RS, COMM_NONE, CG>(args, stream);
+    case MODE_A2A:
+      return launch_one<BN, MODE_A2A, COMM_NONE, CG>(args, stream);
     case MODE_AG:
       if (comm == COMM_TMA) return launch_one<BN, MODE_AG, COMM_TMA, CG>(args, stream);
       if (comm == COMM_LDST) return launch_one<BN, MODE_AG, COMM_LDST, CG>(args, stream);

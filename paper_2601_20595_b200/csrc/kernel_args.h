@@ -17,7 +17,14 @@
 
 namespace ao {
 
-enum KernelMode : int { MODE_GEMM = 0, MODE_AG = 1, MODE_RS = 2 };
+enum KernelMode : int { MODE_GEMM = 0, MODE_AG = 1, MODE_RS = 2, MODE_A2A = 3 };
+
+// u32 flag words per epoch parity in every rank's symmetric workspace.  The last
+// kA2ATailWords hold the A2A count exchange (count flags [W] | count table [W][W]); no op
+// uses them as chunk flags (a count could otherwise satisfy another op's epoch wait).
+constexpr uint32_t kFlagWordsPerParity = 1u << 18;
+constexpr uint32_t kA2ATailWords = 128;
+constexpr uint32_t kA2ACountFlags = kFlagWordsPerParity - kA2ATailWords;
 enum CommKind : int { COMM_NONE = 0, COMM_TMA = 1, COMM_LDST = 2 };
 
 // Host-mapped record of the first device-side spin timeout.
@@ -68,6 +75,28 @@ struct alignas(64) RankArgs {
   int32_t rank, W, crows, n_chunks, n_tiles, n_items, n_nb, n_slices, n_comm_items, n_cta;
   uint32_t epoch;
   int32_t rs_atomic;  // RS: 1 = reduce-add into one accumulator (slot 0) instead of per-source slots
+  // A2A (NEXT-3): chunk flags [W][maxJ] at word 0, count flags [W] at kA2ACountFlags, count
+  // table [W][W] (row s = source s's per-expert counts) after them; receive buffer = peer_data.
+  const int32_t* a2a_perm;  // [W][T] this rank's token ids grouped by destination expert
+  int32_t T, topk, maxJ, gm;
+};
+
+// A2A prep kernel (routing -> counts, permutation, count exchange, route positions).
+struct A2APrepRank {
+  const int32_t* topk_idx;  // [T, k]
+  int32_t* perm;            // [W][T] out
+  int32_t* lpos;            // [T, k] out: position inside the (source, expert) block
+  int32_t* route_pos;       // [T, k] out: row in the expert's Y
+  int32_t* recv_rows;       // [1] out
+  uint32_t* peer_flags[AO_MAX_WORLD];  // every rank's flag words (current parity)
+  int32_t rank;
+};
+struct A2APrepArgs {
+  A2APrepRank rk[AO_MAX_WORLD];
+  int32_t n_group, W, T, topk, maxJ;
+  uint32_t epoch;
+  uint64_t timeout_ns;
+  ErrorInfo* err;
 };
 
 // In-kernel trace event (AO tracing): 32 bytes, %globaltimer nanoseconds.
@@ -104,6 +133,7 @@ struct KernelArgs {
   uint32_t trace_seq;          // launch sequence number stamped into events (kind >> 8)
   int32_t exp;                 // timing experiments only (ao_debug_set "exp"); 0 in normal runs
   int32_t l2_hint;             // 0: A evict_first / B evict_last (row order); 1: A evict_last / B evict_first
+  int32_t a2a_ts;              // A2A: time-sliced group (all CTAs serve every rank, rank after rank)
 };
 
 // Host-side launcher (fused.cu).
@@ -112,5 +142,6 @@ static_assert(sizeof(KernelArgs) <= 32764, "KernelArgs exceeds the kernel parame
 
 // bn: tile N (128/256); cg: 1 (BM = 128) or 2 (CTA pair, BM = 256); comm: CommKind.
 cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream);
+cudaError_t launch_a2a_prep(const A2APrepArgs& args, cudaStream_t stream);
 
 }  // namespace ao

@@ -18,7 +18,7 @@ const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 static const char* op_name(int op) {
-  return op == AO_OP_AG_GEMM ? "ag_gemm" : (op == AO_OP_GEMM_RS ? "gemm_rs" : "gemm_ar");
+  return op == AO_OP_AG_GEMM ? "ag_gemm" : (op == AO_OP_GEMM_RS ? "gemm_rs" : (op == AO_OP_GEMM_AR ? "gemm_ar" : "a2a_gemm"));
 }
 static const char* tensor_name(int t) { return t == TENSOR_A ? "A" : (t == TENSOR_P ? "P" : "C"); }
 static const char* backend_name(int b) { return b == AO_BACKEND_CE ? "ce" : (b == AO_BACKEND_TMA ? "tma" : "ldst"); }
@@ -31,14 +31,27 @@ static int workers(const ao_plan_desc& d, int sm_count) { return d.n_cta > 0 ? d
 std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   std::vector<std::string> v;
   if (d.struct_size != sizeof(ao_plan_desc)) v.push_back("struct_size");
-  if (d.op != AO_OP_AG_GEMM && d.op != AO_OP_GEMM_RS && d.op != AO_OP_GEMM_AR) v.push_back("op");
+  if (d.op != AO_OP_AG_GEMM && d.op != AO_OP_GEMM_RS && d.op != AO_OP_GEMM_AR && d.op != AO_OP_A2A_GEMM)
+    v.push_back("op");
   const int W = d.world_size;
   if (W < 1 || W > AO_MAX_WORLD) v.push_back("world_size");
   if (!(d.rank >= 0 && d.rank < std::max(W, 1))) v.push_back("rank");
   if (d.M < 0 || d.N < 0 || d.K < 0) v.push_back("shape");
-  if (W >= 1 && d.M % W != 0) v.push_back("M % world_size");
+  const bool a2a = d.op == AO_OP_A2A_GEMM;
+  if (a2a) {
+    // M = tokens per rank T; the received rows R_e <= W*T are routing-dependent (Q25)
+    if (d.topk < 1 || d.topk > W) v.push_back("topk");
+    if (d.chunk_rows <= 0 || d.chunk_rows % 8 != 0) v.push_back("chunk_rows");
+    if (d.backend != AO_BACKEND_LDST) v.push_back("backend for a2a_gemm");
+    if (d.dir != AO_DIR_PUSH) v.push_back("dir for a2a_gemm");
+    if (d.comm_ctas != 0) v.push_back("comm_ctas with a2a_gemm");
+  } else {
+    if (d.topk != 0) v.push_back("topk");
+    if (W >= 1 && d.M % W != 0) v.push_back("M % world_size");
+  }
   const int64_t S = W >= 1 ? d.M / W : 0;
-  if (d.chunk_rows <= 0 || d.chunk_rows % 8 != 0 || (S > 0 && S % d.chunk_rows != 0)) v.push_back("chunk_rows");
+  if (!a2a && (d.chunk_rows <= 0 || d.chunk_rows % 8 != 0 || (S > 0 && S % d.chunk_rows != 0)))
+    v.push_back("chunk_rows");
   if (d.K % 8 != 0) v.push_back("K % 8");
   if (d.N % 8 != 0) v.push_back("N % 8");
   if (d.backend < AO_BACKEND_CE || d.backend > AO_BACKEND_LDST) v.push_back("backend");
@@ -74,6 +87,19 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
 // waves = ceil(T / n); exact comparison by cross-multiplication; ties ->
 // larger BM*BN, then larger BN.
 bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
+  if (d.op == AO_OP_A2A_GEMM) {
+    // the tile grid is routing-dependent: explicit tile, else the largest candidate that
+    // divides the receive capacity W*T (row blocks never straddle its end)
+    const int64_t cap = int64_t(d.world_size) * d.M;
+    for (int i = 0; i < kNumTileCandidates; ++i) {
+      const TileShape c = kTileCandidates[i];
+      if (d.tile_m != 0 && !(c.bm == d.tile_m && c.bn == d.tile_n)) continue;
+      if (cap % c.bm != 0) continue;
+      *out = c;
+      return true;
+    }
+    return false;
+  }
   const int64_t S = d.M / d.world_size;
   bool have = false;
   int64_t best_num = 0, best_eff = 1, best_area = -1, best_bn = -1;
@@ -113,13 +139,18 @@ size_t ar_reduced_offset(const ao_plan_desc& d) {
 
 size_t data_bytes_per_parity(const ao_plan_desc& d) {
   if (d.op == AO_OP_AG_GEMM) return size_t(d.M) * size_t(d.K) * 2;  // gathered A
+  if (d.op == AO_OP_A2A_GEMM) return size_t(d.world_size) * size_t(d.M) * size_t(d.K) * 2;  // receive buffer
   if (d.op == AO_OP_GEMM_AR)  // (slots) + the owner's reduced rows [S, N] bf16
     return ar_reduced_offset(d) + size_t(d.world_size > 0 ? d.M / d.world_size : 0) * size_t(d.N) * 2;
   const size_t eb = d.rs_wire == AO_WIRE_BF16 ? 2 : 4;
   return size_t(d.M) * size_t(d.N) * eb;  // W slots of [S, N]
 }
 
+size_t a2a_max_chunks(const ao_plan_desc& d) { return d.chunk_rows > 0 ? size_t(ceil_div(d.M, d.chunk_rows)) : 0; }
+
 size_t flag_words_needed(const ao_plan_desc& d) {
+  if (d.op == AO_OP_A2A_GEMM)  // chunk flags [W][maxJ] (the count exchange uses the reserved tail)
+    return size_t(d.world_size) * a2a_max_chunks(d);
   const size_t nch = d.chunk_rows > 0 ? size_t(d.M / d.chunk_rows) : 0;
   if (d.op == AO_OP_AG_GEMM) return nch * size_t(d.backend == AO_BACKEND_CE ? 1 : d.n_slices);
   if (d.op == AO_OP_GEMM_AR) return nch * size_t(d.world_size) + nch;  // + per-chunk "reduced" flags
@@ -195,6 +226,7 @@ static std::string rank_independent_key(const HostPlan& p) {
   o.put("n_slices", d.backend == AO_BACKEND_CE ? 1 : d.n_slices);
   o.put("rs_wire", d.rs_wire);
   o.put("rs_reduce", d.rs_reduce);
+  if (d.op == AO_OP_A2A_GEMM) o.put("topk", d.topk);
   return o.str();
 }
 
@@ -214,8 +246,40 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
   P.C = d.chunk_rows;
   P.is_ag = d.op == AO_OP_AG_GEMM;
   P.is_ar = d.op == AO_OP_GEMM_AR;
+  P.is_a2a = d.op == AO_OP_A2A_GEMM;
   pick_tile(d, sm_count, &P.tile);
   P.n_cta = std::max(1, workers(d, sm_count) / P.tile.cg);
+  if (P.is_a2a) {
+    // A2A (NEXT-3): the chunk table, dependency table and tile order are functions of the
+    // routing counts, built on the device after the count exchange (Q25); the
+    // host plan fixes the rest of the schedule: chunk rows, tile, workers, intra order.
+    P.S = d.M;
+    P.n_c = int(a2a_max_chunks(d));
+    P.n_chunks = P.W * P.n_c;
+    P.n_nb = int(ceil_div(P.N, P.tile.bn));
+    P.n_mb = int(int64_t(P.W) * P.M / P.tile.bm);
+    P.n_tiles = P.n_mb * P.n_nb;  // capacity; the launched count is routing-dependent
+    Obj o;
+    o.put_str("op", op_name(d.op));
+    o.put("world_size", P.W);
+    o.put("rank", P.rank);
+    o.put("M", P.M);
+    o.put("N", P.N);
+    o.put("K", P.K);
+    o.put("topk", d.topk);
+    o.put("chunk_rows", P.C);
+    o.put("tile", int_list(std::vector<int>{P.tile.bm, P.tile.bn, P.tile.cg}));
+    o.put_str("backend", backend_name(d.backend));
+    o.put_str("dir", dir_name(d.dir));
+    o.put_str("intra", intra_name(d.intra));
+    o.put("group_m", d.group_m);
+    o.put("n_cta", P.n_cta);
+    o.put("max_chunks_per_source", P.n_c);
+    o.put("dynamic", 1);
+    P.json = o.str();
+    P.hash = fnv1a64(rank_independent_key(P));
+    return {};
+  }
   P.n_chunks = int(P.M / P.C);
   P.n_c = int(P.S / P.C);
   P.n_mb = int(P.M / P.tile.bm);

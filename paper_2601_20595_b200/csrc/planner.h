@@ -48,6 +48,7 @@ struct HostPlan {
   int n_cta = 1;  // workers (CTAs, or CTA pairs when cg == 2)
   int n_mb = 0, n_nb = 0, n_tiles = 0;
   bool is_ag = true;
+  bool is_a2a = false;  // A2A-GEMM (NEXT-3): routing-dependent tables built on the device
   bool is_ar = false;  // GEMM-AR: the RS schedule + a pull AllGather of the reduced chunks
   // tables
   std::vector<std::array<int, 5>> chunks;  // g, row0, rows, src_or_owner, pos
@@ -72,6 +73,7 @@ size_t data_bytes_per_parity(const ao_plan_desc& d);
 // GEMM-AR: byte offset of the owner's reduced bf16 rows [S, N] inside a data parity half.
 size_t ar_reduced_offset(const ao_plan_desc& d);
 // Flag words per parity this desc needs.
+size_t a2a_max_chunks(const ao_plan_desc& d);
 size_t flag_words_needed(const ao_plan_desc& d);
 
 uint64_t fnv1a64(const std::string& s);

@@ -50,7 +50,7 @@ ao_status fail(ao_status s, const char* fmt, ...) {
                                        __FILE__, __LINE__);                                   \
   } while (0)
 
-constexpr size_t kFlagWordsPerParity = size_t(1) << 18;  // 1 MiB of u32 per parity
+using ao::kFlagWordsPerParity;  // 1 MiB of u32 per parity (kernel_args.h)
 constexpr size_t kCounterWords = size_t(1) << 16;
 constexpr uint32_t kBlobMagic = 0x414f5648u;  // "AOVH"
 constexpr size_t kMaxCeGraphs = 16;
@@ -160,6 +160,7 @@ struct ao_plan {
   const ao::CommItem* d_comm = nullptr;
   int n_comm = 0;
   int comm_kind = ao::COMM_NONE;
+  int32_t* d_a2a = nullptr;  // A2A: token permutation [W][T] | block positions [T][k] (local)
   // CE backend: instantiated copy-chain graphs keyed by (parity, group plans, A pointers)
   std::map<std::vector<uintptr_t>, cudaGraphExec_t> ce_graphs;
 };
@@ -170,8 +171,9 @@ ao_status upload_tables(ao_plan* p) {
   const ao::HostPlan& hp = p->hp;
   std::vector<int> wait_off(hp.n_cta + 1, 0);
   std::vector<int2> waits;
-  for (int c = 0; c < hp.n_cta; ++c) {
-    for (auto& w : hp.waits[c]) waits.push_back(make_int2(w[0], w[1]));
+  for (int c = 0; c < hp.n_cta; ++c) {  // (A2A: waits are built on the device)
+    if (size_t(c) < hp.waits.size())
+      for (auto& w : hp.waits[c]) waits.push_back(make_int2(w[0], w[1]));
     wait_off[c + 1] = int(waits.size());
   }
   std::vector<int> items;  // (no separate reduce items: the own-tile epilogue reduces)
@@ -354,6 +356,23 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
   }
   const int bn = hp.tile.bn;
   ao_status s;
+  if (hp.is_a2a && ctx) {
+    // receive buffer [W*T, K] (current parity) is the GEMM's A; the caller's X is the
+    // source of the dispatch row gathers
+    R->A_shard = static_cast<const char*>(A);
+    R->a2a_perm = p->d_a2a;
+    R->T = int32_t(hp.M);
+    R->topk = hp.desc.topk;
+    R->maxJ = hp.n_c;
+    R->gm = hp.desc.intra == AO_INTRA_GROUPED ? std::max(1, hp.desc.group_m) : 1;
+    if (hp.K > 0) {
+      s = encode_2d(&R->tmA, R->peer_data[hp.rank], int64_t(hp.W) * hp.M, hp.K, 128);
+      if (s != AO_OK) return s;
+      s = encode_2d(&R->tmB, B, hp.N, hp.K, bn / hp.tile.cg);
+      if (s != AO_OK) return s;
+    }
+    return AO_OK;
+  }
   if (hp.K > 0) {
     if (hp.is_ag && ctx) {
       s = encode_2d(&R->tmA, R->peer_data[hp.rank], hp.M, hp.K, 128);
@@ -516,6 +535,7 @@ ao_status ao_plan_destroy(ao_plan* p) {
     cudaSetDevice(p->device);
     for (auto& kv : p->ce_graphs) cudaGraphExecDestroy(kv.second);
     cudaFree(p->d_tables);
+    if (p->d_a2a) cudaFree(p->d_a2a);
     cudaSetDevice(cur);
   }
   delete p;
@@ -703,11 +723,17 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
   if (d->op == AO_OP_GEMM_RS && d->rs_reduce == AO_RS_ATOMIC &&
       size_t(d->M / d->world_size) * size_t(d->N) * 4 > c->acc_half)
     return fail(AO_ERR_INVALID_ARG, "workspace too small for the RS accumulator");
-  if (ao::flag_words_needed(*d) > kFlagWordsPerParity)
+  if (ao::flag_words_needed(*d) > ao::kA2ACountFlags)
     return fail(AO_ERR_INVALID_ARG, "too many chunk flags (%zu)", ao::flag_words_needed(*d));
   if (size_t(p->hp.n_chunks) > kCounterWords) return fail(AO_ERR_INVALID_ARG, "too many chunks");
   if (d->rs_wire != AO_WIRE_FP32 && d->op == AO_OP_GEMM_RS)
     return fail(AO_ERR_UNSUPPORTED, "bf16 RS wire is not implemented (non-conforming, DESIGN.md Q14)");
+  if (p->hp.is_a2a) {
+    if (p->hp.n_mb > 128)
+      return fail(AO_ERR_INVALID_ARG, "a2a_gemm: W*T / tile_m = %d row blocks exceeds 128", p->hp.n_mb);
+    const size_t n = size_t(d->world_size) * size_t(d->M) + size_t(d->M) * size_t(d->topk);
+    AO_CUDA(cudaMalloc(&p->d_a2a, std::max<size_t>(n, 1) * 4));
+  }
   p->ctx = c;
   p->device = c->device;
   s = upload_tables(p);
@@ -797,7 +823,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   const ao::HostPlan& h0 = p0->hp;
   if (h0.desc.op != op)
     return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is %s",
-                h0.is_ag ? "ag_gemm" : (h0.is_ar ? "gemm_ar" : "gemm_rs"));
+                h0.is_ag ? "ag_gemm" : (h0.is_ar ? "gemm_ar" : (h0.is_a2a ? "a2a_gemm" : "gemm_rs")));
   for (int i = 0; i < n; ++i) {
     ao_plan* p = plans[i];
     if (!p || !p->ctx) return fail(AO_ERR_STATE, "plan %d not bound", i);
@@ -999,6 +1025,102 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
     }
   }
   return AO_OK;
+}
+
+// A2A-GEMM (NEXT-3): prep kernel (counts, permutation, count exchange, route positions),
+// then the fused kernel (dispatch row gathers by warp 7, arrival-ordered expert GEMM).
+static ao_status launch_a2a(int n, ao_plan* const* plans, const void* const* Xs, const int32_t* const* idxs,
+                            const void* const* Bs, void* const* Ys, int32_t* const* route_pos,
+                            int32_t* const* recv_rows, void* stream_v) {
+  if (n < 1 || n > AO_MAX_WORLD || !plans) return fail(AO_ERR_INVALID_ARG, "bad group size %d", n);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  ao_plan* p0 = plans[0];
+  if (!p0 || !p0->ctx) return fail(AO_ERR_STATE, "plan is not bound to a ctx");
+  const ao::HostPlan& h0 = p0->hp;
+  if (!h0.is_a2a) return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is not a2a_gemm");
+  for (int i = 0; i < n; ++i) {
+    ao_plan* p = plans[i];
+    if (!p || !p->ctx) return fail(AO_ERR_STATE, "plan %d not bound", i);
+    if (!p->ctx->imported) return fail(AO_ERR_STATE, "ctx of rank %d: handles not imported", p->ctx->rank);
+    if (p->hp.hash != h0.hash) return fail(AO_ERR_PEER, "plan hash mismatch inside group");
+    if (p->ctx->device != p0->ctx->device) return fail(AO_ERR_INVALID_ARG, "group spans devices");
+    for (int j = 0; j < i; ++j)
+      if (plans[j]->ctx == p->ctx) return fail(AO_ERR_INVALID_ARG, "two plans of one ctx in a group");
+    if (!aligned16(Xs[i]) || !aligned16(Bs[i]) || !aligned16(Ys[i]) || !idxs[i] || !route_pos[i] || !recv_rows[i])
+      return fail(AO_ERR_INVALID_ARG, "operands must be 16-byte aligned device pointers (index arrays non-null)");
+    ao_status s = take_async_error(p->ctx);
+    if (s != AO_OK) return s;
+  }
+  AO_CUDA(cudaSetDevice(p0->ctx->device));
+  std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
+  memset(ka.get(), 0, sizeof(ao::KernelArgs));
+  ka->n_group = n;
+  ka->ctas_per_rank = h0.n_cta * h0.tile.cg;
+  ka->mode = ao::MODE_A2A;
+  ka->timeout_ns = h0.desc.timeout_ns ? h0.desc.timeout_ns : 5000000000ull;
+  ka->err = p0->ctx->err_dev;
+  ka->skip_wait = -1;
+  ka->exp = int32_t(g_debug.exp);
+  ka->trace = p0->ctx->trace;
+  ka->trace_cursor = p0->ctx->trace_cursor;
+  ka->trace_cap = p0->ctx->trace_cap;
+  ka->trace_seq = p0->ctx->trace ? p0->ctx->trace_seq++ : 0;
+  ka->l2_hint = g_debug.l2_hint >= 0 ? int32_t(g_debug.l2_hint) : 2;
+  const int64_t grid = int64_t(n) * ka->ctas_per_rank;
+  if (grid > p0->ctx->sm_count) {
+    if (n == h0.W && ka->ctas_per_rank <= p0->ctx->sm_count)
+      ka->a2a_ts = 1;  // time-sliced whole-world group: expert after expert over all SMs
+    else
+      return fail(AO_ERR_INVALID_ARG, "grid of %lld CTAs exceeds the %d SMs (lower n_cta)", (long long)grid,
+                  p0->ctx->sm_count);
+  }
+  std::unique_ptr<ao::A2APrepArgs> pa(new ao::A2APrepArgs());
+  memset(pa.get(), 0, sizeof(ao::A2APrepArgs));
+  pa->n_group = n;
+  pa->W = h0.W;
+  pa->T = int32_t(h0.M);
+  pa->topk = h0.desc.topk;
+  pa->maxJ = h0.n_c;
+  pa->timeout_ns = ka->timeout_ns;
+  pa->err = p0->ctx->err_dev;
+  std::vector<uint32_t> epochs(n);
+  for (int i = 0; i < n; ++i) {
+    ao_ctx* c = plans[i]->ctx;
+    epochs[i] = c->epoch + 1;
+    if (epochs[i] != epochs[0]) return fail(AO_ERR_STATE, "ranks of a group disagree on the epoch");
+    ao_status s = fill_rank(&ka->rk[i], plans[i], epochs[i], Xs[i], Bs[i], Ys[i]);
+    if (s != AO_OK) return s;
+    ao::A2APrepRank& r = pa->rk[i];
+    r.topk_idx = idxs[i];
+    r.perm = plans[i]->d_a2a;
+    r.lpos = plans[i]->d_a2a + size_t(h0.W) * size_t(h0.M);
+    r.route_pos = route_pos[i];
+    r.recv_rows = recv_rows[i];
+    r.rank = plans[i]->hp.rank;
+    for (int q = 0; q < h0.W; ++q) r.peer_flags[q] = c->flags(q, epochs[i] & 1);
+  }
+  pa->epoch = epochs[0];
+  if (h0.M > 0) {
+    cudaError_t e = ao::launch_a2a_prep(*pa, stream);
+    if (e != cudaSuccess) return fail(AO_ERR_CUDA, "a2a prep launch: %s", cudaGetErrorString(e));
+    e = ao::launch_fused(*ka, h0.tile.bn, h0.tile.cg, ao::COMM_NONE, stream);
+    if (e != cudaSuccess) return fail(AO_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(e));
+  } else {
+    for (int i = 0; i < n; ++i) AO_CUDA(cudaMemsetAsync(recv_rows[i], 0, 4, stream));
+  }
+  for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
+  return AO_OK;
+}
+
+ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs, const int32_t* const* topk_idxs,
+                            const void* const* Bs, void* const* Ys, int32_t* const* route_pos,
+                            int32_t* const* recv_rows, void* stream) {
+  return launch_a2a(n, plans, Xs, topk_idxs, Bs, Ys, route_pos, recv_rows, stream);
+}
+
+ao_status ao_a2a_gemm(ao_plan* plan, const void* X, const int32_t* topk_idx, const void* B, void* Y,
+                      int32_t* route_pos, int32_t* recv_rows, void* stream) {
+  return launch_a2a(1, &plan, &X, &topk_idx, &B, &Y, &route_pos, &recv_rows, stream);
 }
 
 ao_status ao_ag_gemm_group(int n, ao_plan* const* plans, const void* const* A_shards, const void* const* Bs,

@@ -1,0 +1,144 @@
+"""GPU parity of A2A-GEMM (NEXT-3: MoE All-to-All dispatch + expert GEMM) vs the fp64 oracle
+(oracle/a2a.py), through the C ABI.  Received row counts and route positions are integer
+results (bit-exact); Y within the north-star tolerance (1e-2 per element relative to
+max(1, |ref|), Frobenius 2e-3); provenance rows bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import a2a as oa
+from oracle import numeric as on
+from synthetic import inputs as si
+
+pytestmark = pytest.mark.gpu
+SMS = 148
+
+
+@pytest.fixture(scope="module")
+def ao():
+    from paper_2601_20595_b200 import build
+    build.build(verbose=False)
+    import paper_2601_20595_b200.api as api
+    return api
+
+
+def _world(ao, W, T, H, N, k, C, ts, **kw):
+    d = dict(op="a2a_gemm", world_size=W, M=T, N=N, K=H, topk=k, chunk_rows=C, backend="ldst",
+             n_cta=SMS if ts else SMS // W, timeout_ns=2_000_000_000)
+    d.update(kw)
+    ctxs = ao.loopback_world(0, W, ao.workspace_bytes(d))
+    return ctxs, [ao.Plan(ctxs[r], dict(d, rank=r)) for r in range(W)]
+
+
+def _run(ao, ctxs, plans, X, idx, B, N):
+    W = len(plans)
+    T, k = idx[0].shape
+    Y = [torch.full((W * T, N), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    rp = [torch.full((T, k), -1, dtype=torch.int32, device="cuda") for _ in range(W)]
+    rr = [torch.full((1,), -1, dtype=torch.int32, device="cuda") for _ in range(W)]
+    ao.a2a_gemm_group(plans, [x.cuda() for x in X], [i.cuda() for i in idx], [b.cuda() for b in B], Y, rp, rr)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    return Y, rp, [int(r.item()) for r in rr]
+
+
+def _check_all(Y, rp, rr, X, idx, B, what):
+    W = len(Y)
+    Xn = [si.to_f64(x) for x in X]
+    In = [i.numpy().astype(np.int64) for i in idx]
+    ref = oa.a2a_gemm(Xn, In, [si.to_f64(b) for b in B])
+    pos = oa.route_positions(In)
+    for e in range(W):
+        assert rr[e] == ref[e].shape[0], f"{what}: expert {e} received {rr[e]} rows, oracle {ref[e].shape[0]}"
+        np.testing.assert_array_equal(rp[e].cpu().numpy(), pos[e], err_msg=f"{what}: route_pos of rank {e}")
+        if rr[e]:
+            ok, el, fr = on.check_tolerance(Y[e][: rr[e]].float().cpu().numpy(), ref[e])
+            assert ok, f"{what}: expert {e}: max elem err {el:.3e}, frob {fr:.3e}"
+
+
+@pytest.mark.parametrize("ts", [False, True])
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+@pytest.mark.parametrize("W,T,k,C", [(2, 128, 1, 64), (4, 128, 2, 16), (8, 128, 2, 32), (8, 96, 2, 24)])
+def test_a2a_vs_oracle(ao, W, T, k, C, tile, ts):
+    if (W * T) % tile[0]:
+        pytest.skip("receive capacity not a multiple of the tile rows")
+    H, N = 256, 520
+    X, idx, B = si.moe_inputs(W, T, H, N, topk=k, salt=W + T + C)
+    ctxs, plans = _world(ao, W, T, H, N, k, C, ts, tile_m=tile[0], tile_n=tile[1])
+    Y, rp, rr = _run(ao, ctxs, plans, X, idx, B, N)
+    _check_all(Y, rp, rr, X, idx, B, f"a2a W={W} T={T} k={k} C={C} tile={tile} ts={ts}")
+
+
+@pytest.mark.parametrize("ts", [False, True])
+def test_a2a_zipf_skew_and_epochs(ao, ts):
+    """Zipf-skewed routing (one expert receives most rows, another may receive none),
+    three back-to-back calls (both parities, re-sent count tables)."""
+    W, T, H, N, k = 8, 256, 128, 256, 2
+    ctxs, plans = _world(ao, W, T, H, N, k, 64, ts, tile_m=256, tile_n=256, intra="grouped", group_m=4)
+    for it, z in enumerate((1.5, 0.0, 3.0)):
+        X, idx, B = si.moe_inputs(W, T, H, N, topk=k, zipf=z, salt=100 + it)
+        Y, rp, rr = _run(ao, ctxs, plans, X, idx, B, N)
+        _check_all(Y, rp, rr, X, idx, B, f"zipf={z} it={it} ts={ts}")
+
+
+def test_a2a_degenerate_routings(ao):
+    """All tokens to expert 0 (others receive nothing), then all-local routing."""
+    W, T, H, N = 4, 128, 64, 256
+    ctxs, plans = _world(ao, W, T, H, N, 1, 32, False, tile_m=128, tile_n=128)
+    X, _, B = si.moe_inputs(W, T, H, N, topk=1, salt=77)
+    for idx in ([torch.zeros(T, 1, dtype=torch.int32) for _ in range(W)],
+                [torch.full((T, 1), s, dtype=torch.int32) for s in range(W)]):
+        Y, rp, rr = _run(ao, ctxs, plans, X, idx, B, N)
+        _check_all(Y, rp, rr, X, idx, B, "degenerate")
+
+
+@pytest.mark.parametrize("ts", [False, True])
+def test_a2a_provenance_exact(ao, ts):
+    W, T, H, N, k = 8, 128, 64, 256, 2
+    _, idx, _ = si.moe_inputs(W, T, H, N, topk=k, salt=5)
+    ctxs, plans = _world(ao, W, T, H, N, k, 16, ts, tile_m=256, tile_n=256)
+    In = [i.numpy().astype(np.int64) for i in idx]
+    for ep in range(1, 4):
+        X, idx2, B = si.moe_provenance_inputs(W, T, H, N, idx, epoch=ep)
+        Y, rp, rr = _run(ao, ctxs, plans, X, idx2, B, N)
+        for e in range(W):
+            y = Y[e][: rr[e]].float().cpu()
+            gid = (y[:, 0] + 32 * y[:, 1] + 1024 * y[:, 2]).numpy()
+            want = [s * T + t for s in range(W) for t in range(T) if e in In[s][t]]
+            np.testing.assert_array_equal(gid, want)
+            assert torch.all(y[:, 3] == ep % 32)
+
+
+def test_a2a_rejects_bad_plans(ao):
+    W, T = 2, 128
+    base = dict(op="a2a_gemm", world_size=W, M=T, N=256, K=64, topk=2, chunk_rows=32, backend="ldst")
+    for bad in (dict(topk=3), dict(topk=0), dict(backend="ce"), dict(chunk_rows=12), dict(tile_m=256, tile_n=256, M=64)):
+        assert ao.validate(dict(base, rank=0, **bad)), bad
+    assert not ao.validate(dict(base, rank=0))
+
+
+def test_a2a_mixtral_fullsize_sampled(ao):
+    """BASELINE configs[3]: Mixtral-8x7B MoE, 8 experts over 8 ranks (loopback, time-sliced
+    over all SMs), top-2 of 8192 tokens (1024 per rank), H = 4096, w1||w3 (N = 28672):
+    counts and route positions exact, sampled Y rows (every block boundary) vs fp64."""
+    W, T, H, N, k = 8, 1024, 4096, 2 * 14336, 2
+    X, idx, B = si.moe_inputs(W, T, H, N, topk=k)
+    ctxs, plans = _world(ao, W, T, H, N, k, 128, True, tile_m=256, tile_n=256, intra="grouped", group_m=8,
+                         timeout_ns=10_000_000_000)
+    Y, rp, rr = _run(ao, ctxs, plans, X, idx, B, N)
+    Xn = [si.to_f64(x) for x in X]
+    In = [i.numpy().astype(np.int64) for i in idx]
+    cnt = oa.counts(In, W)
+    pos = oa.route_positions(In)
+    rng = np.random.default_rng(3)
+    for e in range(W):
+        assert rr[e] == cnt[:, e].sum()
+        np.testing.assert_array_equal(rp[e].cpu().numpy(), pos[e])
+    for e in (0, 3, 7):
+        starts = np.concatenate([[0], np.cumsum(cnt[:, e])])
+        rows = np.unique(np.concatenate([starts[:-1], np.maximum(starts[1:] - 1, 0), rng.integers(0, rr[e], 8)]))
+        rows = rows[rows < rr[e]]
+        ref = oa.a2a_gemm_rows(Xn, In, si.to_f64(B[e]), e, rows)
+        ok, el, fr = on.check_tolerance(Y[e][torch.as_tensor(rows)].float().cpu().numpy(), ref)
+        assert ok, f"fullsize expert {e}: {el:.3e} {fr:.3e}"

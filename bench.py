@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--exp", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--debug", action="append", default=[], help=argparse.SUPPRESS)
     ap.add_argument("--no-ar", action="store_true", help="skip the GEMM-AR (NEXT-1) leg")
+    ap.add_argument("--no-a2a", action="store_true", help="skip the A2A-GEMM (NEXT-3, Mixtral) leg")
+    ap.add_argument("--a2a-chunk", type=int, default=64, help="A2A chunk rows")
+    ap.add_argument("--a2a-zipf", type=float, default=0.0, help="A2A routing skew (0 = top-2 of N(0,1) logits)")
     ap.add_argument("--ar-chunk", type=int, default=256, help="GEMM-AR chunk rows")
     ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
     ap.add_argument("--chunk", type=int, default=1024)
@@ -279,6 +282,11 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_ar:
         ar = ar_leg(torch, ao, ctxs, my_ranks, ar_desc, Cu, Bd, M, W, args, dev, loop, world, dist)
 
+    # --- A2A-GEMM (NEXT-3): Mixtral-8x7B MoE dispatch + expert GEMM, BASELINE configs[3] -----
+    a2a = None
+    if not args.no_a2a:
+        a2a = a2a_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
+
     # --- e2e through the public API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:
@@ -322,6 +330,7 @@ def run_ours(args, rank, world, local_rank):
         "baseline_kernel_level": baseline,
         "gemm_only": gemm_only,
         "gemm_ar": ar,
+        "a2a_gemm": a2a,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(W, M, budget_s=12.0)
@@ -413,6 +422,80 @@ def ar_leg(torch, ao, ctxs, my_ranks, ar_desc, Cu, Bd, M, W, args, dev, loop, wo
             "rs_reduce": ar_desc["rs_reduce"], "chunk_rows": ar_desc["chunk_rows"],
             "chunk_order": ar_desc["chunk_order"],
             "tile": [info["tile_m"], info["tile_n"]], "launches": k * (1 if loop else 1)}
+
+
+def a2a_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms):
+    """NEXT-3 (BASELINE configs[3]): Mixtral-8x7B MoE, 8 experts over 8 ranks, top-2 of 8192
+    tokens (1024 per rank), H = 4096, expert w1||w3 (N = 2 * 14336): All-to-All dispatch fused
+    with the expert GEMM.  Loopback: the 8 ranks time-sliced over all SMs; N > 1: one rank per
+    GPU.  Also the same expert GEMMs on pre-dispatched rows (ao_gemm_batched, no dispatch).
+    FLOPs = 2 * (rows received, summed over experts = W*T*k) * N * H."""
+    W = 8 if loop else world
+    T, H, N, k = 8192 // W, HIDDEN, 2 * FFN, 2
+    my = list(range(W)) if loop else [rank]
+    X, idx, B = si.moe_inputs(W, T, H, N, topk=k, zipf=args.a2a_zipf)
+    desc = dict(op="a2a_gemm", world_size=W, M=T, N=N, K=H, topk=k, chunk_rows=args.a2a_chunk, backend="ldst",
+                tile_m=256, tile_n=256, intra="grouped", group_m=8, n_cta=sms, timeout_ns=10_000_000_000)
+    ctxs = ao.loopback_world(local_rank, W, ao.workspace_bytes(desc)) if loop else \
+        [ao.dist_world(local_rank, ao.workspace_bytes(desc))]
+    plans = [ao.Plan(c, dict(desc, rank=r)) for c, r in zip(ctxs, my)]
+    Xd = [X[r].to(dev) for r in my]
+    Id = [idx[r].to(dev) for r in my]
+    Bd = [B[r].to(dev) for r in my]
+    del B
+    Y = [torch.empty(W * T, N, dtype=torch.bfloat16, device=dev) for _ in my]
+    rp = [torch.empty(T, k, dtype=torch.int32, device=dev) for _ in my]
+    rr = [torch.empty(1, dtype=torch.int32, device=dev) for _ in my]
+
+    def run():
+        if loop:
+            ao.a2a_gemm_group(plans, Xd, Id, Bd, Y, rp, rr)
+        else:
+            ao.a2a_gemm(plans[0], Xd[0], Id[0], Bd[0], Y[0], rp[0], rr[0])
+
+    def timed(fn, n):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(n):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / n
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    n = max(5, args.steps // 5)
+    ms = timed(run, n)
+    for c in ctxs:
+        c.check_async()
+    rows = [int(r.item()) for r in rr]
+    flops = 2.0 * W * T * k * N * H / (1 if loop else W)
+    # GEMM-only reference: the experts' GEMMs on already-dispatched rows (the mean row count,
+    # rounded to the tile), same kernel and workers, no dispatch / waits
+    Rm = (W * T * k // W + 255) // 256 * 256
+    A_d = [torch.randn(Rm, H, device=dev).to(torch.bfloat16) for _ in my]
+    Y_d = [torch.empty(Rm, N, dtype=torch.bfloat16, device=dev) for _ in my]
+    g_ms = timed(lambda: ao.gemm_batched(A_d, Bd, Y_d, 256, 256, 8, sms), n)
+    g_flops = 2.0 * Rm * N * H * len(my)
+    peaks, _ = load_peaks()
+    tf = flops / (ms * 1e-3) / 1e12
+    for p in plans:
+        p.close()
+    return {"what": "MoE All-to-All dispatch fused with the expert GEMM (NEXT-3), Mixtral-8x7B 8 experts, top-2",
+            "workload": "mixtral-8x7b-moe-ep8-a2a-gemm-" + ("loopback" if loop else "nvlink"),
+            "tokens": W * T, "hidden": H, "n_expert_out": N, "topk": k, "zipf": args.a2a_zipf,
+            "chunk_rows": args.a2a_chunk, "ms": round(ms, 4), "tflops": round(tf, 1),
+            "frac_of_peak": round(tf / peaks["bf16_tflops"], 4), "rows_per_expert": rows if loop else rows[0],
+            "gemm_only_ms_equal_rows": round(g_ms, 4),
+            "gemm_only_tflops": round(g_flops / (g_ms * 1e-3) / 1e12, 1), "launches_per_op": 2}
 
 
 def gemm_only_leg(torch, ao, pa, pr, A, Bu, Bd, W, M, F, args, dev, loop):

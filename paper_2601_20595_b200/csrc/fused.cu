@@ -43,12 +43,16 @@ constexpr uint32_t kCtaBufBytes = 12288;
 constexpr int kOperandBudget = 196608;  // bytes of smem for the A/B stage ring
 constexpr int kAhead = 4;  // AG (copy engine): tiles whose chunk waits the wait warp may run ahead
 
-template <int BN, int CG>
+constexpr int kA2ABuf = 8192;        // A2A dispatch: bytes per TMA staging buffer
+constexpr int kA2ABufs = 4;          // A2A dispatch: staging buffers (loads in flight)
+constexpr int kA2AOperandBudget = 163840;  // A2A: one ring stage less, for the staging buffers
+
+template <int BN, int CG, int BUDGET = kOperandBudget>
 struct Cfg {
   static constexpr int kStageA = kSubM * kBK * 2;
   static constexpr int kStageB = (BN / CG) * kBK * 2;
   static constexpr int kStage = kStageA + kStageB;
-  static constexpr int kStages = kOperandBudget / kStage;
+  static constexpr int kStages = BUDGET / kStage;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kBM = kSubM * CG;
 };
@@ -73,15 +77,15 @@ struct A2ASched {
   uint8_t order[AO_MAX_WORLD][kA2AMaxMb];  // row blocks in execution order
 };
 
-template <int BN, int CG>
+template <int BN, int CG, int BUDGET = kOperandBudget>
 __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg, bool a2a = false) {
-  using C_ = Cfg<BN, CG>;
+  using C_ = Cfg<BN, CG, BUDGET>;
   SmemLayout L{};
   L.off_a = 0;
   L.off_b = C_::kStages * C_::kStageA;
   L.off_stg = C_::kStages * C_::kStage;
   L.off_comm = L.off_stg + (dbl_stg ? 8 : 4) * kStageWarpBytes;  // RS: 2 buffers per warp (TMA reduce)
-  const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : 0;
+  const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : (a2a ? kA2ABufs * kA2ABuf : 0);
   L.off_bar = L.off_comm + comm;
   const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs + 2 * kAhead;
   L.off_slot = L.off_bar + nbars * 8;
@@ -479,6 +483,56 @@ __device__ __noinline__ void a2a_push_chunk(const A2ASched& sm, const RankArgs& 
   __syncwarp();
 }
 
+// Same chunk through the TMA unit (lane 0): pieces of <= kA2ABuf bytes of the gathered
+// rows, global -> smem (kA2ABufs loads in flight) -> the expert's receive buffer; then
+// the flag (s, j) is released.  `par` carries the staging barriers' parities across items.
+__device__ __noinline__ void a2a_push_chunk_tma(const A2ASched& sm, const RankArgs& S_, const KernelArgs& A, int e, int j,
+                                                uint8_t* buf, uint64_t* bars, uint32_t& par) {
+  const int s = S_.rank, C = S_.crows;
+  const int cnt = sm.tab[s][e];
+  const int i0 = j * C, i1 = min(cnt, i0 + C);
+  const int64_t row_bytes = S_.K * 2;
+  const int np = int((row_bytes + kA2ABuf - 1) / kA2ABuf);
+  const int total = (i1 - i0) * np;
+  const int32_t* perm = S_.a2a_perm + int64_t(e) * S_.T;
+  char* dst0 = S_.peer_data[e] + (int64_t(sm.offd[e][s]) + i0) * row_bytes;
+  auto piece = [&](int q, const char** src, char** dst) -> uint32_t {
+    const int i = i0 + q / np, part = q % np;
+    const int64_t o = int64_t(part) * kA2ABuf;
+    *src = S_.A_shard + int64_t(perm[i]) * row_bytes + o;
+    *dst = dst0 + int64_t(i - i0) * row_bytes + o;
+    const int64_t rem = row_bytes - o;
+    return uint32_t(rem < int64_t(kA2ABuf) ? rem : int64_t(kA2ABuf));
+  };
+  for (int q = 0; q < min(kA2ABufs, total); ++q) {
+    const char* src;
+    char* dst;
+    const uint32_t len = piece(q, &src, &dst);
+    mbar_arrive_expect_tx(&bars[q], len);
+    bulk_g2s(buf + q * kA2ABuf, src, len, &bars[q]);
+  }
+  for (int q = 0; q < total; ++q) {
+    const int b = q % kA2ABufs;
+    const char* src;
+    char* dst;
+    const uint32_t len = piece(q, &src, &dst);
+    mbar_wait(&bars[b], (par >> b) & 1u);
+    par ^= 1u << b;
+    bulk_s2g(dst, buf + b * kA2ABuf, len);
+    bulk_commit();
+    if (q + kA2ABufs < total) {
+      bulk_wait_read<0>();  // the store just issued has read buffer b
+      const uint32_t l2 = piece(q + kA2ABufs, &src, &dst);
+      mbar_arrive_expect_tx(&bars[b], l2);
+      bulk_g2s(buf + b * kA2ABuf, src, l2, &bars[b]);
+    }
+  }
+  bulk_wait<0>();  // writes performed
+  fence_proxy_async_global();
+  fence_sys();
+  st_release_sys(S_.peer_flags[e] + s * S_.maxJ + j, S_.epoch);
+}
+
 template <int BN, int MODE, int COMM, int CG>
 __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constant__ KernelArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -508,10 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   }
 
   // ------------------------------------------------------------------ GEMM CTA
-  using C_ = Cfg<BN, CG>;
+  constexpr int kBudget = MODE == MODE_A2A ? kA2AOperandBudget : kOperandBudget;
+  using C_ = Cfg<BN, CG, kBudget>;
   constexpr int BM = C_::kBM;
   constexpr bool kTmaComm = (MODE == MODE_AG && COMM == COMM_TMA);
-  constexpr SmemLayout L = gemm_layout<BN, CG>(kTmaComm, MODE == MODE_RS, MODE == MODE_A2A);
+  constexpr SmemLayout L = gemm_layout<BN, CG, kBudget>(kTmaComm, MODE == MODE_RS, MODE == MODE_A2A);
   const int grp = blockIdx.x / args.ctas_per_rank;
   const int lcta = blockIdx.x % args.ctas_per_rank;  // CTA index inside the rank group
   const int wk = lcta / CG;                          // plan worker (CTA pair when CG == 2)
@@ -1163,13 +1218,21 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         const int w = ts ? int(blockIdx.x) : lcta;
         const int gs0 = ts ? 0 : grp, gs1 = ts ? args.n_group : grp + 1;
         int it = 0;
+        uint32_t par = 0;
         for (int ei = 0; ei < W; ++ei) {
           for (int gs = gs0; gs < gs1; ++gs) {
             const RankArgs& S_ = args.rk[gs];
             const int e = ts ? args.rk[ei].rank : (S_.rank + ei) % W;
             const int nj = (a2s.tab[S_.rank][e] + S_.crows - 1) / S_.crows;
-            for (int jj = 0; jj < nj; ++jj, ++it)
-              if (it % nw == w) a2a_push_chunk(a2s, S_, args, e, jj);
+            for (int jj = 0; jj < nj; ++jj, ++it) {
+              if (it % nw != w) continue;
+              if (args.exp & 4096) {  // timing experiment: 16-byte ld/st row copies
+                a2a_push_chunk(a2s, S_, args, e, jj);
+              } else {
+                if (lane == 0) a2a_push_chunk_tma(a2s, S_, args, e, jj, smem + L.off_comm, commbars, par);
+                __syncwarp();
+              }
+            }
           }
         }
       }
@@ -1214,7 +1277,9 @@ template <int BN, int MODE, int COMM, int CG>
 cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   auto kern = dev::fused_kernel<BN, MODE, COMM, CG>;
   constexpr bool tma_comm = (MODE == MODE_AG && COMM == COMM_TMA);
-  const size_t smem_gemm = dev::gemm_layout<BN, CG>(tma_comm, MODE == MODE_RS, MODE == MODE_A2A).total;
+  const size_t smem_gemm =
+      dev::gemm_layout<BN, CG, MODE == MODE_A2A ? dev::kA2AOperandBudget : dev::kOperandBudget>(
+          tma_comm, MODE == MODE_RS, MODE == MODE_A2A).total;
   const size_t smem_comm = (MODE == MODE_AG && COMM != COMM_NONE) ? dev::comm_cta_layout().total : 0;
   const size_t smem = smem_gemm > smem_comm ? smem_gemm : smem_comm;
   static bool attr_set = false;

@@ -66,6 +66,23 @@ if os.path.exists(rep):
             tot += float(r[j]) * scale[units[j]]
         tr[name] = int(tot)
     json.dump(tr, open(os.path.join(P, "traffic.json"), "w"), indent=1)
+rep = os.path.join(G, "prof_%s_a2a.ncu-rep" % tag)
+if os.path.exists(rep):  # A2A-GEMM (NEXT-3) kernel, one launch
+    raw = run(["ncu", "-i", rep, "--page", "raw", "--csv"])
+    open(os.path.join(P, "%s_ncu_a2a_raw.csv" % tag), "w").write(raw)
+    summ = run([sys.executable, "scripts/ncu_summary.py", rep])
+    open(os.path.join(P, "%s_ncu_a2a_summary.txt" % tag), "w").write(summ)
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+    tot = 0
+    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        j = hdr.index(m)
+        tot += float(rows[2][j]) * scale[units[j]]
+    tp_ = os.path.join(P, "traffic.json")
+    tr = json.load(open(tp_)) if os.path.exists(tp_) else {}
+    tr["a2a_gemm"] = int(tot)
+    json.dump(tr, open(tp_, "w"), indent=1)
 tp = os.path.join(G, "trace_%s.json" % tag)
 if os.path.exists(tp):
     open(os.path.join(P, "%s_trace_summary.txt" % tag), "w").write(run([sys.executable, "scripts/trace_summary.py", tp]))

@@ -3,6 +3,7 @@ canonical JSON exports must be byte-identical (SURVEY.md §8(c) "Schedule result
 both must accept / reject the same descs.  Also checks that the C-ABI library exports
 every symbol include/autooverlap.h declares.  No GPU needed."""
 import itertools
+import json
 import os
 import re
 import subprocess
@@ -126,3 +127,24 @@ def test_host_only_calls_need_no_gpu(ao):
     if not torch.cuda.is_available():
         with pytest.raises(ao.AOError):
             ao.Context(0, 0, 1, 1 << 20)
+
+
+def test_a2a_host_plan(ao):
+    """A2A-GEMM (NEXT-3) host plan: validation rules of the header, the dynamic schedule's
+    static part in the canonical JSON, rank-independent hash, workspace = 2 parities of the
+    [W*T, K] bf16 receive buffer."""
+    base = dict(op="a2a_gemm", world_size=8, M=1024, N=28672, K=4096, topk=2, chunk_rows=64, backend="ldst",
+                tile_m=256, tile_n=256, n_cta=148)
+    assert ao.validate(dict(base, rank=0)) == []
+    for bad, why in ((dict(topk=9), "topk"), (dict(topk=0), "topk"), (dict(backend="ce"), "backend"),
+                     (dict(dir="pull"), "dir"), (dict(chunk_rows=20), "chunk_rows"), (dict(comm_ctas=2), "comm_ctas")):
+        v = ao.validate(dict(base, rank=0, **bad))
+        assert any(why in x for x in v), (bad, v)
+    assert any("topk" in x for x in ao.validate(dict(op="ag_gemm", world_size=2, rank=0, M=512, N=512, K=512,
+                                                     chunk_rows=64, topk=2)))
+    j = json.loads(ao.plan_json(dict(base, rank=3)))
+    assert j["op"] == "a2a_gemm" and j["dynamic"] == 1 and j["topk"] == 2
+    assert j["max_chunks_per_source"] == 1024 // 64 and j["tile"] == [256, 256, 2] and j["n_cta"] == 74
+    hashes = {ao.Plan(None, dict(base, rank=r)).hash() for r in range(8)}
+    assert len(hashes) == 1
+    assert ao.workspace_bytes(dict(base, rank=0)) == 2 * 8 * 1024 * 4096 * 2

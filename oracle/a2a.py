@@ -88,3 +88,40 @@ def a2a_gemm_rows(X_list, idx_list, B_e, e: int, rows):
         t = send_sets(idx_list[s], W)[e][r - starts[s]]
         A[i] = np.asarray(X_list[s][t], dtype=np.float64)
     return A @ np.asarray(B_e, dtype=np.float64).T
+
+
+def schedule(cnt, e: int, T: int, C: int, BM: int, n_nb: int, gm: int):
+    """The chunk-ordered tile list of expert e (Q26), row by row:
+
+      * chunk (s, j) = rows j*C .. (j+1)*C - 1 of source s's block (S(s -> e) in the
+        receive layout), arrival position pos(s, j) = ((e - s) mod W) * maxJ + j with
+        maxJ = ceil(T / C) (the push rotation of Lst.2 P:249-265: own rows first, then the
+        sources e-1, e-2, ... as each pushes to its next peer);
+      * row block mb (rows mb*BM .. of the R_e received rows) depends on every chunk that
+        one of its rows belongs to (chunk_before_tile) and joins the latest of them
+        (S:430);
+      * row blocks are ordered by that position (ties by block index), then tiles follow
+        Triton's GROUP_M swizzle over the ordered blocks (Fig.6).
+
+    Returns [(mb, nb), ...] in execution order."""
+    cnt = np.asarray(cnt)
+    W = cnt.shape[0]
+    maxJ = -(-T // C)
+    owner_of_row = []  # (source, chunk) of every received row, by walking the blocks
+    for s in range(W):
+        for i in range(int(cnt[s, e])):
+            owner_of_row.append((s, i // C))
+    R = len(owner_of_row)
+    nmb = -(-R // BM)
+    key = []
+    for mb in range(nmb):
+        key.append(max(((e - s) % W) * maxJ + j for s, j in owner_of_row[mb * BM:(mb + 1) * BM]))
+    blocks = sorted(range(nmb), key=lambda mb: (key[mb], mb))
+    out = []
+    per = gm * n_nb
+    for k in range(nmb * n_nb):
+        first = (k // per) * gm
+        size = min(nmb - first, gm)
+        r = k % per
+        out.append((blocks[first + r % size], r // size))
+    return out

@@ -142,3 +142,45 @@ def test_a2a_mixtral_fullsize_sampled(ao):
         ref = oa.a2a_gemm_rows(Xn, In, si.to_f64(B[e]), e, rows)
         ok, el, fr = on.check_tolerance(Y[e][torch.as_tensor(rows)].float().cpu().numpy(), ref)
         assert ok, f"fullsize expert {e}: {el:.3e} {fr:.3e}"
+
+
+@pytest.mark.parametrize("ts", [False, True])
+def test_a2a_device_schedule_matches_oracle(ao, ts, tmp_path):
+    """The routing-dependent tile order built on the device (chunk->tile join on ragged
+    source blocks, arrival sort, GROUP_M) equals oracle.a2a.schedule tile for tile: the
+    MMA trace events give each worker's tiles in execution order, and worker w's m-th tile
+    is list position w + m * n_workers (Lst.1's persistent stride)."""
+    import json
+    W, T, H, N, k, C, gm = 4, 256, 64, 384, 2, 32, 2
+    X, idx, B = si.moe_inputs(W, T, H, N, topk=k, zipf=1.3, salt=61)
+    n_cta = SMS if ts else 3
+    ctxs, plans = _world(ao, W, T, H, N, k, C, ts, tile_m=128, tile_n=128, intra="grouped", group_m=gm,
+                         n_cta=n_cta)
+    _run(ao, ctxs, plans, X, idx, B, N)  # warm (epoch 1)
+    ctxs[0].trace_enable(1 << 20)
+    _run(ao, ctxs, plans, X, idx, B, N)
+    path = str(tmp_path / "a2a_trace.json")
+    ctxs[0].trace_dump(path)
+    ctxs[0].trace_enable(0)
+    ev = [e for e in json.load(open(path))["traceEvents"] if e["cat"] == "mma"]
+    cnt = oa.counts([i.numpy().astype(np.int64) for i in idx], W)
+    n_nb = -(-N // 128)
+    sched = [oa.schedule(cnt, e, T, C, 128, n_nb, gm) for e in range(W)]
+    if ts:
+        glob = [(e, t) for e in range(W) for t in sched[e]]
+        got = {}
+        for cta in sorted({e["tid"] // 8 for e in ev}):
+            mine = sorted((e for e in ev if e["tid"] // 8 == cta), key=lambda e: e["ts"])
+            for m, e in enumerate(mine):
+                got[cta + m * n_cta] = (e["pid"], int(e["name"].split()[1]))
+        assert len(got) == len(glob)
+        for i, (e, (mb, nb)) in enumerate(glob):
+            assert got[i] == (e, mb * n_nb + nb), (i, got[i], (e, mb, nb))
+    else:
+        for e in range(W):
+            got = {}
+            for cta in range(n_cta):
+                mine = sorted((x for x in ev if x["pid"] == e and x["tid"] // 8 == cta), key=lambda x: x["ts"])
+                for m, x in enumerate(mine):
+                    got[cta + m * n_cta] = int(x["name"].split()[1])
+            assert [got[i] for i in range(len(sched[e]))] == [mb * n_nb + nb for mb, nb in sched[e]], e

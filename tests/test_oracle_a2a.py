@@ -141,3 +141,42 @@ def test_generator_routing_is_distinct_topk():
     _, idx, _ = si.moe_inputs(W, 4096, 4, 4, topk=2, zipf=1.5)
     c = np.bincount(np.concatenate([t.numpy().ravel() for t in idx]), minlength=W)
     assert c[0] > 2 * c[W - 1]  # skewed toward expert 0
+
+
+def test_schedule_is_a_permutation_and_follows_arrival():
+    """Every tile exactly once; with GROUP_M = 1 the arrival position of a tile's latest
+    chunk never decreases along the order; own rows (position 0) first."""
+    W, T, C, BM = 8, 256, 64, 128
+    _, idx, _ = si.moe_inputs(W, T, 8, 8, topk=2, zipf=1.1, salt=29)
+    cnt = oa.counts(_ids(idx), W)
+    for e in range(W):
+        for gm in (1, 4):
+            sch = oa.schedule(cnt, e, T, C, BM, n_nb=3, gm=gm)
+            R = int(cnt[:, e].sum())
+            nmb = -(-R // BM)
+            assert sorted(sch) == [(mb, nb) for mb in range(nmb) for nb in range(3)]
+        sch = oa.schedule(cnt, e, T, C, BM, n_nb=3, gm=1)
+        starts = np.concatenate([[0], np.cumsum(cnt[:, e])])
+        def latest(mb):
+            rows = range(mb * BM, min((mb + 1) * BM, starts[-1]))
+            best = -1
+            for r in rows:
+                s = int(np.searchsorted(starts, r, side="right") - 1)
+                best = max(best, ((e - s) % W) * (T // C) + (r - starts[s]) // C)
+            return best
+        keys = [latest(mb) for mb, _ in sch]
+        assert keys == sorted(keys)
+        if cnt[e, e] >= BM:
+            assert sch[0][0] == starts[e] // BM  # a block of the own rows runs first
+
+
+def test_schedule_closed_form_uniform():
+    """cnt = 2T/W everywhere, C = BM = block size: expert e's blocks arrive own block
+    first, then the blocks of sources e-1, e-2, ... (the rotation), each block once."""
+    W, T, C = 4, 128, 64
+    cnt = np.full((W, W), C, dtype=np.int64)  # every source sends exactly one chunk to every expert
+    for e in range(W):
+        sch = oa.schedule(cnt, e, T, C, BM=C, n_nb=2, gm=1)
+        want_blocks = [(e - d) % W for d in range(W)]  # block index == source index here
+        assert [mb for mb, nb in sch[::2]] == want_blocks
+        assert [nb for _, nb in sch] == [0, 1] * W

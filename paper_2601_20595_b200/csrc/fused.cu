@@ -46,6 +46,8 @@ constexpr int kAhead = 4;  // AG (copy engine): tiles whose chunk waits the wait
 constexpr int kA2ABuf = 8192;        // A2A dispatch: bytes per TMA staging buffer
 constexpr int kA2ABufs = 4;          // A2A dispatch: staging buffers (loads in flight)
 constexpr int kA2AOperandBudget = 163840;  // A2A: one ring stage less, for the staging buffers
+constexpr int kRsStg = 2;                  // RS: TMA-reduce staging buffers per epilogue warp
+constexpr int kRsOperandBudget = 196608;   // RS ring (4 staging buffers + a 5-stage ring measured no faster)
 
 template <int BN, int CG, int BUDGET = kOperandBudget>
 struct Cfg {
@@ -84,7 +86,7 @@ __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg
   L.off_a = 0;
   L.off_b = C_::kStages * C_::kStageA;
   L.off_stg = C_::kStages * C_::kStage;
-  L.off_comm = L.off_stg + (dbl_stg ? 8 : 4) * kStageWarpBytes;  // RS: 2 buffers per warp (TMA reduce)
+  L.off_comm = L.off_stg + (dbl_stg ? 4 * kRsStg : 4) * kStageWarpBytes;  // RS: kRsStg buffers per warp (TMA reduce)
   const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : (a2a ? kA2ABufs * kA2ABuf : 0);
   L.off_bar = L.off_comm + comm;
   const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs + 2 * kAhead;
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
   }
 
   // ------------------------------------------------------------------ GEMM CTA
-  constexpr int kBudget = MODE == MODE_A2A ? kA2AOperandBudget : kOperandBudget;
+  constexpr int kBudget = MODE == MODE_A2A ? kA2AOperandBudget : (MODE == MODE_RS ? kRsOperandBudget : kOperandBudget);
   using C_ = Cfg<BN, CG, kBudget>;
   constexpr int BM = C_::kBM;
   constexpr bool kTmaComm = (MODE == MODE_AG && COMM == COMM_TMA);
@@ -1066,15 +1068,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
         if (col0 >= N) break;  // warp-uniform
         if (tma_red) {
           uint4* sg = stg + sb * (4 * kStageWarpBytes / 16);
-          if (lane == 0) bulk_wait_read<1>();  // the reduce that last read buffer sb is done reading
+          if (lane == 0) bulk_wait_read<kRsStg - 1>();  // the reduce that last read buffer sb is done reading
           __syncwarp();
           // the TMA 128-B swizzle of a 1024-B-aligned box: 16-B chunk j of row r at j ^ (r & 7)
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             sg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA) reads
+          if (!(args.exp & 8192)) fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA) reads
           __syncwarp();
-          if (lane == 0 && !((args.exp & 1024) && ((cc / CW) & 1))) {  // exp 1024: half the reduces (timing only)
+          if (lane == 0 && !((args.exp & 1024) && ((cc / CW) & 1)) && !(args.exp & 16384)) {  // exp 1024/16384: half / no reduces (timing only)
             if (args.exp & 256)  // timing experiment: keep the accumulator lines in L2
               tma_reduce_add_2d_hint(&R.tmAcc[owner], sg, int(col0), int(row0 - int64_t(owner) * S),
                                      policy_evict_last());
@@ -1082,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
               tma_reduce_add_2d(&R.tmAcc[owner], sg, int(col0), int(row0 - int64_t(owner) * S));
           }
           if (lane == 0) bulk_commit();
-          sb ^= 1;
+          sb = (sb + 1) % kRsStg;
           continue;
         }
         // stage row `lane` (128 B) with a 16-byte XOR swizzle (conflict-free both ways)
@@ -1278,7 +1280,8 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   auto kern = dev::fused_kernel<BN, MODE, COMM, CG>;
   constexpr bool tma_comm = (MODE == MODE_AG && COMM == COMM_TMA);
   const size_t smem_gemm =
-      dev::gemm_layout<BN, CG, MODE == MODE_A2A ? dev::kA2AOperandBudget : dev::kOperandBudget>(
+      dev::gemm_layout<BN, CG, MODE == MODE_A2A ? dev::kA2AOperandBudget
+                                                : (MODE == MODE_RS ? dev::kRsOperandBudget : dev::kOperandBudget)>(
           tma_comm, MODE == MODE_RS, MODE == MODE_A2A).total;
   const size_t smem_comm = (MODE == MODE_AG && COMM != COMM_NONE) ? dev::comm_cta_layout().total : 0;
   const size_t smem = smem_gemm > smem_comm ? smem_gemm : smem_comm;

@@ -27,8 +27,10 @@ CE_MIN_CHUNK_BYTES = 1 << 20
 
 
 def candidate_space(op: str, W: int, M: int, N: int, K: int, chunks=None, backends=None, intras=None,
-                    tiles=None, orders=None, dirs=None):
-    """Enumerate descs of one op (dicts with the oracle/planner desc keys)."""
+                    tiles=None, orders=None, dirs=None, scheds=None):
+    """Enumerate descs of one op (dicts with the oracle/planner desc keys).  `scheds`
+    (optional) adds the loopback group schedule as key "sched": "space" (SMs/W CTAs per
+    rank, ranks concurrent) or "time" (every rank over all SMs, Q24)."""
     S = M // W
     chunks = chunks or [c for c in (128, 256, 512, 1024, 2048, 4096) if c <= S and S % c == 0]
     backends = backends or (["ce", "tma", "ldst"] if op == "ag_gemm" and W > 1 else ["ce"])
@@ -38,8 +40,10 @@ def candidate_space(op: str, W: int, M: int, N: int, K: int, chunks=None, backen
     dirs = dirs or (["push", "pull"] if op == "ag_gemm" and W > 1 else ["push"])
     out = []
     for c, b, (intra, gm), (tm, tn), o, dr in itertools.product(chunks, backends, intras, tiles, orders, dirs):
-        out.append(dict(op=op, world_size=W, M=M, N=N, K=K, chunk_rows=c, backend=b, intra=intra, group_m=gm,
-                        tile_m=tm, tile_n=tn, chunk_order=o, dir=dr, n_slices=2))
+        d = dict(op=op, world_size=W, M=M, N=N, K=K, chunk_rows=c, backend=b, intra=intra, group_m=gm,
+                 tile_m=tm, tile_n=tn, chunk_order=o, dir=dr, n_slices=2)
+        for sc in (scheds or [None]):
+            out.append(d if sc is None else dict(d, sched=sc))
     return out
 
 
@@ -50,6 +54,9 @@ def prune(descs, sm_count: int = 148):
         v = api.validate(dict(d, rank=0), sm_count)
         if v:
             pruned.append((d, "invalid: " + ";".join(v)))
+            continue
+        if d.get("sched") == "time" and not (d["op"] == "gemm_rs" or (d["backend"] == "ce" and d["dir"] == "push")):
+            pruned.append((d, "invalid: time-sliced groups need copy-engine push (AG) or GEMM-RS"))
             continue
         if d["op"] == "ag_gemm" and d["backend"] == "ce" and d["world_size"] > 1:
             if d["chunk_rows"] * d["K"] * 2 < CE_MIN_CHUNK_BYTES:
@@ -117,7 +124,7 @@ def tune_loopback(op: str, W: int, M: int, N: int, K: int, device: int = 0, budg
             pruned.append((d, "budget exhausted"))
             continue
         try:
-            ms, info = _time_loopback(d, W, device, A, B, C, warmup, iters, sms // W)
+            ms, info = _time_loopback(d, W, device, A, B, C, warmup, iters, sms if d.get("sched") == "time" else sms // W)
         except api.AOError as exc:  # e.g. workspace / launch limits on this device
             pruned.append((d, "failed: %s" % exc))
             continue

@@ -24,21 +24,22 @@ M, N, K = a.tokens, FFN // W, HIDDEN
 S = M // W
 chunks = [c for c in (64, 128, 256, 512, 1024, 2048, 4096) if c <= S and S % c == 0]
 space = tune.candidate_space("ag_gemm", W, M, N, K, chunks=chunks, backends=["ce", "tma", "ldst"],
-                             intras=[("grouped", 4)], tiles=[(0, 0)], dirs=["push"])
+                             intras=[("grouped", 4)], tiles=[(256, 256)], dirs=["push"], scheds=["space", "time"])
 rows, pruned = tune.tune_loopback("ag_gemm", W, M, N, K, budget_s=a.budget, warmup=2, iters=10, space=space)
 with open(a.out, "w") as f:
     for r in rows:
         d = r["desc"]
         f.write(json.dumps({"chunk_rows": d["chunk_rows"], "chunk_mib": d["chunk_rows"] * K * 2 / 2**20,
-                            "backend": d["backend"], "ms": round(r["ms"], 4), "tflops": round(r["tflops"], 1),
-                            "tile": r["tile"]}) + "\n")
+                            "backend": d["backend"], "sched": d["sched"], "ms": round(r["ms"], 4),
+                            "tflops": round(r["tflops"], 1), "tile": r["tile"]}) + "\n")
     for d, why in pruned:
         f.write(json.dumps({"chunk_rows": d["chunk_rows"], "backend": d["backend"], "pruned": why}) + "\n")
-by = {(r["desc"]["chunk_rows"], r["desc"]["backend"]): r["tflops"] for r in rows}
+by = {(r["desc"]["chunk_rows"], r["desc"]["backend"], r["desc"]["sched"]): r["tflops"] for r in rows}
+cols = [("ce", "time"), ("ce", "space"), ("tma", "space"), ("ldst", "space")]
 print(f"config 5 loopback W={W} M={M} N={N}/rank K={K}: TFLOP/s (all 8 ranks)")
-print("chunk rows  MiB   " + "  ".join(f"{b:>6s}" for b in ("ce", "tma", "ldst")))
+print("chunk rows  MiB   " + "  ".join(f"{b + '/' + s:>10s}" for b, s in cols))
 for c in chunks:
     print(f"{c:10d} {c * K * 2 / 2**20:5.0f}  " + "  ".join(
-        f"{by.get((c, b), float('nan')):6.0f}" for b in ("ce", "tma", "ldst")))
+        f"{by.get((c, b, s), float('nan')):10.0f}" for b, s in cols))
 for d, why in pruned:
     print("pruned", d["chunk_rows"], d["backend"], why)

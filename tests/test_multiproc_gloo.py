@@ -118,3 +118,18 @@ def test_bench_reference_arm_under_torchrun():
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_two_ranks_agree_on_a2a_plans():
+    """A2A-GEMM (NEXT-3): the static part of the schedule agrees across ranks (the ops are
+    collective: same hash), and each rank's export names itself."""
+    descs = [dict(op="a2a_gemm", world_size=2, M=512, N=512, K=256, topk=2, chunk_rows=64, backend="ldst"),
+             dict(op="a2a_gemm", world_size=2, M=1024, N=768, K=128, topk=1, chunk_rows=128, backend="ldst",
+                  intra="grouped", group_m=4, tile_m=128, tile_n=256)]
+    res = _run(descs)
+    for d, allv in zip(descs, res):
+        assert len({h for h, _ in allv}) == 1, d
+        for r, (_, js) in enumerate(allv):
+            P = json.loads(js)
+            assert P["rank"] == r and P["dynamic"] == 1 and P["topk"] == d["topk"]
+            assert P["max_chunks_per_source"] == -(-d["M"] // d["chunk_rows"])

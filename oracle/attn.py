@@ -1,0 +1,57 @@
+"""CPU fp64 oracle for sequence-parallel attention with all-gathered (ring-ordered) KV
+("sequence-parallel (SP) schedules, including the
+overlapped RingAttention", Fig.4(c) ring AllGather P:310).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+`cpu_baseline` / `--impl reference` legs may import this module.  It shares no code with
+the CUDA path (paper_2601_20595_b200/), and the CUDA path never imports it.
+
+Reading (Q27): W ranks split the sequence; rank r holds Q_r, K_r, V_r of its
+S_loc tokens for all H heads, laid out [H, S_loc, d].  Non-causal scaled dot-product
+attention (Vaswani et al., the paper's attention workloads P:459) over the full sequence:
+
+    O_r[h] = softmax( Q_r[h] . K[h]^T * scale ) . V[h],   K[h] = concat_s K_s[h] (rank order)
+
+with scale = 1/sqrt(d).  The ring order in which the GPU consumes the KV shards does not
+change the exact result (softmax over a set); the oracle uses the plain definition.
+
+Pins (tests/test_oracle_attn.py): constant scores give the mean of V, a one-hot score
+selects one V row, permutation invariance over KV rows, W = 1 reduces to single-device
+attention computed with an explicit per-element loop, exact rational arithmetic on a
+tiny case.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def attention(Q, K, V, scale: float):
+    """Single-device attention, fp64: softmax(Q K^T * scale) V per head.  Q [H, Sq, d],
+    K/V [H, Sk, d]."""
+    Q = np.asarray(Q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    S = np.einsum("hqd,hkd->hqk", Q, K) * scale
+    S = S - S.max(axis=-1, keepdims=True)
+    P = np.exp(S)
+    P /= P.sum(axis=-1, keepdims=True)
+    return np.einsum("hqk,hkd->hqd", P, V)
+
+
+def sp_attention(Q_list, K_list, V_list, rank: int, scale: float):
+    """Rank `rank`'s output of sequence-parallel attention: its queries against the
+    all-gathered keys/values (concatenation of the shards in rank order)."""
+    K = np.concatenate([np.asarray(k, dtype=np.float64) for k in K_list], axis=1)
+    V = np.concatenate([np.asarray(v, dtype=np.float64) for v in V_list], axis=1)
+    return attention(Q_list[rank], K, V, scale)
+
+
+def sp_attention_rows(Q_list, K_list, V_list, rank: int, scale: float, heads, rows):
+    """Selected (head, row) outputs (full-size sampled checks)."""
+    K = np.concatenate([np.asarray(k, dtype=np.float64) for k in K_list], axis=1)
+    V = np.concatenate([np.asarray(v, dtype=np.float64) for v in V_list], axis=1)
+    Q = np.asarray(Q_list[rank], dtype=np.float64)
+    out = []
+    for h in heads:
+        out.append(attention(Q[h:h + 1, rows], K[h:h + 1], V[h:h + 1], scale)[0])
+    return np.stack(out)

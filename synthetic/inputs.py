@@ -151,6 +151,16 @@ def moe_provenance_inputs(world_size: int, T: int, H: int, N: int, idxs, epoch: 
     return X, idxs, B
 
 
+def attn_inputs(world_size: int, H: int, S_loc: int, d: int, salt: int = 0):
+    """Sequence-parallel attention inputs (NEXT-4; Llama-3 attention shapes: d = 128): per
+    rank Q_r, K_r, V_r [H, S_loc, d] bf16, N(0,1) (seeds 4000/5000/6000 + r + salt).
+    With N(0,1) q and k the scaled scores q.k/sqrt(d) are ~N(0,1), like trained models'."""
+    Q = [_randn((H, S_loc, d), 4000 + r + salt) for r in range(world_size)]
+    K = [_randn((H, S_loc, d), 5000 + r + salt) for r in range(world_size)]
+    V = [_randn((H, S_loc, d), 6000 + r + salt) for r in range(world_size)]
+    return Q, K, V
+
+
 def to_f64(t: torch.Tensor):
     """bf16 -> float64 numpy (exact widening; no rounding happens here)."""
     return t.to(torch.float64).numpy()

@@ -1,0 +1,81 @@
+"""Pins of the SP-attention oracle (oracle/attn.py) against facts that do not come from it."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import attn as oa
+from synthetic import inputs as si
+
+
+def _np(ts):
+    return [si.to_f64(t) for t in ts]
+
+
+def test_constant_scores_give_mean_of_v():
+    rng = np.random.default_rng(0)
+    H, Sq, Sk, d = 2, 3, 7, 4
+    Q = np.zeros((H, Sq, d))
+    K = rng.standard_normal((H, Sk, d))
+    V = rng.standard_normal((H, Sk, d))
+    np.testing.assert_allclose(oa.attention(Q, K, V, 0.5), np.broadcast_to(V.mean(axis=1, keepdims=True), (H, Sq, d)),
+                               rtol=0, atol=1e-14)
+
+
+def test_one_hot_score_selects_a_row():
+    H, Sk, d = 1, 5, 4
+    K = np.zeros((H, Sk, d))
+    K[0, 3, 0] = 1.0
+    Q = np.zeros((H, 1, d))
+    Q[0, 0, 0] = 1e4  # score 1e4 * scale on row 3, 0 elsewhere
+    V = np.arange(Sk * d, dtype=np.float64).reshape(H, Sk, d)
+    np.testing.assert_allclose(oa.attention(Q, K, V, 1.0), V[:, 3:4], rtol=0, atol=1e-12)
+
+
+def test_kv_order_invariance_and_ring_gather():
+    W, H, S, d = 4, 2, 8, 16
+    Q, K, V = (_np(x) for x in si.attn_inputs(W, H, S, d, salt=3))
+    ref = oa.sp_attention(Q, K, V, 1, d ** -0.5)
+    perm = [2, 0, 3, 1]  # any KV order (e.g. the ring arrival order) gives the same softmax
+    alt = oa.sp_attention(Q, [K[p] for p in perm], [V[p] for p in perm], 1, d ** -0.5)
+    np.testing.assert_allclose(alt, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_single_rank_matches_element_loop():
+    H, S, d = 2, 6, 8
+    Q, K, V = (_np(x) for x in si.attn_inputs(1, H, S, d, salt=5))
+    scale = d ** -0.5
+    got = oa.sp_attention(Q, K, V, 0, scale)
+    for h in range(H):
+        for i in range(S):
+            s = [sum(Q[0][h, i, x] * K[0][h, j, x] for x in range(d)) * scale for j in range(S)]
+            m = max(s)
+            e = [np.exp(v - m) for v in s]
+            z = sum(e)
+            for x in range(d):
+                assert abs(got[h, i, x] - sum(e[j] * V[0][h, j, x] for j in range(S)) / z) < 1e-12
+
+
+def test_exact_rational_tiny():
+    """scale = ln 2 and integer q.k make every weight a power of two: exact rationals."""
+    import math
+    H, d = 1, 2
+    Q = np.array([[[1.0, 0.0], [0.0, 1.0]]])
+    K = np.array([[[0.0, 0.0], [1.0, 0.0], [2.0, 1.0]]])
+    V = np.array([[[1.0, 0.0], [0.0, 4.0], [3.0, 3.0]]])
+    got = oa.attention(Q, K, V, math.log(2.0))
+    for i in range(2):
+        w = [Fraction(2) ** int(np.dot(Q[0, i], K[0, j])) for j in range(3)]
+        z = sum(w)
+        for x in range(d):
+            want = sum(w[j] * Fraction(V[0, j, x]) for j in range(3)) / z
+            assert abs(got[0, i, x] - float(want)) < 1e-14
+
+
+def test_sampled_rows_match():
+    W, H, S, d = 2, 3, 16, 8
+    Q, K, V = (_np(x) for x in si.attn_inputs(W, H, S, d, salt=7))
+    full = oa.sp_attention(Q, K, V, 1, d ** -0.5)
+    rows = np.array([0, 5, 15])
+    np.testing.assert_allclose(oa.sp_attention_rows(Q, K, V, 1, d ** -0.5, [0, 2], rows), full[[0, 2]][:, rows],
+                               rtol=1e-13, atol=1e-13)

@@ -59,7 +59,8 @@ typedef enum {
 } ao_status;
 
 typedef enum { AO_OP_AG_GEMM = 0, AO_OP_GEMM_RS = 1, AO_OP_GEMM_AR = 2 /* NEXT-1 */,
-               AO_OP_A2A_GEMM = 3 /* NEXT-3: MoE All-to-All dispatch + expert GEMM */ } ao_op;
+               AO_OP_A2A_GEMM = 3 /* NEXT-3: MoE All-to-All dispatch + expert GEMM */,
+               AO_OP_SP_ATTN = 4 /* NEXT-4: sequence-parallel attention over all-gathered KV */ } ao_op;
 /* Transfer backends of P:397 / Fig.7.  CE = copy-engine peer memcpy on a side
  * stream with stream-memop flags; TMA = cp.async.bulk peer copies issued from
  * communication warps; LDST = 16-byte vector ld/st over NVSwitch from CUDA cores. */
@@ -218,6 +219,22 @@ ao_status ao_a2a_gemm(ao_plan* plan, const void* X, const int32_t* topk_idx, con
 ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs, const int32_t* const* topk_idxs,
                             const void* const* Bs, void* const* Ys, int32_t* const* route_pos,
                             int32_t* const* recv_rows, void* stream);
+
+/* ---- SP attention (NEXT-4; "sequence-parallel (SP) schedules, including the
+ * overlapped RingAttention", Fig.4c ring AllGather P:310) ----------------------------------
+ * Rank r holds Q, K, V [H, S_loc, 128] bf16 (heads x its S_loc tokens x head dim 128) and
+ * gets O [H, S_loc, 128] bf16 = softmax(Q K_all^T / sqrt(128)) V_all per head, non-causal,
+ * over the keys/values of all ranks (concatenated in rank order).  The peers' K/V shards
+ * are pushed by the copy engine in chunks of chunk_rows rows of the [H*S_loc, 128] view
+ * (ring rotation), each released by a per-chunk flag; every (head, 128-query) tile
+ * consumes its KV blocks in arrival order (own shard first, then r-1, r-2, ...) with an
+ * online softmax, so the result does not depend on the order (Q27).  Plan: op
+ * AO_OP_SP_ATTN, M = S_loc (multiple of 128), N = H, K = 128, chunk_rows a multiple of 128
+ * dividing H*S_loc, backend AO_BACKEND_CE, dir PUSH, comm_ctas 0.  Collective rules and
+ * errors as ao_ag_gemm. */
+ao_status ao_sp_attn(ao_plan* plan, const void* Q, const void* K, const void* V, void* O, void* stream);
+ao_status ao_sp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
+                           const void* const* Vs, void* const* Os, void* stream);
 
 /* ---- plain local GEMM through the same tcgen05 mainloop (no communication) -------------
  * C[M, N] = A[M, K] . B[N, K]^T, bf16 in / fp32 accumulate / bf16 out (Lst.1's local

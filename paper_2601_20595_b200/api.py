@@ -210,6 +210,20 @@ def a2a_gemm_group(plans, Xs, topk_idxs, Bs, Ys, route_pos, recv_rows, stream=No
                                   _arr(route_pos), _arr(recv_rows), _stream(stream)))
 
 
+def sp_attn(plan: Plan, Q, K, V, O, stream=None):
+    """ao_sp_attn (NEXT-4): O = softmax(Q K_all^T / sqrt(128)) V_all per head; Q/K/V/O
+    [H, S_loc, 128] bf16, K/V gathered from all ranks in ring (arrival) order."""
+    _require_bf16_cuda(Q, K, V, O)
+    check(lib().ao_sp_attn(plan.handle, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _stream(stream)))
+
+
+def sp_attn_group(plans, Qs, Ks, Vs, Os, stream=None):
+    """ao_sp_attn_group: one launch for co-located ranks (loopback)."""
+    _require_bf16_cuda(*Qs, *Ks, *Vs, *Os)
+    check(lib().ao_sp_attn_group(len(plans), _plans(plans), _arr(Qs), _arr(Ks), _arr(Vs), _arr(Os),
+                                 _stream(stream)))
+
+
 def _arr(ts):
     return (ctypes.c_void_p * len(ts))(*[0 if t is None else int(t.data_ptr()) for t in ts])
 

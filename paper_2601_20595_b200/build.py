@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libautooverlap.so")
-SOURCES = ["planner.cpp", "runtime.cpp", "fused.cu", "a2a.cu"]
+SOURCES = ["planner.cpp", "runtime.cpp", "fused.cu", "a2a.cu", "attn.cu"]
 HEADERS = ["planner.h", "kernel_args.h", "ptx.cuh"]
 
 

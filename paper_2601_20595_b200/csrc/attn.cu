@@ -1,0 +1,368 @@
+// attn.cu -- sequence-parallel attention with all-gathered KV (
+// PAPER.md P:459 "sequence-parallel (SP) schedules, including the overlapped
+// RingAttention", Fig.4(c) ring AllGather P:310).
+//
+// Rank r computes O_r[h] = softmax(Q_r[h] K[h]^T / sqrt(128)) V[h] over the whole sequence.
+// The peers' K/V shards arrive chunk by chunk (copy-engine pushes in the ring rotation,
+// per-chunk flags); every query tile consumes its KV blocks in ARRIVAL order -- own shard
+// first, then ranks r-1, r-2, ... -- which the online softmax makes order-free: the
+// RingAttention schedule expressed as the paper's chunk-ordered tile loop.
+//
+// Persistent kernel, 1 CTA / SM, one work item = (head, 128 query rows), FlashAttention-
+// style with tcgen05 (5th-gen tensor cores):
+//   warp 0      TMA producer: Q tile once per item, K+V blocks into a 2-stage ring
+//   warp 1      MMA issuer: S = Q K^T into TMEM (two S buffers), O += P V into TMEM
+//               (P from shared memory, V as an MN-major operand)
+//   warps 2..5  softmax: TMEM S -> online max / exp2 / sum -> bf16 P in smem, O row
+//               rescale in TMEM, final O / l -> global
+//   warp 6      wait warp: per-chunk flag acquires for remote KV blocks, ahead of warp 0
+// TMEM: S0 [0,128), S1 [128,256), O [256,384) fp32 columns.
+#include <cuda_runtime.h>
+
+#include "kernel_args.h"
+#include "ptx.cuh"
+
+namespace ao {
+namespace dev {
+
+constexpr int kAThreads = 256;
+constexpr int kBlk = 128;                  // query rows per item = KV rows per block
+constexpr uint32_t kHalf = 16384;          // one 128-row x 64-column bf16 box
+constexpr uint32_t kQBytes = 2 * kHalf;    // Q tile (d = 128: two boxes)
+constexpr uint32_t kKVBytes = 4 * kHalf;   // K block + V block
+constexpr int kKVStages = 2;
+constexpr int kAttnAhead = 4;
+constexpr uint32_t kAttnSmem = kQBytes + kKVStages * kKVBytes + 2 * kHalf + 1024 + 1024;
+
+struct AttnBars {
+  uint64_t qfull, qempty, kvfull[kKVStages], kvempty[kKVStages], sfull[2], sfree[2], pfull, ofull, ofree;
+  uint64_t wrdy[kAttnAhead], wfre[kAttnAhead];
+  uint32_t tmem_slot;
+  uint8_t waited[kAttnAhead];
+};
+
+__device__ __noinline__ void attn_spin(const uint32_t* p, uint32_t target, const AttnArgs& A, int rank, int cta, int w) {
+  if (ld_acquire_sys(p) >= target) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t ns = 32;
+  while (ld_acquire_sys(p) < target) {
+    if (globaltimer() - t0 > A.timeout_ns) {
+      if (atomicCAS(&A.err->claim, 0u, 1u) == 0u) {
+        A.err->rank = rank;
+        A.err->cta = cta;
+        A.err->chunk = w;
+        A.err->epoch = target;
+        A.err->seen = ld_acquire_sys(p);
+        __threadfence_system();
+        st_release_sys(const_cast<uint32_t*>(&A.err->flag), 1u);
+      }
+      return;
+    }
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+// Work items of this CTA in order: (rank group, item).  Space-sliced: its own group's items
+// with the persistent stride; time-sliced: every group's items, rank after rank.
+template <class F>
+__device__ __forceinline__ void attn_walk(const AttnArgs& a, int n_items, F&& f) {
+  if (!a.ts) {
+    const int g = blockIdx.x / a.ctas_per_rank, w = blockIdx.x % a.ctas_per_rank;
+    for (int i = w; i < n_items; i += a.ctas_per_rank) f(g, i);
+  } else {
+    for (int i = blockIdx.x; i < a.n_group * n_items; i += gridDim.x) f(i / n_items, i % n_items);
+  }
+}
+
+__global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constant__ AttnArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + kQBytes;
+  uint8_t* sP = sKV + kKVStages * kKVBytes;
+  AttnBars& B = *reinterpret_cast<AttnBars*>(sP + 2 * kHalf);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = args.W, S = args.S_loc, nqb = S / kBlk, nkb = S / kBlk;
+  const int n_items = args.H * nqb, nkv = W * nkb;
+
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(&B.qfull, 1);
+      mbar_init(&B.qempty, 1);
+      for (int s = 0; s < kKVStages; ++s) {
+        mbar_init(&B.kvfull[s], 1);
+        mbar_init(&B.kvempty[s], 1);
+      }
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(&B.sfull[s], 1);
+        mbar_init(&B.sfree[s], 4);
+      }
+      mbar_init(&B.pfull, 4);
+      mbar_init(&B.ofull, 1);
+      mbar_init(&B.ofree, 4);
+      for (int s = 0; s < kAttnAhead; ++s) {
+        mbar_init(&B.wrdy[s], 1);
+        mbar_init(&B.wfre[s], 1);
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(&B.tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_slot;
+
+  if (warp == 0) {
+    // ===================================================================== TMA producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_normal();
+      uint32_t t = 0, n = 0, q = 0;
+      attn_walk(args, n_items, [&](int g, int item) {
+        const AttnRank& R = args.rk[g];
+        const int h = item / nqb, qb = item % nqb;
+        mbar_wait(&B.qempty, (t & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&B.qfull, kQBytes);
+        tma_load_2d(sQ, &R.tmQ, &B.qfull, 0, h * S + qb * kBlk, pol);
+        tma_load_2d(sQ + kHalf, &R.tmQ, &B.qfull, 64, h * S + qb * kBlk, pol);
+        for (int j = 0; j < nkv; ++j, ++n) {
+          const int d = j / nkb, kb = j % nkb;
+          const int src = (R.rank - d + W) % W;
+          const int krow = h * S + kb * kBlk;
+          const int slot = int(q % kAttnAhead);
+          mbar_wait(&B.wrdy[slot], (q / kAttnAhead) & 1u);
+          const bool waited = B.waited[slot] != 0;
+          mbar_arrive(&B.wfre[slot]);
+          ++q;
+          if (waited) fence_proxy_async_global();  // generic-proxy acquire -> TMA reads
+          const uint32_t st = n % kKVStages;
+          mbar_wait(&B.kvempty[st], ((n / kKVStages) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&B.kvfull[st], kKVBytes);
+          uint8_t* dst = sKV + st * kKVBytes;
+          const CUtensorMap* mk = d == 0 ? &R.tmK_loc : &R.tmK;
+          const CUtensorMap* mv = d == 0 ? &R.tmV_loc : &R.tmV;
+          const int row = d == 0 ? krow : src * args.H * S + krow;
+          tma_load_2d(dst, mk, &B.kvfull[st], 0, row, pol);
+          tma_load_2d(dst + kHalf, mk, &B.kvfull[st], 64, row, pol);
+          tma_load_2d(dst + 2 * kHalf, mv, &B.kvfull[st], 0, row, pol);
+          tma_load_2d(dst + 3 * kHalf, mv, &B.kvfull[st], 64, row, pol);
+        }
+        ++t;
+      });
+    }
+  } else if (warp == 1) {
+    // ===================================================================== MMA issuer
+    constexpr uint32_t idesc_s = make_idesc_bf16(kBlk, kBlk);      // S = Q . K^T
+    constexpr uint32_t idesc_o = make_idesc_bf16_bmn(kBlk, 128);   // O += P . V (V MN-major)
+    const uint32_t tS[2] = {tmem, tmem + 128};
+    const uint32_t tO = tmem + 256;
+    uint32_t t = 0, n = 0;
+    auto issue_s = [&](uint32_t nn) {
+      const uint32_t st = nn % kKVStages, sb = nn & 1u;
+      mbar_wait(&B.kvfull[st], (nn / kKVStages) & 1u);
+      mbar_wait(&B.sfree[sb], ((nn >> 1) & 1u) ^ 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint8_t* kb = sKV + st * kKVBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t a = make_smem_desc_sw128(smem_u32(sQ + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
+          const uint64_t b = make_smem_desc_sw128(smem_u32(kb + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
+          mma_bf16_ss(tS[sb], a, b, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&B.sfull[sb]);
+      }
+      __syncwarp();
+    };
+    attn_walk(args, n_items, [&](int g, int item) {
+      (void)g;
+      (void)item;
+      mbar_wait(&B.qfull, t & 1u);
+      tc_fence_after();
+      issue_s(n);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) {
+          issue_s(n + j + 1);
+        } else if (lane == 0) {
+          mma_commit(&B.qempty);  // every S of this item issued: Q is free once they complete
+        }
+        __syncwarp();
+        if (j == 0) mbar_wait(&B.ofree, (t & 1u) ^ 1u);  // the previous item's O was read
+        mbar_wait(&B.pfull, (n + j) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = (n + j) % kKVStages;
+          const uint8_t* vb = sKV + st * kKVBytes + 2 * kHalf;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t a = make_smem_desc_sw128(smem_u32(sP + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
+            const uint64_t b = make_smem_desc_sw128_mn(smem_u32(vb + kk * 16 * 128), kHalf);
+            mma_bf16_ss(tO, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&B.kvempty[st]);
+          mma_commit(&B.ofull);
+        }
+        __syncwarp();
+      }
+      n += nkv;
+      ++t;
+    });
+  } else if (warp < 6) {
+    // ===================================================================== softmax
+    const int qd = warp & 3;  // TMEM lane quadrant
+    const int r = qd * 32 + lane;
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const float sl2 = args.scale_log2;
+    uint32_t n = 0, ocnt = 0;
+    attn_walk(args, n_items, [&](int g, int item) {
+      const AttnRank& R = args.rk[g];
+      const int h = item / nqb, qb = item % nqb;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j) {
+        const uint32_t nn = n + j, sb = nn & 1u;
+        mbar_wait(&B.sfull[sb], (nn >> 1) & 1u);
+        tc_fence_after();
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem + lane_off + sb * 128 + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.sfree[sb]);
+        float mx = s[0];
+#pragma unroll
+        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+        const float m_new = fmaxf(m, mx * sl2);
+        const float alpha = exp2f(m - m_new);
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          s[i] = exp2f(fmaf(s[i], sl2, -m_new));
+          sum += s[i];
+        }
+        l = l * alpha + sum;
+        m = m_new;
+        if (j > 0) {  // PV of the previous block done: O is stable and the P buffer is free
+          mbar_wait(&B.ofull, ocnt & 1u);
+          ++ocnt;
+          tc_fence_after();
+        }
+        // P row r (bf16) into the K-major SW128 A-operand layout: two 64-column blocks
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const uint4 w = make_uint4(pack_bf16x2(s[8 * c], s[8 * c + 1]), pack_bf16x2(s[8 * c + 2], s[8 * c + 3]),
+                                     pack_bf16x2(s[8 * c + 4], s[8 * c + 5]), pack_bf16x2(s[8 * c + 6], s[8 * c + 7]));
+          *reinterpret_cast<uint4*>(sP + (c >> 3) * kHalf + r * 128 + (((c & 7) ^ (r & 7)) * 16)) = w;
+        }
+        if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {  // rescale the O row by alpha
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tmem + lane_off + 256 + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(tmem + lane_off + 256 + c * 32, v);
+          }
+          tmem_wait_st();
+        }
+        fence_proxy_async_smem();  // P (generic smem writes) -> the MMA's async-proxy reads
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.pfull);
+      }
+      // final O row / l -> bf16 -> global
+      mbar_wait(&B.ofull, ocnt & 1u);
+      ++ocnt;
+      tc_fence_after();
+      const float inv = 1.f / l;
+      char* orow = R.O + (int64_t(h) * S + qb * kBlk + r) * 256;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + 256 + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 w = make_uint4(pack_bf16x2(__uint_as_float(v[8 * i]) * inv, __uint_as_float(v[8 * i + 1]) * inv),
+                                     pack_bf16x2(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv),
+                                     pack_bf16x2(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv),
+                                     pack_bf16x2(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv));
+          *reinterpret_cast<uint4*>(orow + c * 64 + i * 16) = w;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&B.ofree);
+      n += nkv;
+    });
+  } else if (warp == 6) {
+    // ===================================================================== wait warp
+    if (lane == 0) {
+      uint64_t got[AO_MAX_WORLD] = {};
+      uint32_t q = 0;
+      attn_walk(args, n_items, [&](int g, int item) {
+        const AttnRank& R = args.rk[g];
+        const int h = item / nqb;
+        for (int j = 0; j < nkv; ++j) {
+          const int slot = int(q % kAttnAhead);
+          mbar_wait(&B.wfre[slot], ((q / kAttnAhead) & 1u) ^ 1u);
+          const int d = j / nkb, kb = j % nkb;
+          bool waited = false;
+          if (d > 0) {
+            const int src = (R.rank - d + W) % W;
+            const int w = src * args.nch + (h * S + kb * kBlk) / args.crows;
+            if (!(w < 64 && ((got[g] >> w) & 1u))) {
+              attn_spin(R.flags + w, R.epoch, args, R.rank, int(blockIdx.x), w);
+              if (w < 64) got[g] |= 1ull << w;
+              waited = true;
+            }
+          }
+          B.waited[slot] = waited ? 1 : 0;
+          mbar_arrive(&B.wrdy[slot]);
+          ++q;
+        }
+      });
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace dev
+
+cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dev::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(dev::kAttnSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(args.ts ? args.ctas_per_rank : args.n_group * args.ctas_per_rank);
+  cfg.blockDim = dim3(dev::kAThreads);
+  cfg.dynamicSmemBytes = dev::kAttnSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // spin-waiting persistent CTAs must be co-resident
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dev::attn_kernel, args);
+}
+
+}  // namespace ao

@@ -99,6 +99,28 @@ struct A2APrepArgs {
   ErrorInfo* err;
 };
 
+// SP attention (NEXT-4): rank r's queries against the all-gathered K/V, head dim 128.
+// Q/K/V/O are [H, S_loc, 128] bf16 viewed as [H*S_loc, 128]; the gathered K and V buffers
+// are [W][H*S_loc][128] (source-major) in the symmetric data half (K, then V).
+struct AttnRank {
+  CUtensorMap tmQ, tmK_loc, tmV_loc, tmK, tmV;  // 2-D maps, boxes of 64 elements x 128 rows
+  char* O;                                      // [H*S_loc, 128] bf16
+  const uint32_t* flags;                        // this rank's flag words: chunk (src, c) at src*nch + c
+  int32_t rank;
+  uint32_t epoch;
+};
+struct AttnArgs {
+  AttnRank rk[AO_MAX_WORLD];
+  int32_t n_group, W, H, S_loc, crows, nch;  // crows: rows of the [H*S_loc] view per chunk
+  int32_t ctas_per_rank, ts;                 // ts: time-sliced whole-world group (rank after rank)
+  float scale_log2;                          // softmax scale * log2(e)
+  uint64_t timeout_ns;
+  ErrorInfo* err;
+  struct TraceEvent* trace;
+  uint32_t* trace_cursor;
+  uint32_t trace_cap, trace_seq;
+};
+
 // In-kernel trace event (AO tracing): 32 bytes, %globaltimer nanoseconds.
 enum TraceKind : uint32_t { TR_WAIT = 1, TR_LOAD = 2, TR_MMA = 3, TR_EPI = 4, TR_COMM = 5, TR_RED = 6, TR_REDWAIT = 7 };
 struct TraceEvent {
@@ -143,5 +165,6 @@ static_assert(sizeof(KernelArgs) <= 32764, "KernelArgs exceeds the kernel parame
 // bn: tile N (128/256); cg: 1 (BM = 128) or 2 (CTA pair, BM = 256); comm: CommKind.
 cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream);
 cudaError_t launch_a2a_prep(const A2APrepArgs& args, cudaStream_t stream);
+cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream);
 
 }  // namespace ao

@@ -213,6 +213,19 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 32 lanes x 32 consecutive 32-bit columns from registers (thread i -> TMEM lane base+i).
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, K-major operand, 128-byte swizzle: rows of 64 bf16
 // (128 B), 8-row core-matrix groups 1024 B apart (SBO), LBO unused (=1), version 1.
@@ -220,6 +233,17 @@ __device__ __forceinline__ uint64_t make_smem_desc_sw128(uint32_t smem_addr) {
   uint64_t d = 0;
   d |= uint64_t((smem_addr & 0x3FFFF) >> 4);  // start address  [0,14)
   d |= uint64_t(1) << 16;                      // LBO (ignored)  [16,30)
+  d |= uint64_t(1024 >> 4) << 32;              // SBO = 1024 B   [32,46)
+  d |= uint64_t(1) << 46;                      // version = 1    [46,48)
+  d |= uint64_t(2) << 61;                      // SWIZZLE_128B   [61,64)
+  return d;
+}
+// UMMA shared-memory descriptor, MN-major operand, 128-byte swizzle: 64-element (128 B)
+// MN rows, 8-row K groups 1024 B apart (SBO), MN atoms `lbo` bytes apart (LBO).
+__device__ __forceinline__ uint64_t make_smem_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr & 0x3FFFF) >> 4);  // start address  [0,14)
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;    // LBO            [16,30)
   d |= uint64_t(1024 >> 4) << 32;              // SBO = 1024 B   [32,46)
   d |= uint64_t(1) << 46;                      // version = 1    [46,48)
   d |= uint64_t(2) << 61;                      // SWIZZLE_128B   [61,64)
@@ -233,6 +257,9 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
          | (uint32_t(N >> 3) << 17)   // N / 8
          | (uint32_t(M >> 4) << 24);  // M / 16
 }
+
+// ... with B MN-major (transposed B, bit 16): D = A . B for B stored [K rows][N contiguous].
+__host__ __device__ constexpr uint32_t make_idesc_bf16_bmn(int M, int N) { return make_idesc_bf16(M, N) | (1u << 16); }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // RNE (cvt.rn.bf16x2.f32)

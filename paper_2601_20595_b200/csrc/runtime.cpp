@@ -15,6 +15,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -823,7 +824,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   const ao::HostPlan& h0 = p0->hp;
   if (h0.desc.op != op)
     return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is %s",
-                h0.is_ag ? "ag_gemm" : (h0.is_ar ? "gemm_ar" : (h0.is_a2a ? "a2a_gemm" : "gemm_rs")));
+                h0.is_ag ? "ag_gemm" : (h0.is_ar ? "gemm_ar" : (h0.is_a2a ? "a2a_gemm" : (h0.is_attn ? "sp_attn" : "gemm_rs"))));
   for (int i = 0; i < n; ++i) {
     ao_plan* p = plans[i];
     if (!p || !p->ctx) return fail(AO_ERR_STATE, "plan %d not bound", i);
@@ -1121,6 +1122,157 @@ ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs,
 ao_status ao_a2a_gemm(ao_plan* plan, const void* X, const int32_t* topk_idx, const void* B, void* Y,
                       int32_t* route_pos, int32_t* recv_rows, void* stream) {
   return launch_a2a(1, &plan, &X, &topk_idx, &B, &Y, &route_pos, &recv_rows, stream);
+}
+
+// SP attention (NEXT-4): copy-engine pushes of every source's K/V chunks to every peer's
+// gathered buffers (ring rotation; destination-major when time-sliced), each followed by
+// the epoch copied into the destination's flag (src, chunk); then the attention kernel.
+static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
+                                   const void* const* Vs, void* const* Os, void* stream_v) {
+  if (n < 1 || n > AO_MAX_WORLD || !plans) return fail(AO_ERR_INVALID_ARG, "bad group size %d", n);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  ao_plan* p0 = plans[0];
+  if (!p0 || !p0->ctx) return fail(AO_ERR_STATE, "plan is not bound to a ctx");
+  const ao::HostPlan& h0 = p0->hp;
+  if (!h0.is_attn) return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is not sp_attn");
+  for (int i = 0; i < n; ++i) {
+    ao_plan* p = plans[i];
+    if (!p || !p->ctx) return fail(AO_ERR_STATE, "plan %d not bound", i);
+    if (!p->ctx->imported) return fail(AO_ERR_STATE, "ctx of rank %d: handles not imported", p->ctx->rank);
+    if (p->hp.hash != h0.hash) return fail(AO_ERR_PEER, "plan hash mismatch inside group");
+    if (p->ctx->device != p0->ctx->device) return fail(AO_ERR_INVALID_ARG, "group spans devices");
+    for (int j = 0; j < i; ++j)
+      if (plans[j]->ctx == p->ctx) return fail(AO_ERR_INVALID_ARG, "two plans of one ctx in a group");
+    if (!aligned16(Qs[i]) || !aligned16(Ks[i]) || !aligned16(Vs[i]) || !aligned16(Os[i]))
+      return fail(AO_ERR_INVALID_ARG, "operands must be 16-byte aligned device pointers");
+    ao_status s = take_async_error(p->ctx);
+    if (s != AO_OK) return s;
+  }
+  AO_CUDA(cudaSetDevice(p0->ctx->device));
+  const int W = h0.W, H = int(h0.N), S = int(h0.M), crows = h0.C, nch = h0.n_c;
+  const int64_t rows = int64_t(H) * S, row_bytes = 256;  // [H*S_loc, 128] bf16
+  std::unique_ptr<ao::AttnArgs> ka(new ao::AttnArgs());
+  memset(ka.get(), 0, sizeof(ao::AttnArgs));
+  ka->n_group = n;
+  ka->W = W;
+  ka->H = H;
+  ka->S_loc = S;
+  ka->crows = crows;
+  ka->nch = nch;
+  ka->ctas_per_rank = h0.n_cta;
+  ka->scale_log2 = float(1.4426950408889634 / std::sqrt(128.0));
+  ka->timeout_ns = h0.desc.timeout_ns ? h0.desc.timeout_ns : 5000000000ull;
+  ka->err = p0->ctx->err_dev;
+  if (int64_t(n) * h0.n_cta > p0->ctx->sm_count) {
+    if (n == W && h0.n_cta <= p0->ctx->sm_count)
+      ka->ts = 1;  // time-sliced whole-world group: rank after rank over all SMs (Q24)
+    else
+      return fail(AO_ERR_INVALID_ARG, "grid of %lld CTAs exceeds the %d SMs (lower n_cta)",
+                  (long long)(int64_t(n) * h0.n_cta), p0->ctx->sm_count);
+  }
+  std::vector<uint32_t> epochs(n);
+  for (int i = 0; i < n; ++i) {
+    ao_ctx* c = plans[i]->ctx;
+    epochs[i] = c->epoch + 1;
+    if (epochs[i] != epochs[0]) return fail(AO_ERR_STATE, "ranks of a group disagree on the epoch");
+    const uint32_t par = epochs[i] & 1;
+    const int r = plans[i]->hp.rank;
+    ao::AttnRank& R = ka->rk[i];
+    char* gK = c->data(r, par);
+    char* gV = gK + int64_t(W) * rows * row_bytes;
+    ao_status s;
+    if ((s = encode_2d(&R.tmQ, Qs[i], rows, 128, 128)) != AO_OK) return s;
+    if ((s = encode_2d(&R.tmK_loc, Ks[i], rows, 128, 128)) != AO_OK) return s;
+    if ((s = encode_2d(&R.tmV_loc, Vs[i], rows, 128, 128)) != AO_OK) return s;
+    if ((s = encode_2d(&R.tmK, gK, int64_t(W) * rows, 128, 128)) != AO_OK) return s;
+    if ((s = encode_2d(&R.tmV, gV, int64_t(W) * rows, 128, 128)) != AO_OK) return s;
+    R.O = static_cast<char*>(Os[i]);
+    R.flags = c->flags(r, par);
+    R.rank = r;
+    R.epoch = epochs[i];
+  }
+  ao_ctx* c0 = p0->ctx;
+  const uint32_t par = epochs[0] & 1;
+  const bool ce = W > 1 && rows > 0;
+  if (ce) {
+    AO_CUDA(cudaEventRecord(c0->ev_start, stream));
+    AO_CUDA(cudaStreamWaitEvent(c0->side, c0->ev_start, 0));
+    DriverFns* drv = nullptr;
+    ao_status s = get_driver(&drv);
+    if (s != AO_OK) return s;
+    CUresult cr = drv->write32(c0->side, reinterpret_cast<CUdeviceptr>(c0->epoch_cell), epochs[0], 0);
+    if (cr != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(cr));
+    std::vector<uintptr_t> key{uintptr_t(0xA77Eu), uintptr_t(par), uintptr_t(n), uintptr_t(ka->ts)};
+    for (int i = 0; i < n; ++i) {
+      key.push_back(reinterpret_cast<uintptr_t>(plans[i]));
+      key.push_back(reinterpret_cast<uintptr_t>(Ks[i]));
+      key.push_back(reinterpret_cast<uintptr_t>(Vs[i]));
+    }
+    cudaGraphExec_t exec = nullptr;
+    auto it = p0->ce_graphs.find(key);
+    if (it != p0->ce_graphs.end()) {
+      exec = it->second;
+    } else {
+      cudaGraph_t graph;
+      AO_CUDA(cudaGraphCreate(&graph, 0));
+      for (int i = 0; i < n; ++i) {  // one chain per source rank in this group
+        const int src = plans[i]->hp.rank;
+        std::vector<int> dests;
+        for (int ds = 1; ds < W; ++ds) dests.push_back((src + ds) % W);  // ring rotation
+        if (ka->ts) std::sort(dests.begin(), dests.end());              // destination-major
+        std::vector<cudaGraphNode_t> prev;
+        for (int dst : dests) {
+          ao_ctx* dc = nullptr;  // the destination's buffers, mapped in this process
+          for (int q = 0; q < n; ++q)
+            if (plans[q]->hp.rank == dst) dc = plans[q]->ctx;
+          char* gK = (dc ? dc : plans[i]->ctx)->data(dst, par);
+          if (!dc) gK = plans[i]->ctx->data(dst, par);
+          char* gV = gK + int64_t(W) * rows * row_bytes;
+          uint32_t* fl = plans[i]->ctx->flags(dst, par);
+          for (int cch = 0; cch < nch; ++cch) {
+            const int64_t off = (int64_t(src) * rows + int64_t(cch) * crows) * row_bytes;
+            const int64_t soff = int64_t(cch) * crows * row_bytes;
+            const size_t bytes = size_t(crows) * row_bytes;
+            cudaGraphNode_t nk = nullptr, nv = nullptr, nf = nullptr;
+            AO_CUDA(cudaGraphAddMemcpyNode1D(&nk, graph, prev.data(), prev.size(), gK + off,
+                                             static_cast<const char*>(Ks[i]) + soff, bytes, cudaMemcpyDeviceToDevice));
+            AO_CUDA(cudaGraphAddMemcpyNode1D(&nv, graph, &nk, 1, gV + off, static_cast<const char*>(Vs[i]) + soff,
+                                             bytes, cudaMemcpyDeviceToDevice));
+            AO_CUDA(cudaGraphAddMemcpyNode1D(&nf, graph, &nv, 1, fl + src * nch + cch, c0->epoch_cell, 4,
+                                             cudaMemcpyDeviceToDevice));
+            prev.assign(1, nf);
+          }
+        }
+      }
+      cudaError_t ge = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ge != cudaSuccess) return fail(AO_ERR_CUDA, "CE graph instantiate: %s", cudaGetErrorString(ge));
+      if (p0->ce_graphs.size() >= kMaxCeGraphs) {
+        AO_CUDA(cudaStreamSynchronize(c0->side));
+        cudaGraphExecDestroy(p0->ce_graphs.begin()->second);
+        p0->ce_graphs.erase(p0->ce_graphs.begin());
+      }
+      p0->ce_graphs[key] = exec;
+    }
+    AO_CUDA(cudaGraphLaunch(exec, c0->side));
+    AO_CUDA(cudaEventRecord(c0->ev_done, c0->side));
+  }
+  if (rows > 0) {
+    cudaError_t e = ao::launch_attn(*ka, stream);
+    if (e != cudaSuccess) return fail(AO_ERR_CUDA, "attention kernel launch: %s", cudaGetErrorString(e));
+  }
+  for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
+  if (ce) AO_CUDA(cudaStreamWaitEvent(stream, c0->ev_done, 0));
+  return AO_OK;
+}
+
+ao_status ao_sp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
+                           const void* const* Vs, void* const* Os, void* stream) {
+  return launch_attn_group(n, plans, Qs, Ks, Vs, Os, stream);
+}
+
+ao_status ao_sp_attn(ao_plan* plan, const void* Q, const void* K, const void* V, void* O, void* stream) {
+  return launch_attn_group(1, &plan, &Q, &K, &V, &O, stream);
 }
 
 ao_status ao_ag_gemm_group(int n, ao_plan* const* plans, const void* const* A_shards, const void* const* Bs,

@@ -1,0 +1,97 @@
+"""GPU parity of SP attention (NEXT-4: sequence-parallel attention over all-gathered KV,
+consumed in ring/arrival order) vs the fp64 oracle (oracle/attn.py), through the C ABI.
+
+Tolerance: the north-star bound (1e-2 per element relative to max(1, |ref|)) and a
+Frobenius bound of 5e-3: P enters the P.V MMA as bf16 (the method's bf16-in/fp32-accumulate
+arithmetic, Q27), which alone gives ~2^-9/sqrt(3) relative error, plus the bf16
+output rounding."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attn as oatt
+from oracle import numeric as on
+from synthetic import inputs as si
+
+pytestmark = pytest.mark.gpu
+SMS = 148
+FROB = 5e-3
+
+
+@pytest.fixture(scope="module")
+def ao():
+    from paper_2601_20595_b200 import build
+    build.build(verbose=False)
+    import paper_2601_20595_b200.api as api
+    return api
+
+
+def _world(ao, W, H, S, C, n_cta, **kw):
+    d = dict(op="sp_attn", world_size=W, M=S, N=H, K=128, chunk_rows=C, backend="ce", n_cta=n_cta,
+             timeout_ns=2_000_000_000)
+    d.update(kw)
+    ctxs = ao.loopback_world(0, W, ao.workspace_bytes(d))
+    return ctxs, [ao.Plan(ctxs[r], dict(d, rank=r)) for r in range(W)]
+
+
+def _run(ao, ctxs, plans, Q, K, V):
+    O = [torch.full_like(q, float("nan"), device="cuda") for q in Q]
+    ao.sp_attn_group(plans, [q.cuda() for q in Q], [k.cuda() for k in K], [v.cuda() for v in V], O)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    return O
+
+
+def _check(O, Q, K, V, what):
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    for r in range(len(O)):
+        ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5)
+        got = O[r].float().cpu().numpy()
+        ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
+        assert ok, f"{what} rank {r}: max elem err {e:.3e}, frob {f:.3e}"
+
+
+@pytest.mark.parametrize("W,H,S,C", [(1, 1, 128, 128), (1, 2, 256, 128), (2, 2, 256, 256), (4, 2, 128, 128),
+                                     (8, 1, 256, 128)])
+def test_sp_attn_vs_oracle(ao, W, H, S, C):
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=W * 10 + H)
+    ctxs, plans = _world(ao, W, H, S, C, max(1, SMS // W))
+    O = _run(ao, ctxs, plans, Q, K, V)
+    _check(O, Q, K, V, f"sp_attn W={W} H={H} S={S} C={C}")
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_sp_attn_timesliced_and_epochs(ao, W):
+    H, S = 3, 256
+    ctxs, plans = _world(ao, W, H, S, 256, SMS)
+    for it in range(3):  # both parities, flags re-armed by the epoch
+        Q, K, V = si.attn_inputs(W, H, S, 128, salt=100 + it)
+        O = _run(ao, ctxs, plans, Q, K, V)
+        _check(O, Q, K, V, f"sp_attn ts W={W} it={it}")
+
+
+def test_sp_attn_few_ctas_many_items(ao):
+    """More items than CTAs (each CTA loops over several (head, q-block) items and
+    several KV blocks per source): the barrier phases across items."""
+    W, H, S = 2, 4, 512
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=7)
+    ctxs, plans = _world(ao, W, H, S, 512, 3)
+    O = _run(ao, ctxs, plans, Q, K, V)
+    _check(O, Q, K, V, "sp_attn few ctas")
+
+
+def test_sp_attn_llama_sampled(ao):
+    """Llama-3-8B attention shape, SP over 8 ranks (loopback, time-sliced): 32 heads,
+    d = 128, 16384 tokens (2048 per rank); sampled rows of three heads vs fp64."""
+    W, H, S = 8, 32, 2048
+    Q, K, V = si.attn_inputs(W, H, S, 128)
+    ctxs, plans = _world(ao, W, H, S, 2048, SMS, timeout_ns=10_000_000_000)
+    O = _run(ao, ctxs, plans, Q, K, V)
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    rows = np.array([0, 127, 128, 1000, 2047])
+    for r in (0, 5):
+        ref = oatt.sp_attention_rows(Qn, Kn, Vn, r, 128 ** -0.5, [0, 13, 31], rows)
+        got = O[r][[0, 13, 31]][:, rows].float().cpu().numpy()
+        ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
+        assert ok, f"llama sampled rank {r}: {e:.3e} {f:.3e}"

@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--debug", action="append", default=[], help=argparse.SUPPRESS)
     ap.add_argument("--no-ar", action="store_true", help="skip the GEMM-AR (NEXT-1) leg")
     ap.add_argument("--no-a2a", action="store_true", help="skip the A2A-GEMM (NEXT-3, Mixtral) leg")
+    ap.add_argument("--no-attn", action="store_true", help="skip the SP-attention (NEXT-4) leg")
+    ap.add_argument("--attn-seq", type=int, default=32768, help="SP attention: total sequence length")
     ap.add_argument("--a2a-chunk", type=int, default=64, help="A2A chunk rows")
     ap.add_argument("--a2a-zipf", type=float, default=0.0, help="A2A routing skew (0 = top-2 of N(0,1) logits)")
     ap.add_argument("--ar-chunk", type=int, default=256, help="GEMM-AR chunk rows")
@@ -287,6 +289,11 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_a2a:
         a2a = a2a_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
 
+    # --- SP attention (NEXT-4): Llama-3-8B attention, sequence-parallel over W ranks ---------
+    attn = None
+    if not args.no_attn:
+        attn = attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
+
     # --- e2e through the public API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:
@@ -331,6 +338,7 @@ def run_ours(args, rank, world, local_rank):
         "gemm_only": gemm_only,
         "gemm_ar": ar,
         "a2a_gemm": a2a,
+        "sp_attn": attn,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(W, M, budget_s=12.0)
@@ -496,6 +504,79 @@ def a2a_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms):
             "frac_of_peak": round(tf / peaks["bf16_tflops"], 4), "rows_per_expert": rows if loop else rows[0],
             "gemm_only_ms_equal_rows": round(g_ms, 4),
             "gemm_only_tflops": round(g_flops / (g_ms * 1e-3) / 1e12, 1), "launches_per_op": 2}
+
+
+def attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms):
+    """NEXT-4: sequence-parallel attention with the KV all-gathered in ring order, Llama-3-8B
+    attention (32 heads, d = 128), non-causal, --attn-seq tokens split over 8 ranks (loopback,
+    time-sliced) or over the N GPUs.  FLOPs = 4 * S_total^2 * d * H (QK^T and PV).  Beside it:
+    torch SDPA (library flash attention) on the same gathered K/V, per rank."""
+    import torch.nn.functional as Fn
+    W = 8 if loop else world
+    H, d = 32, 128
+    S = args.attn_seq // W
+    my = list(range(W)) if loop else [rank]
+    Q, K, V = si.attn_inputs(W, H, S, d)
+    desc = dict(op="sp_attn", world_size=W, M=S, N=H, K=d, chunk_rows=S, backend="ce", n_cta=sms,
+                timeout_ns=10_000_000_000)
+    ctxs = ao.loopback_world(local_rank, W, ao.workspace_bytes(desc)) if loop else \
+        [ao.dist_world(local_rank, ao.workspace_bytes(desc))]
+    plans = [ao.Plan(c, dict(desc, rank=r)) for c, r in zip(ctxs, my)]
+    Qd = [Q[r].to(dev) for r in my]
+    Kd = [K[r].to(dev) for r in my]
+    Vd = [V[r].to(dev) for r in my]
+    Od = [torch.empty_like(q) for q in Qd]
+
+    def run():
+        if loop:
+            ao.sp_attn_group(plans, Qd, Kd, Vd, Od)
+        else:
+            ao.sp_attn(plans[0], Qd[0], Kd[0], Vd[0], Od[0])
+
+    def timed(fn, n):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(n):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / n
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    n = max(3, args.steps // 10)
+    ms = timed(run, n)
+    for c in ctxs:
+        c.check_async()
+    Stot = S * W
+    flops = 4.0 * Stot * Stot * d * H / (1 if loop else W)
+    # library reference: SDPA per rank over its gathered K/V (already resident)
+    if loop:
+        Kf = torch.cat([k.to(dev) for k in K], 1).unsqueeze(0)
+        Vf = torch.cat([v.to(dev) for v in V], 1).unsqueeze(0)
+        sd = lambda: [Fn.scaled_dot_product_attention(q.unsqueeze(0), Kf, Vf) for q in Qd]
+        sd_ms = timed(sd, n)
+        del Kf, Vf
+    else:
+        sd_ms = None
+    peaks, _ = load_peaks()
+    tf = flops / (ms * 1e-3) / 1e12
+    for p in plans:
+        p.close()
+    return {"what": "sequence-parallel attention over the all-gathered KV in ring order (NEXT-4), non-causal",
+            "workload": "llama3-8b-attn-sp%d-%s" % (W, "loopback" if loop else "nvlink"),
+            "seq_total": Stot, "heads": H, "head_dim": d, "ms": round(ms, 4), "tflops": round(tf, 1),
+            "frac_of_peak": round(tf / peaks["bf16_tflops"], 4),
+            "sdpa_same_gpu_ms": None if sd_ms is None else round(sd_ms, 4),
+            "sdpa_tflops": None if sd_ms is None else round(flops / (sd_ms * 1e-3) / 1e12, 1)}
 
 
 def gemm_only_leg(torch, ao, pa, pr, A, Bu, Bd, W, M, F, args, dev, loop):

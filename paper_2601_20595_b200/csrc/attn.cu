@@ -32,10 +32,11 @@ constexpr uint32_t kQBytes = 2 * kHalf;    // Q tile (d = 128: two boxes)
 constexpr uint32_t kKVBytes = 4 * kHalf;   // K block + V block
 constexpr int kKVStages = 2;
 constexpr int kAttnAhead = 4;
-constexpr uint32_t kAttnSmem = kQBytes + kKVStages * kKVBytes + 2 * kHalf + 1024 + 1024;
+constexpr uint32_t kPBytes = 2 * kHalf;   // one P tile (128 x 128 bf16)
+constexpr uint32_t kAttnSmem = kQBytes + kKVStages * kKVBytes + 2 * kPBytes + 1024 + 1024;
 
 struct AttnBars {
-  uint64_t qfull, qempty, kvfull[kKVStages], kvempty[kKVStages], sfull[2], sfree[2], pfull, ofull, ofree;
+  uint64_t qfull, qempty, kvfull[kKVStages], kvempty[kKVStages], sfull[2], sfree[2], pfull, pvdone[2], ofree;
   uint64_t wrdy[kAttnAhead], wfre[kAttnAhead];
   uint32_t tmem_slot;
   uint8_t waited[kAttnAhead];
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + kQBytes;
   uint8_t* sP = sKV + kKVStages * kKVBytes;
-  AttnBars& B = *reinterpret_cast<AttnBars*>(sP + 2 * kHalf);
+  AttnBars& B = *reinterpret_cast<AttnBars*>(sP + 2 * kPBytes);  // sP: two P buffers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = args.W, S = args.S_loc, nqb = S / kBlk, nkb = S / kBlk;
   const int n_items = args.H * nqb, nkv = W * nkb;
@@ -99,7 +100,8 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         mbar_init(&B.sfree[s], 4);
       }
       mbar_init(&B.pfull, 4);
-      mbar_init(&B.ofull, 1);
+      mbar_init(&B.pvdone[0], 1);
+      mbar_init(&B.pvdone[1], 1);
       mbar_init(&B.ofree, 4);
       for (int s = 0; s < kAttnAhead; ++s) {
         mbar_init(&B.wrdy[s], 1);
@@ -198,12 +200,13 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
           const uint8_t* vb = sKV + st * kKVBytes + 2 * kHalf;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t a = make_smem_desc_sw128(smem_u32(sP + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
+            const uint64_t a =
+                make_smem_desc_sw128(smem_u32(sP + ((n + j) & 1u) * kPBytes + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
             const uint64_t b = make_smem_desc_sw128_mn(smem_u32(vb + kk * 16 * 128), kHalf);
             mma_bf16_ss(tO, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&B.kvempty[st]);
-          mma_commit(&B.ofull);
+          mma_commit(&B.pvdone[(n + j) & 1u]);  // P buffer (n+j)&1 free, O updated
         }
         __syncwarp();
       }
@@ -216,7 +219,17 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
     const int r = qd * 32 + lane;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const float sl2 = args.scale_log2;
-    uint32_t n = 0, ocnt = 0;
+    uint32_t n = 0;
+    uint32_t cons[2] = {0, 0};  // phases of pvdone[b] consumed (PV of blocks b, b+2, ... done)
+    // wait until PV of global block nb is done (in order per buffer; never skips a phase)
+    auto pv_wait = [&](uint32_t nb) {
+      const uint32_t b = nb & 1u;
+      while (cons[b] <= (nb >> 1)) {
+        mbar_wait(&B.pvdone[b], cons[b] & 1u);
+        ++cons[b];
+      }
+      tc_fence_after();
+    };
     attn_walk(args, n_items, [&](int g, int item) {
       const AttnRank& R = args.rk[g];
       const int h = item / nqb, qb = item % nqb;
@@ -237,32 +250,44 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&B.sfree[sb]);
-        float mx = s[0];
+        // row max and sum with 8 independent partials (a single serial chain of 128
+        // dependent fmax / fadd is latency-bound: ~4 cycles each, one warp per SMSP)
+        float mp[8];
 #pragma unroll
-        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
-        const float m_new = fmaxf(m, mx * sl2);
-        const float alpha = exp2f(m - m_new);
-        float sum = 0.f;
+        for (int u = 0; u < 8; ++u) mp[u] = s[u];
+#pragma unroll
+        for (int i = 8; i < 128; ++i) mp[i & 7] = fmaxf(mp[i & 7], s[i]);
+        const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+        // lazy rescale: the exponent base m moves only when the row max exceeds it by more
+        // than 8 (p <= 2^8 stays exact enough in fp32 / bf16); otherwise alpha = 1 and the
+        // O row in TMEM is left alone (the final O / l is consistent for any base)
+        const float mxs = mx * sl2;
+        const bool grow = mxs > m + 8.f;
+        const float m_new = grow ? mxs : m;
+        const float alpha = grow ? exp2f(m - m_new) : 1.f;
+        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < 128; ++i) {
           s[i] = exp2f(fmaf(s[i], sl2, -m_new));
-          sum += s[i];
+          sp[i & 7] += s[i];
         }
+        const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
         l = l * alpha + sum;
         m = m_new;
-        if (j > 0) {  // PV of the previous block done: O is stable and the P buffer is free
-          mbar_wait(&B.ofull, ocnt & 1u);
-          ++ocnt;
-          tc_fence_after();
-        }
+        // P buffer nn&1 was last read by the PV of block nn-2 (double-buffered P: the PV of
+        // block nn-1 may still be running while this P is written)
+        if (nn >= 2) pv_wait(nn - 2);
+        uint8_t* pb = sP + (nn & 1u) * kPBytes;
         // P row r (bf16) into the K-major SW128 A-operand layout: two 64-column blocks
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           const uint4 w = make_uint4(pack_bf16x2(s[8 * c], s[8 * c + 1]), pack_bf16x2(s[8 * c + 2], s[8 * c + 3]),
                                      pack_bf16x2(s[8 * c + 4], s[8 * c + 5]), pack_bf16x2(s[8 * c + 6], s[8 * c + 7]));
-          *reinterpret_cast<uint4*>(sP + (c >> 3) * kHalf + r * 128 + (((c & 7) ^ (r & 7)) * 16)) = w;
+          *reinterpret_cast<uint4*>(pb + (c >> 3) * kHalf + r * 128 + (((c & 7) ^ (r & 7)) * 16)) = w;
         }
-        if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {  // rescale the O row by alpha
+        const bool rescale = j > 0 && __any_sync(0xffffffffu, alpha < 1.f);
+        if (rescale) pv_wait(nn - 1);  // O holds every PV up to block nn-1
+        if (rescale) {  // rescale the O row by alpha
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t v[32];
@@ -280,9 +305,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         if (lane == 0) mbar_arrive(&B.pfull);
       }
       // final O row / l -> bf16 -> global
-      mbar_wait(&B.ofull, ocnt & 1u);
-      ++ocnt;
-      tc_fence_after();
+      pv_wait(n + nkv - 1);
       const float inv = 1.f / l;
       char* orow = R.O + (int64_t(h) * S + qb * kBlk + r) * 256;
 #pragma unroll 1

@@ -25,7 +25,8 @@
 namespace ao {
 namespace dev {
 
-constexpr int kAThreads = 256;
+constexpr int kAThreads = 352;   // 11 warps
+constexpr int kSmWarps = 8;      // softmax warps: two per TMEM lane quadrant, 64 columns each
 constexpr int kBlk = 128;                  // query rows per item = KV rows per block
 constexpr uint32_t kHalf = 16384;          // one 128-row x 64-column bf16 box
 constexpr uint32_t kQBytes = 2 * kHalf;    // Q tile (d = 128: two boxes)
@@ -33,13 +34,16 @@ constexpr uint32_t kKVBytes = 4 * kHalf;   // K block + V block
 constexpr int kKVStages = 2;
 constexpr int kAttnAhead = 4;
 constexpr uint32_t kPBytes = 2 * kHalf;   // one P tile (128 x 128 bf16)
-constexpr uint32_t kAttnSmem = kQBytes + kKVStages * kKVBytes + 2 * kPBytes + 1024 + 1024;
+constexpr uint32_t kAttnSmem = kQBytes + kKVStages * kKVBytes + kPBytes + 3072 + 1024;
 
 struct AttnBars {
-  uint64_t qfull, qempty, kvfull[kKVStages], kvempty[kKVStages], sfull[2], sfree[2], pfull, pvdone[2], ofree;
+  uint64_t qfull, qempty, kfull[kKVStages], kempty[kKVStages], vfull[kKVStages], vempty[kKVStages];
+  uint64_t sfull[2], sfree[2], pfull, pvdone[2], ofree;
   uint64_t wrdy[kAttnAhead], wfre[kAttnAhead];
   uint32_t tmem_slot;
   uint8_t waited[kAttnAhead];
+  float xmax[2][128];  // per column half: partial row max of the current block
+  float xsum[2][128];  // per column half: partial row sum at the end of an item
 };
 
 __device__ __noinline__ void attn_spin(const uint32_t* p, uint32_t target, const AttnArgs& A, int rank, int cta, int w) {
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + kQBytes;
   uint8_t* sP = sKV + kKVStages * kKVBytes;
-  AttnBars& B = *reinterpret_cast<AttnBars*>(sP + 2 * kPBytes);  // sP: two P buffers
+  AttnBars& B = *reinterpret_cast<AttnBars*>(sP + kPBytes);  // one P buffer (smem: 8 softmax warps' xmax)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = args.W, S = args.S_loc, nqb = S / kBlk, nkb = S / kBlk;
   const int n_items = args.H * nqb, nkv = W * nkb;
@@ -92,17 +96,19 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
       mbar_init(&B.qfull, 1);
       mbar_init(&B.qempty, 1);
       for (int s = 0; s < kKVStages; ++s) {
-        mbar_init(&B.kvfull[s], 1);
-        mbar_init(&B.kvempty[s], 1);
+        mbar_init(&B.kfull[s], 1);
+        mbar_init(&B.kempty[s], 1);
+        mbar_init(&B.vfull[s], 1);
+        mbar_init(&B.vempty[s], 1);
       }
       for (int s = 0; s < 2; ++s) {
         mbar_init(&B.sfull[s], 1);
-        mbar_init(&B.sfree[s], 4);
+        mbar_init(&B.sfree[s], kSmWarps);
       }
-      mbar_init(&B.pfull, 4);
+      mbar_init(&B.pfull, kSmWarps);
       mbar_init(&B.pvdone[0], 1);
       mbar_init(&B.pvdone[1], 1);
-      mbar_init(&B.ofree, 4);
+      mbar_init(&B.ofree, kSmWarps);
       for (int s = 0; s < kAttnAhead; ++s) {
         mbar_init(&B.wrdy[s], 1);
         mbar_init(&B.wfre[s], 1);
@@ -140,17 +146,21 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
           mbar_arrive(&B.wfre[slot]);
           ++q;
           if (waited) fence_proxy_async_global();  // generic-proxy acquire -> TMA reads
-          const uint32_t st = n % kKVStages;
-          mbar_wait(&B.kvempty[st], ((n / kKVStages) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&B.kvfull[st], kKVBytes);
+          // K and V of a block in separate rings: K is released as soon as S = Q K^T is
+          // done, so the next K loads while the softmax and P V of this block run
+          const uint32_t st = n % kKVStages, ph = ((n / kKVStages) & 1u) ^ 1u;
           uint8_t* dst = sKV + st * kKVBytes;
           const CUtensorMap* mk = d == 0 ? &R.tmK_loc : &R.tmK;
           const CUtensorMap* mv = d == 0 ? &R.tmV_loc : &R.tmV;
           const int row = d == 0 ? krow : src * args.H * S + krow;
-          tma_load_2d(dst, mk, &B.kvfull[st], 0, row, pol);
-          tma_load_2d(dst + kHalf, mk, &B.kvfull[st], 64, row, pol);
-          tma_load_2d(dst + 2 * kHalf, mv, &B.kvfull[st], 0, row, pol);
-          tma_load_2d(dst + 3 * kHalf, mv, &B.kvfull[st], 64, row, pol);
+          mbar_wait(&B.kempty[st], ph);
+          mbar_arrive_expect_tx(&B.kfull[st], kKVBytes / 2);
+          tma_load_2d(dst, mk, &B.kfull[st], 0, row, pol);
+          tma_load_2d(dst + kHalf, mk, &B.kfull[st], 64, row, pol);
+          mbar_wait(&B.vempty[st], ph);
+          mbar_arrive_expect_tx(&B.vfull[st], kKVBytes / 2);
+          tma_load_2d(dst + 2 * kHalf, mv, &B.vfull[st], 0, row, pol);
+          tma_load_2d(dst + 3 * kHalf, mv, &B.vfull[st], 64, row, pol);
         }
         ++t;
       });
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
     uint32_t t = 0, n = 0;
     auto issue_s = [&](uint32_t nn) {
       const uint32_t st = nn % kKVStages, sb = nn & 1u;
-      mbar_wait(&B.kvfull[st], (nn / kKVStages) & 1u);
+      mbar_wait(&B.kfull[st], (nn / kKVStages) & 1u);
       mbar_wait(&B.sfree[sb], ((nn >> 1) & 1u) ^ 1u);
       tc_fence_after();
       if (lane == 0) {
@@ -176,6 +186,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
           mma_bf16_ss(tS[sb], a, b, idesc_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(&B.sfull[sb]);
+        mma_commit(&B.kempty[st]);  // K block consumed
       }
       __syncwarp();
     };
@@ -194,6 +205,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         __syncwarp();
         if (j == 0) mbar_wait(&B.ofree, (t & 1u) ^ 1u);  // the previous item's O was read
         mbar_wait(&B.pfull, (n + j) & 1u);
+        mbar_wait(&B.vfull[(n + j) % kKVStages], ((n + j) / kKVStages) & 1u);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t st = (n + j) % kKVStages;
@@ -201,11 +213,11 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t a =
-                make_smem_desc_sw128(smem_u32(sP + ((n + j) & 1u) * kPBytes + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
+                make_smem_desc_sw128(smem_u32(sP + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
             const uint64_t b = make_smem_desc_sw128_mn(smem_u32(vb + kk * 16 * 128), kHalf);
             mma_bf16_ss(tO, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&B.kvempty[st]);
+          mma_commit(&B.vempty[st]);
           mma_commit(&B.pvdone[(n + j) & 1u]);  // P buffer (n+j)&1 free, O updated
         }
         __syncwarp();
@@ -213,11 +225,15 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
       n += nkv;
       ++t;
     });
-  } else if (warp < 6) {
+  } else if (warp < 2 + kSmWarps) {
     // ===================================================================== softmax
+    // warps 2..9: two per TMEM lane quadrant (row r), column half hf (64 of the 128 S / P /
+    // O columns); the pair combines its partial row maxima through smem every block.
     const int qd = warp & 3;  // TMEM lane quadrant
+    const int hf = (warp - 2) >> 2;
     const int r = qd * 32 + lane;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t pair_bar = 1 + qd;  // named barrier of the two warps of quadrant qd
     const float sl2 = args.scale_log2;
     uint32_t n = 0;
     uint32_t cons[2] = {0, 0};  // phases of pvdone[b] consumed (PV of blocks b, b+2, ... done)
@@ -238,11 +254,11 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         const uint32_t nn = n + j, sb = nn & 1u;
         mbar_wait(&B.sfull[sb], (nn >> 1) & 1u);
         tc_fence_after();
-        float s[128];
+        float s[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_off + sb * 128 + c * 32, v);
+          tmem_ld_32x32b_x32(tmem + lane_off + sb * 128 + hf * 64 + c * 32, v);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
@@ -250,14 +266,17 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&B.sfree[sb]);
-        // row max and sum with 8 independent partials (a single serial chain of 128
-        // dependent fmax / fadd is latency-bound: ~4 cycles each, one warp per SMSP)
+        // row max over the pair's two halves (8 independent partials per half)
         float mp[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mp[u] = s[u];
 #pragma unroll
-        for (int i = 8; i < 128; ++i) mp[i & 7] = fmaxf(mp[i & 7], s[i]);
-        const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+        for (int i = 8; i < 64; ++i) mp[i & 7] = fmaxf(mp[i & 7], s[i]);
+        const float mh = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+        B.xmax[hf][r] = mh;
+        named_bar_sync(pair_bar, 64);
+        const float mx = fmaxf(mh, B.xmax[hf ^ 1][r]);
+        named_bar_sync(pair_bar, 64);  // both read before the next block overwrites
         // lazy rescale: the exponent base m moves only when the row max exceeds it by more
         // than 8 (p <= 2^8 stays exact enough in fp32 / bf16); otherwise alpha = 1 and the
         // O row in TMEM is left alone (the final O / l is consistent for any base)
@@ -267,35 +286,35 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         const float alpha = grow ? exp2f(m - m_new) : 1.f;
         float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
+        for (int i = 0; i < 64; ++i) {
           s[i] = exp2f(fmaf(s[i], sl2, -m_new));
           sp[i & 7] += s[i];
         }
         const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
         l = l * alpha + sum;
         m = m_new;
-        // P buffer nn&1 was last read by the PV of block nn-2 (double-buffered P: the PV of
-        // block nn-1 may still be running while this P is written)
-        if (nn >= 2) pv_wait(nn - 2);
-        uint8_t* pb = sP + (nn & 1u) * kPBytes;
-        // P row r (bf16) into the K-major SW128 A-operand layout: two 64-column blocks
+        // the P buffer was last read by the PV of block nn-1 (a second P buffer measured no
+        // faster and the 8 softmax warps' exchange space needs the shared memory)
+        if (nn >= 1) pv_wait(nn - 1);
+        uint8_t* pb = sP;
+        // this half of P row r (bf16) = K-major SW128 block hf of the A operand
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < 8; ++c) {
           const uint4 w = make_uint4(pack_bf16x2(s[8 * c], s[8 * c + 1]), pack_bf16x2(s[8 * c + 2], s[8 * c + 3]),
                                      pack_bf16x2(s[8 * c + 4], s[8 * c + 5]), pack_bf16x2(s[8 * c + 6], s[8 * c + 7]));
-          *reinterpret_cast<uint4*>(pb + (c >> 3) * kHalf + r * 128 + (((c & 7) ^ (r & 7)) * 16)) = w;
+          *reinterpret_cast<uint4*>(pb + hf * kHalf + r * 128 + ((c ^ (r & 7)) * 16)) = w;
         }
         const bool rescale = j > 0 && __any_sync(0xffffffffu, alpha < 1.f);
         if (rescale) pv_wait(nn - 1);  // O holds every PV up to block nn-1
-        if (rescale) {  // rescale the O row by alpha
+        if (rescale) {  // rescale this half of the O row by alpha
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             uint32_t v[32];
-            tmem_ld_32x32b_x32(tmem + lane_off + 256 + c * 32, v);
+            tmem_ld_32x32b_x32(tmem + lane_off + 256 + hf * 64 + c * 32, v);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            tmem_st_32x32b_x32(tmem + lane_off + 256 + c * 32, v);
+            tmem_st_32x32b_x32(tmem + lane_off + 256 + hf * 64 + c * 32, v);
           }
           tmem_wait_st();
         }
@@ -304,14 +323,17 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         __syncwarp();
         if (lane == 0) mbar_arrive(&B.pfull);
       }
-      // final O row / l -> bf16 -> global
+      // final O half row / l -> bf16 -> global (l = the two halves' partial sums)
       pv_wait(n + nkv - 1);
-      const float inv = 1.f / l;
-      char* orow = R.O + (int64_t(h) * S + qb * kBlk + r) * 256;
+      B.xsum[hf][r] = l;
+      named_bar_sync(pair_bar, 64);
+      const float inv = 1.f / (l + B.xsum[hf ^ 1][r]);
+      named_bar_sync(pair_bar, 64);
+      char* orow = R.O + (int64_t(h) * S + qb * kBlk + r) * 256 + hf * 128;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem + lane_off + 256 + c * 32, v);
+        tmem_ld_32x32b_x32(tmem + lane_off + 256 + hf * 64 + c * 32, v);
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -327,7 +349,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
       if (lane == 0) mbar_arrive(&B.ofree);
       n += nkv;
     });
-  } else if (warp == 6) {
+  } else if (warp == 2 + kSmWarps) {
     // ===================================================================== wait warp
     if (lane == 0) {
       uint64_t got[AO_MAX_WORLD] = {};

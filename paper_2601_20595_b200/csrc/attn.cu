@@ -31,19 +31,25 @@ constexpr int kBlk = 128;                  // query rows per item = KV rows per 
 constexpr uint32_t kHalf = 16384;          // one 128-row x 64-column bf16 box
 constexpr uint32_t kQBytes = 2 * kHalf;    // Q tile (d = 128: two boxes)
 constexpr uint32_t kKVBytes = 4 * kHalf;   // K block + V block
-constexpr int kKVStages = 2;
+#ifndef AO_ATTN_KST
+#define AO_ATTN_KST 2
+#endif
+#ifndef AO_ATTN_VST
+#define AO_ATTN_VST 3
+#endif
+constexpr int kKStages = AO_ATTN_KST;  // K ring (32 KB stages)
+constexpr int kVStages = AO_ATTN_VST;  // V ring (32 KB stages)
 constexpr int kAttnAhead = 4;
 constexpr uint32_t kPBytes = 2 * kHalf;   // one P tile (128 x 128 bf16)
-constexpr uint32_t kAttnSmem = kQBytes + kKVStages * kKVBytes + kPBytes + 3072 + 1024;
+constexpr uint32_t kAttnSmem = kQBytes + (kKStages + kVStages) * (kKVBytes / 2) + kPBytes + 2048 + 1024;
 
 struct AttnBars {
-  uint64_t qfull, qempty, kfull[kKVStages], kempty[kKVStages], vfull[kKVStages], vempty[kKVStages];
+  uint64_t qfull, qempty, kfull[kKStages], kempty[kKStages], vfull[kVStages], vempty[kVStages];
   uint64_t sfull[2], sfree[2], pfull, pvdone[2], ofree;
   uint64_t wrdy[kAttnAhead], wfre[kAttnAhead];
   uint32_t tmem_slot;
   uint8_t waited[kAttnAhead];
-  float xmax[2][128];  // per column half: partial row max of the current block
-  float xsum[2][128];  // per column half: partial row sum at the end of an item
+  float xmax[2][128];  // per column half: partial row max of a block (row sums at an item's end)
 };
 
 __device__ __noinline__ void attn_spin(const uint32_t* p, uint32_t target, const AttnArgs& A, int rank, int cta, int w) {
@@ -84,8 +90,9 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sKV = sQ + kQBytes;
-  uint8_t* sP = sKV + kKVStages * kKVBytes;
+  uint8_t* sK = sQ + kQBytes;
+  uint8_t* sV = sK + kKStages * (kKVBytes / 2);
+  uint8_t* sP = sV + kVStages * (kKVBytes / 2);
   AttnBars& B = *reinterpret_cast<AttnBars*>(sP + kPBytes);  // one P buffer (smem: 8 softmax warps' xmax)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = args.W, S = args.S_loc, nqb = S / kBlk, nkb = S / kBlk;
@@ -95,9 +102,11 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
     if (lane == 0) {
       mbar_init(&B.qfull, 1);
       mbar_init(&B.qempty, 1);
-      for (int s = 0; s < kKVStages; ++s) {
+      for (int s = 0; s < kKStages; ++s) {
         mbar_init(&B.kfull[s], 1);
         mbar_init(&B.kempty[s], 1);
+      }
+      for (int s = 0; s < kVStages; ++s) {
         mbar_init(&B.vfull[s], 1);
         mbar_init(&B.vempty[s], 1);
       }
@@ -148,19 +157,21 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
           if (waited) fence_proxy_async_global();  // generic-proxy acquire -> TMA reads
           // K and V of a block in separate rings: K is released as soon as S = Q K^T is
           // done, so the next K loads while the softmax and P V of this block run
-          const uint32_t st = n % kKVStages, ph = ((n / kKVStages) & 1u) ^ 1u;
-          uint8_t* dst = sKV + st * kKVBytes;
+          const uint32_t kst = n % kKStages, kph = ((n / kKStages) & 1u) ^ 1u;
+          const uint32_t vst = n % kVStages, vph = ((n / kVStages) & 1u) ^ 1u;
+          uint8_t* kdst = sK + kst * (kKVBytes / 2);
+          uint8_t* vdst = sV + vst * (kKVBytes / 2);
           const CUtensorMap* mk = d == 0 ? &R.tmK_loc : &R.tmK;
           const CUtensorMap* mv = d == 0 ? &R.tmV_loc : &R.tmV;
           const int row = d == 0 ? krow : src * args.H * S + krow;
-          mbar_wait(&B.kempty[st], ph);
-          mbar_arrive_expect_tx(&B.kfull[st], kKVBytes / 2);
-          tma_load_2d(dst, mk, &B.kfull[st], 0, row, pol);
-          tma_load_2d(dst + kHalf, mk, &B.kfull[st], 64, row, pol);
-          mbar_wait(&B.vempty[st], ph);
-          mbar_arrive_expect_tx(&B.vfull[st], kKVBytes / 2);
-          tma_load_2d(dst + 2 * kHalf, mv, &B.vfull[st], 0, row, pol);
-          tma_load_2d(dst + 3 * kHalf, mv, &B.vfull[st], 64, row, pol);
+          mbar_wait(&B.kempty[kst], kph);
+          mbar_arrive_expect_tx(&B.kfull[kst], kKVBytes / 2);
+          tma_load_2d(kdst, mk, &B.kfull[kst], 0, row, pol);
+          tma_load_2d(kdst + kHalf, mk, &B.kfull[kst], 64, row, pol);
+          mbar_wait(&B.vempty[vst], vph);
+          mbar_arrive_expect_tx(&B.vfull[vst], kKVBytes / 2);
+          tma_load_2d(vdst, mv, &B.vfull[vst], 0, row, pol);
+          tma_load_2d(vdst + kHalf, mv, &B.vfull[vst], 64, row, pol);
         }
         ++t;
       });
@@ -173,12 +184,12 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
     const uint32_t tO = tmem + 256;
     uint32_t t = 0, n = 0;
     auto issue_s = [&](uint32_t nn) {
-      const uint32_t st = nn % kKVStages, sb = nn & 1u;
-      mbar_wait(&B.kfull[st], (nn / kKVStages) & 1u);
+      const uint32_t st = nn % kKStages, sb = nn & 1u;
+      mbar_wait(&B.kfull[st], (nn / kKStages) & 1u);
       mbar_wait(&B.sfree[sb], ((nn >> 1) & 1u) ^ 1u);
       tc_fence_after();
       if (lane == 0) {
-        const uint8_t* kb = sKV + st * kKVBytes;
+        const uint8_t* kb = sK + st * (kKVBytes / 2);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t a = make_smem_desc_sw128(smem_u32(sQ + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
@@ -205,11 +216,11 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         __syncwarp();
         if (j == 0) mbar_wait(&B.ofree, (t & 1u) ^ 1u);  // the previous item's O was read
         mbar_wait(&B.pfull, (n + j) & 1u);
-        mbar_wait(&B.vfull[(n + j) % kKVStages], ((n + j) / kKVStages) & 1u);
+        mbar_wait(&B.vfull[(n + j) % kVStages], ((n + j) / kVStages) & 1u);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t st = (n + j) % kKVStages;
-          const uint8_t* vb = sKV + st * kKVBytes + 2 * kHalf;
+          const uint32_t st = (n + j) % kVStages;
+          const uint8_t* vb = sV + st * (kKVBytes / 2);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t a =
@@ -325,9 +336,9 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
       }
       // final O half row / l -> bf16 -> global (l = the two halves' partial sums)
       pv_wait(n + nkv - 1);
-      B.xsum[hf][r] = l;
+      B.xmax[hf][r] = l;  // (the exchange slots carry the row sums here)
       named_bar_sync(pair_bar, 64);
-      const float inv = 1.f / (l + B.xsum[hf ^ 1][r]);
+      const float inv = 1.f / (l + B.xmax[hf ^ 1][r]);
       named_bar_sync(pair_bar, 64);
       char* orow = R.O + (int64_t(h) * S + qb * kBlk + r) * 256 + hf * 128;
 #pragma unroll 1

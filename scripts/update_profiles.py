@@ -83,6 +83,10 @@ if os.path.exists(rep):  # A2A-GEMM (NEXT-3) kernel, one launch
     tr = json.load(open(tp_)) if os.path.exists(tp_) else {}
     tr["a2a_gemm"] = int(tot)
     json.dump(tr, open(tp_, "w"), indent=1)
+rep = os.path.join(G, "prof_%s_attn.ncu-rep" % tag)
+if os.path.exists(rep):  # SP attention (NEXT-4) kernel, one launch
+    open(os.path.join(P, "%s_ncu_attn_summary.txt" % tag), "w").write(run([sys.executable, "scripts/ncu_summary.py", rep]))
+    open(os.path.join(P, "%s_ncu_attn_lines.txt" % tag), "w").write(run([sys.executable, "scripts/ncu_lines.py", rep, "0", "30"]))
 tp = os.path.join(G, "trace_%s.json" % tag)
 if os.path.exists(tp):
     open(os.path.join(P, "%s_trace_summary.txt" % tag), "w").write(run([sys.executable, "scripts/trace_summary.py", tp]))

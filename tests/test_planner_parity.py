@@ -148,3 +148,18 @@ def test_a2a_host_plan(ao):
     hashes = {ao.Plan(None, dict(base, rank=r)).hash() for r in range(8)}
     assert len(hashes) == 1
     assert ao.workspace_bytes(dict(base, rank=0)) == 2 * 8 * 1024 * 4096 * 2
+
+
+def test_sp_attn_host_plan(ao):
+    """SP attention (NEXT-4) host plan: validation, canonical JSON, rank-independent hash,
+    workspace = 2 parities x (gathered K + gathered V)."""
+    base = dict(op="sp_attn", world_size=8, M=4096, N=32, K=128, chunk_rows=4096, backend="ce", n_cta=148)
+    assert ao.validate(dict(base, rank=0)) == []
+    for bad, why in ((dict(K=64), "head dim"), (dict(M=100), "S_loc"), (dict(chunk_rows=192), "chunk_rows"),
+                     (dict(backend="tma"), "backend"), (dict(dir="pull"), "dir"), (dict(N=0), "heads")):
+        v = ao.validate(dict(base, rank=0, **bad))
+        assert any(why in x for x in v), (bad, v)
+    j = json.loads(ao.plan_json(dict(base, rank=2)))
+    assert j["op"] == "sp_attn" and j["chunks_per_source"] == 32 * 4096 // 4096 and j["items"] == 32 * 32
+    assert len({ao.Plan(None, dict(base, rank=r)).hash() for r in range(8)}) == 1
+    assert ao.workspace_bytes(dict(base, rank=0)) == 2 * 2 * 8 * 32 * 4096 * 128 * 2

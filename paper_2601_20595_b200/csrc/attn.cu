@@ -32,7 +32,7 @@ constexpr uint32_t kHalf = 16384;          // one 128-row x 64-column bf16 box
 constexpr uint32_t kQBytes = 2 * kHalf;    // Q tile (d = 128: two boxes)
 constexpr uint32_t kKVBytes = 4 * kHalf;   // K block + V block
 #ifndef AO_ATTN_KST
-#define AO_ATTN_KST 2
+#define AO_ATTN_KST 3
 #endif
 #ifndef AO_ATTN_VST
 #define AO_ATTN_VST 3
@@ -40,8 +40,7 @@ constexpr uint32_t kKVBytes = 4 * kHalf;   // K block + V block
 constexpr int kKStages = AO_ATTN_KST;  // K ring (32 KB stages)
 constexpr int kVStages = AO_ATTN_VST;  // V ring (32 KB stages)
 constexpr int kAttnAhead = 4;
-constexpr uint32_t kPBytes = 2 * kHalf;   // one P tile (128 x 128 bf16)
-constexpr uint32_t kAttnSmem = kQBytes + (kKStages + kVStages) * (kKVBytes / 2) + kPBytes + 2048 + 1024;
+constexpr uint32_t kAttnSmem = kQBytes + (kKStages + kVStages) * (kKVBytes / 2) + 2048 + 1024;  // P lives in TMEM
 
 struct AttnBars {
   uint64_t qfull, qempty, kfull[kKStages], kempty[kKStages], vfull[kVStages], vempty[kVStages];
@@ -92,8 +91,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + kQBytes;
   uint8_t* sV = sK + kKStages * (kKVBytes / 2);
-  uint8_t* sP = sV + kVStages * (kKVBytes / 2);
-  AttnBars& B = *reinterpret_cast<AttnBars*>(sP + kPBytes);  // one P buffer (smem: 8 softmax warps' xmax)
+  AttnBars& B = *reinterpret_cast<AttnBars*>(sV + kVStages * (kKVBytes / 2));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = args.W, S = args.S_loc, nqb = S / kBlk, nkb = S / kBlk;
   const int n_items = args.H * nqb, nkv = W * nkb;
@@ -187,6 +185,8 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
       const uint32_t st = nn % kKStages, sb = nn & 1u;
       mbar_wait(&B.kfull[st], (nn / kKStages) & 1u);
       mbar_wait(&B.sfree[sb], ((nn >> 1) & 1u) ^ 1u);
+      // P of block nn-2 lives in this S buffer's columns: its P.V must have read it
+      if (nn >= 2) mbar_wait(&B.pvdone[sb], ((nn >> 1) - 1) & 1u);
       tc_fence_after();
       if (lane == 0) {
         const uint8_t* kb = sK + st * (kKVBytes / 2);
@@ -221,12 +221,11 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         if (lane == 0) {
           const uint32_t st = (n + j) % kVStages;
           const uint8_t* vb = sV + st * (kKVBytes / 2);
+          const uint32_t tP = tS[(n + j) & 1u];  // P (bf16 pairs) over the S columns
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t a =
-                make_smem_desc_sw128(smem_u32(sP + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
             const uint64_t b = make_smem_desc_sw128_mn(smem_u32(vb + kk * 16 * 128), kHalf);
-            mma_bf16_ss(tO, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16_ts(tO, tP + kk * 8, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&B.vempty[st]);
           mma_commit(&B.pvdone[(n + j) & 1u]);  // P buffer (n+j)&1 free, O updated
@@ -264,6 +263,10 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
       for (int j = 0; j < nkv; ++j) {
         const uint32_t nn = n + j, sb = nn & 1u;
         mbar_wait(&B.sfull[sb], (nn >> 1) & 1u);
+        // S of block nn exists, so the P.V of block nn-2 has completed (the MMA waited for it
+        // before writing this buffer): consume that phase, keeping the per-buffer phase count
+        // at most one behind (mbarrier parity waits must never fall two phases behind)
+        if (nn >= 2) pv_wait(nn - 2);
         tc_fence_after();
         float s[64];
 #pragma unroll
@@ -304,16 +307,14 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
         l = l * alpha + sum;
         m = m_new;
-        // the P buffer was last read by the PV of block nn-1 (a second P buffer measured no
-        // faster and the 8 softmax warps' exchange space needs the shared memory)
-        if (nn >= 1) pv_wait(nn - 1);
-        uint8_t* pb = sP;
-        // this half of P row r (bf16) = K-major SW128 block hf of the A operand
+        // this half of P row r as bf16 pairs into TMEM over the S columns just read (the
+        // A operand of P.V, 32 packed columns per half); the MMA issued the next S into this
+        // buffer only after the previous P.V read it
+        {
+          uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 w = make_uint4(pack_bf16x2(s[8 * c], s[8 * c + 1]), pack_bf16x2(s[8 * c + 2], s[8 * c + 3]),
-                                     pack_bf16x2(s[8 * c + 4], s[8 * c + 5]), pack_bf16x2(s[8 * c + 6], s[8 * c + 7]));
-          *reinterpret_cast<uint4*>(pb + hf * kHalf + r * 128 + ((c ^ (r & 7)) * 16)) = w;
+          for (int c = 0; c < 32; ++c) pk[c] = pack_bf16x2(s[2 * c], s[2 * c + 1]);
+          tmem_st_32x32b_x32(tmem + lane_off + sb * 128 + hf * 32, pk);
         }
         const bool rescale = j > 0 && __any_sync(0xffffffffu, alpha < 1.f);
         if (rescale) pv_wait(nn - 1);  // O holds every PV up to block nn-1
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
           }
           tmem_wait_st();
         }
-        fence_proxy_async_smem();  // P (generic smem writes) -> the MMA's async-proxy reads
+        tmem_wait_st();  // P (and a rescaled O) in TMEM before the MMA reads them
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&B.pfull);

@@ -19,6 +19,8 @@
 // TMEM: S0 [0,128), S1 [128,256), O [256,384) fp32 columns.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernel_args.h"
 #include "ptx.cuh"
 
@@ -399,27 +401,322 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
   }
 }
 
+
+// ---- ping-pong variant: two query tiles per item (S_loc % 256 == 0) ------------------------
+// Item = (head, 256 queries) = tiles x = 0, 1 sharing every K/V block.  Each tile has its own
+// softmax warpgroup (warps 2-5 and 6-9), S buffer and O accumulator in TMEM, so the tensor
+// core works on one tile's QK^T / PV while the other tile's softmax runs (the FA4 schedule).
+// 10 warps (the producer acquires the chunk flags itself) and at most 168 registers per
+// thread, so that 320 x 168 registers leave room on every SM for the copy kernels that
+// execute same-device memcpy nodes (the loopback "copy engine" pushes): with 352 x 168 they
+// could not be scheduled while this persistent kernel ran and the chunk waits timed out.
+constexpr int kPPThreads = 320;
+constexpr int kPPK = 2, kPPV = 2;  // K and V ring stages (32 KB each)
+constexpr uint32_t kPPSmem = 2 * kQBytes + (kPPK + kPPV) * (kKVBytes / 2) + 2048 + 1024;
+
+struct PPBars {
+  uint64_t qfull, qempty, kfull[kPPK], kempty[kPPK], vfull[kPPV], vempty[kPPV];
+  uint64_t sfull[2], pfull[2], pvdone[2], ofree[2];  // per tile
+  uint64_t wrdy[kAttnAhead], wfre[kAttnAhead];
+  uint32_t tmem_slot;
+  uint8_t waited[kAttnAhead];
+};
+
+// (bound 512 threads: caps the registers at 128 per thread; launched with 320)
+__global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__ AttnArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;  // tile 0 at +0, tile 1 at +kQBytes
+  uint8_t* sK = sQ + 2 * kQBytes;
+  uint8_t* sV = sK + kPPK * (kKVBytes / 2);
+  PPBars& B = *reinterpret_cast<PPBars*>(sV + kPPV * (kKVBytes / 2));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = args.W, S = args.S_loc, nqp = S / (2 * kBlk), nkb = S / kBlk;
+  const int n_items = args.H * nqp, nkv = W * nkb;
+
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(&B.qfull, 1);
+      mbar_init(&B.qempty, 1);
+      for (int s = 0; s < kPPK; ++s) {
+        mbar_init(&B.kfull[s], 1);
+        mbar_init(&B.kempty[s], 1);
+      }
+      for (int s = 0; s < kPPV; ++s) {
+        mbar_init(&B.vfull[s], 1);
+        mbar_init(&B.vempty[s], 1);
+      }
+      for (int x = 0; x < 2; ++x) {
+        mbar_init(&B.sfull[x], 1);
+        mbar_init(&B.pfull[x], 4);
+        mbar_init(&B.pvdone[x], 1);
+        mbar_init(&B.ofree[x], 4);
+      }
+      for (int s = 0; s < kAttnAhead; ++s) {
+        mbar_init(&B.wrdy[s], 1);
+        mbar_init(&B.wfre[s], 1);
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(&B.tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_slot;  // S_x at x*128, O_x at 256 + x*128
+
+  if (warp == 0) {
+    // ===================================================================== TMA producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_normal();
+      uint32_t t = 0, n = 0;
+      uint64_t got[AO_MAX_WORLD] = {};  // acquired chunk flags per rank group (w < 64)
+      attn_walk(args, n_items, [&](int g, int item) {
+        const AttnRank& R = args.rk[g];
+        const int h = item / nqp, qp = item % nqp;
+        mbar_wait(&B.qempty, (t & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&B.qfull, 2 * kQBytes);
+        const int qrow = h * S + qp * 2 * kBlk;
+        tma_load_2d(sQ, &R.tmQ, &B.qfull, 0, qrow, pol);
+        tma_load_2d(sQ + kHalf, &R.tmQ, &B.qfull, 64, qrow, pol);
+        tma_load_2d(sQ + kQBytes, &R.tmQ, &B.qfull, 0, qrow + kBlk, pol);
+        tma_load_2d(sQ + kQBytes + kHalf, &R.tmQ, &B.qfull, 64, qrow + kBlk, pol);
+        for (int j = 0; j < nkv; ++j, ++n) {
+          const int d = j / nkb, kb = j % nkb;
+          const int src = (R.rank - d + W) % W;
+          const int krow = h * S + kb * kBlk;
+          if (d > 0) {  // the chunk (src, h*S + kb*128) must have landed
+            const int w = src * args.nch + krow / args.crows;
+            if (!(w < 64 && ((got[g] >> w) & 1u))) {
+              attn_spin(R.flags + w, R.epoch, args, R.rank, int(blockIdx.x), w);
+              if (w < 64) got[g] |= 1ull << w;
+              fence_proxy_async_global();  // generic-proxy acquire -> TMA reads
+            }
+          }
+          const uint32_t kst = n % kPPK, vst = n % kPPV;
+          const CUtensorMap* mk = d == 0 ? &R.tmK_loc : &R.tmK;
+          const CUtensorMap* mv = d == 0 ? &R.tmV_loc : &R.tmV;
+          const int row = d == 0 ? krow : src * args.H * S + krow;
+          uint8_t* kdst = sK + kst * (kKVBytes / 2);
+          uint8_t* vdst = sV + vst * (kKVBytes / 2);
+          mbar_wait(&B.kempty[kst], ((n / kPPK) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&B.kfull[kst], kKVBytes / 2);
+          tma_load_2d(kdst, mk, &B.kfull[kst], 0, row, pol);
+          tma_load_2d(kdst + kHalf, mk, &B.kfull[kst], 64, row, pol);
+          mbar_wait(&B.vempty[vst], ((n / kPPV) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&B.vfull[vst], kKVBytes / 2);
+          tma_load_2d(vdst, mv, &B.vfull[vst], 0, row, pol);
+          tma_load_2d(vdst + kHalf, mv, &B.vfull[vst], 64, row, pol);
+        }
+        ++t;
+      });
+    }
+  } else if (warp == 1) {
+    // ===================================================================== MMA issuer
+    constexpr uint32_t idesc_s = make_idesc_bf16(kBlk, kBlk);
+    constexpr uint32_t idesc_o = make_idesc_bf16_bmn(kBlk, 128);
+    uint32_t t = 0, n = 0;
+    auto issue_s = [&](int x, uint32_t nn) {  // S_x = Q_x . K(nn)^T
+      const uint32_t st = nn % kPPK;
+      mbar_wait(&B.kfull[st], (nn / kPPK) & 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint8_t* kb = sK + st * (kKVBytes / 2);
+        const uint8_t* qa = sQ + x * kQBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t a = make_smem_desc_sw128(smem_u32(qa + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
+          const uint64_t b = make_smem_desc_sw128(smem_u32(kb + (kk >> 2) * kHalf)) + uint64_t((kk & 3) * 2);
+          mma_bf16_ss(tmem + x * 128, a, b, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&B.sfull[x]);
+        if (x == 1) mma_commit(&B.kempty[st]);  // both tiles have read K(nn)
+      }
+      __syncwarp();
+    };
+    attn_walk(args, n_items, [&](int g, int item) {
+      (void)g;
+      (void)item;
+      mbar_wait(&B.qfull, t & 1u);
+      for (int x = 0; x < 2; ++x) {
+        if (n > 0) mbar_wait(&B.pvdone[x], (n - 1) & 1u);  // P_x of the previous item was read
+        issue_s(x, n);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const uint32_t nn = n + j;
+        if (j + 1 == nkv && lane == 0) mma_commit(&B.qempty);  // every S of this item issued
+        __syncwarp();
+        for (int x = 0; x < 2; ++x) {
+          if (j == 0) mbar_wait(&B.ofree[x], (t & 1u) ^ 1u);  // O_x of the previous item read
+          mbar_wait(&B.pfull[x], nn & 1u);
+          if (x == 0) mbar_wait(&B.vfull[nn % kPPV], (nn / kPPV) & 1u);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint8_t* vb = sV + (nn % kPPV) * (kKVBytes / 2);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint64_t b = make_smem_desc_sw128_mn(smem_u32(vb + kk * 16 * 128), kHalf);
+              mma_bf16_ts(tmem + 256 + x * 128, tmem + x * 128 + kk * 8, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&B.pvdone[x]);
+            if (x == 1) mma_commit(&B.vempty[nn % kPPV]);
+          }
+          __syncwarp();
+          if (j + 1 < nkv) {
+            mbar_wait(&B.pvdone[x], nn & 1u);  // P_x(nn) read before S_x(nn+1) overwrites it
+            issue_s(x, nn + 1);
+          }
+        }
+      }
+      n += nkv;
+      ++t;
+    });
+  } else if (warp < 10) {
+    // ===================================================================== softmax (tile x)
+    const int x = (warp - 2) >> 2;
+    const int qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t tS = tmem + lane_off + x * 128, tO = tmem + lane_off + 256 + x * 128;
+    const float sl2 = args.scale_log2;
+    uint32_t n = 0, cons = 0;
+    auto pv_wait = [&](uint32_t nb) {
+      while (cons <= nb) {
+        mbar_wait(&B.pvdone[x], cons & 1u);
+        ++cons;
+      }
+      tc_fence_after();
+    };
+    attn_walk(args, n_items, [&](int g, int item) {
+      const AttnRank& R = args.rk[g];
+      const int h = item / nqp, qp = item % nqp;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j) {
+        const uint32_t nn = n + j;
+        mbar_wait(&B.sfull[x], nn & 1u);
+        tc_fence_after();
+        if (nn >= 1) pv_wait(nn - 1);  // S_x(nn) exists, so the PV of block nn-1 is done
+        // two passes over the S row in TMEM (max, then exp) keep 64 values live instead of
+        // 128: the kernel's registers must leave room for the memcpy kernels (see kPPThreads)
+        float mp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mp[u] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tS + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(v[i]));
+        }
+        const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+        const float mxs = mx * sl2;
+        const bool grow = mxs > m + 8.f;  // lazy rescale (see attn_kernel)
+        const float m_new = grow ? mxs : m;
+        const float alpha = grow ? exp2f(m - m_new) : 1.f;
+        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[2][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {  // exp per 32 columns; P row r as bf16 pairs
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tS + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a = exp2f(fmaf(__uint_as_float(v[2 * i]), sl2, -m_new));
+            const float b = exp2f(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -m_new));
+            sp[(2 * i) & 7] += a;
+            sp[(2 * i + 1) & 7] += b;
+            pk[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(a, b);
+          }
+        }
+        l = l * alpha + (((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7])));
+        m = m_new;
+        // P over the first 64 S columns: every S value of the row is already read (above)
+        tmem_st_32x32b_x32(tS, pk[0]);
+        tmem_st_32x32b_x32(tS + 32, pk[1]);
+        if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tO + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(tO + c * 32, v);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.pfull[x]);
+      }
+      pv_wait(n + nkv - 1);
+      const float inv = 1.f / l;
+      char* orow = R.O + (int64_t(h) * S + qp * 2 * kBlk + x * kBlk + r) * 256;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tO + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 w = make_uint4(pack_bf16x2(__uint_as_float(v[8 * i]) * inv, __uint_as_float(v[8 * i + 1]) * inv),
+                                     pack_bf16x2(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv),
+                                     pack_bf16x2(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv),
+                                     pack_bf16x2(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv));
+          *reinterpret_cast<uint4*>(orow + c * 64 + i * 16) = w;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&B.ofree[x]);
+      n += nkv;
+    });
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace dev
 
 cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  // two-tile ping-pong kernel when S_loc is a multiple of 256 (AO_ATTN_SINGLE=1 forces the
+  // one-tile kernel)
+  static const bool single = getenv("AO_ATTN_SINGLE") && getenv("AO_ATTN_SINGLE")[0] == '1';
+  const bool pp = !single && args.S_loc % (2 * dev::kBlk) == 0;
+  static bool attr = false, attr_pp = false;
+  if (!pp && !attr) {
     cudaError_t e = cudaFuncSetAttribute(dev::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(dev::kAttnSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  if (pp && !attr_pp) {
+    cudaError_t e = cudaFuncSetAttribute(dev::attn_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(dev::kPPSmem));
+    if (e != cudaSuccess) return e;
+    attr_pp = true;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(args.ts ? args.ctas_per_rank : args.n_group * args.ctas_per_rank);
-  cfg.blockDim = dim3(dev::kAThreads);
-  cfg.dynamicSmemBytes = dev::kAttnSmem;
+  cfg.blockDim = dim3(pp ? dev::kPPThreads : dev::kAThreads);
+  cfg.dynamicSmemBytes = pp ? dev::kPPSmem : dev::kAttnSmem;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;  // spin-waiting persistent CTAs must be co-resident
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, dev::attn_kernel, args);
+  // Not a cooperative launch: a cooperative kernel was measured to stall the copy-engine
+  // chunk pushes on other streams until it exits (the spin-waits then time out).  Co-
+  // residency of the spin-waiting CTAs holds by construction instead: grid <= SMs and one
+  // CTA per SM (shared memory), as for the cluster-launched GEMM kernels.
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;
+  return pp ? cudaLaunchKernelEx(&cfg, dev::attn_pp_kernel, args) : cudaLaunchKernelEx(&cfg, dev::attn_kernel, args);
 }
 
 }  // namespace ao

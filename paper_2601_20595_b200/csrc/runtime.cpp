@@ -1257,6 +1257,7 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
     AO_CUDA(cudaGraphLaunch(exec, c0->side));
     AO_CUDA(cudaEventRecord(c0->ev_done, c0->side));
   }
+  if (ce && (g_debug.exp & 65536)) AO_CUDA(cudaStreamWaitEvent(stream, c0->ev_done, 0));  // debug: gather first
   if (rows > 0) {
     cudaError_t e = ao::launch_attn(*ka, stream);
     if (e != cudaSuccess) return fail(AO_ERR_CUDA, "attention kernel launch: %s", cudaGetErrorString(e));

@@ -535,8 +535,13 @@ __device__ __noinline__ void a2a_push_chunk_tma(const A2ASched& sm, const RankAr
   st_release_sys(S_.peer_flags[e] + s * S_.maxJ + j, S_.epoch);
 }
 
+// AG (copy-engine pushes) and plain GEMM are bounded at 168 registers per thread (the 384-
+// thread bound; launched with 256): the loopback pushes are same-device memcpys that run as
+// SM kernels beside this persistent kernel and need registers left on every SM (DESIGN.md
+// §8: a persistent kernel without that headroom stalled them and its chunk waits timed out).
 template <int BN, int MODE, int COMM, int CG>
-__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constant__ KernelArgs args) {
+__global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 : kThreads, 1)
+    fused_kernel(const __grid_constant__ KernelArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int warp = threadIdx.x >> 5;

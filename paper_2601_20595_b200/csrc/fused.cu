@@ -174,11 +174,10 @@ __device__ __forceinline__ void st_v4(int4* p, const int4& v) {
 // Each worker is one warp; worker w handles items w, w + n_workers, ... of this rank's
 // ordered item list (plan order, so early chunks go first on every worker).
 template <int COMM>
-__device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, int n_workers, uint8_t* staging,
-                            uint32_t buf_bytes, uint64_t* bars) {
+__device__ void comm_item(const RankArgs& R, const KernelArgs& A, int i, int worker, uint8_t* staging,
+                          uint32_t buf_bytes, uint64_t* bars, uint32_t& phase_bits) {
   const int lane = lane_id();
-  uint32_t phase_bits = 0;
-  for (int i = worker; i < R.n_comm_items; i += n_workers) {
+  {
     const uint64_t t_item = A.trace ? globaltimer() : 0;
     if (A.delay_ns && lane == 0) inject_delay(A.delay_ns, uint32_t(i));  // fault injection
     __syncwarp();
@@ -258,6 +257,34 @@ __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, 
       trace_event(A, TR_COMM, R.rank, worker, i, t_item);
     }
     __syncwarp();
+  }
+}
+
+template <int COMM>
+__device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, int n_workers, uint8_t* staging,
+                            uint32_t buf_bytes, uint64_t* bars) {
+  uint32_t phase_bits = 0;
+  for (int i = worker; i < R.n_comm_items; i += n_workers)
+    comm_item<COMM>(R, A, i, worker, staging, buf_bytes, bars, phase_bits);
+}
+
+// Time-sliced AG group (in-kernel push backends): the comm warps of every CTA serve every
+// source rank's items, destination-major in the order the ranks' tiles run (each rank's
+// chunks land before its turn), like the copy-engine chains of a time-sliced group.
+template <int COMM>
+__device__ void comm_worker_ts(const KernelArgs& A, int worker, int n_workers, uint8_t* staging, uint32_t buf_bytes,
+                               uint64_t* bars) {
+  uint32_t phase_bits = 0;
+  int cnt = 0;
+  for (int gi = 0; gi < A.n_group; ++gi) {
+    const int e = A.rk[gi].rank;  // destination, in execution order
+    for (int gs = 0; gs < A.n_group; ++gs) {
+      const RankArgs& R = A.rk[gs];
+      for (int i = 0; i < R.n_comm_items; ++i) {
+        if (R.comm_items[i].peer != e) continue;
+        if (cnt++ % n_workers == worker) comm_item<COMM>(R, A, i, worker, staging, buf_bytes, bars, phase_bits);
+      }
+    }
   }
 }
 
@@ -1255,9 +1282,14 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {
       if (args.comm_ctas_per_rank == 0) {
         const int cw = warp - kCommWarp0;
-        comm_worker<COMM>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps,
-                          smem + L.off_comm + cw * kCommBufs * kColocBufBytes, kColocBufBytes,
-                          commbars + cw * kCommBufs);
+        if (ts)
+          comm_worker_ts<COMM>(args, int(blockIdx.x) * kColocCommWarps + cw, int(gridDim.x) * kColocCommWarps,
+                               smem + L.off_comm + cw * kCommBufs * kColocBufBytes, kColocBufBytes,
+                               commbars + cw * kCommBufs);
+        else
+          comm_worker<COMM>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps,
+                            smem + L.off_comm + cw * kCommBufs * kColocBufBytes, kColocBufBytes,
+                            commbars + cw * kCommBufs);
       }
     }
   }

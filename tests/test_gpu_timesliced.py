@@ -63,13 +63,15 @@ def _rs(ao, ctxs, plans, A, B):
     return Cs
 
 
+@pytest.mark.parametrize("backend", ["ce", "tma"])
 @pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
 @pytest.mark.parametrize("W", [2, 4, 8])
-def test_ag_timesliced_vs_oracle(ao, W, tile):
+def test_ag_timesliced_vs_oracle(ao, W, tile, backend):
     M, K, N, C = 256 * W, 512, 520, 64
     A, B = si.ag_inputs(W, M, K, N, salt=41)
-    ctxs, plans = _world(ao, dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=C, backend="ce",
-                                  tile_m=tile[0], tile_n=tile[1], n_cta=SMS, timeout_ns=2_000_000_000), W)
+    ctxs, plans = _world(ao, dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=C, backend=backend,
+                                  n_slices=2, tile_m=tile[0], tile_n=tile[1], n_cta=SMS,
+                                  timeout_ns=2_000_000_000), W)
     Cs, G = _ag(ao, ctxs, plans, _dev(A), _dev(B), gather=True)
     A64 = [si.to_f64(a) for a in A]
     full = torch.cat(A, 0)
@@ -78,13 +80,14 @@ def test_ag_timesliced_vs_oracle(ao, W, tile):
         assert torch.equal(G[r].cpu(), full), "gathered A must be a bit-exact copy"
 
 
+@pytest.mark.parametrize("backend", ["ce", "tma"])
 @pytest.mark.parametrize("W", [4, 8])
-def test_ag_timesliced_provenance_epochs(ao, W):
+def test_ag_timesliced_provenance_epochs(ao, W, backend):
     """Row-id / epoch digits decode exactly across back-to-back epochs (both parities),
     with chunks smaller than a tile (multi-chunk waits) and N spanning several tiles."""
     M, K, N = 256 * W, 64, 768
-    ctxs, plans = _world(ao, dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend="ce",
-                                  tile_m=256, tile_n=256, n_cta=SMS, timeout_ns=2_000_000_000), W)
+    ctxs, plans = _world(ao, dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend=backend,
+                                  n_slices=3, tile_m=256, tile_n=256, n_cta=SMS, timeout_ns=2_000_000_000), W)
     for it in range(5):
         A, B = si.ag_provenance_inputs(W, M, K, N, epoch=it + 1)
         Cs, _ = _ag(ao, ctxs, plans, _dev(A), _dev(B))
@@ -173,13 +176,13 @@ def test_gemm_batched_timesliced(ao, n):
 
 
 def test_timesliced_rejects_unsupported(ao):
-    """Groups that cannot be time-sliced keep the co-residency error: in-kernel comm
-    backends, GEMM-AR, or a partial world."""
+    """Groups that cannot be time-sliced keep the co-residency error: the ld/st comm
+    backend, GEMM-AR, or a partial world."""
     W, M, K, N = 2, 512, 64, 256
     A = [torch.zeros(M // W, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
     B = [torch.zeros(N, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
     C = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
-    d = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend="tma", n_cta=SMS)
+    d = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend="ldst", n_cta=SMS)
     ctxs, plans = _world(ao, d, W)
     with pytest.raises(ao.AOError, match="INVALID_ARG"):
         ao.ag_gemm_group(plans, A, B, C)

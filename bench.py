@@ -164,6 +164,7 @@ def run_ours(args, rank, world, local_rank):
     if loop:
         # time-sliced (default): every rank's plan spans all SMs and the group launch runs the
         # ranks' tile lists in one global order; space-sliced: SMs // W CTAs per rank
+        # GEMM-AR stays space-sliced: time-sliced it measured 4.3 vs 1.2 ms
         ar_desc["n_cta"] = sms // W
         ag_desc["n_cta"] = rs_desc["n_cta"] = sms if args.sched == "time" else sms // W
         if args.sched == "time":

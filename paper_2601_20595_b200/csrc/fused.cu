@@ -1275,8 +1275,12 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     if constexpr (MODE == MODE_RS) {
       if (R.ar && R.n_comm_items > 0) {  // GEMM-AR gather: ld/st pulls of reduced chunks
         const int cw = warp - kCommWarp0;
-        comm_worker<COMM_LDST>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps, nullptr,
-                               0, nullptr);
+        if (ts)  // every rank's pulls, owner after owner (the order the owners' reductions finish)
+          comm_worker_ts<COMM_LDST>(args, int(blockIdx.x) * kColocCommWarps + cw, int(gridDim.x) * kColocCommWarps,
+                                    nullptr, 0, nullptr);
+        else
+          comm_worker<COMM_LDST>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps, nullptr,
+                                 0, nullptr);
       }
     }
     if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {

@@ -764,7 +764,7 @@ static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArg
   const ao::HostPlan& h0 = plans[0]->hp;
   const int64_t BM = int64_t(h0.tile.bm);
   if (mode == ao::MODE_RS) {
-    if (h0.is_ar || h0.S % BM != 0) return false;
+    if (h0.S % BM != 0) return false;
     struct Run { int key0, key1, key2, k0; ao::Seg s; };
     std::vector<Run> runs;
     for (int i = 0; i < n; ++i) {

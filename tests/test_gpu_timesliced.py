@@ -164,6 +164,30 @@ def test_timesliced_and_space_sliced_mix_on_one_world(ao):
                 _check(Cs[r], on.gemm_rs(Ar64, Br64, r), f"{key} r{r}")
 
 
+@pytest.mark.parametrize("reduce", ["slots", "atomic"])
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_gemm_ar_timesliced_vs_oracle(ao, W, reduce):
+    """GEMM-AR (NEXT-1) time-sliced: the RS phase owner after owner, every CTA's gather warps
+    pulling the owners' reduced chunks in the same order; every rank's full C vs fp64."""
+    M, K, N = 256 * W, 256, 520
+    A, B = si.rs_inputs(W, M, K, N, salt=47)
+    ctxs, plans = _world(ao, dict(op="gemm_ar", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend="ldst",
+                                  n_slices=4, rs_reduce=reduce, tile_m=256, tile_n=256, n_cta=SMS,
+                                  timeout_ns=2_000_000_000), W)
+    ref = on.gemm_ar([si.to_f64(a) for a in A], [si.to_f64(b) for b in B])
+    dA, dB = _dev(A), _dev(B)
+    for it in range(2):
+        Cs = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+        ao.gemm_ar_group(plans, dA, dB, Cs)
+        torch.cuda.synchronize()
+        for c in ctxs:
+            c.check_async()
+        for r in range(W):
+            _check(Cs[r], ref, f"ar ts W={W} {reduce} it={it} r{r}")
+        for r in range(1, W):
+            assert torch.equal(Cs[r], Cs[0]), "every rank gathers the same reduced rows"
+
+
 @pytest.mark.parametrize("n", [2, 8])
 def test_gemm_batched_timesliced(ao, n):
     M, N, K = 512, 520, 1000
@@ -177,7 +201,7 @@ def test_gemm_batched_timesliced(ao, n):
 
 def test_timesliced_rejects_unsupported(ao):
     """Groups that cannot be time-sliced keep the co-residency error: the ld/st comm
-    backend, GEMM-AR, or a partial world."""
+    backend or a partial world."""
     W, M, K, N = 2, 512, 64, 256
     A = [torch.zeros(M // W, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
     B = [torch.zeros(N, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
@@ -186,11 +210,12 @@ def test_timesliced_rejects_unsupported(ao):
     ctxs, plans = _world(ao, d, W)
     with pytest.raises(ao.AOError, match="INVALID_ARG"):
         ao.ag_gemm_group(plans, A, B, C)
-    dar = dict(op="gemm_ar", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend="ldst", n_cta=SMS)
-    ctxs2, plans2 = _world(ao, dar, W)
-    Ar = [torch.zeros(M, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    W4 = 4  # two ranks of a 4-rank world in one launch: a partial world cannot be time-sliced
+    dpart = dict(d, world_size=W4, backend="ce")
+    ctxs3, plans3 = _world(ao, dpart, W4)
+    A4 = [torch.zeros(M // W4, K, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
     with pytest.raises(ao.AOError, match="INVALID_ARG"):
-        ao.gemm_ar_group(plans2, Ar, B, C)
+        ao.ag_gemm_group(plans3[:2], A4, B, C)
 
 
 def test_bench_config_timesliced_fullsize(ao):

@@ -115,6 +115,8 @@ typedef struct {
   uint64_t timeout_ns;  /* device spin bound (0 = 5 s) */
   int32_t rs_reduce;    /* ao_rs_reduce (RS only) */
   int32_t topk;         /* A2A: experts per token (k); other ops: 0 */
+  int32_t causal;       /* SP attention: 1 = causal mask over global token positions; other ops: 0 */
+  int32_t reserved;
 } ao_plan_desc;
 
 /* ---- status / version ---------------------------------------------------------------- */
@@ -230,8 +232,10 @@ ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs,
  * consumes its KV blocks in arrival order (own shard first, then r-1, r-2, ...) with an
  * online softmax, so the result does not depend on the order (Q27).  Plan: op
  * AO_OP_SP_ATTN, M = S_loc (multiple of 128), N = H, K = 128, chunk_rows a multiple of 128
- * dividing H*S_loc, backend AO_BACKEND_CE, dir PUSH, comm_ctas 0.  Collective rules and
- * errors as ao_ag_gemm. */
+ * dividing H*S_loc, backend AO_BACKEND_CE, dir PUSH, comm_ctas 0.  causal = 1: query
+ * i of rank r (global position r*S_loc + i) sees keys at positions <= its own (RingAttention
+ * with the causal mask: ranks s > r are skipped, rank r's own shard is masked on the
+ * diagonal blocks); requires S_loc % 256 == 0.  Collective rules and errors as ao_ag_gemm. */
 ao_status ao_sp_attn(ao_plan* plan, const void* Q, const void* K, const void* V, void* O, void* stream);
 ao_status ao_sp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
                            const void* const* Vs, void* const* Os, void* stream);

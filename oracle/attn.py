@@ -15,6 +15,9 @@ attention (Vaswani et al., the paper's attention workloads P:459) over the full 
 with scale = 1/sqrt(d).  The ring order in which the GPU consumes the KV shards does not
 change the exact result (softmax over a set); the oracle uses the plain definition.
 
+Causal (ring attention for decoders): query i of rank r is token r*S_loc + i and sees keys
+at positions <= its own.
+
 Pins (tests/test_oracle_attn.py): constant scores give the mean of V, a one-hot score
 selects one V row, permutation invariance over KV rows, W = 1 reduces to single-device
 attention computed with an explicit per-element loop, exact rational arithmetic on a
@@ -25,33 +28,43 @@ from __future__ import annotations
 import numpy as np
 
 
-def attention(Q, K, V, scale: float):
+def attention(Q, K, V, scale: float, q_pos=None, k_pos=None):
     """Single-device attention, fp64: softmax(Q K^T * scale) V per head.  Q [H, Sq, d],
-    K/V [H, Sk, d]."""
+    K/V [H, Sk, d].  With q_pos / k_pos (global token positions) the causal mask: query i
+    sees key j iff k_pos[j] <= q_pos[i] (Vaswani et al.'s decoder masking)."""
     Q = np.asarray(Q, dtype=np.float64)
     K = np.asarray(K, dtype=np.float64)
     V = np.asarray(V, dtype=np.float64)
     S = np.einsum("hqd,hkd->hqk", Q, K) * scale
+    if q_pos is not None:
+        S = np.where(np.asarray(k_pos)[None, None, :] <= np.asarray(q_pos)[None, :, None], S, -np.inf)
     S = S - S.max(axis=-1, keepdims=True)
     P = np.exp(S)
     P /= P.sum(axis=-1, keepdims=True)
     return np.einsum("hqk,hkd->hqd", P, V)
 
 
-def sp_attention(Q_list, K_list, V_list, rank: int, scale: float):
+def sp_attention(Q_list, K_list, V_list, rank: int, scale: float, causal: bool = False):
     """Rank `rank`'s output of sequence-parallel attention: its queries against the
-    all-gathered keys/values (concatenation of the shards in rank order)."""
+    all-gathered keys/values (concatenation of the shards in rank order).  causal:
+    rank r's query i is global token r*S_loc + i and sees keys up to that position."""
     K = np.concatenate([np.asarray(k, dtype=np.float64) for k in K_list], axis=1)
     V = np.concatenate([np.asarray(v, dtype=np.float64) for v in V_list], axis=1)
-    return attention(Q_list[rank], K, V, scale)
+    if not causal:
+        return attention(Q_list[rank], K, V, scale)
+    S_loc = np.asarray(Q_list[rank]).shape[1]
+    return attention(Q_list[rank], K, V, scale, np.arange(S_loc) + rank * S_loc, np.arange(K.shape[1]))
 
 
-def sp_attention_rows(Q_list, K_list, V_list, rank: int, scale: float, heads, rows):
+def sp_attention_rows(Q_list, K_list, V_list, rank: int, scale: float, heads, rows, causal: bool = False):
     """Selected (head, row) outputs (full-size sampled checks)."""
     K = np.concatenate([np.asarray(k, dtype=np.float64) for k in K_list], axis=1)
     V = np.concatenate([np.asarray(v, dtype=np.float64) for v in V_list], axis=1)
     Q = np.asarray(Q_list[rank], dtype=np.float64)
+    S_loc = Q.shape[1]
+    qp = (np.asarray(rows) + rank * S_loc) if causal else None
+    kp = np.arange(K.shape[1]) if causal else None
     out = []
     for h in heads:
-        out.append(attention(Q[h:h + 1, rows], K[h:h + 1], V[h:h + 1], scale)[0])
+        out.append(attention(Q[h:h + 1, rows], K[h:h + 1], V[h:h + 1], scale, qp, kp)[0])
     return np.stack(out)

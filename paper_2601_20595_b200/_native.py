@@ -56,6 +56,8 @@ class PlanDesc(ctypes.Structure):
         ("timeout_ns", ctypes.c_uint64),
         ("rs_reduce", ctypes.c_int32),
         ("topk", ctypes.c_int32),
+        ("causal", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -154,4 +156,5 @@ def make_desc(d: dict) -> PlanDesc:
     x.timeout_ns = int(d.get("timeout_ns", 0))
     x.rs_reduce = RS_REDUCE[d.get("rs_reduce", "slots")]
     x.topk = int(d.get("topk", 0))
+    x.causal = int(d.get("causal", 0))
     return x

@@ -52,6 +52,8 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
     if (d.dir != AO_DIR_PUSH) v.push_back("dir for sp_attn");
     if (d.comm_ctas != 0) v.push_back("comm_ctas with sp_attn");
     if (d.topk != 0) v.push_back("topk");
+    if (d.causal != 0 && d.causal != 1) v.push_back("causal");
+    if (d.causal == 1 && d.M % 256 != 0) v.push_back("causal needs S_loc (M) % 256");
     if (d.n_cta < 0) v.push_back("n_cta");
     return v;
   }
@@ -59,6 +61,7 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   if (W < 1 || W > AO_MAX_WORLD) v.push_back("world_size");
   if (!(d.rank >= 0 && d.rank < std::max(W, 1))) v.push_back("rank");
   if (d.M < 0 || d.N < 0 || d.K < 0) v.push_back("shape");
+  if (d.causal != 0) v.push_back("causal");
   const bool a2a = d.op == AO_OP_A2A_GEMM;
   if (a2a) {
     // M = tokens per rank T; the received rows R_e <= W*T are routing-dependent (Q25)
@@ -253,6 +256,7 @@ static std::string rank_independent_key(const HostPlan& p) {
   o.put("rs_wire", d.rs_wire);
   o.put("rs_reduce", d.rs_reduce);
   if (d.op == AO_OP_A2A_GEMM) o.put("topk", d.topk);
+  if (d.op == AO_OP_SP_ATTN) o.put("causal", d.causal);
   return o.str();
 }
 
@@ -299,6 +303,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
     o.put("n_cta", P.n_cta);
     o.put("items", P.n_tiles);
     o.put_str("kv_order", "ring");
+    o.put("causal", d.causal);
     P.json = o.str();
     P.hash = fnv1a64(rank_independent_key(P));
     return {};

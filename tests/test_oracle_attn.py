@@ -79,3 +79,35 @@ def test_sampled_rows_match():
     rows = np.array([0, 5, 15])
     np.testing.assert_allclose(oa.sp_attention_rows(Q, K, V, 1, d ** -0.5, [0, 2], rows), full[[0, 2]][:, rows],
                                rtol=1e-13, atol=1e-13)
+
+
+def test_causal_single_rank_element_loop_and_first_row():
+    """Causal: row i averages V over keys 0..i with softmax weights (element loop); the first
+    query of the sequence returns V[0] exactly."""
+    W, H, S, d = 2, 1, 4, 8
+    Q, K, V = (_np(x) for x in si.attn_inputs(W, H, S, d, salt=11))
+    scale = d ** -0.5
+    Kf = np.concatenate(K, 1)
+    Vf = np.concatenate(V, 1)
+    for r in range(W):
+        got = oa.sp_attention(Q, K, V, r, scale, causal=True)
+        for i in range(S):
+            n = r * S + i + 1  # visible keys
+            s = [sum(Q[r][0, i, x] * Kf[0, j, x] for x in range(d)) * scale for j in range(n)]
+            m = max(s)
+            e = [np.exp(v - m) for v in s]
+            for x in range(d):
+                assert abs(got[0, i, x] - sum(e[j] * Vf[0, j, x] for j in range(n)) / sum(e)) < 1e-12
+    np.testing.assert_array_equal(oa.sp_attention(Q, K, V, 0, scale, causal=True)[0, 0], V[0][0, 0])
+
+
+def test_causal_last_rank_last_row_equals_full():
+    """The last token of the sequence sees every key: causal == non-causal on that row."""
+    W, H, S, d = 3, 2, 8, 16
+    Q, K, V = (_np(x) for x in si.attn_inputs(W, H, S, d, salt=13))
+    c = oa.sp_attention(Q, K, V, W - 1, d ** -0.5, causal=True)
+    f = oa.sp_attention(Q, K, V, W - 1, d ** -0.5)
+    np.testing.assert_allclose(c[:, -1], f[:, -1], rtol=1e-13, atol=1e-13)
+    rows = np.array([0, 3, 7])
+    np.testing.assert_allclose(oa.sp_attention_rows(Q, K, V, 1, d ** -0.5, [1], rows, causal=True),
+                               oa.sp_attention(Q, K, V, 1, d ** -0.5, causal=True)[[1]][:, rows], rtol=1e-13, atol=1e-13)

@@ -559,6 +559,21 @@ def attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
         c.check_async()
     Stot = S * W
     flops = 4.0 * Stot * Stot * d * H / (1 if loop else W)
+    # causal variant (RingAttention for decoders): half the score matrix; same inputs
+    cplans = [ao.Plan(c, dict(desc, rank=r, causal=1)) for c, r in zip(ctxs, my)]
+
+    def run_c():
+        if loop:
+            ao.sp_attn_group(cplans, Qd, Kd, Vd, Od)
+        else:
+            ao.sp_attn(cplans[0], Qd[0], Kd[0], Vd[0], Od[0])
+
+    ms_c = timed(run_c, n)
+    for c in ctxs:
+        c.check_async()
+    flops_c = 2.0 * Stot * Stot * d * H / (1 if loop else W)
+    for p in cplans:
+        p.close()
     # library reference: SDPA per rank over its gathered K/V (already resident)
     if loop:
         Kf = torch.cat([k.to(dev) for k in K], 1).unsqueeze(0)
@@ -576,6 +591,7 @@ def attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
             "workload": "llama3-8b-attn-sp%d-%s" % (W, "loopback" if loop else "nvlink"),
             "seq_total": Stot, "heads": H, "head_dim": d, "ms": round(ms, 4), "tflops": round(tf, 1),
             "frac_of_peak": round(tf / peaks["bf16_tflops"], 4),
+            "causal_ms": round(ms_c, 4), "causal_tflops": round(flops_c / (ms_c * 1e-3) / 1e12, 1),
             "sdpa_same_gpu_ms": None if sd_ms is None else round(sd_ms, 4),
             "sdpa_tflops": None if sd_ms is None else round(flops / (sd_ms * 1e-3) / 1e12, 1)}
 

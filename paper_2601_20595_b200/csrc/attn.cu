@@ -422,7 +422,9 @@ struct PPBars {
   uint8_t waited[kAttnAhead];
 };
 
-// (bound 512 threads: caps the registers at 128 per thread; launched with 320)
+// (bound 512 threads: caps the registers at 128 per thread; launched with 320).  CAUSAL is a
+// template parameter so the non-causal kernel carries no mask code (registers are tight).
+template <bool CAUSAL>
 __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__ AttnArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -432,7 +434,23 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
   PPBars& B = *reinterpret_cast<PPBars*>(sV + kPPV * (kKVBytes / 2));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = args.W, S = args.S_loc, nqp = S / (2 * kBlk), nkb = S / kBlk;
-  const int n_items = args.H * nqp, nkv = W * nkb;
+  const int n_items = args.H * nqp;
+  // KV blocks of an item, in arrival order: the own shard first (kb = 0, 1, ...), then the
+  // sources rank-1, rank-2, ... (the push rotation).  Causal: only the own blocks up to the
+  // item's last query (kb <= 2qp+1) and only the sources below this rank (RingAttention
+  // skips the future shards).
+  auto nkv_of = [&](const AttnRank& R, int qp) -> int { return CAUSAL ? R.rank * nkb + 2 * qp + 2 : W * nkb; };
+  auto kv_of = [&](const AttnRank& R, int qp, int j, int& d, int& kb) {
+    const int own = CAUSAL ? 2 * qp + 2 : nkb;
+    if (j < own) {
+      d = 0;
+      kb = j;
+    } else {
+      d = 1 + (j - own) / nkb;
+      kb = (j - own) % nkb;
+    }
+    (void)R;
+  };
 
   if (warp == 1) {
     if (lane == 0) {
@@ -483,8 +501,10 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
         tma_load_2d(sQ + kHalf, &R.tmQ, &B.qfull, 64, qrow, pol);
         tma_load_2d(sQ + kQBytes, &R.tmQ, &B.qfull, 0, qrow + kBlk, pol);
         tma_load_2d(sQ + kQBytes + kHalf, &R.tmQ, &B.qfull, 64, qrow + kBlk, pol);
+        const int nkv = nkv_of(R, qp);
         for (int j = 0; j < nkv; ++j, ++n) {
-          const int d = j / nkb, kb = j % nkb;
+          int d, kb;
+          kv_of(R, qp, j, d, kb);
           const int src = (R.rank - d + W) % W;
           const int krow = h * S + kb * kBlk;
           if (d > 0) {  // the chunk (src, h*S + kb*128) must have landed
@@ -537,8 +557,7 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
       __syncwarp();
     };
     attn_walk(args, n_items, [&](int g, int item) {
-      (void)g;
-      (void)item;
+      const int nkv = nkv_of(args.rk[g], item % nqp);
       mbar_wait(&B.qfull, t & 1u);
       for (int x = 0; x < 2; ++x) {
         if (n > 0) mbar_wait(&B.pvdone[x], (n - 1) & 1u);  // P_x of the previous item was read
@@ -592,12 +611,33 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
     attn_walk(args, n_items, [&](int g, int item) {
       const AttnRank& R = args.rk[g];
       const int h = item / nqp, qp = item % nqp;
+      const int nkv = nkv_of(R, qp);
+      const int qloc = qp * 2 * kBlk + x * kBlk + r;  // this thread's query (local position)
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         const uint32_t nn = n + j;
+        int d, kb;
+        kv_of(R, qp, j, d, kb);
+        // causal: keys kb*128 + c beyond this query are masked (own diagonal blocks only)
+        const int kmax = (CAUSAL && d == 0) ? qloc - kb * kBlk : 1 << 30;
         mbar_wait(&B.sfull[x], nn & 1u);
         tc_fence_after();
         if (nn >= 1) pv_wait(nn - 1);  // S_x(nn) exists, so the PV of block nn-1 is done
+        if (CAUSAL && d == 0 && kb >= 2 * qp) {
+          // causal diagonal blocks (two per item): keys past this query become -inf in TMEM,
+          // so the passes below stay mask-free (registers are tight)
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tS + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i > kmax) v[i] = 0xff800000u;  // -inf
+            tmem_st_32x32b_x32(tS + c * 32, v);
+          }
+          tmem_wait_st();
+        }
         // two passes over the S row in TMEM (max, then exp) keep 64 values live instead of
         // 128: the kernel's registers must leave room for the memcpy kernels (see kPPThreads)
         float mp[8];
@@ -691,19 +731,25 @@ cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream) {
   // two-tile ping-pong kernel when S_loc is a multiple of 256 (AO_ATTN_SINGLE=1 forces the
   // one-tile kernel)
   static const bool single = getenv("AO_ATTN_SINGLE") && getenv("AO_ATTN_SINGLE")[0] == '1';
-  const bool pp = !single && args.S_loc % (2 * dev::kBlk) == 0;
-  static bool attr = false, attr_pp = false;
+  const bool pp = args.causal || (!single && args.S_loc % (2 * dev::kBlk) == 0);  // causal: pp only
+  static bool attr = false, attr_pp = false, attr_ppc = false;
   if (!pp && !attr) {
     cudaError_t e = cudaFuncSetAttribute(dev::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(dev::kAttnSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (pp && !attr_pp) {
-    cudaError_t e = cudaFuncSetAttribute(dev::attn_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (pp && !args.causal && !attr_pp) {
+    cudaError_t e = cudaFuncSetAttribute(dev::attn_pp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(dev::kPPSmem));
     if (e != cudaSuccess) return e;
     attr_pp = true;
+  }
+  if (pp && args.causal && !attr_ppc) {
+    cudaError_t e = cudaFuncSetAttribute(dev::attn_pp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(dev::kPPSmem));
+    if (e != cudaSuccess) return e;
+    attr_ppc = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(args.ts ? args.ctas_per_rank : args.n_group * args.ctas_per_rank);
@@ -716,7 +762,9 @@ cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream) {
   // CTA per SM (shared memory), as for the cluster-launched GEMM kernels.
   cfg.attrs = nullptr;
   cfg.numAttrs = 0;
-  return pp ? cudaLaunchKernelEx(&cfg, dev::attn_pp_kernel, args) : cudaLaunchKernelEx(&cfg, dev::attn_kernel, args);
+  if (!pp) return cudaLaunchKernelEx(&cfg, dev::attn_kernel, args);
+  return args.causal ? cudaLaunchKernelEx(&cfg, dev::attn_pp_kernel<true>, args)
+                     : cudaLaunchKernelEx(&cfg, dev::attn_pp_kernel<false>, args);
 }
 
 }  // namespace ao

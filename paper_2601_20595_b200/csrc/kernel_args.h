@@ -113,6 +113,7 @@ struct AttnArgs {
   AttnRank rk[AO_MAX_WORLD];
   int32_t n_group, W, H, S_loc, crows, nch;  // crows: rows of the [H*S_loc] view per chunk
   int32_t ctas_per_rank, ts;                 // ts: time-sliced whole-world group (rank after rank)
+  int32_t causal;                            // causal mask over global token positions (ping-pong kernel)
   float scale_log2;                          // softmax scale * log2(e)
   uint64_t timeout_ns;
   ErrorInfo* err;

@@ -1161,6 +1161,7 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
   ka->nch = nch;
   ka->ctas_per_rank = h0.n_cta;
   ka->scale_log2 = float(1.4426950408889634 / std::sqrt(128.0));
+  ka->causal = h0.desc.causal;
   ka->timeout_ns = h0.desc.timeout_ns ? h0.desc.timeout_ns : 5000000000ull;
   ka->err = p0->ctx->err_dev;
   if (int64_t(n) * h0.n_cta > p0->ctx->sm_count) {

@@ -95,3 +95,32 @@ def test_sp_attn_llama_sampled(ao):
         got = O[r][[0, 13, 31]][:, rows].float().cpu().numpy()
         ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
         assert ok, f"llama sampled rank {r}: {e:.3e} {f:.3e}"
+
+
+@pytest.mark.parametrize("W,H,S", [(1, 2, 256), (2, 2, 256), (4, 1, 512), (8, 2, 256)])
+@pytest.mark.parametrize("ts", [False, True])
+def test_sp_attn_causal_vs_oracle(ao, W, H, S, ts):
+    """Causal ring attention: rank r's queries see the shards of ranks <= r (own shard
+    masked on the diagonal blocks); per-rank work differs (rank 0 has the least)."""
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=70 + W)
+    ctxs, plans = _world(ao, W, H, S, S, SMS if ts else max(1, SMS // W), causal=1)
+    O = _run(ao, ctxs, plans, Q, K, V)
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    for r in range(W):
+        ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=True)
+        ok, e, f = on.check_tolerance(O[r].float().cpu().numpy(), ref, frob_rel=FROB)
+        assert ok, f"causal W={W} H={H} S={S} ts={ts} rank {r}: {e:.3e} {f:.3e}"
+
+
+def test_sp_attn_causal_llama_sampled(ao):
+    W, H, S = 8, 32, 2048
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=3)
+    ctxs, plans = _world(ao, W, H, S, 2048, SMS, causal=1, timeout_ns=10_000_000_000)
+    O = _run(ao, ctxs, plans, Q, K, V)
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    rows = np.array([0, 127, 128, 255, 256, 1000, 2047])
+    for r in (0, 3, 7):
+        ref = oatt.sp_attention_rows(Qn, Kn, Vn, r, 128 ** -0.5, [0, 31], rows, causal=True)
+        got = O[r][[0, 31]][:, rows].float().cpu().numpy()
+        ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
+        assert ok, f"causal llama rank {r}: {e:.3e} {f:.3e}"

@@ -559,6 +559,7 @@ __device__ __noinline__ void a2a_push_chunk_tma(const A2ASched& sm, const RankAr
   bulk_wait<0>();  // writes performed
   fence_proxy_async_global();
   fence_sys();
+  if (A.delay_ns) inject_delay(A.delay_ns, uint32_t(s * 977 + e * 131 + j));  // fault injection
   st_release_sys(S_.peer_flags[e] + s * S_.maxJ + j, S_.epoch);
 }
 
@@ -1216,7 +1217,9 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             // the (source, chunk) blocks of this tile's received rows
             const int r0 = a2a_tile(a2s, R, grp, k).x * BM;
             const uint64_t tw = args.trace ? globaltimer() : 0;
-            waited = a2a_wait(a2s, R, args, wc, grp, lcta, r0, min(a2s.rows[grp], r0 + BM));
+            // debug mutation: CTA 0 of rank group 0 skips the waits of its skip_wait-th tile
+            if (!(args.skip_wait >= 0 && blockIdx.x == 0 && grp == 0 && int(q) == args.skip_wait))
+              waited = a2a_wait(a2s, R, args, wc, grp, lcta, r0, min(a2s.rows[grp], r0 + BM));
             if (waited) trace_event(args, TR_WAIT, R.rank, lcta, r0 / BM, tw);
           } else if (ts) {
             const int64_t r0 = int64_t(R.order[k] / R.n_nb) * BM;

@@ -1060,7 +1060,8 @@ static ao_status launch_a2a(int n, ao_plan* const* plans, const void* const* Xs,
   ka->mode = ao::MODE_A2A;
   ka->timeout_ns = h0.desc.timeout_ns ? h0.desc.timeout_ns : 5000000000ull;
   ka->err = p0->ctx->err_dev;
-  ka->skip_wait = -1;
+  ka->skip_wait = int32_t(g_debug.skip_wait);
+  ka->delay_ns = uint32_t(g_debug.delay_ns);
   ka->exp = int32_t(g_debug.exp);
   ka->trace = p0->ctx->trace;
   ka->trace_cursor = p0->ctx->trace_cursor;

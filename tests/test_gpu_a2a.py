@@ -184,3 +184,34 @@ def test_a2a_device_schedule_matches_oracle(ao, ts, tmp_path):
                 for m, x in enumerate(mine):
                     got[cta + m * n_cta] = int(x["name"].split()[1])
             assert [got[i] for i in range(len(sched[e]))] == [mb * n_nb + nb for mb, nb in sched[e]], e
+
+
+def test_a2a_delays_are_safe_and_a_dropped_wait_is_caught(ao):
+    """Fault injection: random delays before every chunk-flag release never
+    change the result; dropping the waits of one tile while pushes are delayed is caught by
+    the provenance decode (the chunk waits are load-bearing); recovery afterwards."""
+    W, T, H, N, k = 4, 256, 64, 256, 2
+    _, idx, _ = si.moe_inputs(W, T, H, N, topk=k, salt=9)
+    ctxs, plans = _world(ao, W, T, H, N, k, 64, False, tile_m=128, tile_n=128, n_cta=4)
+    In = [i.numpy().astype(np.int64) for i in idx]
+
+    def decode_ok(ep):
+        X, idx2, B = si.moe_provenance_inputs(W, T, H, N, idx, epoch=ep)
+        Y, rp, rr = _run(ao, ctxs, plans, X, idx2, B, N)
+        ok = True
+        for e in range(W):
+            y = Y[e][: rr[e]].float().cpu()
+            gid = (y[:, 0] + 32 * y[:, 1] + 1024 * y[:, 2]).numpy()
+            want = [s * T + t for s in range(W) for t in range(T) if e in In[s][t]]
+            ok &= bool(np.array_equal(gid, want)) and bool(torch.all(y[:, 3] == ep % 32))
+        return ok
+
+    try:
+        ao.debug_set("delay_ns", 2_000_000)
+        assert decode_ok(1), "delayed pushes must not change the result"
+        ao.debug_set("skip_wait", 0)
+        assert not decode_ok(2), "a dropped wait must be observable (mutation kill)"
+    finally:
+        ao.debug_set("skip_wait", -1)
+        ao.debug_set("delay_ns", 0)
+    assert decode_ok(3)

@@ -215,7 +215,10 @@ ao_status ao_gemm_ar_group(int n, ao_plan* const* plans, const void* const* As, 
  * and release a per-(source, chunk) flag that the tiles covering those rows wait on; the
  * tile order follows the arrival order (own rows, then sources e-1, e-2, ...).  Plan:
  * op AO_OP_A2A_GEMM, backend AO_BACKEND_LDST, dir PUSH, comm_ctas 0, 1 <= topk <= W,
- * (W*T) % tile_m == 0.  Same collective rules and errors as ao_ag_gemm. */
+ * (W*T) % tile_m == 0.  Same collective rules and errors as ao_ag_gemm.  The ranks' prep
+ * kernels wait for each other (count exchange): ranks sharing one device must use
+ * ao_a2a_gemm_group (per-rank calls on separate streams of one process can be serialised
+ * by the driver's stream-to-hardware-queue mapping and time out). */
 ao_status ao_a2a_gemm(ao_plan* plan, const void* X, const int32_t* topk_idx, const void* B, void* Y,
                       int32_t* route_pos, int32_t* recv_rows, void* stream);
 ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs, const int32_t* const* topk_idxs,

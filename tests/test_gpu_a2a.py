@@ -215,3 +215,4 @@ def test_a2a_delays_are_safe_and_a_dropped_wait_is_caught(ao):
         ao.debug_set("skip_wait", -1)
         ao.debug_set("delay_ns", 0)
     assert decode_ok(3)
+

@@ -124,3 +124,26 @@ def test_sp_attn_causal_llama_sampled(ao):
         got = O[r][[0, 31]][:, rows].float().cpu().numpy()
         ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
         assert ok, f"causal llama rank {r}: {e:.3e} {f:.3e}"
+
+
+@pytest.mark.parametrize("causal", [0, 1])
+def test_sp_attn_per_rank_calls_on_separate_streams(ao, causal):
+    """One ao_sp_attn call per rank (n_group = 1), each on its own stream with its own
+    copy-engine chain, as with one process per GPU."""
+    W, H, S = 2, 2, 512
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=90 + causal)
+    ctxs, plans = _world(ao, W, H, S, 512, 32, causal=causal)
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    dQ, dK, dV = [q.cuda() for q in Q], [k.cuda() for k in K], [v.cuda() for v in V]
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    for it in range(2):
+        O = [torch.empty_like(q) for q in dQ]
+        for r in (1, 0) if it % 2 else (0, 1):
+            ao.sp_attn(plans[r], dQ[r], dK[r], dV[r], O[r], stream=streams[r])
+        torch.cuda.synchronize()
+        for c in ctxs:
+            c.check_async()
+        for r in range(W):
+            ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=bool(causal))
+            ok, e, f = on.check_tolerance(O[r].float().cpu().numpy(), ref, frob_rel=FROB)
+            assert ok, f"per-rank attn causal={causal} it={it} r{r}: {e:.3e} {f:.3e}"

@@ -869,12 +869,12 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
     const int64_t grid = int64_t(n) * (ka->ctas_per_rank + ka->comm_ctas_per_rank);
     if (grid > p0->ctx->sm_count && n > 1 && n == h0.W && ka->ctas_per_rank <= p0->ctx->sm_count &&
         ka->comm_ctas_per_rank == 0 &&
-        (mode == ao::MODE_RS || (h0.desc.dir == AO_DIR_PUSH && h0.desc.backend != AO_BACKEND_LDST)))
+        (mode == ao::MODE_RS || h0.desc.dir == AO_DIR_PUSH))
       time_sliced = build_segments(n, plans, mode, ka.get());
     if (grid > p0->ctx->sm_count && !time_sliced)
       return fail(AO_ERR_INVALID_ARG, "grid of %lld CTAs exceeds the %d SMs: the persistent CTAs would not be "
-                  "co-resident (lower n_cta / comm_ctas; a whole-world loopback group of AG copy-engine push or "
-                  "GEMM-RS plans with n_cta <= SMs runs time-sliced)", (long long)grid, p0->ctx->sm_count);
+                  "co-resident (lower n_cta / comm_ctas; a whole-world loopback group of AG push, GEMM-RS or "
+                  "GEMM-AR plans with n_cta <= SMs runs time-sliced)", (long long)grid, p0->ctx->sm_count);
     if (h0.tile.cg == 2 && (ka->comm_ctas_per_rank % 2) != 0)
       return fail(AO_ERR_INVALID_ARG, "comm_ctas must be even with CTA-pair tiles (cluster launch)");
   }

@@ -63,7 +63,7 @@ def _rs(ao, ctxs, plans, A, B):
     return Cs
 
 
-@pytest.mark.parametrize("backend", ["ce", "tma"])
+@pytest.mark.parametrize("backend", ["ce", "tma", "ldst"])
 @pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
 @pytest.mark.parametrize("W", [2, 4, 8])
 def test_ag_timesliced_vs_oracle(ao, W, tile, backend):
@@ -80,7 +80,7 @@ def test_ag_timesliced_vs_oracle(ao, W, tile, backend):
         assert torch.equal(G[r].cpu(), full), "gathered A must be a bit-exact copy"
 
 
-@pytest.mark.parametrize("backend", ["ce", "tma"])
+@pytest.mark.parametrize("backend", ["ce", "tma", "ldst"])
 @pytest.mark.parametrize("W", [4, 8])
 def test_ag_timesliced_provenance_epochs(ao, W, backend):
     """Row-id / epoch digits decode exactly across back-to-back epochs (both parities),
@@ -199,23 +199,17 @@ def test_gemm_batched_timesliced(ao, n):
         _check(Cs[i], on.gemm(si.to_f64(A[i]), si.to_f64(B[i])), f"gemm_batched ts n={n} #{i}")
 
 
-def test_timesliced_rejects_unsupported(ao):
-    """Groups that cannot be time-sliced keep the co-residency error: the ld/st comm
-    backend or a partial world."""
-    W, M, K, N = 2, 512, 64, 256
-    A = [torch.zeros(M // W, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
-    B = [torch.zeros(N, K, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
-    C = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
-    d = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend="ldst", n_cta=SMS)
+def test_timesliced_rejects_a_partial_world(ao):
+    """Only a whole world can be time-sliced: two ranks of a 4-rank world whose plans ask
+    for all SMs keep the co-residency error."""
+    W, M, K, N = 4, 512, 64, 256
+    B = [torch.zeros(N, K, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    C = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    A = [torch.zeros(M // W, K, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    d = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=64, backend="ce", n_cta=SMS)
     ctxs, plans = _world(ao, d, W)
     with pytest.raises(ao.AOError, match="INVALID_ARG"):
-        ao.ag_gemm_group(plans, A, B, C)
-    W4 = 4  # two ranks of a 4-rank world in one launch: a partial world cannot be time-sliced
-    dpart = dict(d, world_size=W4, backend="ce")
-    ctxs3, plans3 = _world(ao, dpart, W4)
-    A4 = [torch.zeros(M // W4, K, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
-    with pytest.raises(ao.AOError, match="INVALID_ARG"):
-        ao.ag_gemm_group(plans3[:2], A4, B, C)
+        ao.ag_gemm_group(plans[:2], A, B, C)
 
 
 def test_bench_config_timesliced_fullsize(ao):

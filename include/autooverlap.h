@@ -175,7 +175,13 @@ ao_status ao_ctx_destroy(ao_ctx* ctx);
  * ao_gemm_rs: A [M, K], B [N, K] (this rank's K shard), C_shard [M/W, N].
  * ao_*_group: ONE fused launch for n ranks of a world that live in this process on the
  *   same device (loopback).  plans[i] must belong to distinct ctxs of one world; the
- *   pointer arrays are indexed like plans.  The n=1 case equals the single-rank call. */
+ *   pointer arrays are indexed like plans.  The n=1 case equals the single-rank call.
+ *   Space-sliced when n * (plan CTAs) <= SMs (each rank on its own CTAs, concurrently);
+ *   TIME-SLICED when n == world_size and each plan asks for more than SMs / n CTAs (up to
+ *   all SMs): every CTA serves every rank, walking one global list of the ranks' tile runs
+ *   (AG rank after rank with destination-major pushes; RS / GEMM-AR owner after owner, the
+ *   owner's own tiles after their contributions), with per-tile chunk waits (DESIGN.md
+ *   Q24).  Otherwise AO_ERR_INVALID_ARG (the spin-waiting CTAs must be co-resident). */
 ao_status ao_plan_create(ao_ctx* ctx, const ao_plan_desc* desc, ao_plan** out);
 ao_status ao_ag_gemm(ao_plan* plan, const void* A_shard, const void* B, void* C, void* A_gathered_out,
                      void* stream);

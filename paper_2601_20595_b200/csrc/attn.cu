@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < 8; ++u) mp[u] = s[u];
 #pragma unroll
-        for (int i = 8; i < 64; ++i) mp[i & 7] = fmaxf(mp[i & 7], s[i]);
+        for (int i = 4; i < 32; ++i) mp[i & 7] = max3f(mp[i & 7], s[2 * i], s[2 * i + 1]);
         const float mh = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
         B.xmax[hf][r] = mh;
         named_bar_sync(pair_bar, 64);
@@ -300,12 +300,21 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
         const bool grow = mxs > m + 8.f;
         const float m_new = grow ? mxs : m;
         const float alpha = grow ? exp2f(m - m_new) : 1.f;
-        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // s * scale_log2 - m as FFMA2 pairs, exp2 on the MUFU, row sums as FADD2 pairs
+        const uint64_t sc2 = f2_pack(__float_as_uint(sl2), __float_as_uint(sl2));
+        const uint64_t nm2 = f2_pack(__float_as_uint(-m_new), __float_as_uint(-m_new));
+        uint64_t sp2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          s[i] = exp2f(fmaf(s[i], sl2, -m_new));
-          sp[i & 7] += s[i];
+        for (int i = 0; i < 32; ++i) {
+          float a, b;
+          f2_unpack(f2_fma(f2_pack(__float_as_uint(s[2 * i]), __float_as_uint(s[2 * i + 1])), sc2, nm2), a, b);
+          s[2 * i] = ex2_ftz(a);
+          s[2 * i + 1] = ex2_ftz(b);
+          sp2[i & 3] = f2_add(sp2[i & 3], f2_pack(__float_as_uint(s[2 * i]), __float_as_uint(s[2 * i + 1])));
         }
+        float sp[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) f2_unpack(sp2[u], sp[2 * u], sp[2 * u + 1]);
         const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
         l = l * alpha + sum;
         m = m_new;
@@ -649,15 +658,18 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
           tmem_ld_32x32b_x32(tS + c * 32, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(v[i]));
+          for (int i = 0; i < 16; ++i) mp[i & 7] = max3f(mp[i & 7], __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
         }
         const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
         const float mxs = mx * sl2;
         const bool grow = mxs > m + 8.f;  // lazy rescale (see attn_kernel)
         const float m_new = grow ? mxs : m;
         const float alpha = grow ? exp2f(m - m_new) : 1.f;
-        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[2][32];
+        // s * scale_log2 - m as FFMA2 pairs, exp2 on the MUFU, row sums as FADD2 pairs
+        const uint64_t sc2 = f2_pack(__float_as_uint(sl2), __float_as_uint(sl2));
+        const uint64_t nm2 = f2_pack(__float_as_uint(-m_new), __float_as_uint(-m_new));
+        uint64_t sp2[4] = {0ull, 0ull, 0ull, 0ull};
+        uint32_t pk[32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {  // exp per 32 columns; P row r as bf16 pairs
           uint32_t v[32];
@@ -665,18 +677,21 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float a = exp2f(fmaf(__uint_as_float(v[2 * i]), sl2, -m_new));
-            const float b = exp2f(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -m_new));
-            sp[(2 * i) & 7] += a;
-            sp[(2 * i + 1) & 7] += b;
-            pk[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(a, b);
+            float a, b;
+            f2_unpack(f2_fma(f2_pack(v[2 * i], v[2 * i + 1]), sc2, nm2), a, b);
+            a = ex2_ftz(a);
+            b = ex2_ftz(b);
+            sp2[i & 3] = f2_add(sp2[i & 3], f2_pack(__float_as_uint(a), __float_as_uint(b)));
+            pk[(c & 1) * 16 + i] = pack_bf16x2(a, b);
           }
+          // P columns 32(c/2) .. +31 overwrite S columns this thread has already read
+          if (c & 1) tmem_st_32x32b_x32(tS + (c >> 1) * 32, pk);
         }
+        float sp[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) f2_unpack(sp2[u], sp[2 * u], sp[2 * u + 1]);
         l = l * alpha + (((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7])));
         m = m_new;
-        // P over the first 64 S columns: every S value of the row is already read (above)
-        tmem_st_32x32b_x32(tS, pk[0]);
-        tmem_st_32x32b_x32(tS + 32, pk[1]);
         if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {

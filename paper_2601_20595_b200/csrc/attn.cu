@@ -592,10 +592,10 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
             if (x == 1) mma_commit(&B.vempty[nn % kPPV]);
           }
           __syncwarp();
-          if (j + 1 < nkv) {
-            mbar_wait(&B.pvdone[x], nn & 1u);  // P_x(nn) read before S_x(nn+1) overwrites it
-            issue_s(x, nn + 1);
-          }
+          // S_x(nn+1) overwrites P_x(nn) in TMEM: tcgen05.mma ops of one thread execute in
+          // issue order, so it is issued right behind PV_x(nn) without waiting for its
+          // completion (waiting left a commit -> mbarrier round trip as a pipe bubble per block)
+          if (j + 1 < nkv) issue_s(x, nn + 1);
         }
       }
       n += nkv;
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__
         const int kmax = (CAUSAL && d == 0) ? qloc - kb * kBlk : 1 << 30;
         mbar_wait(&B.sfull[x], nn & 1u);
         tc_fence_after();
-        if (nn >= 1) pv_wait(nn - 1);  // S_x(nn) exists, so the PV of block nn-1 is done
+        if (nn >= 1) pv_wait(nn - 1);  // PV(nn-1) done before O is rescaled / P(nn) written
         if (CAUSAL && d == 0 && kb >= 2 * qp) {
           // causal diagonal blocks (two per item): keys past this query become -inf in TMEM,
           // so the passes below stay mask-free (registers are tight)

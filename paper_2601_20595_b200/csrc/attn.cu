@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
       const uint32_t st = nn % kKStages, sb = nn & 1u;
       mbar_wait(&B.kfull[st], (nn / kKStages) & 1u);
       mbar_wait(&B.sfree[sb], ((nn >> 1) & 1u) ^ 1u);
-      // P of block nn-2 lives in this S buffer's columns: its P.V must have read it
-      if (nn >= 2) mbar_wait(&B.pvdone[sb], ((nn >> 1) - 1) & 1u);
+      // P of block nn-2 lives in this S buffer's columns: its P.V was issued before this S
+      // by this thread (the loop below), and tcgen05.mma ops execute in issue order
       tc_fence_after();
       if (lane == 0) {
         const uint8_t* kb = sK + st * (kKVBytes / 2);
@@ -415,9 +415,9 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_kernel(const __grid_constan
 // Item = (head, 256 queries) = tiles x = 0, 1 sharing every K/V block.  Each tile has its own
 // softmax warpgroup (warps 2-5 and 6-9), S buffer and O accumulator in TMEM, so the tensor
 // core works on one tile's QK^T / PV while the other tile's softmax runs (the FA4 schedule).
-// 10 warps (the producer acquires the chunk flags itself) and at most 168 registers per
-// thread, so that 320 x 168 registers leave room on every SM for the copy kernels that
-// execute same-device memcpy nodes (the loopback "copy engine" pushes): with 352 x 168 they
+// 10 warps (the producer acquires the chunk flags itself) and at most 152 registers per
+// thread, so that 320 x 152 registers leave room on every SM for the copy kernels that
+// execute same-device memcpy nodes (the loopback "copy engine" pushes): with 320 x 168 they
 // could not be scheduled while this persistent kernel ran and the chunk waits timed out.
 constexpr int kPPThreads = 320;
 constexpr int kPPK = 2, kPPV = 2;  // K and V ring stages (32 KB each)
@@ -431,10 +431,11 @@ struct PPBars {
   uint8_t waited[kAttnAhead];
 };
 
-// (bound 512 threads: caps the registers at 128 per thread; launched with 320).  CAUSAL is a
-// template parameter so the non-causal kernel carries no mask code (registers are tight).
+// 152 registers x 320 threads = 48.6K of the SM's 64K: the rest stays free for the memcpy
+// kernels that carry the loopback K/V pushes (53.7K stalled them; 128 measured 3 % slower
+// causal).  CAUSAL is a template parameter so the non-causal kernel carries no mask code.
 template <bool CAUSAL>
-__global__ void __launch_bounds__(512, 1) attn_pp_kernel(const __grid_constant__ AttnArgs args) {
+__global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;  // tile 0 at +0, tile 1 at +kQBytes

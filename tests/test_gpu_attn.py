@@ -147,3 +147,22 @@ def test_sp_attn_per_rank_calls_on_separate_streams(ao, causal):
             ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=bool(causal))
             ok, e, f = on.check_tolerance(O[r].float().cpu().numpy(), ref, frob_rel=FROB)
             assert ok, f"per-rank attn causal={causal} it={it} r{r}: {e:.3e} {f:.3e}"
+
+
+@pytest.mark.parametrize("S,causal", [(256, 0), (256, 1), (128, 0)])
+def test_sp_attn_peaked_scores_rescale_and_underflow(ao, S, causal):
+    """Sharp softmax: q scaled by 6 and rank s's keys by (s + 1) / 2, so scaled scores reach
+    ~+-60 (the row max moves by more than the 2^8 lazy-rescale threshold between KV blocks
+    in ring order, and most exponentials underflow to 0 in the ftz exp2).  S = 128 runs
+    the one-tile kernel, S = 256 the ping-pong kernel."""
+    W, H = 4, 2
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=200 + S + causal)
+    Q = [(q.float() * 6.0).to(torch.bfloat16) for q in Q]
+    K = [(k.float() * (0.5 * (s + 1))).to(torch.bfloat16) for s, k in enumerate(K)]
+    ctxs, plans = _world(ao, W, H, S, S, SMS, causal=causal)
+    O = _run(ao, ctxs, plans, Q, K, V)
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    for r in range(W):
+        ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=bool(causal))
+        ok, e, f = on.check_tolerance(O[r].float().cpu().numpy(), ref, frob_rel=FROB)
+        assert ok, f"peaked S={S} causal={causal} rank {r}: {e:.3e} {f:.3e}"

@@ -205,6 +205,25 @@ ao_status ao_gemm_ar(ao_plan* plan, const void* A, const void* B, void* C, void*
 ao_status ao_gemm_ar_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
                            void* const* Cs, void* stream);
 
+/* ---- launch-level schedule of a group call (host-only; Q24) -------------------
+ * What ao_{ag_gemm,gemm_rs,gemm_ar}_group(n, plans, ...) would run on a device with
+ * `sm_count` SMs, as canonical JSON (sorted keys, no whitespace, integers only), written
+ * like ao_plan_export_json (min(cap, needed) bytes incl. NUL; *needed = size incl. NUL).
+ * plans: n plans (host-only ones suffice) in group order, equal hash; op: their ao_op
+ * (AG_GEMM, GEMM_RS or GEMM_AR).
+ *   {"mode":"space_sliced"}: each rank runs its own plan tables on its own CTAs;
+ *   {"mode":"time_sliced","n_total":T,"n_workers":w,"segments":[[rank,k0,k1,o],...],
+ *    "waits":[[worker,[[i,rank,g],...]],...]}: one global list of T tile positions --
+ *   positions [k0,k1) of rank's plan order at global indices [o, o+k1-k0); worker w runs
+ *   indices w, w+w_n, ... (Lst.1 persistent stride) and, before the tile at
+ *   global index i, acquires the flags of chunk g of `rank` (AG: a chunk from another
+ *   source that the tile's rows read; RS/AR: a chunk of the rank's own rows, from every
+ *   other source), once per (worker, rank, chunk) (minimal waits).
+ * Errors: AO_ERR_INVALID_ARG (bad n / op, or a group that cannot be co-resident: the
+ * same condition under which the launch fails), AO_ERR_PEER (plan hashes differ). */
+ao_status ao_group_schedule_export(int n, ao_plan* const* plans, int32_t op, int sm_count, char* buf, size_t cap,
+                                   size_t* needed);
+
 /* ---- A2A-GEMM (NEXT-3; P:437 / P:529 "A2A-GEMM"; BASELINE configs[3]) -------------------
  * Expert-parallel MoE dispatch fused with the expert GEMM: expert e lives on rank e
  * (W experts).  Rank s holds T = desc.M tokens X [T, K] bf16 and routing topk_idx [T, k]

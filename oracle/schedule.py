@@ -391,3 +391,85 @@ def sm_utilization(n_tiles, sm_count):
     """S:334: tile_count / (wave_count * sm_count)."""
     waves = math.ceil(n_tiles / sm_count)
     return n_tiles / (waves * sm_count)
+
+
+def group_schedule(descs, sm_count=148):
+    """Launch-level schedule of a group call over the ranks `descs` (group order), by
+    enumeration (Q24 -- one GPU standing in for W ranks).  Returns
+    {"mode": "space_sliced"} when the ranks' persistent CTAs fit side by side, the
+    time-sliced list otherwise, or None when the launch is refused (CTAs not co-resident).
+
+    Time-sliced: every worker serves every rank, walking one global list of (rank, plan
+    position) entries with Lst.1's persistent stride:
+      * AG -- rank after rank, each rank's plan order intact;
+      * RS / AR -- owner after owner; for owner o the positions of source ranks o+1, o+2,
+        ..., o+W-1 (the rotation) whose tile rows o owns, then o's own positions (its
+        tiles wait on every other source's contribution, so they come after them).
+    Waits: before each tile a worker acquires the chunks the tile's rows intersect
+    that it needs from peers -- AG: chunks of another source; RS: the own tile's chunks --
+    the first time the worker needs (rank, chunk)."""
+    plans = [plan(d, sm_count) for d in descs]
+    d0, p0 = descs[0], plans[0]
+    n, W = len(descs), d0["world_size"]
+    bm, _, cg = p0["tile"]
+    ctas = p0["n_cta"] * cg
+    is_ag = d0["op"] == "ag_gemm"
+    comm = is_ag and d0["backend"] != "ce" and W > 1
+    comm_ctas = d0["comm_ctas"] if comm else 0
+    if n * (ctas + comm_ctas) <= sm_count:
+        return {"mode": "space_sliced"}
+    if not (n > 1 and n == W and ctas <= sm_count and comm_ctas == 0 and (not is_ag or d0["dir"] == "push")):
+        return None
+    M, C = d0["M"], d0["chunk_rows"]
+    S = M // W
+    n_nb = _ceil_div(d0["N"], p0["tile"][1])
+    gi_of = {d["rank"]: gi for gi, d in enumerate(descs)}
+
+    def rows_of(gi, k):
+        t = plans[gi]["order"][k]
+        mb = t // n_nb
+        return range(mb * bm, min(M, (mb + 1) * bm))
+
+    seq = []
+    if is_ag:
+        for gi in range(n):
+            for k in range(len(plans[gi]["order"])):
+                seq.append((gi, k))
+    else:
+        if S % bm != 0:
+            return None
+        for o in range(W):
+            for step in list(range(1, W)) + [0]:
+                gi = gi_of[(o + step) % W]
+                for k in range(len(plans[gi]["order"])):
+                    if rows_of(gi, k)[0] // S == o:
+                        seq.append((gi, k))
+    segments = []
+    for i, (gi, k) in enumerate(seq):
+        if segments and segments[-1][0] == gi and segments[-1][2] == k:
+            segments[-1][2] = k + 1
+        else:
+            segments.append([gi, k, k + 1, i])
+    if len(segments) > 256:
+        return None
+    n_wk = ctas // cg
+    waits = []
+    for w in range(n_wk):
+        seen = set()
+        lst = []
+        for i in range(w, len(seq), n_wk):
+            gi, k = seq[i]
+            r = descs[gi]["rank"]
+            rows = rows_of(gi, k)
+            chunks = sorted({x // C for x in rows})
+            if is_ag:
+                need = [g for g in chunks if (g * C) // S != r]
+            else:
+                need = chunks if rows[0] // S == r else []
+            for g in need:
+                if (gi, g) not in seen:
+                    seen.add((gi, g))
+                    lst.append([i, r, g])
+        waits.append([w, lst])
+    return {"mode": "time_sliced", "n_total": len(seq), "n_workers": n_wk,
+            "segments": [[descs[gi]["rank"], k0, k1, o] for gi, k0, k1, o in segments], "waits": waits}

@@ -95,6 +95,9 @@ _SIGS = {
     "ao_gemm_rs_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p]),
     "ao_gemm_ar": (ctypes.c_int, [ctypes.c_void_p] * 5),
     "ao_gemm_ar_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 4 + [ctypes.c_void_p]),
+    "ao_group_schedule_export": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                                ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t,
+                                                ctypes.POINTER(ctypes.c_size_t)]),
     "ao_a2a_gemm": (ctypes.c_int, [ctypes.c_void_p] * 8),
     "ao_a2a_gemm_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 7 + [ctypes.c_void_p]),
     "ao_sp_attn": (ctypes.c_int, [ctypes.c_void_p] * 6),

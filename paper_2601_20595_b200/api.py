@@ -108,6 +108,18 @@ def plan_json(desc: dict, sm_count: int = 148) -> str:
         p.close()
 
 
+def group_schedule_json(plans, sm_count: int = 148) -> str:
+    """ao_group_schedule_export: the launch-level (time-sliced / space-sliced) schedule of a
+    group call over `plans` (host-only plans suffice)."""
+    arr = (ctypes.c_void_p * len(plans))(*[p.handle.value for p in plans])
+    op = N.OPS[plans[0].desc.get("op", "ag_gemm")]
+    need = ctypes.c_size_t(0)
+    check(lib().ao_group_schedule_export(len(plans), arr, op, sm_count, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(lib().ao_group_schedule_export(len(plans), arr, op, sm_count, buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
+
+
 # ------------------------------------------------------------------------- contexts
 class Context:
     def __init__(self, device: int, rank: int, world_size: int, workspace: int):

@@ -37,16 +37,36 @@ def needs_rebuild():
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    """Compiles every translation unit in parallel (one nvcc per file), then links."""
     if not force and not needs_rebuild():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     nvcc = nvcc_path()
-    cmd = [nvcc, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
-           "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-shared", "-I", INCLUDE, "-I", CSRC,
-           "-Xptxas", "-v" if os.environ.get("AO_PTXAS_VERBOSE") else "-O3",
-           "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    base = [nvcc, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
+            "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC,
+            "-Xptxas", "-v" if os.environ.get("AO_PTXAS_VERBOSE") else "-O3"]
+    extra = os.environ.get("AO_NVCC_FLAGS", "").split()
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src + ".o")
+        cmd = base + extra + ["-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.stderr:
+            sys.stderr.write(r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}")
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"] + objs
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

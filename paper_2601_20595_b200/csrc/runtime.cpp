@@ -813,6 +813,31 @@ static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArg
   return true;
 }
 
+// How a group launch is scheduled (shared by launch_group and ao_group_schedule_export):
+// sets ka->ctas_per_rank / comm_ctas_per_rank and, when the group runs time-sliced, the
+// segment list.  Fails when the persistent CTAs could not all be co-resident (H3).
+static ao_status group_schedule(int n, ao_plan* const* plans, int mode, int sm_count, ao::KernelArgs* ka,
+                                bool* time_sliced) {
+  const ao::HostPlan& h0 = plans[0]->hp;
+  const bool comm = mode == ao::MODE_AG && h0.desc.backend != AO_BACKEND_CE && h0.W > 1;
+  ka->ctas_per_rank = h0.n_cta * h0.tile.cg;
+  ka->comm_ctas_per_rank = comm ? h0.desc.comm_ctas : 0;
+  ka->n_seg = 0;
+  ka->n_total = 0;
+  *time_sliced = false;
+  const int64_t grid = int64_t(n) * (ka->ctas_per_rank + ka->comm_ctas_per_rank);
+  if (grid > sm_count && n > 1 && n == h0.W && ka->ctas_per_rank <= sm_count && ka->comm_ctas_per_rank == 0 &&
+      (mode == ao::MODE_RS || h0.desc.dir == AO_DIR_PUSH))
+    *time_sliced = build_segments(n, plans, mode, ka);
+  if (grid > sm_count && !*time_sliced)
+    return fail(AO_ERR_INVALID_ARG, "grid of %lld CTAs exceeds the %d SMs: the persistent CTAs would not be "
+                "co-resident (lower n_cta / comm_ctas; a whole-world loopback group of AG push, GEMM-RS or "
+                "GEMM-AR plans with n_cta <= SMs runs time-sliced)", (long long)grid, sm_count);
+  if (h0.tile.cg == 2 && (ka->comm_ctas_per_rank % 2) != 0)
+    return fail(AO_ERR_INVALID_ARG, "comm_ctas must be even with CTA-pair tiles (cluster launch)");
+  return AO_OK;
+}
+
 // ------------------------------------------------------------------------------ op calls
 static ao_status launch_group(int n, ao_plan* const* plans, const void* const* As, const void* const* Bs,
                               void* const* Cs, void* const* Gouts, void* stream_v, int op) {
@@ -862,21 +887,10 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
                                             : 0);
   const bool ce = mode == ao::MODE_AG && h0.desc.backend == AO_BACKEND_CE && h0.W > 1;
   const int comm = mode == ao::MODE_AG ? p0->comm_kind : ao::COMM_NONE;
-  ka->comm_ctas_per_rank = (comm != ao::COMM_NONE) ? h0.desc.comm_ctas : 0;
   bool time_sliced = false;
   {
-    // Persistent spin-waiting CTAs must all be co-resident (1 CTA per SM).
-    const int64_t grid = int64_t(n) * (ka->ctas_per_rank + ka->comm_ctas_per_rank);
-    if (grid > p0->ctx->sm_count && n > 1 && n == h0.W && ka->ctas_per_rank <= p0->ctx->sm_count &&
-        ka->comm_ctas_per_rank == 0 &&
-        (mode == ao::MODE_RS || h0.desc.dir == AO_DIR_PUSH))
-      time_sliced = build_segments(n, plans, mode, ka.get());
-    if (grid > p0->ctx->sm_count && !time_sliced)
-      return fail(AO_ERR_INVALID_ARG, "grid of %lld CTAs exceeds the %d SMs: the persistent CTAs would not be "
-                  "co-resident (lower n_cta / comm_ctas; a whole-world loopback group of AG push, GEMM-RS or "
-                  "GEMM-AR plans with n_cta <= SMs runs time-sliced)", (long long)grid, p0->ctx->sm_count);
-    if (h0.tile.cg == 2 && (ka->comm_ctas_per_rank % 2) != 0)
-      return fail(AO_ERR_INVALID_ARG, "comm_ctas must be even with CTA-pair tiles (cluster launch)");
+    ao_status s = group_schedule(n, plans, mode, p0->ctx->sm_count, ka.get(), &time_sliced);
+    if (s != AO_OK) return s;
   }
   // The epoch advances only once the op is actually enqueued (a failed call leaves every
   // ctx of the group at its previous epoch, so the world stays in step).
@@ -1304,6 +1318,82 @@ ao_status ao_gemm_rs(ao_plan* plan, const void* A, const void* B, void* C_shard,
 
 ao_status ao_gemm_ar(ao_plan* plan, const void* A, const void* B, void* C, void* stream) {
   return launch_group(1, &plan, &A, &B, &C, nullptr, stream, AO_OP_GEMM_AR);
+}
+
+// ------------------------------------------------------------- group schedule export
+// The launch-level schedule of a group call (Q24), canonical JSON:
+//   {"mode":"space_sliced"} -- every rank runs its own plan's tables on its own CTAs; or
+//   {"mode":"time_sliced","n_total":T,"n_workers":w,"segments":[[rank,k0,k1,o],...],
+//    "waits":[[worker,[[i,rank,g],...]],...]}
+// segments: positions [k0,k1) of `rank`'s tile order occupy global list indices
+// [o, o+k1-k0); worker w runs indices w, w+n_workers, ... (Lst.1 stride).
+// waits: per worker, in walk order, the (global index, rank, chunk) before whose tile the
+// worker acquires that chunk's flags -- the chunks the tile's rows intersect that
+// it needs from peers (AG: chunks of other sources; RS/AR: the own rows' chunks, from
+// every other source), once per (worker, rank, chunk).
+ao_status ao_group_schedule_export(int n, ao_plan* const* plans, int32_t op, int sm_count, char* buf, size_t cap,
+                                   size_t* needed) {
+  if (n < 1 || n > AO_MAX_WORLD || !plans) return fail(AO_ERR_INVALID_ARG, "bad group size %d", n);
+  for (int i = 0; i < n; ++i) {
+    if (!plans[i]) return fail(AO_ERR_INVALID_ARG, "null plan %d", i);
+    if (plans[i]->hp.hash != plans[0]->hp.hash) return fail(AO_ERR_PEER, "plan hash mismatch inside group");
+  }
+  const ao::HostPlan& h0 = plans[0]->hp;
+  if (h0.desc.op != op || !(op == AO_OP_AG_GEMM || op == AO_OP_GEMM_RS || op == AO_OP_GEMM_AR))
+    return fail(AO_ERR_INVALID_ARG, "op mismatch or op without a group schedule");
+  const int mode = op == AO_OP_AG_GEMM ? ao::MODE_AG : ao::MODE_RS;
+  std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
+  memset(ka.get(), 0, sizeof(ao::KernelArgs));
+  ka->n_group = n;
+  bool ts = false;
+  ao_status s = group_schedule(n, plans, mode, sm_count > 0 ? sm_count : 148, ka.get(), &ts);
+  if (s != AO_OK) return s;
+  std::string out;
+  if (!ts) {
+    out = "{\"mode\":\"space_sliced\"}";
+  } else {
+    const int n_wk = ka->ctas_per_rank / h0.tile.cg;
+    const int64_t BM = h0.tile.bm;
+    out = "{\"mode\":\"time_sliced\",\"n_total\":" + std::to_string(ka->n_total) +
+          ",\"n_workers\":" + std::to_string(n_wk) + ",\"segments\":[";
+    for (int i = 0; i < ka->n_seg; ++i) {
+      const ao::Seg& g = ka->seg[i];
+      out += (i ? ",[" : "[") + std::to_string(plans[g.g]->hp.rank) + "," + std::to_string(g.k0) + "," +
+             std::to_string(g.k1) + "," + std::to_string(g.o) + "]";
+    }
+    out += "],\"waits\":[";
+    for (int w = 0; w < n_wk; ++w) {
+      std::vector<std::vector<char>> got(n);
+      for (int i = 0; i < n; ++i) got[i].assign(plans[i]->hp.n_chunks, 0);
+      std::string lst;
+      int si = 0;
+      for (int i = w; i < ka->n_total; i += n_wk) {
+        while (i >= ka->seg[si].o + (ka->seg[si].k1 - ka->seg[si].k0)) ++si;
+        const int grp = ka->seg[si].g;
+        const ao::HostPlan& hp = plans[grp]->hp;
+        const int t = hp.order[ka->seg[si].k0 + (i - ka->seg[si].o)];
+        const int64_t r0 = int64_t(t / hp.n_nb) * BM, r1 = std::min<int64_t>(hp.M, r0 + BM);
+        const bool own_tile = r0 / hp.S == hp.rank;
+        if (mode == ao::MODE_RS && !own_tile) continue;
+        for (int g = int(r0 / hp.C); g <= int((r1 - 1) / hp.C); ++g) {
+          if (mode == ao::MODE_AG && (int64_t(g) * hp.C) / hp.S == hp.rank) continue;
+          if (got[grp][g]) continue;
+          got[grp][g] = 1;
+          lst += (lst.empty() ? "[" : ",[") + std::to_string(i) + "," + std::to_string(hp.rank) + "," +
+                 std::to_string(g) + "]";
+        }
+      }
+      out += (w ? ",[" : "[") + std::to_string(w) + ",[" + lst + "]]";
+    }
+    out += "]}";
+  }
+  if (needed) *needed = out.size() + 1;
+  if (buf && cap) {
+    const size_t k = std::min(cap - 1, out.size());
+    memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+  return AO_OK;
 }
 
 // ----------------------------------------------------------------------- plain GEMM entry

@@ -248,3 +248,57 @@ def test_bench_config_timesliced_fullsize(ao):
     for r in (0, 5, 7):
         ref = on.gemm_rs_rows(Cu64, Bd64, r, lrows)
         _check(Cd[r][torch.as_tensor(lrows)], ref, f"fullsize rs ts r{r}")
+
+
+@pytest.mark.parametrize("op", ["ag_gemm", "gemm_rs", "gemm_ar"])
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+@pytest.mark.parametrize("W", [2, 4])
+def test_timesliced_mma_order_matches_oracle(ao, op, tile, W, tmp_path):
+    """The time-sliced launch order executed on the device equals the oracle's enumeration
+    (oracle.schedule.group_schedule) tile for tile: the MMA trace gives each worker's tiles
+    in issue order, and worker w's m-th tile must be global list entry w + m * n_workers."""
+    import json
+
+    from oracle import schedule as osch
+    M, K, N, C = 256 * W, 256, 768, 64
+    desc = dict(op=op, world_size=W, M=M, N=N, K=K, chunk_rows=C, tile_m=tile[0], tile_n=tile[1], n_cta=SMS,
+                intra="grouped", group_m=2, backend="ldst" if op == "gemm_ar" else "ce",
+                rs_reduce="atomic" if op == "gemm_rs" else "slots", timeout_ns=2_000_000_000)
+    ctxs, plans = _world(ao, desc, W)
+    if op == "ag_gemm":
+        A, B = si.ag_inputs(W, M, K, N, salt=43)
+        run = lambda: _ag(ao, ctxs, plans, _dev(A), _dev(B))  # noqa: E731
+    else:
+        A, B = si.rs_inputs(W, M, K, N, salt=44)
+        if op == "gemm_rs":
+            run = lambda: _rs(ao, ctxs, plans, _dev(A), _dev(B))  # noqa: E731
+        else:
+            def run():
+                Cs = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+                ao.gemm_ar_group(plans, _dev(A), _dev(B), Cs)
+                torch.cuda.synchronize()
+    run()
+    ctxs[0].trace_enable(1 << 20)
+    run()
+    path = str(tmp_path / "ts_trace.json")
+    ctxs[0].trace_dump(path)
+    ctxs[0].trace_enable(0)
+    ev = [e for e in json.load(open(path))["traceEvents"] if e["cat"] == "mma"]
+    descs = [osch.default_desc(**{k: v for k, v in dict(desc, rank=r).items() if k != "timeout_ns"})
+             for r in range(W)]
+    sched = osch.group_schedule(descs, SMS)
+    assert sched["mode"] == "time_sliced"
+    # the library's own export says the same
+    hp = [ao.Plan(None, d, SMS) for d in descs]
+    assert ao.group_schedule_json(hp, SMS) == osch.export_json(sched)
+    orders = {d["rank"]: osch.plan(d, SMS)["order"] for d in descs}
+    seq = [(r, orders[r][k]) for r, k0, k1, o in sched["segments"] for k in range(k0, k1)]
+    nw, cg = sched["n_workers"], tile[0] // 128
+    got = {}
+    for cta in sorted({e["tid"] // 8 for e in ev}):
+        mine = sorted((e for e in ev if e["tid"] // 8 == cta), key=lambda e: e["ts"])
+        for m, e in enumerate(mine):
+            got[cta // cg + m * nw] = (e["pid"], int(e["name"].split()[1]))
+    assert len(got) == len(seq)
+    for i, want in enumerate(seq):
+        assert got[i] == want, (i, got[i], want)

@@ -46,10 +46,22 @@ import math
 # (BM, BN, cta_group).  Shared *specification* with the C++ planner (Q19);
 # each side types it independently.
 TILE_CANDIDATES = [(256, 256, 2), (256, 128, 2), (128, 256, 1), (128, 128, 1)]
+# Narrower CTA-pair widths (wave-quantization-free tiles for the per-GPU TP shapes, Q19),
+# built for AG with the copy-engine backend only.
+PAIR_TILES_AG_CE = [(256, 224, 2), (256, 208, 2), (256, 192, 2), (256, 160, 2), (256, 144, 2), (256, 112, 2)]
 # Relative mainloop efficiency (percent) of each candidate, measured on B200 with the plain
 # GEMM 8192x14336x4096 (profiles/r01: 1440 / 974 / 1275 / ~860 TFLOP/s).  Planner spec
 # constant shared with the C++ planner (Q19).
-TILE_EFF = {(256, 256, 2): 100, (256, 128, 2): 68, (128, 256, 1): 88, (128, 128, 1): 60}
+TILE_EFF = {(256, 256, 2): 100, (256, 128, 2): 68, (128, 256, 1): 88, (128, 128, 1): 60,
+            (256, 224, 2): 0, (256, 208, 2): 0, (256, 192, 2): 0, (256, 160, 2): 0, (256, 144, 2): 0,
+            (256, 112, 2): 0}  # 0 = explicit tile only (never picked automatically)
+
+
+def tile_candidates(desc):
+    """The shapes a desc may use (in planner order)."""
+    if desc["op"] == "ag_gemm" and desc["backend"] == "ce":
+        return TILE_CANDIDATES + PAIR_TILES_AG_CE
+    return list(TILE_CANDIDATES)
 
 BK = 64  # K-block of the mainloop (TMA 128-B swizzle => 64 bf16), DESIGN.md
 
@@ -112,11 +124,13 @@ def validate(desc, sm_count=148):
         v.append("n_cta")
     if desc["n_slices"] < 1 or desc["n_slices"] > 64:
         v.append("n_slices")
+    if desc.get("rs_wire", "fp32") == "bf16" and desc["op"] in ("gemm_rs", "gemm_ar"):
+        v.append("rs_wire bf16")  # DESIGN.md Q14: bf16 partials break the per-element bound
     if desc.get("rs_reduce", "slots") not in ("slots", "atomic"):
         v.append("rs_reduce")
     if (desc["tile_m"] == 0) != (desc["tile_n"] == 0):
         v.append("tile")
-    if desc["tile_m"] and (desc["tile_m"], desc["tile_n"]) not in [(a, b) for a, b, _ in TILE_CANDIDATES]:
+    if desc["tile_m"] and (desc["tile_m"], desc["tile_n"]) not in [(a, b) for a, b, _ in tile_candidates(desc)]:
         v.append("tile")
     if not v and pick_tile(desc, sm_count) is None:
         v.append("no tile shape fits")
@@ -135,9 +149,11 @@ def pick_tile(desc, sm_count):
     from fractions import Fraction
     W, M, N = desc["world_size"], desc["M"], desc["N"]
     S = M // W
-    cands = TILE_CANDIDATES
+    cands = tile_candidates(desc)
     if desc["tile_m"]:
-        cands = [c for c in TILE_CANDIDATES if (c[0], c[1]) == (desc["tile_m"], desc["tile_n"])]
+        cands = [c for c in cands if (c[0], c[1]) == (desc["tile_m"], desc["tile_n"])]
+    else:
+        cands = [c for c in cands if TILE_EFF[c] > 0]
     best = None
     for bm, bn, cg in cands:
         if S % bm != 0:
@@ -145,7 +161,7 @@ def pick_tile(desc, sm_count):
         n = max(1, n_workers(desc, sm_count) // cg)
         T = (M // bm) * _ceil_div(N, bn)
         waves = _ceil_div(T, n)
-        cost = Fraction(waves * (bm * bn // cg), TILE_EFF[(bm, bn, cg)])
+        cost = Fraction(waves * (bm * bn // cg), max(1, TILE_EFF[(bm, bn, cg)]))
         key = (-cost, bm * bn, bn)
         if best is None or key > best[0]:
             best = (key, (bm, bn, cg))

@@ -38,6 +38,25 @@ def _require_bf16_cuda(*ts):
             raise ValueError("operands must be contiguous bf16 CUDA tensors")
 
 
+def _expect(plan, **named):
+    """Shape and device of every operand against the plan's desc (the kernels take their
+    extents from the plan, so an undersized tensor would be read / written out of bounds)."""
+    dev = plan.ctx.device if plan.ctx is not None else None
+    for name, (t, shape) in named.items():
+        if t is None:
+            continue
+        if tuple(t.shape) != tuple(int(x) for x in shape):
+            raise AOError(1, f"{name}: shape {tuple(t.shape)} != {tuple(shape)} required by the plan")
+        if dev is not None and t.device.index != dev:
+            raise AOError(1, f"{name}: on cuda:{t.device.index}, the plan's ctx is on cuda:{dev}")
+
+
+def _op_shapes(plan):
+    d = plan.desc
+    W, M, N, K = int(d.get("world_size", 1)), int(d["M"]), int(d["N"]), int(d["K"])
+    return W, M, N, K
+
+
 # ----------------------------------------------------------------------------- plans
 def validate(desc: dict, sm_count: int = 148):
     d = make_desc(desc)
@@ -181,12 +200,16 @@ def dist_world(device: int, workspace: int, group=None):
 def ag_gemm(plan: Plan, A_shard, B, C, A_gathered_out=None, stream=None):
     """ao_ag_gemm: C[M, N] = concat_p(A_p) . B^T for this rank."""
     _require_bf16_cuda(A_shard, B, C, A_gathered_out)
+    W, M, N, K = _op_shapes(plan)
+    _expect(plan, A_shard=(A_shard, (M // W, K)), B=(B, (N, K)), C=(C, (M, N)), A_gathered_out=(A_gathered_out, (M, K)))
     check(lib().ao_ag_gemm(plan.handle, _ptr(A_shard), _ptr(B), _ptr(C), _ptr(A_gathered_out), _stream(stream)))
 
 
 def gemm_rs(plan: Plan, A, B, C_shard, stream=None):
     """ao_gemm_rs: C_shard[S, N] = (sum_s A_s . B_s^T)[rank rows]."""
     _require_bf16_cuda(A, B, C_shard)
+    W, M, N, K = _op_shapes(plan)
+    _expect(plan, A=(A, (M, K)), B=(B, (N, K)), C_shard=(C_shard, (M // W, N)))
     check(lib().ao_gemm_rs(plan.handle, _ptr(A), _ptr(B), _ptr(C_shard), _stream(stream)))
 
 
@@ -194,6 +217,8 @@ def gemm_ar(plan: Plan, A, B, C, stream=None):
     """ao_gemm_ar (NEXT-1): C[M, N] = sum_s A_s . B_s^T on every rank (partition-based
     AllReduce fused with the GEMM)."""
     _require_bf16_cuda(A, B, C)
+    W, M, N, K = _op_shapes(plan)
+    _expect(plan, A=(A, (M, K)), B=(B, (N, K)), C=(C, (M, N)))
     check(lib().ao_gemm_ar(plan.handle, _ptr(A), _ptr(B), _ptr(C), _stream(stream)))
 
 
@@ -204,12 +229,25 @@ def _require_i32_cuda(*ts):
             raise AOError(1, "index arrays must be contiguous int32 CUDA tensors")
 
 
+def _a2a_expect(plan, X, topk_idx, B, Y, route_pos, recv_rows):
+    W, T, N, K = _op_shapes(plan)
+    k = int(plan.desc.get("topk", 0))
+    _expect(plan, X=(X, (T, K)), topk_idx=(topk_idx, (T, k)), B=(B, (N, K)), Y=(Y, (W * T, N)),
+            route_pos=(route_pos, (T, k)), recv_rows=(recv_rows, (1,)))
+
+
+def _attn_expect(plan, Q, K, V, O):
+    _, S, H, D = _op_shapes(plan)
+    _expect(plan, Q=(Q, (H, S, D)), K=(K, (H, S, D)), V=(V, (H, S, D)), O=(O, (H, S, D)))
+
+
 def a2a_gemm(plan: Plan, X, topk_idx, B, Y, route_pos, recv_rows, stream=None):
     """ao_a2a_gemm (NEXT-3): MoE All-to-All dispatch fused with the expert GEMM.  X [T, K]
     bf16 tokens, topk_idx [T, k] int32 experts, B [N, K] this rank's expert; Y [W*T, N]
     (rows [0, recv_rows) valid), route_pos [T, k] int32, recv_rows [1] int32."""
     _require_bf16_cuda(X, B, Y)
     _require_i32_cuda(topk_idx, route_pos, recv_rows)
+    _a2a_expect(plan, X, topk_idx, B, Y, route_pos, recv_rows)
     check(lib().ao_a2a_gemm(plan.handle, _ptr(X), _ptr(topk_idx), _ptr(B), _ptr(Y), _ptr(route_pos),
                             _ptr(recv_rows), _stream(stream)))
 
@@ -218,6 +256,8 @@ def a2a_gemm_group(plans, Xs, topk_idxs, Bs, Ys, route_pos, recv_rows, stream=No
     """ao_a2a_gemm_group: one launch pair (prep + fused) for co-located ranks (loopback)."""
     _require_bf16_cuda(*Xs, *Bs, *Ys)
     _require_i32_cuda(*topk_idxs, *route_pos, *recv_rows)
+    for i, p in enumerate(plans):
+        _a2a_expect(p, Xs[i], topk_idxs[i], Bs[i], Ys[i], route_pos[i], recv_rows[i])
     check(lib().ao_a2a_gemm_group(len(plans), _plans(plans), _arr(Xs), _arr(topk_idxs), _arr(Bs), _arr(Ys),
                                   _arr(route_pos), _arr(recv_rows), _stream(stream)))
 
@@ -226,12 +266,15 @@ def sp_attn(plan: Plan, Q, K, V, O, stream=None):
     """ao_sp_attn (NEXT-4): O = softmax(Q K_all^T / sqrt(128)) V_all per head; Q/K/V/O
     [H, S_loc, 128] bf16, K/V gathered from all ranks in ring (arrival) order."""
     _require_bf16_cuda(Q, K, V, O)
+    _attn_expect(plan, Q, K, V, O)
     check(lib().ao_sp_attn(plan.handle, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _stream(stream)))
 
 
 def sp_attn_group(plans, Qs, Ks, Vs, Os, stream=None):
     """ao_sp_attn_group: one launch for co-located ranks (loopback)."""
     _require_bf16_cuda(*Qs, *Ks, *Vs, *Os)
+    for i, p in enumerate(plans):
+        _attn_expect(p, Qs[i], Ks[i], Vs[i], Os[i])
     check(lib().ao_sp_attn_group(len(plans), _plans(plans), _arr(Qs), _arr(Ks), _arr(Vs), _arr(Os),
                                  _stream(stream)))
 
@@ -249,16 +292,26 @@ def ag_gemm_group(plans, A_shards, Bs, Cs, A_gathered_outs=None, stream=None):
     _require_bf16_cuda(*A_shards, *Bs, *Cs)
     n = len(plans)
     gouts = A_gathered_outs if A_gathered_outs is not None else [None] * n
+    for i, p in enumerate(plans):
+        W, M, N, K = _op_shapes(p)
+        _expect(p, A_shard=(A_shards[i], (M // W, K)), B=(Bs[i], (N, K)), C=(Cs[i], (M, N)),
+                A_gathered_out=(gouts[i], (M, K)))
     check(lib().ao_ag_gemm_group(n, _plans(plans), _arr(A_shards), _arr(Bs), _arr(Cs), _arr(gouts), _stream(stream)))
 
 
 def gemm_rs_group(plans, As, Bs, C_shards, stream=None):
     _require_bf16_cuda(*As, *Bs, *C_shards)
+    for i, p in enumerate(plans):
+        W, M, N, K = _op_shapes(p)
+        _expect(p, A=(As[i], (M, K)), B=(Bs[i], (N, K)), C_shard=(C_shards[i], (M // W, N)))
     check(lib().ao_gemm_rs_group(len(plans), _plans(plans), _arr(As), _arr(Bs), _arr(C_shards), _stream(stream)))
 
 
 def gemm_ar_group(plans, As, Bs, Cs, stream=None):
     _require_bf16_cuda(*As, *Bs, *Cs)
+    for i, p in enumerate(plans):
+        W, M, N, K = _op_shapes(p)
+        _expect(p, A=(As[i], (M, K)), B=(Bs[i], (N, K)), C=(Cs[i], (M, N)))
     check(lib().ao_gemm_ar_group(len(plans), _plans(plans), _arr(As), _arr(Bs), _arr(Cs), _stream(stream)))
 
 
@@ -268,6 +321,9 @@ def gemm(A, B, C=None, tile_n: int = 0, tile_m: int = 0, stream=None):
     if C is None:
         C = torch.empty(A.shape[0], B.shape[0], dtype=torch.bfloat16, device=A.device)
     _require_bf16_cuda(A, B, C)
+    if A.shape[1] != B.shape[1] or tuple(C.shape) != (A.shape[0], B.shape[0]) or not (A.device == B.device == C.device):
+        raise AOError(1, f"gemm: A {tuple(A.shape)}, B {tuple(B.shape)}, C {tuple(C.shape)} (need A [M,K], B [N,K], "
+                         "C [M,N] on one device)")
     check(lib().ao_gemm(A.device.index, _ptr(A), _ptr(B), _ptr(C), A.shape[0], B.shape[0], A.shape[1], tile_m,
                         tile_n, _stream(stream)))
     return C
@@ -279,6 +335,10 @@ def gemm_batched(As, Bs, Cs, tile_m: int = 0, tile_n: int = 0, group_m: int = 0,
     _require_bf16_cuda(*As, *Bs, *Cs)
     M, K = As[0].shape
     N = Bs[0].shape[0]
+    for a, b, c in zip(As, Bs, Cs):
+        if tuple(a.shape) != (M, K) or tuple(b.shape) != (N, K) or tuple(c.shape) != (M, N) or \
+                not (a.device == b.device == c.device == As[0].device):
+            raise AOError(1, "gemm_batched: every problem must be A [M,K], B [N,K], C [M,N] of one shape on one device")
     check(lib().ao_gemm_batched(As[0].device.index, len(As), _arr(As), _arr(Bs), _arr(Cs), M, N, K, tile_m, tile_n,
                                 group_m, n_cta, _stream(stream)))
     return Cs

@@ -50,7 +50,28 @@ __global__ void __launch_bounds__(kPrepThreads) a2a_prep_kernel(const __grid_con
   for (int base = 0; base < T; base += kPrepThreads) {
     const int t = base + tid;
     int ids[AO_MAX_WORLD];
-    for (int j = 0; j < k; ++j) ids[j] = t < T ? R.topk_idx[int64_t(t) * k + j] : -1;
+    for (int j = 0; j < k; ++j) {
+      // the ABI requires k distinct expert ids in [0, W): an out-of-range or repeated id is
+      // reported (AO_ERR_INVALID_ARG through the error record) and that entry is dropped
+      // (route_pos = -1) instead of indexing out of bounds
+      int id = t < T ? R.topk_idx[int64_t(t) * k + j] : -1;
+      bool bad = t < T && (id < 0 || id >= W);
+      for (int jj = 0; jj < j && !bad && t < T; ++jj) bad = id == ids[jj];
+      if (bad) {
+        if (atomicCAS(&a.err->claim, 0u, 1u) == 0u) {
+          a.err->rank = R.rank;
+          a.err->cta = kErrBadRouting;
+          a.err->chunk = t;
+          a.err->epoch = uint32_t(j);
+          a.err->seen = uint32_t(id);
+          __threadfence_system();
+          st_release_sys(const_cast<uint32_t*>(&a.err->flag), 1u);
+        }
+        R.lpos[int64_t(t) * k + j] = -1;
+        id = -1;
+      }
+      ids[j] = id;
+    }
     for (int e = 0; e < W; ++e) {
       int jj = -1;
       for (int j = 0; j < k; ++j)
@@ -96,10 +117,15 @@ __global__ void __launch_bounds__(kPrepThreads) a2a_prep_kernel(const __grid_con
   __syncthreads();
   // 4. route positions and the received row count
   for (int x = tid; x < T * k; x += kPrepThreads) {
+    const int lp = R.lpos[x];
+    if (lp < 0) {  // dropped (invalid) routing entry
+      R.route_pos[x] = -1;
+      continue;
+    }
     const int e = R.topk_idx[x];
     int base = 0;
     for (int q = 0; q < R.rank; ++q) base += tab[q][e];
-    R.route_pos[x] = base + R.lpos[x];
+    R.route_pos[x] = base + lp;
   }
   if (tid == 0) {
     int r = 0;

@@ -55,7 +55,9 @@ struct Cfg {
   static constexpr int kStageB = (BN / CG) * kBK * 2;
   static constexpr int kStage = kStageA + kStageB;
   static constexpr int kStages = BUDGET / kStage;
-  static constexpr int kTmemCols = 2 * BN;
+  // two accumulators of BN fp32 columns; tcgen05.alloc takes a power of two >= 32
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static_assert(BN % (8 * CG) == 0 && BN <= 256 && BN >= 16, "tile N: multiple of 8 * cta_group, at most 256");
   static constexpr int kBM = kSubM * CG;
 };
 
@@ -570,6 +572,7 @@ __device__ __noinline__ void a2a_push_chunk_tma(const A2ASched& sm, const RankAr
 template <int BN, int MODE, int COMM, int CG>
 __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 : kThreads, 1)
     fused_kernel(const __grid_constant__ KernelArgs args) {
+  static_assert((MODE != MODE_RS && MODE != MODE_A2A) || BN % 32 == 0, "RS / A2A epilogues step 32 columns");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -1126,7 +1129,9 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
           stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         __syncwarp();
         const int c = lane & 7;
-        const bool ok = col0 + c * EPS < N;  // N % 8 == 0: a segment is all-valid or all-out
+        // N % 8 == 0: a segment is all-valid or all-out; columns past this tile's BN (a
+        // BN that is not a multiple of the step) belong to the next tile and are not stored
+        const bool ok = col0 + c * EPS < N && (BN % CW == 0 || cc + c * EPS < BN);
         char* colp = dst_base + (col0 + c * EPS) * EB;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -1365,6 +1370,15 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   return e;
 }
 
+// Extra CTA-pair tile widths (Q19: wave-quantization-free tiles for the per-GPU
+// TP shapes): plain GEMM and AG with copy-engine transfers only.
+template <int BN>
+cudaError_t launch_bn_pair_extra(const KernelArgs& args, int comm, cudaStream_t stream) {
+  if (args.mode == MODE_GEMM) return launch_one<BN, MODE_GEMM, COMM_NONE, 2>(args, stream);
+  if (args.mode == MODE_AG && comm == COMM_NONE) return launch_one<BN, MODE_AG, COMM_NONE, 2>(args, stream);
+  return cudaErrorInvalidValue;
+}
+
 template <int BN, int CG>
 cudaError_t launch_bn(const KernelArgs& args, int comm, cudaStream_t stream) {
   switch (args.mode) {
@@ -1385,8 +1399,16 @@ cudaError_t launch_bn(const KernelArgs& args, int comm, cudaStream_t stream) {
 
 cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream) {
   if (cg == 2) {
-    if (bn == 256) return launch_bn<256, 2>(args, comm, stream);
-    if (bn == 128) return launch_bn<128, 2>(args, comm, stream);
+    switch (bn) {
+      case 256: return launch_bn<256, 2>(args, comm, stream);
+      case 128: return launch_bn<128, 2>(args, comm, stream);
+      case 224: return launch_bn_pair_extra<224>(args, comm, stream);
+      case 208: return launch_bn_pair_extra<208>(args, comm, stream);
+      case 192: return launch_bn_pair_extra<192>(args, comm, stream);
+      case 160: return launch_bn_pair_extra<160>(args, comm, stream);
+      case 144: return launch_bn_pair_extra<144>(args, comm, stream);
+      case 112: return launch_bn_pair_extra<112>(args, comm, stream);
+    }
   } else {
     if (bn == 256) return launch_bn<256, 1>(args, comm, stream);
     if (bn == 128) return launch_bn<128, 1>(args, comm, stream);

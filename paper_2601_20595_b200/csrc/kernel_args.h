@@ -27,6 +27,10 @@ constexpr uint32_t kA2ATailWords = 128;
 constexpr uint32_t kA2ACountFlags = kFlagWordsPerParity - kA2ATailWords;
 enum CommKind : int { COMM_NONE = 0, COMM_TMA = 1, COMM_LDST = 2 };
 
+// ErrorInfo.cta value of an A2A prep record: an invalid routing entry (chunk = token,
+// epoch = choice j, seen = the id) rather than a spin timeout.
+constexpr int32_t kErrBadRouting = -101;
+
 // Host-mapped record of the first device-side spin timeout.
 struct ErrorInfo {
   volatile uint32_t flag;   // published (set after the fields below are written)

@@ -9,10 +9,16 @@
 
 namespace ao {
 
-const TileShape kTileCandidates[] = {{256, 256, 2}, {256, 128, 2}, {128, 256, 1}, {128, 128, 1}};
-// Relative mainloop efficiency (percent) per candidate, measured on B200 (plain GEMM
-// 8192x14336x4096; Q19).
-static const int kTileEff[] = {100, 68, 88, 60};
+// The first four shapes run every op; the narrower CTA-pair widths after them (wave-
+// quantization-free tiles for the per-GPU TP shapes) are built for AG with copy-engine
+// transfers (and the plain GEMM, which plans as a one-rank AG) only.
+const TileShape kTileCandidates[] = {{256, 256, 2}, {256, 128, 2}, {128, 256, 1}, {128, 128, 1},
+                                     {256, 224, 2}, {256, 208, 2}, {256, 192, 2}, {256, 160, 2},
+                                     {256, 144, 2}, {256, 112, 2}};
+constexpr int kNumAllOpTiles = 4;
+// Relative mainloop efficiency (percent) per candidate, measured on B200 (Q19);
+// 0 = never picked automatically (explicit tile only).
+static const int kTileEff[] = {100, 68, 88, 60, 0, 0, 0, 0, 0, 0};
 const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[0]);
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -31,6 +37,11 @@ static const char* chunk_order_name(int o) { return o == AO_CHUNK_SHARD_MAJOR ? 
 static const char* intra_name(int i) { return i == AO_INTRA_ROW ? "row" : (i == AO_INTRA_COL ? "col" : "grouped"); }
 
 static int workers(const ao_plan_desc& d, int sm_count) { return d.n_cta > 0 ? d.n_cta : sm_count - d.comm_ctas; }
+
+// Candidate i exists for this desc's op / backend (the narrow pair widths: AG + CE only).
+static bool tile_allowed(const ao_plan_desc& d, int i) {
+  return i < kNumAllOpTiles || (d.op == AO_OP_AG_GEMM && d.backend == AO_BACKEND_CE);
+}
 
 std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   std::vector<std::string> v;
@@ -93,12 +104,15 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   if (d.n_cta < 0) v.push_back("n_cta");
   if (d.n_slices < 1 || d.n_slices > 64) v.push_back("n_slices");
   if (d.rs_wire != AO_WIRE_FP32 && d.rs_wire != AO_WIRE_BF16) v.push_back("rs_wire");
+  // the bf16 partial wire breaks the per-element bound (Q14) and is not built:
+  // rejected for every op that has partials, so validate, create and the hash agree
+  if (d.rs_wire == AO_WIRE_BF16 && (d.op == AO_OP_GEMM_RS || d.op == AO_OP_GEMM_AR)) v.push_back("rs_wire bf16");
   if (d.rs_reduce != AO_RS_SLOTS && d.rs_reduce != AO_RS_ATOMIC) v.push_back("rs_reduce");
   if ((d.tile_m == 0) != (d.tile_n == 0)) v.push_back("tile");
   if (d.tile_m != 0) {
     bool ok = false;
     for (int i = 0; i < kNumTileCandidates; ++i)
-      if (kTileCandidates[i].bm == d.tile_m && kTileCandidates[i].bn == d.tile_n) ok = true;
+      if (kTileCandidates[i].bm == d.tile_m && kTileCandidates[i].bn == d.tile_n && tile_allowed(d, i)) ok = true;
     if (!ok) v.push_back("tile");
   }
   if (v.empty()) {
@@ -116,7 +130,7 @@ bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
     // the tile grid is routing-dependent: explicit tile, else the largest candidate that
     // divides the receive capacity W*T (row blocks never straddle its end)
     const int64_t cap = int64_t(d.world_size) * d.M;
-    for (int i = 0; i < kNumTileCandidates; ++i) {
+    for (int i = 0; i < kNumAllOpTiles; ++i) {
       const TileShape c = kTileCandidates[i];
       if (d.tile_m != 0 && !(c.bm == d.tile_m && c.bn == d.tile_n)) continue;
       if (cap % c.bm != 0) continue;
@@ -130,12 +144,14 @@ bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
   int64_t best_num = 0, best_eff = 1, best_area = -1, best_bn = -1;
   for (int i = 0; i < kNumTileCandidates; ++i) {
     const TileShape c = kTileCandidates[i];
+    if (!tile_allowed(d, i)) continue;
     if (d.tile_m != 0 && !(c.bm == d.tile_m && c.bn == d.tile_n)) continue;
+    if (d.tile_m == 0 && kTileEff[i] == 0) continue;
     if (S % c.bm != 0) continue;
     const int64_t n = std::max(1, workers(d, sm_count) / c.cg);
     const int64_t T = (d.M / c.bm) * ceil_div(d.N, c.bn);
     const int64_t num = ceil_div(T, n) * (int64_t(c.bm) * c.bn / c.cg);  // cost = num / eff
-    const int64_t eff = kTileEff[i];
+    const int64_t eff = kTileEff[i] > 0 ? kTileEff[i] : 1;
     const int64_t area = int64_t(c.bm) * c.bn;
     bool better;
     if (!have) {

@@ -15,6 +15,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -55,17 +57,22 @@ using ao::kFlagWordsPerParity;  // 1 MiB of u32 per parity (kernel_args.h)
 constexpr size_t kCounterWords = size_t(1) << 16;
 constexpr uint32_t kBlobMagic = 0x414f5648u;  // "AOVH"
 constexpr size_t kMaxCeGraphs = 16;
+constexpr size_t kControlBytes = 4096;
+constexpr size_t kAnnounceOff = 256;
+constexpr uint32_t kAnnounceSlots = 64;
 
 // ------------------------------------------------------------------ driver entry points
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 
 struct DriverFns {
   PFN_encodeTiled encode = nullptr;
   PFN_writeValue32 write32 = nullptr;
   PFN_writeValue32 wait32 = nullptr;  // cuStreamWaitValue32 (same signature)
+  PFN_batchMemOp batch = nullptr;     // cuStreamBatchMemOp
 };
 
 ao_status get_driver(DriverFns** out) {
@@ -87,22 +94,42 @@ ao_status get_driver(DriverFns** out) {
     AO_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q));
     if (!p) return fail(AO_ERR_CUDA, "cuStreamWaitValue32 not found");
     fns.wait32 = reinterpret_cast<PFN_writeValue32>(p);
+    p = nullptr;
+    AO_CUDA(cudaGetDriverEntryPoint("cuStreamBatchMemOp", &p, cudaEnableDefault, &q));
+    if (!p) return fail(AO_ERR_CUDA, "cuStreamBatchMemOp not found");
+    fns.batch = reinterpret_cast<PFN_batchMemOp>(p);
     loaded = true;
   }
   *out = &fns;
   return AO_OK;
 }
 
-uint64_t host_id() {
-  char h[256] = {0};
-  gethostname(h, sizeof h - 1);
-  return ao::fnv1a64(std::string(h));
+// Random per-process identity, drawn once at first use: a peer handle is mapped directly
+// (same address space) only when its token equals ours; pid + hostname can collide across
+// PID namespaces that share a hostname.
+struct ProcessToken {
+  uint64_t a = 0, b = 0;
+};
+const ProcessToken& process_token() {
+  static ProcessToken t = [] {
+    ProcessToken x;
+    FILE* f = fopen("/dev/urandom", "rb");
+    bool ok = f && fread(&x, sizeof x, 1, f) == 1;
+    if (f) fclose(f);
+    if (!ok || (x.a == 0 && x.b == 0)) {  // fallback: time, pid and an address
+      x.a = uint64_t(std::chrono::high_resolution_clock::now().time_since_epoch().count()) ^ uint64_t(getpid()) << 32;
+      x.b = reinterpret_cast<uintptr_t>(&x) ^ 0x9E3779B97F4A7C15ull;
+    }
+    return x;
+  }();
+  return t;
 }
 
 struct Blob {
   uint32_t magic, version;
   int32_t pid, device, rank, world;
-  uint64_t data_half, total, raw_ptr, host;
+  uint64_t data_half, total, raw_ptr;
+  ProcessToken token;
   cudaIpcMemHandle_t ipc;
 };
 static_assert(sizeof(Blob) <= AO_HANDLE_BYTES, "blob too large");
@@ -140,17 +167,27 @@ struct ao_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
 
+  cudaStream_t ctl = nullptr;          // control-page copies (non-blocking: never behind an op)
+  uint64_t* ctl_host = nullptr;        // pinned staging for control-page copies
+  uint32_t announce_seq = 0;           // plans announced so far (collective order)
+
   size_t acc_half = 0;  // RS ATOMIC accumulator per parity (kept all-zero between uses)
   char* data(int q, uint32_t parity) const { return peer_base[q] + parity * data_half; }
   char* acc(int q, uint32_t parity) const { return peer_base[q] + 2 * data_half + parity * acc_half; }
   uint32_t* flags(int q, uint32_t parity) const {
     return reinterpret_cast<uint32_t*>(peer_base[q] + 2 * data_half + 2 * acc_half + parity * kFlagWordsPerParity * 4);
   }
+  // Control page of rank q (kControlBytes, after both flag parities): word 0 = the last
+  // epoch whose op completed on q (stream-written after each op); from byte kAnnounceOff,
+  // kAnnounceSlots {tag, plan hash} pairs (collective plan-hash agreement).
+  char* control(int q) const { return peer_base[q] + 2 * data_half + 2 * acc_half + 2 * kFlagWordsPerParity * 4; }
+  uint32_t* done_word(int q) const { return reinterpret_cast<uint32_t*>(control(q)); }
 };
 
 struct ao_plan {
   ao::HostPlan hp;
   ao_ctx* ctx = nullptr;
+  bool announced = false;  // plan hash published and compared with the peers
   int device = -1;
   char* d_tables = nullptr;
   const int* d_order = nullptr;
@@ -311,6 +348,10 @@ ao_status take_async_error(ao_ctx* ctx) {
     const ao::ErrorInfo e = *ctx->err_host;
     ctx->err_host->flag = 0;
     ctx->err_host->claim = 0;
+    if (e.cta == ao::kErrBadRouting)
+      return fail(AO_ERR_INVALID_ARG, "a2a_gemm: rank %d token %d choice %u has expert id %d: topk_idx must hold "
+                  "k distinct ids in [0, world_size) (the entry was dropped, route_pos = -1)", e.rank, e.chunk,
+                  e.epoch, int(e.seen));
     return fail(AO_ERR_TIMEOUT, "device spin-wait timed out: rank %d cta %d chunk %d epoch %u (flag held %u)", e.rank,
                 e.cta, e.chunk, e.epoch, e.seen);
   }
@@ -561,10 +602,12 @@ ao_status ao_ctx_create(int device, int rank, int world_size, size_t workspace_b
   // RS ATOMIC accumulator: an owner's [S, N] fp32 is 1/W of the slots an RS plan of the
   // same shape needs, so data_half / W always suffices.
   c->acc_half = (c->data_half / world_size + 4095) / 4096 * 4096;
-  c->total = 2 * c->data_half + 2 * c->acc_half + 2 * kFlagWordsPerParity * 4;
+  c->total = 2 * c->data_half + 2 * c->acc_half + 2 * kFlagWordsPerParity * 4 + kControlBytes;
   cudaError_t e = cudaMalloc(&c->base, c->total);
   if (e != cudaSuccess) return fail(AO_ERR_OOM, "cudaMalloc(%zu): %s", c->total, cudaGetErrorString(e));
-  AO_CUDA(cudaMemset(c->base + 2 * c->data_half, 0, 2 * c->acc_half + 2 * kFlagWordsPerParity * 4));
+  AO_CUDA(cudaMemset(c->base + 2 * c->data_half, 0, 2 * c->acc_half + 2 * kFlagWordsPerParity * 4 + kControlBytes));
+  AO_CUDA(cudaStreamCreateWithFlags(&c->ctl, cudaStreamNonBlocking));
+  AO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->ctl_host), 64, cudaHostAllocDefault));
   AO_CUDA(cudaMalloc(&c->epoch_cell, 64));
   AO_CUDA(cudaMemset(c->epoch_cell, 0, 64));
   AO_CUDA(cudaMalloc(&c->counters, kCounterWords * 4));
@@ -595,7 +638,7 @@ ao_status ao_ctx_export_handle(ao_ctx* c, ao_handle_blob* out) {
   b.data_half = c->data_half;
   b.total = c->total;
   b.raw_ptr = reinterpret_cast<uint64_t>(c->base);
-  b.host = host_id();
+  b.token = process_token();
   AO_CUDA(cudaSetDevice(c->device));
   AO_CUDA(cudaIpcGetMemHandle(&b.ipc, c->base));
   memcpy(out->bytes, &b, sizeof b);
@@ -605,7 +648,7 @@ ao_status ao_ctx_export_handle(ao_ctx* c, ao_handle_blob* out) {
 ao_status ao_ctx_import_handles(ao_ctx* c, const ao_handle_blob* all) {
   if (!c || !all) return fail(AO_ERR_INVALID_ARG, "null argument");
   AO_CUDA(cudaSetDevice(c->device));
-  const uint64_t me = host_id();
+  const ProcessToken me = process_token();
   for (int q = 0; q < c->W; ++q) {
     if (q == c->rank) continue;
     Blob b;
@@ -615,7 +658,7 @@ ao_status ao_ctx_import_handles(ao_ctx* c, const ao_handle_blob* all) {
     if (b.data_half != c->data_half || b.total != c->total)
       return fail(AO_ERR_PEER, "handle %d: workspace size mismatch (%llu vs %llu)", q,
                   (unsigned long long)b.data_half, (unsigned long long)c->data_half);
-    if (b.pid == int32_t(getpid()) && b.host == me) {
+    if (b.token.a == me.a && b.token.b == me.b) {
       if (b.device != c->device) {
         cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
@@ -653,6 +696,8 @@ ao_status ao_ctx_destroy(ao_ctx* c) {
   if (c->trace) cudaFree(c->trace);
   if (c->trace_cursor) cudaFree(c->trace_cursor);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->ctl) cudaStreamDestroy(c->ctl);
+  if (c->ctl_host) cudaFreeHost(c->ctl_host);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   delete c;
@@ -727,8 +772,6 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
   if (ao::flag_words_needed(*d) > ao::kA2ACountFlags)
     return fail(AO_ERR_INVALID_ARG, "too many chunk flags (%zu)", ao::flag_words_needed(*d));
   if (size_t(p->hp.n_chunks) > kCounterWords) return fail(AO_ERR_INVALID_ARG, "too many chunks");
-  if (d->rs_wire != AO_WIRE_FP32 && d->op == AO_OP_GEMM_RS)
-    return fail(AO_ERR_UNSUPPORTED, "bf16 RS wire is not implemented (non-conforming, DESIGN.md Q14)");
   if (p->hp.is_a2a) {
     if (p->hp.n_mb > 128)
       return fail(AO_ERR_INVALID_ARG, "a2a_gemm: W*T / tile_m = %d row blocks exceeds 128", p->hp.n_mb);
@@ -743,6 +786,85 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
   return AO_OK;
 }
 
+
+// ------------------------------------------------------------- collective plan agreement
+// SURVEY.md §8(b) "Collective semantics": the first launch of a plan publishes its hash in
+// the rank's control page (slot = the ctx's announce sequence number mod kAnnounceSlots,
+// tagged seq + 1) and compares it with every peer's announcement of the same sequence
+// number -> AO_ERR_PEER on a mismatch.  Peers in other processes are waited for (bounded
+// by the plan's timeout; each first launch blocks until every peer announced, so no rank
+// runs more than one announcement ahead); co-located peers (same process, maybe called
+// later by this same thread) are compared only if they have already announced.
+static ao_status announce_plans(int n, ao_plan* const* plans) {
+  std::vector<int> todo;
+  std::vector<uint32_t> seq(n, 0);
+  for (int i = 0; i < n; ++i)
+    if (!plans[i]->announced) todo.push_back(i);
+  for (int i : todo) {  // publish every member of the group first
+    ao_ctx* c = plans[i]->ctx;
+    seq[i] = c->announce_seq++;
+    plans[i]->announced = true;
+    if (c->W == 1) continue;
+    c->ctl_host[0] = uint64_t(seq[i]) + 1;
+    c->ctl_host[1] = plans[i]->hp.hash;
+    AO_CUDA(cudaMemcpyAsync(c->control(c->rank) + kAnnounceOff + (seq[i] % kAnnounceSlots) * 16, c->ctl_host, 16,
+                            cudaMemcpyHostToDevice, c->ctl));
+    AO_CUDA(cudaStreamSynchronize(c->ctl));
+  }
+  for (int i : todo) {
+    ao_ctx* c = plans[i]->ctx;
+    const uint64_t tag = uint64_t(seq[i]) + 1, h = plans[i]->hp.hash;
+    const uint64_t tmo = plans[i]->hp.desc.timeout_ns ? plans[i]->hp.desc.timeout_ns : 5000000000ull;
+    for (int q = 0; q < c->W; ++q) {
+      if (q == c->rank) continue;
+      const char* src = c->control(q) + kAnnounceOff + (seq[i] % kAnnounceSlots) * 16;
+      const auto t0 = std::chrono::steady_clock::now();
+      while (true) {
+        AO_CUDA(cudaMemcpyAsync(c->ctl_host + 2, src, 16, cudaMemcpyDeviceToHost, c->ctl));
+        AO_CUDA(cudaStreamSynchronize(c->ctl));
+        if (c->ctl_host[2] == tag) {
+          if (c->ctl_host[3] != h)
+            return fail(AO_ERR_PEER,
+                        "collective plan mismatch: rank %d launches plan #%u with hash %016llx, rank %d with "
+                        "%016llx (every rank must issue the same ops with plans that differ only in rank)",
+                        c->rank, seq[i], (unsigned long long)h, q, (unsigned long long)c->ctl_host[3]);
+          break;
+        }
+        if (!c->peer_opened[q]) break;  // co-located peer that has not announced yet
+        const uint64_t el = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                         std::chrono::steady_clock::now() - t0).count());
+        if (el > tmo)
+          return fail(AO_ERR_TIMEOUT, "rank %d did not announce plan #%u within the timeout (collective op "
+                      "sequence out of step?)", q, seq[i]);
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+      }
+    }
+  }
+  return AO_OK;
+}
+
+// Done words: after every op, each rank of the launch records (stream-ordered, one batched
+// memop) the epoch whose op has now completed on it.  An op whose waits do not cover every
+// peer (causal SP attention: a rank waits only on lower ranks) cannot rely on the Q11
+// argument and waits on these before overwriting a peer's parity buffer.
+static ao_status mark_done(int n, ao_plan* const* plans, const std::vector<uint32_t>& epochs, cudaStream_t stream) {
+  if (plans[0]->hp.W == 1) return AO_OK;
+  DriverFns* drv = nullptr;
+  ao_status s = get_driver(&drv);
+  if (s != AO_OK) return s;
+  CUstreamBatchMemOpParams ops[AO_MAX_WORLD];
+  memset(ops, 0, sizeof ops);
+  for (int i = 0; i < n; ++i) {
+    ao_ctx* c = plans[i]->ctx;
+    ops[i].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    ops[i].writeValue.address = reinterpret_cast<CUdeviceptr>(c->done_word(c->rank));
+    ops[i].writeValue.value = epochs[i];
+    ops[i].writeValue.flags = 0;
+  }
+  CUresult r = drv->batch(stream, unsigned(n), ops, 0);
+  if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamBatchMemOp failed (%d)", int(r));
+  return AO_OK;
+}
 
 // ------------------------------------------------------------------ time-sliced groups
 // A whole-world loopback group whose plans each ask for more CTAs than SMs / n runs
@@ -864,6 +986,10 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
     if (s != AO_OK) return s;
   }
   AO_CUDA(cudaSetDevice(p0->ctx->device));
+  {
+    ao_status s = announce_plans(n, plans);
+    if (s != AO_OK) return s;
+  }
   if (h0.M == 0 || h0.N == 0) return AO_OK;
 
   std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
@@ -1023,6 +1149,10 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(e));
   for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
   if (ce) AO_CUDA(cudaStreamWaitEvent(stream, p0->ctx->ev_done, 0));
+  {
+    ao_status s = mark_done(n, plans, epochs, stream);
+    if (s != AO_OK) return s;
+  }
   // optional gathered-A output (bit-exact copy of concat_p A_p)
   if (mode == ao::MODE_AG && Gouts) {
     for (int i = 0; i < n; ++i) {
@@ -1067,6 +1197,10 @@ static ao_status launch_a2a(int n, ao_plan* const* plans, const void* const* Xs,
     if (s != AO_OK) return s;
   }
   AO_CUDA(cudaSetDevice(p0->ctx->device));
+  {
+    ao_status s = announce_plans(n, plans);
+    if (s != AO_OK) return s;
+  }
   std::unique_ptr<ao::KernelArgs> ka(new ao::KernelArgs());
   memset(ka.get(), 0, sizeof(ao::KernelArgs));
   ka->n_group = n;
@@ -1125,7 +1259,7 @@ static ao_status launch_a2a(int n, ao_plan* const* plans, const void* const* Xs,
     for (int i = 0; i < n; ++i) AO_CUDA(cudaMemsetAsync(recv_rows[i], 0, 4, stream));
   }
   for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
-  return AO_OK;
+  return mark_done(n, plans, epochs, stream);
 }
 
 ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs, const int32_t* const* topk_idxs,
@@ -1164,6 +1298,10 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
     if (s != AO_OK) return s;
   }
   AO_CUDA(cudaSetDevice(p0->ctx->device));
+  {
+    ao_status s = announce_plans(n, plans);
+    if (s != AO_OK) return s;
+  }
   const int W = h0.W, H = int(h0.N), S = int(h0.M), crows = h0.C, nch = h0.n_c;
   const int64_t rows = int64_t(H) * S, row_bytes = 256;  // [H*S_loc, 128] bf16
   std::unique_ptr<ao::AttnArgs> ka(new ao::AttnArgs());
@@ -1218,6 +1356,24 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
     if (s != AO_OK) return s;
     CUresult cr = drv->write32(c0->side, reinterpret_cast<CUdeviceptr>(c0->epoch_cell), epochs[0], 0);
     if (cr != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(cr));
+    // WAR on the destination's gathered K/V (parity e % 2, last read by its epoch e-2
+    // kernel).  Non-causal: every rank waits on every source, so a source at epoch e has
+    // seen the destination's e-1 pushes and the Q11 argument applies.  Causal: a rank waits
+    // only on lower ranks, so nothing else orders a source behind a higher destination --
+    // wait for that destination's done word (written after each of its attention kernels)
+    // to reach e-2.  Ranks of this launch are ordered by the stream already.
+    if (h0.desc.causal && epochs[0] > 2) {
+      for (int dst = 0; dst < W; ++dst) {
+        bool in_group = false;
+        for (int q = 0; q < n; ++q) in_group |= plans[q]->hp.rank == dst;
+        bool needed = false;  // some source of this launch pushes to dst (dst > src)
+        for (int q = 0; q < n; ++q) needed |= dst > plans[q]->hp.rank;
+        if (in_group || !needed) continue;
+        cr = drv->wait32(c0->side, reinterpret_cast<CUdeviceptr>(c0->done_word(dst)), epochs[0] - 2,
+                         0x0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+        if (cr != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", int(cr));
+      }
+    }
     std::vector<uintptr_t> key{uintptr_t(0xA77Eu), uintptr_t(par), uintptr_t(n), uintptr_t(ka->ts)};
     for (int i = 0; i < n; ++i) {
       key.push_back(reinterpret_cast<uintptr_t>(plans[i]));
@@ -1234,7 +1390,10 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
       for (int i = 0; i < n; ++i) {  // one chain per source rank in this group
         const int src = plans[i]->hp.rank;
         std::vector<int> dests;
-        for (int ds = 1; ds < W; ++ds) dests.push_back((src + ds) % W);  // ring rotation
+        for (int ds = 1; ds < W; ++ds) {  // ring rotation; causal: only higher ranks read src's shard
+          const int dst = (src + ds) % W;
+          if (!h0.desc.causal || dst > src) dests.push_back(dst);
+        }
         if (ka->ts) std::sort(dests.begin(), dests.end());              // destination-major
         std::vector<cudaGraphNode_t> prev;
         for (int dst : dests) {
@@ -1280,7 +1439,7 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
   }
   for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
   if (ce) AO_CUDA(cudaStreamWaitEvent(stream, c0->ev_done, 0));
-  return AO_OK;
+  return mark_done(n, plans, epochs, stream);
 }
 
 ao_status ao_sp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
@@ -1464,7 +1623,7 @@ ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* 
   if (n < 1 || n > AO_MAX_WORLD || !As || !Bs || !Cs) return fail(AO_ERR_INVALID_ARG, "bad batch size %d", n);
   const int bm = tile_m ? tile_m : (M % 256 == 0 ? 256 : 128);
   const int bn = tile_n ? tile_n : 256;
-  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256) || (bn != 128 && bn != 256) || M % bm != 0 ||
+  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256) || M % bm != 0 ||
       N % 8 != 0 || K % 8 != 0)
     return fail(AO_ERR_INVALID_ARG, "ao_gemm_batched needs M %% tile_m == 0, N %% 8 == 0, K %% 8 == 0");
   for (int i = 0; i < n; ++i)

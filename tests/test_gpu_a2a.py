@@ -216,3 +216,29 @@ def test_a2a_delays_are_safe_and_a_dropped_wait_is_caught(ao):
         ao.debug_set("delay_ns", 0)
     assert decode_ok(3)
 
+
+
+def test_a2a_invalid_routing_is_reported_not_read_out_of_bounds(ao):
+    """topk_idx entries outside [0, W) or repeated within a token are dropped by the prep
+    kernel (route_pos = -1, the token is not dispatched for that choice) and reported as
+    AO_ERR_INVALID_ARG by check_async; valid entries are routed as usual."""
+    W, T, H, N, k, C = 2, 256, 64, 256, 2, 32
+    X, idx, B = si.moe_inputs(W, T, H, N, topk=k, salt=71)
+    bad = [i.clone() for i in idx]
+    bad[0][5, 1] = 7           # out of range
+    bad[0][9, 1] = bad[0][9, 0]  # duplicate
+    bad[1][3, 0] = -1          # negative
+    ctxs, plans = _world(ao, W, T, H, N, k, C, False, tile_m=128, tile_n=128, n_cta=16)
+    Y = [torch.zeros((W * T, N), dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    rp = [torch.zeros((T, k), dtype=torch.int32, device="cuda") for _ in range(W)]
+    rr = [torch.zeros((1,), dtype=torch.int32, device="cuda") for _ in range(W)]
+    ao.a2a_gemm_group(plans, [x.cuda() for x in X], [i.cuda() for i in bad], [b.cuda() for b in B], Y, rp, rr)
+    torch.cuda.synchronize()
+    with pytest.raises(ao.AOError) as ei:
+        for c in ctxs:
+            c.check_async()
+    assert ei.value.status == "AO_ERR_INVALID_ARG"
+    assert int(rp[0][5, 1]) == -1 and int(rp[0][9, 1]) == -1 and int(rp[1][3, 0]) == -1
+    # the valid entries still received rows: total rows = valid (token, choice) pairs
+    n_valid = sum(int((b >= 0).sum()) for b in bad) - 2  # 7 and the duplicate dropped (-1 counted out already)
+    assert sum(int(r.item()) for r in rr) == n_valid

@@ -182,3 +182,35 @@ def test_sp_attn_bitwise_repeatable(ao, causal):
         again = _run(ao, ctxs, plans, Q, K, V)
         for r in range(W):
             assert torch.equal(first[r], again[r]), f"causal={causal} run {it} rank {r} differs"
+
+
+def test_sp_attn_causal_epochs_without_host_sync(ao):
+    """Causal ring attention, per-rank calls on separate streams, 4 epochs back to back
+    with different K/V each epoch and no host synchronisation in between.  A causal rank
+    waits only on lower ranks, so without the done-word ordering rank 0 (the shortest
+    kernels) could push epoch e+2's K/V into a higher rank's parity-(e % 2) buffer while
+    that rank's epoch-e kernel still reads it (Q11)."""
+    W, H, S, E = 3, 2, 256, 4
+    ctxs, plans = _world(ao, W, H, S, 256, 32, causal=1)
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    ins, outs = [], []
+    for e in range(E):
+        Q, K, V = si.attn_inputs(W, H, S, 128, salt=300 + e)
+        ins.append((Q, K, V))
+        dQ, dK, dV = [q.cuda() for q in Q], [k.cuda() for k in K], [v.cuda() for v in V]
+        outs.append(([torch.empty_like(q) for q in dQ], dQ, dK, dV))
+    torch.cuda.synchronize()
+    for e in range(E):  # collective order: every rank issues epoch e before epoch e+1
+        O, dQ, dK, dV = outs[e]
+        for r in range(W):
+            ao.sp_attn(plans[r], dQ[r], dK[r], dV[r], O[r], stream=streams[r])
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    for e in range(E):
+        Q, K, V = ins[e]
+        Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+        for r in range(W):
+            ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=True)
+            ok, el, fr = on.check_tolerance(outs[e][0][r].float().cpu().numpy(), ref, frob_rel=FROB)
+            assert ok, f"causal epoch {e} rank {r}: {el:.3e} {fr:.3e}"

@@ -81,7 +81,9 @@ def test_validation_agrees(ao):
              dict(M=0), dict(K=0), dict(world_size=9, M=9 * 128), dict(rank=2), dict(n_slices=0),
              dict(comm_ctas=200), dict(intra="grouped", group_m=0), dict(chunk_rows=12),
              dict(op="gemm_ar"), dict(op="gemm_ar", backend="ldst"), dict(op="gemm_ar", backend="ldst", dir="pull"),
-             dict(op="gemm_ar", backend="ldst", comm_ctas=4), dict(op="gemm_ar", backend="tma")]
+             dict(op="gemm_ar", backend="ldst", comm_ctas=4), dict(op="gemm_ar", backend="tma"),
+             dict(op="gemm_rs", rs_wire="bf16"), dict(op="gemm_ar", backend="ldst", rs_wire="bf16"),
+             dict(rs_wire="bf16")]
     for kw in cases:
         dd = osch.default_desc(**kw)
         ref_ok = not osch.validate(dd)

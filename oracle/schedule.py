@@ -49,12 +49,13 @@ TILE_CANDIDATES = [(256, 256, 2), (256, 128, 2), (128, 256, 1), (128, 128, 1)]
 # Narrower CTA-pair widths (wave-quantization-free tiles for the per-GPU TP shapes, Q19),
 # built for AG with the copy-engine backend only.
 PAIR_TILES_AG_CE = [(256, 224, 2), (256, 208, 2), (256, 192, 2), (256, 160, 2), (256, 144, 2), (256, 112, 2)]
-# Relative mainloop efficiency (percent) of each candidate, measured on B200 with the plain
-# GEMM 8192x14336x4096 (profiles/r01: 1440 / 974 / 1275 / ~860 TFLOP/s).  Planner spec
-# constant shared with the C++ planner (Q19).
-TILE_EFF = {(256, 256, 2): 100, (256, 128, 2): 68, (128, 256, 1): 88, (128, 128, 1): 60,
-            (256, 224, 2): 0, (256, 208, 2): 0, (256, 192, 2): 0, (256, 160, 2): 0, (256, 144, 2): 0,
-            (256, 112, 2): 0}  # 0 = explicit tile only (never picked automatically)
+# Relative mainloop efficiency (percent) of each candidate: the measurement record
+# profiles/r02_tile_eff.json "eff_pct" (scripts/measure_tile_eff.py on a B200: plain GEMM
+# with ~55 waves of the shape's own tiles, no ragged edge, relative to 256x256).  Planner
+# spec constant shared with the C++ planner (Q19); tests pin it to the record.
+TILE_EFF = {(256, 256, 2): 100, (256, 128, 2): 61, (128, 256, 1): 87, (128, 128, 1): 59,
+            (256, 224, 2): 94, (256, 208, 2): 82, (256, 192, 2): 85, (256, 160, 2): 74, (256, 144, 2): 68,
+            (256, 112, 2): 56}  # 0 would mean: explicit tile only (never picked automatically)
 
 
 def tile_candidates(desc):

@@ -16,9 +16,10 @@ const TileShape kTileCandidates[] = {{256, 256, 2}, {256, 128, 2}, {128, 256, 1}
                                      {256, 224, 2}, {256, 208, 2}, {256, 192, 2}, {256, 160, 2},
                                      {256, 144, 2}, {256, 112, 2}};
 constexpr int kNumAllOpTiles = 4;
-// Relative mainloop efficiency (percent) per candidate, measured on B200 (Q19);
-// 0 = never picked automatically (explicit tile only).
-static const int kTileEff[] = {100, 68, 88, 60, 0, 0, 0, 0, 0, 0};
+// Relative mainloop efficiency (percent) per candidate: profiles/r02_tile_eff.json
+// "eff_pct", written by scripts/measure_tile_eff.py on a B200 (plain GEMM, ~55 waves, no
+// ragged edge, vs the 2-CTA 256x256 tile; Q19).  0 = explicit tile only.
+static const int kTileEff[] = {100, 61, 87, 59, 94, 82, 85, 74, 68, 56};
 const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[0]);
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -15,6 +15,8 @@ import pytest
 
 from oracle import schedule as osch
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
@@ -252,22 +254,47 @@ def test_validation_rejects():
     assert osch.validate(_desc(M=0)) == []  # empty problem is valid (no tiles)
 
 
-def test_tile_heuristic_brute_force():
-    # AG@8 per rank (the real TP=8 shape: M=8192, N=1792) on 148 SMs: the estimated time
-    # waves * per-SM area / efficiency must pick the 256x256 CTA-pair tile (4 waves) over
-    # 256x128 (7 waves of a 0.68-efficient shape) -- recomputed here by brute force.
-    d = _desc(world_size=8, rank=0, M=8192, N=1792, K=4096, chunk_rows=128)
-    picked = osch.pick_tile(d, 148)
-    costs = {}
-    for (a, b, c) in osch.TILE_CANDIDATES:
-        n = 148 // c
-        T = (8192 // a) * (-(-1792 // b))
-        costs[(a, b, c)] = (-(-T // n)) * (a * b // c) / osch.TILE_EFF[(a, b, c)]
-    assert picked == min(costs, key=lambda k: (costs[k], -k[0] * k[1], -k[1]))
-    assert picked == (256, 256, 2)
-    # a one-wave problem: every candidate fits in one wave, so the per-SM work per tile
-    # over its efficiency decides (256x128 pair tile: 16384 / 68 < 16384 / 60 < 32768 / 100)
-    assert osch.pick_tile(_desc(world_size=2, M=512, N=512), 148) == (256, 128, 2)
+def test_tile_eff_is_the_measurement_record():
+    """TILE_EFF is typed from the committed measurement (scripts/measure_tile_eff.py ->
+    profiles/r02_tile_eff.json), not from the planner's own formula."""
+    rec = json.load(open(os.path.join(ROOT, "profiles", "r02_tile_eff.json")))["eff_pct"]
+    assert {f"{a}x{b}": v for (a, b, _), v in osch.TILE_EFF.items()} == rec
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "pick_tile.json")))
+    assert gold["eff_pct"] == rec
+
+
+def test_tile_heuristic_golden_picks():
+    """Hand-derived picks (tests/golden/pick_tile.json, each with its worked costs): wave
+    quantization weighted by the measured efficiency.  A changed efficiency,
+    candidate list or cost rule flips at least one of them."""
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "pick_tile.json")))
+    for case in gold["cases"]:
+        d = osch.default_desc(**case["desc"])
+        assert list(osch.pick_tile(d, case["sm_count"])) == case["pick"], case["name"]
+
+
+def test_tile_heuristic_is_wave_quantization_when_efficiencies_tie():
+    """With equal efficiencies the rule reduces to S:334: least waves x per-SM tile area,
+    i.e. the utilization argmax among shapes of equal area."""
+    saved = dict(osch.TILE_EFF)
+    try:
+        for k in osch.TILE_EFF:
+            osch.TILE_EFF[k] = 50
+        # AG@8: 256x224 (4 waves) vs 256x256 (4 waves): equal waves -> smaller area wins
+        d = osch.default_desc(op="ag_gemm", world_size=8, M=8192, N=1792, K=4096, chunk_rows=128)
+        picked = osch.pick_tile(d, 148)
+        def waves_of(c):
+            tiles = (8192 // c[0]) * ((1792 + c[1] - 1) // c[1])
+            n = 148 // c[2]
+            return (tiles + n - 1) // n
+        waves = {c: waves_of(c) for c in osch.tile_candidates(d)}
+        best = min(waves[c] * c[0] * c[1] // c[2] for c in waves)
+        assert waves[picked] * picked[0] * picked[1] // picked[2] == best
+        # S:334 numbers: 1024 tiles on 132 SMs -> 8 waves (utilization 0.9697)
+        assert osch.sm_utilization(1024, 132) == 1024 / 1056
+    finally:
+        osch.TILE_EFF.clear()
+        osch.TILE_EFF.update(saved)
 
 
 def test_export_is_canonical_and_deterministic():

@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--ar-chunk", type=int, default=256, help="GEMM-AR chunk rows")
     ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
     ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--tile", default="256x256", help="time-sliced AG / RS tile BMxBN (512x256: two CTA pairs "
+                    "sharing B by multicast)")
     ap.add_argument("--sched", default="time", choices=["time", "space"],
                     help="loopback group schedule: time-sliced (all SMs per rank) or space-sliced (SMs/W per rank)")
     ap.add_argument("--tokens", type=int, default=TOKENS)
@@ -168,8 +170,11 @@ def run_ours(args, rank, world, local_rank):
         ar_desc["n_cta"] = sms // W
         ag_desc["n_cta"] = rs_desc["n_cta"] = sms if args.sched == "time" else sms // W
         if args.sched == "time":
+            tm, tn = (int(x) for x in args.tile.split("x"))
             for d in (ag_desc, rs_desc):
-                d["tile_m"], d["tile_n"] = 256, 256
+                d["tile_m"], d["tile_n"] = tm, tn
+                if tm == 512:  # 4-CTA clusters: as many as fit the GPU at once
+                    d["n_cta"] = ao.device_query(local_rank, "cluster4_ctas")
     ws = max(ao.workspace_bytes(ag_desc), ao.workspace_bytes(rs_desc),
              0 if args.no_ar else ao.workspace_bytes(ar_desc))
     if loop:

@@ -106,7 +106,10 @@ typedef struct {
   int32_t chunk_order;  /* ao_chunk_order */
   int32_t intra;        /* ao_intra */
   int32_t group_m;      /* GROUP_M for AO_INTRA_GROUPED */
-  int32_t tile_m;       /* BM (0 = planner picks by wave-quantization utilization) */
+  int32_t tile_m;       /* BM (0 = planner picks by wave-quantization utilization).  Shapes:
+                           128x{128,256} (1 CTA), 256x{256,128} (CTA pair), 256x{224,208,192,160,
+                           144,112} (CTA pair; AG + CE only), 512x256 (two pairs sharing B by
+                           multicast; AG + CE, RS / AR atomic; needs n_cta) */
   int32_t tile_n;       /* BN (0 together with tile_m) */
   int32_t n_cta;        /* persistent GEMM CTAs (0 = SMs - comm_ctas) */
   int32_t comm_ctas;    /* TMA/LDST: 0 = co-located comm warps, >0 = dedicated comm CTAs */
@@ -290,6 +293,15 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
 ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* const* Bs, void* const* Cs,
                           int64_t M, int64_t N, int64_t K, int32_t tile_m, int32_t tile_n, int32_t group_m,
                           int32_t n_cta, void* stream);
+
+/* ---- device queries ---------------------------------------------------------------------
+ * ao_device_query(device, key, out): "sm_count"; "cluster2_ctas" / "cluster4_ctas" = how
+ * many CTAs of the fused kernel can be co-resident (one per SM) when launched in clusters
+ * of 2 / 4 CTAs -- a 4-CTA cluster needs a free slot of 4 SMs inside one GPC, so not every
+ * SM can host one.  The 512-row cluster tiles (tile_m 512, two CTA pairs sharing B by TMA
+ * multicast) take their worker count from this: desc.n_cta = cluster4_ctas at most.
+ * AO_ERR_UNSUPPORTED off sm_100, AO_ERR_INVALID_ARG for an unknown key. */
+ao_status ao_device_query(int device, const char* key, int64_t* out);
 
 /* ---- tracing -------------------------------------------------------------
  * ao_ctx_trace_enable: allocate a device event buffer of `capacity` events (0 = off).  Op

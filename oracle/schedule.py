@@ -49,19 +49,25 @@ TILE_CANDIDATES = [(256, 256, 2), (256, 128, 2), (128, 256, 1), (128, 128, 1)]
 # Narrower CTA-pair widths (wave-quantization-free tiles for the per-GPU TP shapes, Q19),
 # built for AG with the copy-engine backend only.
 PAIR_TILES_AG_CE = [(256, 224, 2), (256, 208, 2), (256, 192, 2), (256, 160, 2), (256, 144, 2), (256, 112, 2)]
+# Two CTA pairs stacked along M sharing B by multicast (a 4-CTA cluster, BM = 512): AG with
+# the copy engine, and RS / AR with the atomic reduction; the worker count (clusters that
+# fit the GPU) is always given explicitly (n_cta).
+CLUSTER_TILES = [(512, 256, 4)]
 # Relative mainloop efficiency (percent) of each candidate: the measurement record
 # profiles/r02_tile_eff.json "eff_pct" (scripts/measure_tile_eff.py on a B200: plain GEMM
 # with ~55 waves of the shape's own tiles, no ragged edge, relative to 256x256).  Planner
 # spec constant shared with the C++ planner (Q19); tests pin it to the record.
 TILE_EFF = {(256, 256, 2): 100, (256, 128, 2): 61, (128, 256, 1): 87, (128, 128, 1): 59,
             (256, 224, 2): 94, (256, 208, 2): 82, (256, 192, 2): 85, (256, 160, 2): 74, (256, 144, 2): 68,
-            (256, 112, 2): 56}  # 0 would mean: explicit tile only (never picked automatically)
+            (256, 112, 2): 56, (512, 256, 4): 0}  # 0: explicit tile only (never picked automatically)
 
 
 def tile_candidates(desc):
     """The shapes a desc may use (in planner order)."""
     if desc["op"] == "ag_gemm" and desc["backend"] == "ce":
-        return TILE_CANDIDATES + PAIR_TILES_AG_CE
+        return TILE_CANDIDATES + PAIR_TILES_AG_CE + CLUSTER_TILES
+    if desc["op"] in ("gemm_rs", "gemm_ar") and desc.get("rs_reduce", "slots") == "atomic":
+        return TILE_CANDIDATES + CLUSTER_TILES
     return list(TILE_CANDIDATES)
 
 BK = 64  # K-block of the mainloop (TMA 128-B swizzle => 64 bf16), DESIGN.md
@@ -133,6 +139,8 @@ def validate(desc, sm_count=148):
         v.append("tile")
     if desc["tile_m"] and (desc["tile_m"], desc["tile_n"]) not in [(a, b) for a, b, _ in tile_candidates(desc)]:
         v.append("tile")
+    elif desc["tile_m"] == 512 and desc["n_cta"] <= 0:
+        v.append("n_cta (512-row cluster tile)")
     if not v and pick_tile(desc, sm_count) is None:
         v.append("no tile shape fits")
     return v

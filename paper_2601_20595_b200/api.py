@@ -344,5 +344,12 @@ def gemm_batched(As, Bs, Cs, tile_m: int = 0, tile_n: int = 0, group_m: int = 0,
     return Cs
 
 
+def device_query(device: int, key: str) -> int:
+    """ao_device_query: "sm_count", "cluster2_ctas", "cluster4_ctas"."""
+    out = ctypes.c_int64(0)
+    check(lib().ao_device_query(int(device), key.encode(), ctypes.byref(out)))
+    return out.value
+
+
 def debug_set(key: str, value: int):
     check(lib().ao_debug_set(key.encode(), int(value)))

@@ -49,15 +49,21 @@ constexpr int kA2AOperandBudget = 163840;  // A2A: one ring stage less, for the 
 constexpr int kRsStg = 2;                  // RS: TMA-reduce staging buffers per epilogue warp
 constexpr int kRsOperandBudget = 196608;   // RS ring (4 staging buffers + a 5-stage ring measured no faster)
 
+// CG = CTAs per cluster: 1 (one CTA, M = 128), 2 (a CTA pair running cta_group::2 MMAs,
+// M = 256) or 4 (two CTA pairs stacked along M, BM = 512, whose B rows are the same: each
+// CTA loads a quarter of the tile's B rows and TMA-multicasts it to the same-position CTA
+// of both pairs, so every B byte crosses the L2 -> SM crossbar once per cluster).
 template <int BN, int CG, int BUDGET = kOperandBudget>
 struct Cfg {
+  static constexpr int kCGM = CG >= 2 ? 2 : 1;  // cta_group of the MMA
+  static constexpr int kNP = CG / kCGM;          // CTA pairs sharing B (multicast) per cluster
   static constexpr int kStageA = kSubM * kBK * 2;
-  static constexpr int kStageB = (BN / CG) * kBK * 2;
+  static constexpr int kStageB = (BN / kCGM) * kBK * 2;
   static constexpr int kStage = kStageA + kStageB;
   static constexpr int kStages = BUDGET / kStage;
   // two accumulators of BN fp32 columns; tcgen05.alloc takes a power of two >= 32
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static_assert(BN % (8 * CG) == 0 && BN <= 256 && BN >= 16, "tile N: multiple of 8 * cta_group, at most 256");
+  static_assert(BN % (8 * CG) == 0 && BN <= 256 && BN >= 16, "tile N: multiple of 8 * CTAs per cluster, at most 256");
   static constexpr int kBM = kSubM * CG;
 };
 
@@ -607,9 +613,12 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
   constexpr SmemLayout L = gemm_layout<BN, CG, kBudget>(kTmaComm, MODE == MODE_RS, MODE == MODE_A2A);
   const int grp = blockIdx.x / args.ctas_per_rank;
   const int lcta = blockIdx.x % args.ctas_per_rank;  // CTA index inside the rank group
-  const int wk = lcta / CG;                          // plan worker (CTA pair when CG == 2)
+  const int wk = lcta / CG;                          // plan worker (the cluster: CTA, pair, 2 pairs)
   const int n_wk = args.ctas_per_rank / CG;
-  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // 0 = leader (even CTA)
+  constexpr int CGM = C_::kCGM, NP = C_::kNP;
+  const uint32_t crk = (CG >= 2) ? cluster_ctarank() : 0u;  // CTA r of the cluster holds rows r*128 of the tile
+  const uint32_t crank = crk & 1u;                           // position in its pair: 0 = leader (even CTA)
+  const uint32_t pp = crk >> 1;                              // pair index in the cluster (CG == 4)
   const bool leader = crank == 0;
   const RankArgs& R0 = args.rk[grp];  // shapes (equal across the group: same plan hash)
 
@@ -645,12 +654,12 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     if (lane == 0) {
       for (int s = 0; s < C_::kStages; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&empty[s], 1);
+        mbar_init(&empty[s], NP);  // CG == 4: both pairs' MMAs read this CTA's B quarter
         mbar_init(&pfull[s], 1);
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 4 * CG);
+        mbar_init(&tempty[a], 4 * CGM);
       }
       for (int a = 0; a < kAhead; ++a) {
         mbar_init(&wrdy[a], 1);
@@ -660,7 +669,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       fence_barrier_init();
     }
     __syncwarp();
-    if constexpr (CG == 2) {
+    if constexpr (CG >= 2) {
       tmem_alloc_cg2(tmem_slot, C_::kTmemCols);
       tmem_relinquish_cg2();
     } else {
@@ -669,7 +678,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     }
   }
   tc_fence_before();
-  if constexpr (CG == 2)
+  if constexpr (CG >= 2)
     cluster_sync();
   else
     __syncthreads();
@@ -752,17 +761,26 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         const int mb = tmn.x, nb = tmn.y;
         const int t = mb * R.n_nb + nb;
         const CUtensorMap* mA = &R.tmA;
-        int arow = mb * BM + int(crank) * kSubM;
+        int arow = mb * BM + int(crk) * kSubM;
         if constexpr (MODE == MODE_AG) {
           if (int64_t(arow) / S == R.rank) {
             mA = &R.tmA_loc;
             arow -= int(R.rank * S);
           }
         }
-        const int brow = nb * BN + int(crank) * (BN / CG);
+        // B rows of this CTA: its pair half (BN/2 rows); CG == 4: the quarter it loads and
+        // multicasts to the same-position CTA of both pairs (the other quarter arrives from
+        // the other pair), stacked in smem so each CTA sees its BN/2 rows contiguously
+        const int brow = nb * BN + int(crank) * (BN / CGM) + int(pp) * (BN / CG);
+        const uint32_t boff = pp * uint32_t(BN / CG) * 128u;
+        const uint16_t bmask = uint16_t((1u << crank) | (1u << (crank + 2)));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if constexpr (CG == 2) {
+          if constexpr (CG == 4) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C_::kStage);
+            tma_load_2d_2sm(sA + stage * C_::kStageA, mA, &full[stage], kb * kBK, arow, pol_a);
+            tma_load_2d_2sm_mc(sB + stage * C_::kStageB + boff, &R.tmB, &full[stage], kb * kBK, brow, bmask, pol_b);
+          } else if constexpr (CG == 2) {
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C_::kStage);
             tma_load_2d_2sm(sA + stage * C_::kStageA, mA, &full[stage], kb * kBK, arow, pol_a);
             tma_load_2d_2sm(sB + stage * C_::kStageB, &R.tmB, &full[stage], kb * kBK, brow, pol_b);
@@ -780,7 +798,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
           // RS-4: an own tile's epilogue fuses the peer reduction; stream the W-1 peer
           // partials of this CTA's 128 rows through the same smem ring (32-column fp32
           // boxes) once the peers' flags for its chunks are released.
-          const int64_t sub0 = int64_t(mb) * BM + int64_t(crank) * kSubM;
+          const int64_t sub0 = int64_t(mb) * BM + int64_t(crk) * kSubM;
           if (R.W > 1 && !R.rs_atomic && sub0 / S == R.rank) {
             const uint64_t tw = args.trace ? globaltimer() : 0;
             if (ts) {
@@ -820,7 +838,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
   } else if (warp == 1) {
     // ================================================================ MMA issuer
     if (leader) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+      constexpr uint32_t idesc = make_idesc_bf16(kSubM * CGM, BN);  // one pair's MMA: M = 128 * cta_group
       // full[] completes only on operand uses of a slot (RS partial stages use pfull[]),
       // so its parity is tracked per slot.
       uint32_t stage = 0, fpar = 0, acc = 0, acc_phase = 0;
@@ -838,12 +856,17 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             const uint64_t bd = make_smem_desc_sw128(smem_u32(sB + stage * C_::kStageB));
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 B per K=16 step inside the swizzle atom
-              if constexpr (CG == 2)
+              if constexpr (CG >= 2)
                 mma_bf16_ss_cg2(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
               else
                 mma_bf16_ss(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
             }
-            if constexpr (CG == 2)
+            // the stage is free once this pair's MMAs read it -- in every CTA that holds
+            // operands of this pair (CG == 4: also the other pair's CTAs, whose B quarters
+            // were multicast here)
+            if constexpr (CG == 4)
+              mma_commit_cg2_mask(&empty[stage], uint16_t(0xF));
+            else if constexpr (CG == 2)
               mma_commit_cg2_mc(&empty[stage]);
             else
               mma_commit(&empty[stage]);
@@ -852,8 +875,8 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
           if (++stage == C_::kStages) stage = 0;
         }
         if (lane == 0) {
-          if constexpr (CG == 2)
-            mma_commit_cg2_mc(&tfull[acc]);
+          if constexpr (CG >= 2)
+            mma_commit_cg2_mask(&tfull[acc], uint16_t(3u << (2 * pp)));  // this pair's CTAs
           else
             mma_commit(&tfull[acc]);
           if (args.trace) {
@@ -910,7 +933,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       const uint64_t t_epi = args.trace ? globaltimer() : 0;
       const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       const int64_t col_base = int64_t(nb) * BN;
-      const int64_t sub0 = int64_t(mb) * BM + int64_t(crank) * kSubM;  // first row of this CTA's half
+      const int64_t sub0 = int64_t(mb) * BM + int64_t(crk) * kSubM;  // first row of this CTA's 128
       const int64_t row0 = sub0 + q * 32;                                // first row of this warp
       int owner = 0;
       bool own_tile = false;
@@ -1149,7 +1172,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2)
+        if constexpr (CG >= 2)
           mbar_arrive_leader(&tempty[acc]);
         else
           mbar_arrive(&tempty[acc]);
@@ -1171,7 +1194,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (CG == 2)
+          if constexpr (CG >= 2)
             mbar_arrive_leader(&tempty[acc]);
           else
             mbar_arrive(&tempty[acc]);
@@ -1307,13 +1330,13 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
   }
 
   tc_fence_before();
-  if constexpr (CG == 2)
+  if constexpr (CG >= 2)
     cluster_sync();
   else
     __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    if constexpr (CG == 2)
+    if constexpr (CG >= 2)
       tmem_dealloc_cg2(tmem_base, C_::kTmemCols);
     else
       tmem_dealloc(tmem_base, C_::kTmemCols);
@@ -1349,9 +1372,9 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  if (CG == 2) {
+  if (CG >= 2) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.x = CG;
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;
@@ -1366,8 +1389,38 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  if (CG == 4) {  // 4-CTA clusters need whole free GPC slots: not every SM can host one
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+      cudaError_t oe = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg);
+      if (oe != cudaSuccess) return oe;
+    }
+    if (int(cfg.gridDim.x) / 4 > max_clusters) return cudaErrorCooperativeLaunchTooLarge;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
   return e;
+}
+
+template <int BN, int MODE, int CG>
+int max_clusters_of() {
+  auto kern = dev::fused_kernel<BN, MODE, COMM_NONE, CG>;
+  const size_t smem = dev::gemm_layout<BN, CG, MODE == MODE_RS ? dev::kRsOperandBudget : dev::kOperandBudget>(
+                          false, MODE == MODE_RS, false).total;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(4 * 64);
+  cfg.blockDim = dim3(dev::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = -1;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return -1;
+  return n;
 }
 
 // Extra CTA-pair tile widths (Q19: wave-quantization-free tiles for the per-GPU
@@ -1397,6 +1450,13 @@ cudaError_t launch_bn(const KernelArgs& args, int comm, cudaStream_t stream) {
 }
 }  // namespace
 
+int max_co_resident_ctas(int cg) {
+  // co-resident CTAs (1 per SM) of the fused kernel in clusters of `cg` CTAs
+  const int a = cg == 4 ? max_clusters_of<256, MODE_RS, 4>() : max_clusters_of<256, MODE_RS, 2>();
+  const int b = cg == 4 ? max_clusters_of<256, MODE_AG, 4>() : max_clusters_of<256, MODE_AG, 2>();
+  return (a < 0 || b < 0) ? -1 : cg * (a < b ? a : b);
+}
+
 cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream) {
   if (cg == 2) {
     switch (bn) {
@@ -1408,6 +1468,12 @@ cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaS
       case 160: return launch_bn_pair_extra<160>(args, comm, stream);
       case 144: return launch_bn_pair_extra<144>(args, comm, stream);
       case 112: return launch_bn_pair_extra<112>(args, comm, stream);
+    }
+  } else if (cg == 4) {  // two CTA pairs sharing B (multicast): GEMM, AG (copy engine), RS (atomic)
+    if (bn == 256) {
+      if (args.mode == MODE_GEMM) return launch_one<256, MODE_GEMM, COMM_NONE, 4>(args, stream);
+      if (args.mode == MODE_AG && comm == COMM_NONE) return launch_one<256, MODE_AG, COMM_NONE, 4>(args, stream);
+      if (args.mode == MODE_RS) return launch_one<256, MODE_RS, COMM_NONE, 4>(args, stream);
     }
   } else {
     if (bn == 256) return launch_bn<256, 1>(args, comm, stream);

@@ -170,6 +170,8 @@ static_assert(sizeof(KernelArgs) <= 32764, "KernelArgs exceeds the kernel parame
 // bn: tile N (128/256); cg: 1 (BM = 128) or 2 (CTA pair, BM = 256); comm: CommKind.
 cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream);
 cudaError_t launch_a2a_prep(const A2APrepArgs& args, cudaStream_t stream);
+// CTAs of the fused kernel that can be co-resident in clusters of cg (2 or 4) CTAs (-1 on error).
+int max_co_resident_ctas(int cg);
 cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream);
 
 }  // namespace ao

@@ -14,12 +14,13 @@ namespace ao {
 // transfers (and the plain GEMM, which plans as a one-rank AG) only.
 const TileShape kTileCandidates[] = {{256, 256, 2}, {256, 128, 2}, {128, 256, 1}, {128, 128, 1},
                                      {256, 224, 2}, {256, 208, 2}, {256, 192, 2}, {256, 160, 2},
-                                     {256, 144, 2}, {256, 112, 2}};
+                                     {256, 144, 2}, {256, 112, 2}, {512, 256, 4}};
 constexpr int kNumAllOpTiles = 4;
+constexpr int kClusterTile = 10;  // two CTA pairs sharing B by multicast (BM = 512)
 // Relative mainloop efficiency (percent) per candidate: profiles/r02_tile_eff.json
 // "eff_pct", written by scripts/measure_tile_eff.py on a B200 (plain GEMM, ~55 waves, no
 // ragged edge, vs the 2-CTA 256x256 tile; Q19).  0 = explicit tile only.
-static const int kTileEff[] = {100, 61, 87, 59, 94, 82, 85, 74, 68, 56};
+static const int kTileEff[] = {100, 61, 87, 59, 94, 82, 85, 74, 68, 56, 0};
 const int kNumTileCandidates = sizeof(kTileCandidates) / sizeof(kTileCandidates[0]);
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -40,8 +41,14 @@ static const char* intra_name(int i) { return i == AO_INTRA_ROW ? "row" : (i == 
 static int workers(const ao_plan_desc& d, int sm_count) { return d.n_cta > 0 ? d.n_cta : sm_count - d.comm_ctas; }
 
 // Candidate i exists for this desc's op / backend (the narrow pair widths: AG + CE only).
+// The 512-row cluster tile: AG + CE, and RS / AR with the atomic reduction (the slots
+// reduction streams peer partials through the operand ring, which the two pairs share).
 static bool tile_allowed(const ao_plan_desc& d, int i) {
-  return i < kNumAllOpTiles || (d.op == AO_OP_AG_GEMM && d.backend == AO_BACKEND_CE);
+  if (i < kNumAllOpTiles) return true;
+  if (i == kClusterTile)
+    return (d.op == AO_OP_AG_GEMM && d.backend == AO_BACKEND_CE) ||
+           ((d.op == AO_OP_GEMM_RS || d.op == AO_OP_GEMM_AR) && d.rs_reduce == AO_RS_ATOMIC);
+  return d.op == AO_OP_AG_GEMM && d.backend == AO_BACKEND_CE;
 }
 
 std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
@@ -115,6 +122,9 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
     for (int i = 0; i < kNumTileCandidates; ++i)
       if (kTileCandidates[i].bm == d.tile_m && kTileCandidates[i].bn == d.tile_n && tile_allowed(d, i)) ok = true;
     if (!ok) v.push_back("tile");
+    // clusters of 4 CTAs do not fit every SM (whole GPC slots): the worker count is the
+    // caller's (ao_device_query "cluster4_ctas"), never derived here
+    if (ok && d.tile_m == 512 && d.n_cta <= 0) v.push_back("n_cta (512-row cluster tile)");
   }
   if (v.empty()) {
     TileShape t;

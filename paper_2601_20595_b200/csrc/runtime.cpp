@@ -140,6 +140,7 @@ struct DebugKnobs {
   int64_t l2_hint = -1;  // -1: follow the plan's tile order
   int64_t gemm_group_m = 16;
   int64_t ts_lag = 0;  // time-sliced RS: lag the own run behind the next owner's first source run
+  int64_t ts_owners = 1;  // time-sliced RS: owners per phase (experiment)
   int64_t exp = 0;  // timing experiments (results invalid when nonzero)  // ao_gemm GROUP_M (measured best)
 };
 DebugKnobs g_debug;
@@ -484,6 +485,7 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   else if (!strcmp(key, "gemm_group_m")) g_debug.gemm_group_m = value;
   else if (!strcmp(key, "exp")) g_debug.exp = value;
   else if (!strcmp(key, "ts_lag")) g_debug.ts_lag = value;
+  else if (!strcmp(key, "ts_owners")) g_debug.ts_owners = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
   return AO_OK;
 }
@@ -888,6 +890,7 @@ static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArg
   if (mode == ao::MODE_RS) {
     if (h0.S % BM != 0) return false;
     struct Run { int key0, key1, key2, k0; ao::Seg s; };
+    const int G = int(std::max<int64_t>(1, g_debug.ts_owners));
     std::vector<Run> runs;
     for (int i = 0; i < n; ++i) {
       const ao::HostPlan& hp = plans[i]->hp;
@@ -901,7 +904,11 @@ static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArg
         // (slot 3 of phase o+1), so its contributions have drained when its waits run
         const int rot = ((hp.rank - owner) % hp.W + hp.W) % hp.W;
         const bool own = owner == hp.rank;
-        if (g_debug.ts_lag)  // behind the first ts_lag source runs of the next owner's phase
+        if (G > 1) {  // experiment: G owners per phase, each source's runs of the phase together
+          const int ph = owner / G;
+          const int srot = ((hp.rank - ph * G) % hp.W + hp.W) % hp.W;
+          runs.push_back({ph, own ? 2 * hp.W : 2 * srot, owner, k, {i, k, k1, 0}});
+        } else if (g_debug.ts_lag)  // behind the first ts_lag source runs of the next owner's phase
           runs.push_back({own ? owner + 1 : owner, own ? 2 * int(g_debug.ts_lag) + 1 : 2 * rot, 0, k, {i, k, k1, 0}});
         else
           runs.push_back({owner, own ? 2 * hp.W : 2 * rot, 0, k, {i, k, k1, 0}});
@@ -1555,13 +1562,32 @@ ao_status ao_group_schedule_export(int n, ao_plan* const* plans, int32_t op, int
   return AO_OK;
 }
 
+// ------------------------------------------------------------------------ device queries
+ao_status ao_device_query(int device, const char* key, int64_t* out) {
+  if (!key || !out) return fail(AO_ERR_INVALID_ARG, "null argument");
+  int sm = 0;
+  AO_CUDA(cudaSetDevice(device));
+  ao_status s = check_device_sm100(device, &sm);
+  if (s != AO_OK) return s;
+  if (!strcmp(key, "sm_count")) {
+    *out = sm;
+  } else if (!strcmp(key, "cluster2_ctas") || !strcmp(key, "cluster4_ctas")) {
+    const int n = ao::max_co_resident_ctas(key[7] == '4' ? 4 : 2);
+    if (n < 0) return fail(AO_ERR_CUDA, "cudaOccupancyMaxActiveClusters failed");
+    *out = n;
+  } else {
+    return fail(AO_ERR_INVALID_ARG, "unknown device query %s", key);
+  }
+  return AO_OK;
+}
+
 // ----------------------------------------------------------------------- plain GEMM entry
 ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int32_t tile_m,
                   int32_t tile_n, void* stream_v) {
   static std::mutex mu;
   static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int, int>, ao_plan*> cache;
   const int bm = tile_m ? tile_m : (M % 256 == 0 ? 256 : 128);
-  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256) || M % bm != 0 || N % 8 != 0 || K % 8 != 0)
+  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256 && bm != 512) || M % bm != 0 || N % 8 != 0 || K % 8 != 0)
     return fail(AO_ERR_INVALID_ARG, "ao_gemm needs M %% tile_m == 0, N %% 8 == 0, K %% 8 == 0 (M=%lld N=%lld K=%lld)",
                 (long long)M, (long long)N, (long long)K);
   if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return fail(AO_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
@@ -1589,6 +1615,11 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
       d.tile_n = bn;
       d.intra = AO_INTRA_GROUPED;  // GROUP_M swizzle: B tiles reused across row blocks in L2
       d.group_m = int32_t(g_debug.gemm_group_m);
+      if (bm == 512) {  // 4-CTA clusters: as many as fit the GPU at once
+        const int n4 = ao::max_co_resident_ctas(4);
+        if (n4 < 4) return fail(AO_ERR_CUDA, "no 4-CTA cluster fits this device");
+        d.n_cta = n4;
+      }
       s = ao_plan_create_host(&d, sm, &p);
       if (s != AO_OK) return s;
       p->device = device;
@@ -1623,7 +1654,7 @@ ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* 
   if (n < 1 || n > AO_MAX_WORLD || !As || !Bs || !Cs) return fail(AO_ERR_INVALID_ARG, "bad batch size %d", n);
   const int bm = tile_m ? tile_m : (M % 256 == 0 ? 256 : 128);
   const int bn = tile_n ? tile_n : 256;
-  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256) || M % bm != 0 ||
+  if (M < 0 || N < 0 || K < 0 || (bm != 128 && bm != 256 && bm != 512) || M % bm != 0 ||
       N % 8 != 0 || K % 8 != 0)
     return fail(AO_ERR_INVALID_ARG, "ao_gemm_batched needs M %% tile_m == 0, N %% 8 == 0, K %% 8 == 0");
   for (int i = 0; i < n; ++i)
@@ -1634,8 +1665,10 @@ ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* 
   int sm = 0;
   ao_status s = check_device_sm100(device, &sm);
   if (s != AO_OK) return s;
-  const int cg = bm == 256 ? 2 : 1;
-  const int ctas = (n_cta > 0 ? n_cta : sm / n) / cg * cg;  // CTAs per problem (whole pairs)
+  const int cg = bm / 128;
+  int cap = sm;
+  if (cg == 4) cap = ao::max_co_resident_ctas(4);
+  const int ctas = std::min(n_cta > 0 ? n_cta : cap / n, cap) / cg * cg;  // CTAs per problem (whole clusters)
   if (ctas < cg || ctas > sm)  // n * ctas > sm: time-sliced (problem after problem)
     return fail(AO_ERR_INVALID_ARG, "%d problems x %d CTAs exceed the %d SMs (or fewer CTAs than a tile needs)", n,
                 n_cta, sm);

@@ -16,7 +16,7 @@ import torch
 import paper_2601_20595_b200 as ao
 
 SHAPES = [(256, 256), (256, 128), (128, 256), (128, 128), (256, 224), (256, 208), (256, 192), (256, 160),
-          (256, 144), (256, 112)]
+          (256, 144), (256, 112), (512, 256)]
 PER_RANK = {"ag_w8": (8192, 1792, 4096), "ag_w4": (8192, 3584, 4096), "ag_w2": (8192, 7168, 4096),
             "rs_w8": (8192, 4096, 1792)}
 
@@ -43,7 +43,7 @@ def main():
     res = {"how": "ao.gemm TFLOP/s, best of 3 x 20 launches after 3 warm-up (CUDA events); "
                   "eff on M=16384, N=64*BN, K=4096", "tflops": {}, "per_rank": {}}
     for bm, bn in SHAPES:
-        M, N, K = 16384, 64 * bn, 4096
+        M, N, K = 16384 * (2 if bm == 512 else 1), 64 * bn, 4096
         A = torch.randn(M, K, device="cuda").bfloat16()
         B = (torch.randn(N, K, device="cuda") / 64).bfloat16()
         C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)

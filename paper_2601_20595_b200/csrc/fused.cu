@@ -28,8 +28,17 @@
 #include "kernel_args.h"
 #include "ptx.cuh"
 
+// Timing experiments (ao_debug_set "exp" bits: skip reduces, waits, ...; results invalid)
+// are compiled in only with -DAO_TIMING_EXPERIMENTS=1 (AO_NVCC_FLAGS); the production
+// build folds every xp() to false.
+#ifndef AO_TIMING_EXPERIMENTS
+#define AO_TIMING_EXPERIMENTS 0
+#endif
+
 namespace ao {
 namespace dev {
+
+__device__ __forceinline__ bool xp(const KernelArgs& a, int bit) { return AO_TIMING_EXPERIMENTS && (a.exp & bit); }
 
 constexpr int kSubM = 128;  // rows per CTA (TMEM lanes)
 constexpr int kBK = 64;
@@ -359,7 +368,11 @@ __device__ __noinline__ void ts_wait_rs(const RankArgs& R, const KernelArgs& A, 
 // one thread after a CTA barrier of the epilogue warps; one sys-scope fence is cumulative
 // over their stores / performed reduces.
 __device__ __forceinline__ void rs_signal(const RankArgs& R, const KernelArgs& A, int64_t sub0, int owner) {
-  if (!(A.exp & 32)) asm volatile("fence.sc.sys;" ::: "memory");
+  // No separate sys fence: the contributing warps' reduces are performed (bulk_wait 0) or
+  // their stores precede the CTA barrier, and st.release.sys below is cumulative over
+  // everything that happens-before it -- the release IS the fence (measured: a
+  // fence.sc.sys here cost ~10 us per launch).
+  if (xp(A, 32)) asm volatile("fence.sc.sys;" ::: "memory");
   const int glo = int(sub0 / R.crows);
   const int ghi = int((sub0 + kSubM - 1) / R.crows);
   for (int g = glo; g <= ghi; ++g) {
@@ -713,7 +726,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       // reused across every column tile of its group, B tiles only by neighbours in time.
       // l2_hint: 0 A first / B last, 1 A last / B first, 2 A last / B normal, 3 both normal
       const int h = args.l2_hint & 3;
-      const uint64_t pol_b = (args.exp & 512) ? policy_evict_first()
+      const uint64_t pol_b = xp(args, 512) ? policy_evict_first()
                              : h == 0 ? policy_evict_last() : (h == 1 ? policy_evict_first() : policy_evict_normal());
       const uint64_t pol_a = h == 0 ? policy_evict_first() : (h == 3 ? policy_evict_normal() : policy_evict_last());
       uint32_t stage = 0, phase = 0;
@@ -955,13 +968,13 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
           // i*4 + l/8, columns 4*(l%8)..+3), store bf16, and re-arm the accumulator (zeros).
           if (etid == 0) {
             const uint64_t tw = args.trace ? globaltimer() : 0;
-            if (ts && !(args.exp & 4)) {
+            if (ts && !xp(args, 4)) {
               const int64_t r0 = int64_t(mb) * BM;
               ts_wait_rs(R, args, wc, grp, lcta, r0, r0 + BM < M ? r0 + BM : M);
             }
             while (!ts && wp_e < we_e && R.waits[wp_e].x <= k) {
               const int g = R.waits[wp_e].y;
-              if (!(grp == 0 && wp_e == args.skip_wait) && !(args.exp & 4)) {
+              if (!(grp == 0 && wp_e == args.skip_wait) && !xp(args, 4)) {
                 for (int s = 0; s < R.W; ++s)
                   if (s != R.rank) spin_flag(R.flags + g * R.W + s, R.epoch, args, R.rank, lcta, g);
               }
@@ -981,7 +994,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             const int64_t off = (lrow0 + (lane >> 3)) * N + col0 + 4 * c;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              dst[i] = (okl && !(args.exp & 2)) ? __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N))
+              dst[i] = (okl && !xp(args, 2)) ? __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N))
                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
           };
           load_acc(col_base, pa);
@@ -1017,7 +1030,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
                 *reinterpret_cast<uint2*>(cout + base_off + int64_t(i) * 4 * N) = o;
                 if (R.ar)  // GEMM-AR: the reduced rows peers gather
                   *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(R.ar_red) + base_off + int64_t(i) * 4 * N) = o;
-                if (!(args.exp & 1))
+                if (!xp(args, 1))
                   st_v4(reinterpret_cast<int4*>(accm + base_off + int64_t(i) * 4 * N), make_int4(0, 0, 0, 0));
               }
             }
@@ -1100,7 +1113,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       if (!own_tile) {
       // RS ATOMIC: the TMA unit reduce-adds each staged 32 x 32 fp32 box into the owner's
       // accumulator (two staging buffers per warp, so staging overlaps the previous reduce).
-      const bool tma_red = MODE == MODE_RS && R.rs_atomic && !(args.exp & 64);  // exp 64: thread red.add
+      const bool tma_red = MODE == MODE_RS && R.rs_atomic && !xp(args, 64);  // exp 64: thread red.add
       int sb = 0;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += CW) {
@@ -1133,10 +1146,10 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             sg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          if (!(args.exp & 8192)) fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA) reads
+          if (!xp(args, 8192)) fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA) reads
           __syncwarp();
-          if (lane == 0 && !((args.exp & 1024) && ((cc / CW) & 1)) && !(args.exp & 16384)) {  // exp 1024/16384: half / no reduces (timing only)
-            if (args.exp & 256)  // timing experiment: keep the accumulator lines in L2
+          if (lane == 0 && !(xp(args, 1024) && ((cc / CW) & 1)) && !xp(args, 16384)) {  // exp 1024/16384: half / no reduces (timing only)
+            if (xp(args, 256))  // timing experiment: keep the accumulator lines in L2
               tma_reduce_add_2d_hint(&R.tmAcc[owner], sg, int(col0), int(row0 - int64_t(owner) * S),
                                      policy_evict_last());
             else
@@ -1160,8 +1173,8 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3);
           const uint4 w = stg[r * 8 + (c ^ (r & 7))];
-          if (ok && !(args.exp & 16) && row0 + r < rlim) {
-            if (MODE == MODE_RS && R.rs_atomic && !(args.exp & 8))
+          if (ok && !xp(args, 16) && row0 + r < rlim) {
+            if (MODE == MODE_RS && R.rs_atomic && !xp(args, 8))
               red_add_v4_f32(colp + r * ld_bytes, w.x, w.y, w.z, w.w);
             else
               st_v4(reinterpret_cast<int4*>(colp + r * ld_bytes), make_int4(w.x, w.y, w.z, w.w));
@@ -1200,7 +1213,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             mbar_arrive(&tempty[acc]);
         }
       }
-      if (MODE == MODE_RS && !own_tile && !(R.rs_atomic && !(args.exp & 64))) {
+      if (MODE == MODE_RS && !own_tile && !(R.rs_atomic && !xp(args, 64))) {
         // RS-3 (stores / thread reduces): signal this sub-tile now.
         named_bar_sync(1, 128);
         if (etid == 0) rs_signal(R, args, sub0, owner);
@@ -1210,8 +1223,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         // owner's "reduced" flag of chunk g (word n_chunks*W + g), which peers' gather
         // warps acquire before pulling the rows (Fig.4d).
         named_bar_sync(1, 128);
-        if (etid == 0) {
-          asm volatile("fence.sc.sys;" ::: "memory");
+        if (etid == 0) {  // (release below is cumulative over the CTA's stores, as in rs_signal)
           const int glo = int(sub0 / R.crows);
           const int ghi = int((sub0 + kSubM - 1) / R.crows);
           for (int g = glo; g <= ghi; ++g) {
@@ -1291,7 +1303,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             const int nj = (a2s.tab[S_.rank][e] + S_.crows - 1) / S_.crows;
             for (int jj = 0; jj < nj; ++jj, ++it) {
               if (it % nw != w) continue;
-              if (args.exp & 4096) {  // timing experiment: 16-byte ld/st row copies
+              if (xp(args, 4096)) {  // timing experiment: 16-byte ld/st row copies
                 a2a_push_chunk(a2s, S_, args, e, jj);
               } else {
                 if (lane == 0) a2a_push_chunk_tma(a2s, S_, args, e, jj, smem + L.off_comm, commbars, par);

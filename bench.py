@@ -285,6 +285,11 @@ def run_ours(args, rank, world, local_rank):
             gemm_only["exposed_comm_ms"] = {"ag_gemm": round(ag_ms - gemm_only["ag_gemm_ms"], 4),
                                             "gemm_rs": round(rs_ms - gemm_only["gemm_rs_ms"], 4)}
 
+    # --- the per-GPU TP shapes: one rank alone, peers' chunks pre-arrived ----------------
+    per_rank = None
+    if loop and not args.no_baseline:
+        per_rank = per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms)
+
     # --- GEMM-AR (NEXT-1) on the down-proj shape, same ctxs ----------------------------
     ar = None
     if not args.no_ar:
@@ -342,6 +347,7 @@ def run_ours(args, rank, world, local_rank):
         "check": check,
         "baseline_kernel_level": baseline,
         "gemm_only": gemm_only,
+        "per_rank_tp": per_rank,
         "gemm_ar": ar,
         "a2a_gemm": a2a,
         "sp_attn": attn,
@@ -599,6 +605,76 @@ def attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
             "causal_ms": round(ms_c, 4), "causal_tflops": round(flops_c / (ms_c * 1e-3) / 1e12, 1),
             "sdpa_same_gpu_ms": None if sd_ms is None else round(sd_ms, 4),
             "sdpa_tflops": None if sd_ms is None else round(flops / (sd_ms * 1e-3) / 1e12, 1)}
+
+
+def per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms):
+    """The per-GPU work of TP=W (the north star's "1 GPU (GEMM only)" point, VERDICT r01 item
+    3): rank 0's fused ag_gemm (M x F x HIDDEN) and gemm_rs (M x HIDDEN x F) alone on all
+    SMs through the per-rank C ABI call, with every peer chunk flag pre-arrived
+    (ao_debug_set prearrive: the waits are satisfied and no copy-engine chain is issued; RS
+    still reduce-adds its partials into the peers' accumulators).  Tiles: the planner's
+    pick, 256x256 and the 512x256 cluster tile; beside each, the plain GEMM (ao.gemm) on the
+    same shape and tile, and cuBLAS."""
+    W_ = W
+    n4 = ao.device_query(dev.index, "cluster4_ctas")
+    res = {"what": "rank 0 of TP=%d alone on the GPU, all SMs, peer chunks pre-arrived" % W_}
+    k = max(10, args.steps)
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(k):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / k
+
+    flops = 2.0 * M * F * HIDDEN
+    base = dict(world_size=W_, rank=0, M=M, chunk_rows=args.chunk, timeout_ns=5_000_000_000, intra=args.intra,
+                group_m=args.group_m)
+    Cd0 = torch.empty(M // W_, HIDDEN, dtype=torch.bfloat16, device=dev)
+    C_up = torch.empty(M, F, dtype=torch.bfloat16, device=dev)
+    C_dn = torch.empty(M, HIDDEN, dtype=torch.bfloat16, device=dev)
+    A_full = torch.cat(A, 0)
+    ao.debug_set("prearrive", 1)
+    try:
+        for op in ("ag_gemm", "gemm_rs"):
+            rows = {}
+            for tile in ("auto", "256x256", "512x256"):
+                d = dict(base, op=op, n_cta=sms)
+                if op == "ag_gemm":
+                    d.update(N=F, K=HIDDEN, backend="ce")
+                else:
+                    d.update(N=HIDDEN, K=F, rs_reduce="atomic")
+                if tile != "auto":
+                    d["tile_m"], d["tile_n"] = (int(x) for x in tile.split("x"))
+                    if d["tile_m"] == 512:
+                        d["n_cta"] = n4
+                p = ao.Plan(ctxs[0], d)
+                info = p.info()
+                if op == "ag_gemm":
+                    ms = timed(lambda: ao.ag_gemm(p, A[0], Bu[0], C_up))
+                    g_ms = timed(lambda: ao.gemm(A_full, Bu[0], C_up, tile_m=info["tile_m"], tile_n=info["tile_n"]))
+                else:
+                    ms = timed(lambda: ao.gemm_rs(p, Cu[0], Bd[0], Cd0))
+                    g_ms = timed(lambda: ao.gemm(Cu[0], Bd[0], C_dn, tile_m=info["tile_m"], tile_n=info["tile_n"]))
+                p.close()
+                rows[tile] = {"tile": [info["tile_m"], info["tile_n"], info["cta_group"]], "workers": info["n_cta"],
+                              "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+                              "gemm_only_tflops": round(flops / (g_ms * 1e-3) / 1e12, 1)}
+            if op == "ag_gemm":
+                cb = timed(lambda: torch.matmul(A_full, Bu[0].t(), out=C_up))
+            else:
+                cb = timed(lambda: torch.matmul(Cu[0], Bd[0].t(), out=C_dn))
+            rows["cublas_tflops"] = round(flops / (cb * 1e-3) / 1e12, 1)
+            res[op] = rows
+    finally:
+        ao.debug_set("prearrive", 0)
+    res["shape"] = {"ag_gemm": [M, F, HIDDEN], "gemm_rs": [M, HIDDEN, F]}
+    return res
 
 
 def gemm_only_leg(torch, ao, pa, pr, A, Bu, Bd, W, M, F, args, dev, loop):

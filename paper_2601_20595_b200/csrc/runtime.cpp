@@ -67,12 +67,14 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+typedef CUresult (*PFN_memsetD32Async)(CUdeviceptr, unsigned int, size_t, CUstream);
 
 struct DriverFns {
   PFN_encodeTiled encode = nullptr;
   PFN_writeValue32 write32 = nullptr;
   PFN_writeValue32 wait32 = nullptr;  // cuStreamWaitValue32 (same signature)
   PFN_batchMemOp batch = nullptr;     // cuStreamBatchMemOp
+  PFN_memsetD32Async memset32 = nullptr;  // cuMemsetD32Async
 };
 
 ao_status get_driver(DriverFns** out) {
@@ -98,6 +100,10 @@ ao_status get_driver(DriverFns** out) {
     AO_CUDA(cudaGetDriverEntryPoint("cuStreamBatchMemOp", &p, cudaEnableDefault, &q));
     if (!p) return fail(AO_ERR_CUDA, "cuStreamBatchMemOp not found");
     fns.batch = reinterpret_cast<PFN_batchMemOp>(p);
+    p = nullptr;
+    AO_CUDA(cudaGetDriverEntryPoint("cuMemsetD32Async", &p, cudaEnableDefault, &q));
+    if (!p) return fail(AO_ERR_CUDA, "cuMemsetD32Async not found");
+    fns.memset32 = reinterpret_cast<PFN_memsetD32Async>(p);
     loaded = true;
   }
   *out = &fns;
@@ -141,6 +147,10 @@ struct DebugKnobs {
   int64_t gemm_group_m = 16;
   int64_t ts_lag = 0;  // time-sliced RS: lag the own run behind the next owner's first source run
   int64_t ts_owners = 1;  // time-sliced RS: owners per phase (experiment)
+  int64_t prearrive = 0;  // per-rank measurement: every chunk flag of the launch's ranks is set
+                          // for the coming epoch before the kernel and no copy-engine chain is
+                          // issued (peers' data "already arrived"; the bench's per-GPU legs,
+                          // results not checked)
   int64_t exp = 0;  // timing experiments (results invalid when nonzero)  // ao_gemm GROUP_M (measured best)
 };
 DebugKnobs g_debug;
@@ -486,6 +496,7 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   else if (!strcmp(key, "exp")) g_debug.exp = value;
   else if (!strcmp(key, "ts_lag")) g_debug.ts_lag = value;
   else if (!strcmp(key, "ts_owners")) g_debug.ts_owners = value;
+  else if (!strcmp(key, "prearrive")) g_debug.prearrive = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
   return AO_OK;
 }
@@ -1036,7 +1047,17 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
     if (s != AO_OK) return s;
   }
   DriverFns* drv = nullptr;
-  if (ce) {
+  if (g_debug.prearrive) {
+    ao_status s = get_driver(&drv);
+    if (s != AO_OK) return s;
+    for (int i = 0; i < n; ++i) {
+      ao_ctx* c = plans[i]->ctx;
+      CUresult r = drv->memset32(reinterpret_cast<CUdeviceptr>(c->flags(c->rank, epochs[i] & 1)), epochs[i],
+                                 ao::flag_words_needed(plans[i]->hp.desc), stream);
+      if (r != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuMemsetD32Async failed (%d)", int(r));
+    }
+  }
+  if (ce && !g_debug.prearrive) {
     ao_status s = get_driver(&drv);
     if (s != AO_OK) return s;
     // CE backend (Fig.7a).  PUSH: every source rank copies its chunks to the peers in
@@ -1155,7 +1176,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
   cudaError_t e = ao::launch_fused(*ka, h0.tile.bn, h0.tile.cg, comm, stream);
   if (e != cudaSuccess) return fail(AO_ERR_CUDA, "fused kernel launch: %s", cudaGetErrorString(e));
   for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
-  if (ce) AO_CUDA(cudaStreamWaitEvent(stream, p0->ctx->ev_done, 0));
+  if (ce && !g_debug.prearrive) AO_CUDA(cudaStreamWaitEvent(stream, p0->ctx->ev_done, 0));
   {
     ao_status s = mark_done(n, plans, epochs, stream);
     if (s != AO_OK) return s;

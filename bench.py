@@ -370,35 +370,79 @@ def load_traffic(kernel):
 
 
 def loopback_baseline(torch, A, Bu, Bd, Cu, W, M, F, args):
-    """Kernel-level decomposition on the same GPU: gather copy, then cuBLAS GEMM per rank;
-    cuBLAS partial GEMMs per rank, then the reduction -- sequential stream order."""
-    out_up = [torch.empty_like(c) for c in Cu]
-    parts = [torch.empty(M, HIDDEN, dtype=torch.bfloat16, device=A[0].device) for _ in range(W)]
-    red = torch.empty(M, HIDDEN, dtype=torch.float32, device=A[0].device)
+    """SURVEY §8(d)(ii), the kernel-level two-stream overlap baseline with the W
+    loopback ranks on this GPU: the op split into s pieces; a comm stream runs the
+    collective of piece i+1 (AG: every rank's gathered copy of piece i's rows of all shards;
+    RS: the owners' sums of piece i's columns of the W partials) while the compute stream
+    runs cuBLAS on piece i.  RS partials in fp32 (cuBLAS bf16 x bf16 -> fp32, precision-
+    matched with the fused kernel's fp32 wire) and in bf16 (the usual practice, reported
+    beside it).  Best s in {1, 2, 4, 8} per precision; the headline comparison is fp32."""
+    dev = A[0].device
+    S = M // W
+    comm = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    A_st = torch.stack(A, 0)  # [W, S, K]: the W ranks' shards (loopback: all on this GPU)
+    Cup = [torch.empty(M, F, dtype=torch.bfloat16, device=dev) for _ in range(W)]
+    Out = [torch.empty(S, HIDDEN, dtype=torch.bfloat16, device=dev) for _ in range(W)]
+    out = {}
+    for prec in ("fp32", "bf16"):
+        pdt = torch.float32 if prec == "fp32" else torch.bfloat16
+        res = {}
+        for s in (1, 2, 4, 8):
+            rows, cols = S // s, HIDDEN // s
+            G = [[torch.empty(W, rows, HIDDEN, dtype=torch.bfloat16, device=dev) for _ in range(s)] for _ in range(W)]
+            P = [torch.empty(W, M, cols, dtype=pdt, device=dev) for _ in range(s)]
+            ev_ag = [torch.cuda.Event() for _ in range(s)]
+            ev_mm = [torch.cuda.Event() for _ in range(s)]
+            ev_rs = [torch.cuda.Event() for _ in range(s)]
 
-    def step():
-        A_full = torch.cat(A, 0)
-        for r in range(W):
-            torch.matmul(A_full, Bu[r].t(), out=out_up[r])
-        for s in range(W):
-            torch.matmul(out_up[s], Bd[s].t(), out=parts[s])
-        red.copy_(parts[0])
-        for s in range(1, W):
-            red.add_(parts[s])
+            def step():
+                comm.wait_stream(main)
+                with torch.cuda.stream(comm):  # AG of piece i into every rank's gathered buffer
+                    for i in range(s):
+                        for r in range(W):
+                            G[r][i].copy_(A_st[:, i * rows:(i + 1) * rows])
+                        ev_ag[i].record(comm)
+                for i in range(s):
+                    main.wait_event(ev_ag[i])
+                    for r in range(W):
+                        y = torch.matmul(G[r][i].view(W * rows, HIDDEN), Bu[r].t())
+                        Cup[r].view(W, S, F)[:, i * rows:(i + 1) * rows].copy_(y.view(W, rows, F))
+                for i in range(s):  # RS: column pieces; partials of every source rank
+                    for q in range(W):
+                        if prec == "fp32":
+                            torch.mm(Cup[q], Bd[q][i * cols:(i + 1) * cols].t(), out_dtype=torch.float32, out=P[i][q])
+                        else:
+                            torch.matmul(Cup[q], Bd[q][i * cols:(i + 1) * cols].t(), out=P[i][q])
+                    ev_mm[i].record(main)
+                    comm.wait_event(ev_mm[i])
+                    with torch.cuda.stream(comm):  # owners' sums (the ReduceScatter)
+                        red = P[i].view(W, W, S, cols).sum(0)
+                        for o in range(W):
+                            Out[o][:, i * cols:(i + 1) * cols].copy_(red[o])
+                        ev_rs[i].record(comm)
+                for i in range(s):
+                    main.wait_event(ev_rs[i])
 
-    for _ in range(3):
-        step()
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n = max(5, args.steps // 2)
-    s.record()
-    for _ in range(n):
-        step()
-    e.record()
-    torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / n
-    return {"what": "torch.cat gather + cuBLAS GEMMs + torch reduction (kernel-level, same GPU)",
-            "ms_per_step": round(ms, 4), "tflops": round(4.0 * M * FFN * HIDDEN / (ms * 1e-3) / 1e12, 2)}
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n = max(5, args.steps // 2)
+            st.record(main)
+            for _ in range(n):
+                step()
+            en.record(main)
+            torch.cuda.synchronize()
+            res[s] = st.elapsed_time(en) / n
+            del G, P
+        best = min(res, key=res.get)
+        out[prec] = {"ms_per_step": round(res[best], 4), "tflops": round(4.0 * M * FFN * HIDDEN / (res[best] * 1e-3) / 1e12, 2),
+                     "best_split": best, "per_split_ms": {str(k): round(v, 4) for k, v in res.items()}}
+    return {"what": "kernel-level two-stream split overlap on this GPU (W loopback ranks): comm-stream "
+                    "gather copies / owner sums + cuBLAS GEMMs per piece, best split s (SURVEY 8(d)(ii))",
+            "ms_per_step": out["fp32"]["ms_per_step"], "tflops": out["fp32"]["tflops"],
+            "rs_partials_fp32": out["fp32"], "rs_partials_bf16": out["bf16"]}
 
 
 def ar_leg(torch, ao, ctxs, my_ranks, ar_desc, Cu, Bd, M, W, args, dev, loop, world, dist):
@@ -716,66 +760,76 @@ def gemm_only_leg(torch, ao, pa, pr, A, Bu, Bd, W, M, F, args, dev, loop):
 
 def nccl_baseline(torch, dist, A_shard, Bu, Bd, W, M, F, args, dev):
     """The paper's kernel-level-overlap baseline ("Triton kernels paired with
-    NCCL collectives"; BASELINE.md §3): NCCL all_gather_into_tensor / reduce_scatter_tensor
+    NCCL collectives"; SURVEY §8(d)(ii)): NCCL all_gather_into_tensor / reduce_scatter_tensor
     + cuBLAS GEMMs, the op split into s pieces with the collective of piece i+1 on a comm
-    stream overlapping the GEMM of piece i.  Best of s in {1, 2, 4}; max over ranks."""
+    stream overlapping the GEMM of piece i.  RS partials in fp32 (cuBLAS bf16 x bf16 -> fp32,
+    precision-matched with the fused kernel's fp32 wire) and bf16 (usual practice).  Best s
+    in {1, 2, 4, 8} per precision; max over ranks."""
     S = M // W
     comm = torch.cuda.Stream()
     main = torch.cuda.current_stream()
     C_up = torch.empty(M, F, dtype=torch.bfloat16, device=dev)
     C_dn = torch.empty(S, HIDDEN, dtype=torch.bfloat16, device=dev)
-    results = {}
-    for s in (1, 2, 4):
-        if S % s or HIDDEN % s:
-            continue
-        rows = S // s
-        g_bufs = [torch.empty(W * rows, HIDDEN, dtype=torch.bfloat16, device=dev) for _ in range(s)]
-        parts = [torch.empty(M, HIDDEN // s, dtype=torch.bfloat16, device=dev) for _ in range(s)]
-        outs = [torch.empty(S, HIDDEN // s, dtype=torch.bfloat16, device=dev) for _ in range(s)]
-        ev_ag = [torch.cuda.Event() for _ in range(s)]
-        ev_mm = [torch.cuda.Event() for _ in range(s)]
-        ev_rs = [torch.cuda.Event() for _ in range(s)]
+    out = {}
+    for prec in ("fp32", "bf16"):
+        pdt = torch.float32 if prec == "fp32" else torch.bfloat16
+        results = {}
+        for s in (1, 2, 4, 8):
+            if S % s or HIDDEN % s:
+                continue
+            rows, cols = S // s, HIDDEN // s
+            g_bufs = [torch.empty(W * rows, HIDDEN, dtype=torch.bfloat16, device=dev) for _ in range(s)]
+            parts = [torch.empty(M, cols, dtype=pdt, device=dev) for _ in range(s)]
+            outs = [torch.empty(S, cols, dtype=pdt, device=dev) for _ in range(s)]
+            ev_ag = [torch.cuda.Event() for _ in range(s)]
+            ev_mm = [torch.cuda.Event() for _ in range(s)]
+            ev_rs = [torch.cuda.Event() for _ in range(s)]
 
-        def step():
-            comm.wait_stream(main)
-            with torch.cuda.stream(comm):  # AG pieces
+            def step():
+                comm.wait_stream(main)
+                with torch.cuda.stream(comm):  # AG pieces
+                    for i in range(s):
+                        dist.all_gather_into_tensor(g_bufs[i], A_shard[i * rows:(i + 1) * rows].contiguous())
+                        ev_ag[i].record(comm)
                 for i in range(s):
-                    dist.all_gather_into_tensor(g_bufs[i], A_shard[i * rows:(i + 1) * rows].contiguous())
-                    ev_ag[i].record(comm)
-            for i in range(s):
-                main.wait_event(ev_ag[i])
-                y = torch.matmul(g_bufs[i], Bu.t())  # [W*rows, F] -> rows p*S + i*rows
-                C_up.view(W, S, F)[:, i * rows:(i + 1) * rows].copy_(y.view(W, rows, F))
-            for i in range(s):  # RS pieces (column splits)
-                torch.matmul(C_up, Bd[i * (HIDDEN // s):(i + 1) * (HIDDEN // s)].t(), out=parts[i])
-                ev_mm[i].record(main)
-                comm.wait_event(ev_mm[i])
-                with torch.cuda.stream(comm):
-                    dist.reduce_scatter_tensor(outs[i], parts[i])
-                    ev_rs[i].record(comm)
-            for i in range(s):
-                main.wait_event(ev_rs[i])
-                C_dn[:, i * (HIDDEN // s):(i + 1) * (HIDDEN // s)].copy_(outs[i])
+                    main.wait_event(ev_ag[i])
+                    y = torch.matmul(g_bufs[i], Bu.t())  # [W*rows, F] -> rows p*S + i*rows
+                    C_up.view(W, S, F)[:, i * rows:(i + 1) * rows].copy_(y.view(W, rows, F))
+                for i in range(s):  # RS pieces (column splits)
+                    if prec == "fp32":
+                        torch.mm(C_up, Bd[i * cols:(i + 1) * cols].t(), out_dtype=torch.float32, out=parts[i])
+                    else:
+                        torch.matmul(C_up, Bd[i * cols:(i + 1) * cols].t(), out=parts[i])
+                    ev_mm[i].record(main)
+                    comm.wait_event(ev_mm[i])
+                    with torch.cuda.stream(comm):
+                        dist.reduce_scatter_tensor(outs[i], parts[i])
+                        ev_rs[i].record(comm)
+                for i in range(s):
+                    main.wait_event(ev_rs[i])
+                    C_dn[:, i * cols:(i + 1) * cols].copy_(outs[i])
 
-        for _ in range(3):
-            step()
-        torch.cuda.synchronize()
-        dist.barrier()
-        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = max(5, args.steps // 2)
-        st.record(main)
-        for _ in range(n):
-            step()
-        en.record(main)
-        torch.cuda.synchronize()
-        t = torch.tensor([st.elapsed_time(en) / n], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        results[s] = t.item()
-    best = min(results, key=results.get)
-    ms = results[best]
-    return {"what": "NCCL all_gather / reduce_scatter (bf16) + cuBLAS, two-stream split overlap (best s)",
-            "ms_per_step": round(ms, 4), "tflops": round(4.0 * M * FFN * HIDDEN / (ms * 1e-3) / 1e12, 2),
-            "best_split": best, "per_split_ms": {str(k): round(v, 4) for k, v in results.items()}}
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n = max(5, args.steps // 2)
+            st.record(main)
+            for _ in range(n):
+                step()
+            en.record(main)
+            torch.cuda.synchronize()
+            t = torch.tensor([st.elapsed_time(en) / n], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            results[s] = t.item()
+        best = min(results, key=results.get)
+        out[prec] = {"ms_per_step": round(results[best], 4),
+                     "tflops": round(4.0 * M * FFN * HIDDEN / (results[best] * 1e-3) / 1e12, 2),
+                     "best_split": best, "per_split_ms": {str(k): round(v, 4) for k, v in results.items()}}
+    return {"what": "NCCL all_gather / reduce_scatter + cuBLAS, two-stream split overlap (best s; SURVEY 8(d)(ii))",
+            "ms_per_step": out["fp32"]["ms_per_step"], "tflops": out["fp32"]["tflops"],
+            "rs_partials_fp32": out["fp32"], "rs_partials_bf16": out["bf16"]}
 
 
 def e2e_leg(torch, dist, args, A, Cd, step, barrier, world, flops_step, dev):

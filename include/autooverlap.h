@@ -294,6 +294,19 @@ ao_status ao_gemm_batched(int device, int n, const void* const* As, const void* 
                           int64_t M, int64_t N, int64_t K, int32_t tile_m, int32_t tile_n, int32_t group_m,
                           int32_t n_cta, void* stream);
 
+/* ---- E4: transfer-backend microbenchmark (Fig.2c,d) ------------
+ * ao_transfer_bench: copy `bytes` from `src` (device, this ctx's GPU) to rank `peer`'s
+ * symmetric data half (an IPC-mapped peer buffer, or this rank's own) in chunks of
+ * chunk_bytes, `iters` times back to back, and return the mean ms per copy (CUDA events).
+ *   AO_BACKEND_CE  : one cudaMemcpyAsync per chunk, round-robin over n_streams streams;
+ *   AO_BACKEND_TMA : n_ctas CTAs x 8 warps, chunk c by warp c mod 8 n_ctas, cp.async.bulk
+ *                    global -> smem -> global (the fused kernel's comm-warp code);
+ *   AO_BACKEND_LDST: the same with 16-byte vector ld/st.
+ * Requires bytes <= the ctx data half, 16-byte alignment.  Blocks until done. */
+ao_status ao_transfer_bench(ao_ctx* ctx, int peer, int32_t backend, const void* src, int64_t bytes,
+                            int64_t chunk_bytes, int32_t n_ctas, int32_t n_streams, int32_t iters,
+                            float* ms_per_iter);
+
 /* ---- device queries ---------------------------------------------------------------------
  * ao_device_query(device, key, out): "sm_count"; "cluster2_ctas" / "cluster4_ctas" = how
  * many CTAs of the fused kernel can be co-resident (one per SM) when launched in clusters

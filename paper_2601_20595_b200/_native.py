@@ -107,6 +107,9 @@ _SIGS = {
     "ao_gemm_batched": (ctypes.c_int, [ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 3 +
                         [ctypes.c_int64] * 3 + [ctypes.c_int32] * 4 + [ctypes.c_void_p]),
     "ao_debug_set": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64]),
+    "ao_transfer_bench": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_float)]),
     "ao_device_query": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
     "ao_ctx_trace_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
     "ao_ctx_trace_dump": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),

@@ -79,6 +79,9 @@ class Plan:
     Plan(ctx, desc) is bound to a ctx and can be launched."""
 
     def __init__(self, ctx, desc: dict, sm_count: int = 148):
+        if desc.get("backend") == "auto":  # the tuned table's winner for this shape (tune.resolve)
+            from .tune import resolve
+            desc = resolve(desc)
         self.desc = dict(desc)
         self.ctx = ctx
         d = make_desc(desc)
@@ -342,6 +345,16 @@ def gemm_batched(As, Bs, Cs, tile_m: int = 0, tile_n: int = 0, group_m: int = 0,
     check(lib().ao_gemm_batched(As[0].device.index, len(As), _arr(As), _arr(Bs), _arr(Cs), M, N, K, tile_m, tile_n,
                                 group_m, n_cta, _stream(stream)))
     return Cs
+
+
+def transfer_bench(ctx, peer: int, backend: str, src, bytes_: int, chunk_bytes: int, n_ctas: int = 16,
+                   n_streams: int = 1, iters: int = 10) -> float:
+    """ao_transfer_bench (E4): mean ms to move bytes_ of `src` into rank `peer`'s symmetric
+    buffer with one backend (CE: n_streams copy streams; TMA / LDST: n_ctas CTAs of 8 warps)."""
+    out = ctypes.c_float(0)
+    check(lib().ao_transfer_bench(ctx.handle, int(peer), N.BACKENDS[backend], _ptr(src), int(bytes_), int(chunk_bytes),
+                                  int(n_ctas), int(n_streams), int(iters), ctypes.byref(out)))
+    return out.value
 
 
 def device_query(device: int, key: str) -> int:

@@ -17,8 +17,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libautooverlap.so")
-SOURCES = ["planner.cpp", "runtime.cpp", "fused.cu", "a2a.cu", "attn.cu"]
-HEADERS = ["planner.h", "kernel_args.h", "ptx.cuh"]
+SOURCES = ["planner.cpp", "runtime.cpp", "fused.cu", "a2a.cu", "attn.cu", "e4.cu"]
+HEADERS = ["planner.h", "kernel_args.h", "ptx.cuh", "transfer.cuh"]
 
 
 def nvcc_path():

@@ -27,6 +27,7 @@
 
 #include "kernel_args.h"
 #include "ptx.cuh"
+#include "transfer.cuh"
 
 // Timing experiments (ao_debug_set "exp" bits: skip reduces, waits, ...; results invalid)
 // are compiled in only with -DAO_TIMING_EXPERIMENTS=1 (AO_NVCC_FLAGS); the production
@@ -176,16 +177,6 @@ __device__ __noinline__ void inject_delay(uint32_t delay, uint32_t salt) {
   while (globaltimer() - t0 < target) __nanosleep(1000);
 }
 
-__device__ __forceinline__ int4 ld_nc_v4(const int4* p) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void st_v4(int4* p, const int4& v) {
-  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
 
 // ---- communication workers (AG in-kernel backends) -----------------------------------------
 // Each worker is one warp; worker w handles items w, w + n_workers, ... of this rank's
@@ -215,52 +206,12 @@ __device__ void comm_item(const RankArgs& R, const KernelArgs& A, int i, int wor
       __syncwarp();
     }
     if constexpr (COMM == COMM_LDST) {
-      const int4* s = reinterpret_cast<const int4*>(src);
-      int4* d = reinterpret_cast<int4*>(dst);
-      const int64_t n = it.bytes / 16;
-      constexpr int U = 8;
-      for (int64_t base = 0; base < n; base += 32 * U) {
-        int4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t j = base + u * 32 + lane;
-          if (j < n) v[u] = remote_src ? __ldcg(s + j) : ld_nc_v4(s + j);  // peer data: coherent
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t j = base + u * 32 + lane;
-          if (j < n) st_v4(d + j, v[u]);
-        }
-      }
+      warp_copy_ldst(dst, src, it.bytes, remote_src);  // peer data: coherent loads
       __syncwarp();
       if (lane == 0) asm volatile("fence.sc.sys;" ::: "memory");
     } else {
       if (lane == 0 && it.bytes > 0) {
-        const int64_t npieces = (it.bytes + buf_bytes - 1) / buf_bytes;
-        auto piece_len = [&](int64_t p) -> uint32_t {
-          const int64_t rem = it.bytes - p * int64_t(buf_bytes);
-          return uint32_t(rem < int64_t(buf_bytes) ? rem : int64_t(buf_bytes));
-        };
-        {
-          const uint32_t n0 = piece_len(0);
-          mbar_arrive_expect_tx(&bars[0], n0);
-          bulk_g2s(staging, src, n0, &bars[0]);
-        }
-        for (int64_t p = 0; p < npieces; ++p) {
-          const int b = int(p & 1);
-          if (p + 1 < npieces) {
-            const int nb = b ^ 1;
-            bulk_wait_read<0>();  // the store that last used buffer nb has read it
-            const uint32_t n1 = piece_len(p + 1);
-            mbar_arrive_expect_tx(&bars[nb], n1);
-            bulk_g2s(staging + nb * buf_bytes, src + (p + 1) * int64_t(buf_bytes), n1, &bars[nb]);
-          }
-          mbar_wait(&bars[b], (phase_bits >> b) & 1);
-          phase_bits ^= (1u << b);
-          bulk_s2g(dst + p * int64_t(buf_bytes), staging + b * buf_bytes, piece_len(p));
-          bulk_commit();
-        }
-        bulk_wait<0>();  // writes performed
+        lane0_copy_tma(dst, src, it.bytes, staging, buf_bytes, bars, phase_bits);
         fence_proxy_async_global();
         fence_sys();
       }

@@ -170,6 +170,10 @@ static_assert(sizeof(KernelArgs) <= 32764, "KernelArgs exceeds the kernel parame
 // bn: tile N (128/256); cg: 1 (BM = 128) or 2 (CTA pair, BM = 256); comm: CommKind.
 cudaError_t launch_fused(const KernelArgs& args, int bn, int cg, int comm, cudaStream_t stream);
 cudaError_t launch_a2a_prep(const A2APrepArgs& args, cudaStream_t stream);
+// E4 microbenchmark: move `bytes` from src to dst in chunks of `chunk` with the in-kernel
+// TMA or LDST backend on n_ctas CTAs of 8 warps (e4.cu).
+cudaError_t launch_transfer(int comm, char* dst, const char* src, int64_t bytes, int64_t chunk, int n_ctas,
+                            cudaStream_t stream);
 // CTAs of the fused kernel that can be co-resident in clusters of cg (2 or 4) CTAs (-1 on error).
 int max_co_resident_ctas(int cg);
 cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream);

@@ -1583,6 +1583,68 @@ ao_status ao_group_schedule_export(int n, ao_plan* const* plans, int32_t op, int
   return AO_OK;
 }
 
+// ---------------------------------------------------------------- E4 backend microbench
+ao_status ao_transfer_bench(ao_ctx* c, int peer, int32_t backend, const void* src, int64_t bytes, int64_t chunk_bytes,
+                            int32_t n_ctas, int32_t n_streams, int32_t iters, float* ms_per_iter) {
+  if (!c || !src || !ms_per_iter || bytes <= 0 || chunk_bytes <= 0 || iters < 1)
+    return fail(AO_ERR_INVALID_ARG, "bad argument");
+  if (peer < 0 || peer >= c->W || !c->peer_base[peer]) return fail(AO_ERR_STATE, "peer %d not mapped", peer);
+  if (size_t(bytes) > c->data_half) return fail(AO_ERR_INVALID_ARG, "message larger than the data half");
+  if (!aligned16(src) || bytes % 16 || chunk_bytes % 16) return fail(AO_ERR_INVALID_ARG, "16-byte alignment");
+  if (backend == AO_BACKEND_CE ? (n_streams < 1 || n_streams > 16) : (n_ctas < 1 || n_ctas > c->sm_count))
+    return fail(AO_ERR_INVALID_ARG, "n_streams in [1,16] (CE) / n_ctas in [1,SMs] (TMA, LDST)");
+  AO_CUDA(cudaSetDevice(c->device));
+  char* dst = c->data(peer, 0);
+  cudaStream_t main_s;
+  AO_CUDA(cudaStreamCreateWithFlags(&main_s, cudaStreamNonBlocking));
+  std::vector<cudaStream_t> ss(backend == AO_BACKEND_CE ? n_streams : 0);
+  for (auto& x : ss) AO_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  cudaEvent_t t0, t1, fork;
+  AO_CUDA(cudaEventCreate(&t0));
+  AO_CUDA(cudaEventCreate(&t1));
+  AO_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  std::vector<cudaEvent_t> join(ss.size());
+  for (auto& e : join) AO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  auto one = [&]() -> ao_status {
+    if (backend == AO_BACKEND_CE) {  // one peer memcpy per chunk, round-robin over the streams
+      AO_CUDA(cudaEventRecord(fork, main_s));
+      for (auto& x : ss) AO_CUDA(cudaStreamWaitEvent(x, fork, 0));
+      int64_t i = 0;
+      for (int64_t off = 0; off < bytes; off += chunk_bytes, ++i) {
+        const size_t len = size_t(std::min<int64_t>(chunk_bytes, bytes - off));
+        AO_CUDA(cudaMemcpyAsync(dst + off, static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToDevice,
+                                ss[size_t(i % int64_t(ss.size()))]));
+      }
+      for (size_t k = 0; k < ss.size(); ++k) {
+        AO_CUDA(cudaEventRecord(join[k], ss[k]));
+        AO_CUDA(cudaStreamWaitEvent(main_s, join[k], 0));
+      }
+    } else {
+      AO_CUDA(ao::launch_transfer(backend == AO_BACKEND_TMA ? ao::COMM_TMA : ao::COMM_LDST, dst,
+                                  static_cast<const char*>(src), bytes, chunk_bytes, n_ctas, main_s));
+    }
+    return AO_OK;
+  };
+  ao_status st = one();  // warm-up
+  if (st == AO_OK) AO_CUDA(cudaEventRecord(t0, main_s));
+  for (int it = 0; it < iters && st == AO_OK; ++it) st = one();
+  if (st == AO_OK) {
+    AO_CUDA(cudaEventRecord(t1, main_s));
+    AO_CUDA(cudaEventSynchronize(t1));
+    float ms = 0.f;
+    AO_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    *ms_per_iter = ms / float(iters);
+  }
+  cudaStreamSynchronize(main_s);
+  for (auto& x : ss) cudaStreamDestroy(x);
+  for (auto& e : join) cudaEventDestroy(e);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaEventDestroy(fork);
+  cudaStreamDestroy(main_s);
+  return st;
+}
+
 // ------------------------------------------------------------------------ device queries
 ao_status ao_device_query(int device, const char* key, int64_t* out) {
   if (!key || !out) return fail(AO_ERR_INVALID_ARG, "null argument");

@@ -469,3 +469,15 @@ def test_gemm_ar_rejects_wrong_op_and_backend(ao):
         ao.gemm_rs_group(plans, A, B, C)  # an AR plan is not an RS plan
     with pytest.raises(ao.AOError, match="INVALID_ARG"):
         ao.Plan(ctxs[0], dict(plans[0].desc, backend="ce"))  # gather transport is ld/st
+
+
+@pytest.mark.parametrize("backend", ["ce", "tma", "ldst"])
+def test_transfer_bench_backends(ao, backend):
+    """E4 microbenchmark entry point: every backend moves a message into a peer's symmetric
+    buffer and reports a positive time (the AG tests check the same code's data)."""
+    ctxs = ao.loopback_world(0, 2, 8 << 20)
+    src = torch.zeros(1 << 21, dtype=torch.bfloat16, device="cuda")
+    ms = ao.transfer_bench(ctxs[0], 1, backend, src, 4 << 20, 1 << 18, n_ctas=8, n_streams=2, iters=3)
+    assert ms > 0
+    for c in ctxs:
+        c.close()

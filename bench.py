@@ -683,6 +683,11 @@ def per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms):
     C_up = torch.empty(M, F, dtype=torch.bfloat16, device=dev)
     C_dn = torch.empty(M, HIDDEN, dtype=torch.bfloat16, device=dev)
     A_full = torch.cat(A, 0)
+    # its own contexts: only rank 0 launches here, which would put the shared world's
+    # epochs and collective plan sequence (AO_ERR_PEER agreement) out of step
+    ws = max(ao.workspace_bytes(dict(base, op="ag_gemm", N=F, K=HIDDEN, n_cta=sms)),
+             ao.workspace_bytes(dict(base, op="gemm_rs", N=HIDDEN, K=F, n_cta=sms, rs_reduce="atomic")))
+    ctxs = ao.loopback_world(dev.index, W_, ws)
     ao.debug_set("prearrive", 1)
     try:
         for op in ("ag_gemm", "gemm_rs"):
@@ -717,6 +722,8 @@ def per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms):
             res[op] = rows
     finally:
         ao.debug_set("prearrive", 0)
+        for c in ctxs:
+            c.close()
     res["shape"] = {"ag_gemm": [M, F, HIDDEN], "gemm_rs": [M, HIDDEN, F]}
     return res
 

@@ -692,27 +692,34 @@ def per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms):
     try:
         for op in ("ag_gemm", "gemm_rs"):
             rows = {}
-            for tile in ("auto", "256x256", "512x256"):
+            # (tile, stream_k): the planner's pick with auto stream-K (Q28), 256x256 without
+            # and with the stream-K tail, the 512x256 cluster tile
+            variants = (("auto", -1), ("256x256", 0), ("256x256+sk", 1), ("512x256", 0)) if op == "ag_gemm" else \
+                (("auto", 0), ("256x256", 0), ("512x256", 0))
+            for tile, sk in variants:
                 d = dict(base, op=op, n_cta=sms)
                 if op == "ag_gemm":
-                    d.update(N=F, K=HIDDEN, backend="ce")
+                    d.update(N=F, K=HIDDEN, backend="ce", stream_k=sk)
                 else:
                     d.update(N=HIDDEN, K=F, rs_reduce="atomic")
                 if tile != "auto":
-                    d["tile_m"], d["tile_n"] = (int(x) for x in tile.split("x"))
+                    d["tile_m"], d["tile_n"] = (int(x) for x in tile.split("+")[0].split("x"))
                     if d["tile_m"] == 512:
                         d["n_cta"] = n4
                 p = ao.Plan(ctxs[0], d)
                 info = p.info()
+                ao.debug_set("gemm_stream_k", sk if info["tile_m"] != 512 else 0)
                 if op == "ag_gemm":
                     ms = timed(lambda: ao.ag_gemm(p, A[0], Bu[0], C_up))
                     g_ms = timed(lambda: ao.gemm(A_full, Bu[0], C_up, tile_m=info["tile_m"], tile_n=info["tile_n"]))
                 else:
                     ms = timed(lambda: ao.gemm_rs(p, Cu[0], Bd[0], Cd0))
                     g_ms = timed(lambda: ao.gemm(Cu[0], Bd[0], C_dn, tile_m=info["tile_m"], tile_n=info["tile_n"]))
+                ao.debug_set("gemm_stream_k", 0)
+                sk_dp = json.loads(p.export_json()).get("sk_dp")
                 p.close()
                 rows[tile] = {"tile": [info["tile_m"], info["tile_n"], info["cta_group"]], "workers": info["n_cta"],
-                              "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+                              "stream_k_dp": sk_dp, "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
                               "gemm_only_tflops": round(flops / (g_ms * 1e-3) / 1e12, 1)}
             if op == "ag_gemm":
                 cb = timed(lambda: torch.matmul(A_full, Bu[0].t(), out=C_up))

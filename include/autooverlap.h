@@ -119,7 +119,11 @@ typedef struct {
   int32_t rs_reduce;    /* ao_rs_reduce (RS only) */
   int32_t topk;         /* A2A: experts per token (k); other ops: 0 */
   int32_t causal;       /* SP attention: 1 = causal mask over global token positions; other ops: 0 */
-  int32_t reserved;
+  int32_t stream_k;     /* AG (copy engine) / plain GEMM, tiles of <= 2 CTAs: split the last two
+                           waves' tiles along K over all workers (data-parallel + stream-K tail,
+                           DESIGN.md Q28) so a tile count that is not a multiple of the workers
+                           leaves no idle tail wave.  0 = off, 1 = on, -1 = auto (on when the
+                           wave utilization T / (ceil(T/n) n) < 0.9) */
 } ao_plan_desc;
 
 /* ---- status / version ---------------------------------------------------------------- */
@@ -327,7 +331,10 @@ ao_status ao_ctx_trace_dump(ao_ctx* ctx, const char* path, int64_t* n_events);
 
 /* ---- test hooks (deterministic fault injection; see tests/) ----------------------------
  * ao_debug_set: key "skip_wait" = index of a wait (global over CTAs) the kernel must skip
- * (-1 = none); "delay_ns" = nanosleep before each transfer/signal (fuzzes arrival order). */
+ * (-1 = none); "delay_ns" = nanosleep before each transfer/signal (fuzzes arrival order);
+ * "prearrive" = 1: every chunk flag of a launch's ranks is set before it and no copy-engine
+ * chain is issued (per-rank measurement with peers simulated as arrived); "gemm_stream_k"
+ * = desc.stream_k of ao_gemm's internal plan (0 / 1 / -1). */
 ao_status ao_debug_set(const char* key, int64_t value);
 
 #ifdef __cplusplus

@@ -56,8 +56,9 @@ def sp_attention(Q_list, K_list, V_list, rank: int, scale: float, causal: bool =
     return attention(Q_list[rank], K, V, scale, np.arange(S_loc) + rank * S_loc, np.arange(K.shape[1]))
 
 
-def sp_attention_rows(Q_list, K_list, V_list, rank: int, scale: float, heads, rows, causal: bool = False):
-    """Selected (head, row) outputs (full-size sampled checks)."""
+def sp_attention_rows(Q_list, K_list, V_list, rank: int, scale: float, heads, rows, causal: bool = False,
+                      p_bf16: bool = False):
+    """Selected (head, row) outputs (full-size sampled checks); p_bf16: attention_p_bf16."""
     K = np.concatenate([np.asarray(k, dtype=np.float64) for k in K_list], axis=1)
     V = np.concatenate([np.asarray(v, dtype=np.float64) for v in V_list], axis=1)
     Q = np.asarray(Q_list[rank], dtype=np.float64)
@@ -66,5 +67,43 @@ def sp_attention_rows(Q_list, K_list, V_list, rank: int, scale: float, heads, ro
     kp = np.arange(K.shape[1]) if causal else None
     out = []
     for h in heads:
-        out.append(attention(Q[h:h + 1, rows], K[h:h + 1], V[h:h + 1], scale, qp, kp)[0])
+        f = attention_p_bf16 if p_bf16 else attention
+        out.append(f(Q[h:h + 1, rows], K[h:h + 1], V[h:h + 1], scale, qp, kp)[0])
     return np.stack(out)
+
+
+def round_bf16(x):
+    """Round-to-nearest-even to bfloat16 (8-bit significand), returned as float64: the
+    float32 value's low 16 bits rounded away (inputs here are finite and in float32 range)."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def attention_p_bf16(Q, K, V, scale: float, q_pos=None, k_pos=None):
+    """The attention above in the arithmetic of a bf16-in / fp32-accumulate P.V contraction
+    (Q27): the unnormalised probabilities p = exp(s - max s) enter the product with
+    V rounded to bf16, the normaliser l = sum p is not rounded.  Everything else fp64.  This
+    is the floor any kernel that feeds P to a bf16 tensor-core MMA shares; not the
+    definition (that is `attention`)."""
+    Q = np.asarray(Q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    S = np.einsum("hqd,hkd->hqk", Q, K) * scale
+    if q_pos is not None:
+        S = np.where(np.asarray(k_pos)[None, None, :] <= np.asarray(q_pos)[None, :, None], S, -np.inf)
+    S = S - S.max(axis=-1, keepdims=True)
+    P = np.exp(S)
+    l = P.sum(axis=-1, keepdims=True)
+    return np.einsum("hqk,hkd->hqd", round_bf16(P), V) / l
+
+
+def sp_attention_p_bf16(Q_list, K_list, V_list, rank: int, scale: float, causal: bool = False):
+    """sp_attention with attention_p_bf16."""
+    K = np.concatenate([np.asarray(k, dtype=np.float64) for k in K_list], axis=1)
+    V = np.concatenate([np.asarray(v, dtype=np.float64) for v in V_list], axis=1)
+    if not causal:
+        return attention_p_bf16(Q_list[rank], K, V, scale)
+    S_loc = np.asarray(Q_list[rank]).shape[1]
+    return attention_p_bf16(Q_list[rank], K, V, scale, np.arange(S_loc) + rank * S_loc, np.arange(K.shape[1]))

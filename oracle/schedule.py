@@ -135,6 +135,11 @@ def validate(desc, sm_count=148):
         v.append("rs_wire bf16")  # DESIGN.md Q14: bf16 partials break the per-element bound
     if desc.get("rs_reduce", "slots") not in ("slots", "atomic"):
         v.append("rs_reduce")
+    sk = desc.get("stream_k", 0)
+    if sk not in (-1, 0, 1):
+        v.append("stream_k")
+    if sk == 1 and (desc["op"] != "ag_gemm" or desc["backend"] != "ce" or desc["tile_m"] == 512):
+        v.append("stream_k (AG with the copy engine, tiles of <= 2 CTAs)")
     if (desc["tile_m"] == 0) != (desc["tile_n"] == 0):
         v.append("tile")
     if desc["tile_m"] and (desc["tile_m"], desc["tile_n"]) not in [(a, b) for a, b, _ in tile_candidates(desc)]:
@@ -356,14 +361,16 @@ def plan(desc, sm_count=148):
     if not is_ag:
         tiles_per_chunk = [sum(1 for t in range(T) if g in tile_chunks[t]) for g in range(len(chunks))]
 
-    # CTA assignment: position k -> CTA k mod n_cta.  Waits: AG tiles wait for their
-    # remote chunks; RS own-row tiles (whose epilogue fuses the peer reduction) wait for
-    # the other sources' contributions to their chunks.
+    # CTA assignment: position k -> CTA k mod n_cta, except a stream-K tail (DESIGN.md
+    # Q28).  Waits: AG tiles wait for their remote chunks; RS own-row tiles (whose epilogue
+    # fuses the peer reduction) wait for the other sources' contributions to their chunks.
+    sk_dp = stream_k_dp(desc, T, n_cta, cg)
+    positions = worker_positions(T, n_cta, sk_dp, _ceil_div(K, BK))
     waits = []
     for c in range(n_cta):
         seen = set()
         lst = []
-        for k in range(c, len(order), n_cta):
+        for k in positions[c]:
             t = order[k]
             if is_ag:
                 need = [g for g in tile_chunks[t] if chunks[g][2] != r]
@@ -404,6 +411,59 @@ def plan(desc, sm_count=148):
     if not is_ag:
         out["tiles_per_chunk"] = tiles_per_chunk
         out["rs_reduce"] = desc.get("rs_reduce", "slots")
+    if sk_dp < T:
+        out["sk_dp"] = sk_dp
+    return out
+
+
+def stream_k_dp(desc, T, n, cg):
+    """Q28 (data-parallel + stream-K tail): the number of tile positions run data-parallel.
+    When T tiles do not fill whole waves of n workers, the last two waves' tiles are split
+    along K instead (sk_dp = (T // n - 1) * n); T when off or not applicable.  'Auto' (-1)
+    turns it on when the wave utilization T / (ceil(T / n) * n) is below 0.9."""
+    from fractions import Fraction
+    nkb = _ceil_div(desc["K"], BK)
+    sk = desc.get("stream_k", 0)
+    able = desc["op"] == "ag_gemm" and desc["backend"] == "ce" and cg <= 2 and nkb > 0 and T > n and T % n != 0
+    want = sk == 1 or (sk == -1 and Fraction(T, _ceil_div(T, n) * n) < Fraction(9, 10))
+    return (T // n - 1) * n if able and want else T
+
+
+def worker_positions(T, n, sk_dp, nkb):
+    """Tile positions each worker runs, in order.  Data-parallel part: worker c runs
+    c, c + n, ... below sk_dp (Lst.1's persistent stride).  Stream-K part: the (T - sk_dp) *
+    nkb (position, k-block) units, in position-major order, are cut into n contiguous
+    ranges, worker c getting units [floor(U c / n), floor(U (c + 1) / n)); it runs every
+    position one of its units belongs to.  Enumerated unit by unit."""
+    pos = [list(range(c, sk_dp, n)) for c in range(n)]
+    U = (T - sk_dp) * nkb
+    bounds = [U * c // n for c in range(n + 1)]
+    c = 0
+    for u in range(U):
+        while u >= bounds[c + 1]:
+            c += 1
+        k = sk_dp + u // nkb
+        if not pos[c] or pos[c][-1] != k:
+            pos[c].append(k)
+    return pos
+
+
+def worker_pieces(T, n, sk_dp, nkb, c):
+    """Worker c's (position, kb0, kb1, role) pieces: role 0 = whole tile, 1 = a tail piece
+    (k-blocks up to the end; stores its fp32 partial), 2 = a head piece (k-blocks from 0;
+    adds the tail's partial and stores the tile).  Enumerated unit by unit."""
+    dp_part = [[k, 0, nkb, 0] for k in range(c, sk_dp, n)]
+    sk_part = []
+    U = (T - sk_dp) * nkb
+    for u in range(U * c // n, U * (c + 1) // n):
+        k, kb = sk_dp + u // nkb, u % nkb
+        if sk_part and sk_part[-1][0] == k:
+            sk_part[-1][2] = kb + 1  # units of one position are consecutive k-blocks
+        else:
+            sk_part.append([k, kb, kb + 1, 0])
+    out = dp_part + sk_part
+    for p in out:
+        p[3] = 0 if (p[1] == 0 and p[2] == nkb) else (1 if p[1] != 0 else 2)
     return out
 
 

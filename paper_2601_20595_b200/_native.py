@@ -57,7 +57,7 @@ class PlanDesc(ctypes.Structure):
         ("rs_reduce", ctypes.c_int32),
         ("topk", ctypes.c_int32),
         ("causal", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("stream_k", ctypes.c_int32),
     ]
 
 
@@ -164,4 +164,5 @@ def make_desc(d: dict) -> PlanDesc:
     x.rs_reduce = RS_REDUCE[d.get("rs_reduce", "slots")]
     x.topk = int(d.get("topk", 0))
     x.causal = int(d.get("causal", 0))
+    x.stream_k = int(d.get("stream_k", 0))
     return x

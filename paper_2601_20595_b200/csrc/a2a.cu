@@ -18,9 +18,12 @@ namespace dev {
 constexpr int kPrepThreads = 1024;
 
 __device__ __forceinline__ void prep_spin(const uint32_t* p, uint32_t target, const A2APrepArgs& A, int rank, int s) {
-  if (ld_acquire_sys(p) >= target) return;
+  if (ld_relaxed_sys(p) >= target) {  // relaxed polls, one acquire (see fused.cu spin_flag)
+    ld_acquire_sys(p);
+    return;
+  }
   const uint64_t t0 = globaltimer();
-  while (ld_acquire_sys(p) < target) {
+  while (ld_relaxed_sys(p) < target) {
     if (globaltimer() - t0 > A.timeout_ns) {
       if (atomicCAS(&A.err->claim, 0u, 1u) == 0u) {
         A.err->rank = rank;
@@ -35,6 +38,7 @@ __device__ __forceinline__ void prep_spin(const uint32_t* p, uint32_t target, co
     }
     __nanosleep(64);
   }
+  ld_acquire_sys(p);
 }
 
 __global__ void __launch_bounds__(kPrepThreads) a2a_prep_kernel(const __grid_constant__ A2APrepArgs a) {

@@ -54,10 +54,13 @@ struct AttnBars {
 };
 
 __device__ __noinline__ void attn_spin(const uint32_t* p, uint32_t target, const AttnArgs& A, int rank, int cta, int w) {
-  if (ld_acquire_sys(p) >= target) return;
+  if (ld_relaxed_sys(p) >= target) {  // relaxed polls, one acquire (see fused.cu spin_flag)
+    ld_acquire_sys(p);
+    return;
+  }
   const uint64_t t0 = globaltimer();
   uint32_t ns = 32;
-  while (ld_acquire_sys(p) < target) {
+  while (ld_relaxed_sys(p) < target) {
     if (globaltimer() - t0 > A.timeout_ns) {
       if (atomicCAS(&A.err->claim, 0u, 1u) == 0u) {
         A.err->rank = rank;
@@ -73,6 +76,7 @@ __device__ __noinline__ void attn_spin(const uint32_t* p, uint32_t target, const
     __nanosleep(ns);
     if (ns < 256) ns <<= 1;
   }
+  ld_acquire_sys(p);
 }
 
 // Work items of this CTA in order: (rank group, item).  Space-sliced: its own group's items

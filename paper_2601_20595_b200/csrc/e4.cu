@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kE4Warps * 32) transfer_kernel(char* dst, cons
     const int64_t off = c * chunk;
     const int64_t len = bytes - off < chunk ? bytes - off : chunk;
     if constexpr (COMM == COMM_LDST) {
-      warp_copy_ldst(dst + off, src + off, len, false);
+      warp_copy_ldst<8>(dst + off, src + off, len, false);
       __syncwarp();
       if (lane == 0) fence_sys();
     } else {

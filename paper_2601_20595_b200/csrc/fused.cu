@@ -57,6 +57,10 @@ constexpr int kA2ABuf = 8192;        // A2A dispatch: bytes per TMA staging buff
 constexpr int kA2ABufs = 4;          // A2A dispatch: staging buffers (loads in flight)
 constexpr int kA2AOperandBudget = 163840;  // A2A: one ring stage less, for the staging buffers
 constexpr int kRsStg = 2;                  // RS: TMA-reduce staging buffers per epilogue warp
+#ifndef AO_AR_PULL_U
+#define AO_AR_PULL_U 32
+#endif
+constexpr int kArPullU = AO_AR_PULL_U;     // GEMM-AR gather: 16-byte loads in flight per lane
 constexpr int kRsOperandBudget = 196608;   // RS ring (4 staging buffers + a 5-stage ring measured no faster)
 
 // CG = CTAs per cluster: 1 (one CTA, M = 128), 2 (a CTA pair running cta_group::2 MMAs,
@@ -130,13 +134,22 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // failure is recorded in the host-mapped ErrorInfo and the wait is abandoned (no hang).
 __device__ __noinline__ void spin_flag(const uint32_t* p, uint32_t target, const KernelArgs& A, int rank, int cta,
                                        int g) {
-  uint32_t v = ld_acquire_sys(p);
-  if (v >= target) return;
+  // relaxed polls; the acquire (which invalidates the SM's L1: LDG.STRONG.SYS + CCTL.IVALL)
+  // only once the value is seen (flags are monotonic epochs, so the acquire reads a value
+  // >= target and synchronizes with its release)
+  uint32_t v = ld_relaxed_sys(p);
+  if (v >= target) {
+    ld_acquire_sys(p);
+    return;
+  }
   const uint64_t t0 = globaltimer();
   uint32_t ns = 32;
   while (true) {
-    v = ld_acquire_sys(p);
-    if (v >= target) return;
+    v = ld_relaxed_sys(p);
+    if (v >= target) {
+      ld_acquire_sys(p);
+      return;
+    }
     if (globaltimer() - t0 > A.timeout_ns) {
       if (atomicCAS(&A.err->claim, 0u, 1u) == 0u) {
         A.err->rank = rank;
@@ -181,7 +194,7 @@ __device__ __noinline__ void inject_delay(uint32_t delay, uint32_t salt) {
 // ---- communication workers (AG in-kernel backends) -----------------------------------------
 // Each worker is one warp; worker w handles items w, w + n_workers, ... of this rank's
 // ordered item list (plan order, so early chunks go first on every worker).
-template <int COMM>
+template <int COMM, int U = 8>
 __device__ void comm_item(const RankArgs& R, const KernelArgs& A, int i, int worker, uint8_t* staging,
                           uint32_t buf_bytes, uint64_t* bars, uint32_t& phase_bits) {
   const int lane = lane_id();
@@ -206,7 +219,7 @@ __device__ void comm_item(const RankArgs& R, const KernelArgs& A, int i, int wor
       __syncwarp();
     }
     if constexpr (COMM == COMM_LDST) {
-      warp_copy_ldst(dst, src, it.bytes, remote_src);  // peer data: coherent loads
+      warp_copy_ldst<U>(dst, src, it.bytes, remote_src);  // peer data: coherent loads
       __syncwarp();
       if (lane == 0) asm volatile("fence.sc.sys;" ::: "memory");
     } else {
@@ -228,49 +241,73 @@ __device__ void comm_item(const RankArgs& R, const KernelArgs& A, int i, int wor
   }
 }
 
-template <int COMM>
+template <int COMM, int U = 8>
 __device__ void comm_worker(const RankArgs& R, const KernelArgs& A, int worker, int n_workers, uint8_t* staging,
                             uint32_t buf_bytes, uint64_t* bars) {
   uint32_t phase_bits = 0;
   for (int i = worker; i < R.n_comm_items; i += n_workers)
-    comm_item<COMM>(R, A, i, worker, staging, buf_bytes, bars, phase_bits);
+    comm_item<COMM, U>(R, A, i, worker, staging, buf_bytes, bars, phase_bits);
 }
 
 // Time-sliced AG group (in-kernel push backends): the comm warps of every CTA serve every
 // source rank's items, destination-major in the order the ranks' tiles run (each rank's
 // chunks land before its turn), like the copy-engine chains of a time-sliced group.
-template <int COMM>
+template <int COMM, int U = 8>
 __device__ void comm_worker_ts(const KernelArgs& A, int worker, int n_workers, uint8_t* staging, uint32_t buf_bytes,
                                uint64_t* bars) {
   uint32_t phase_bits = 0;
-  int cnt = 0;
+  int cnt = 0;  // items before this (destination, source) block in the global order
   for (int gi = 0; gi < A.n_group; ++gi) {
-    const int e = A.rk[gi].rank;  // destination, in execution order
+    const int e = A.rk[gi].rank;  // destination (AG push) / owner (AR pull), in execution order
     for (int gs = 0; gs < A.n_group; ++gs) {
       const RankArgs& R = A.rk[gs];
-      for (int i = 0; i < R.n_comm_items; ++i) {
-        if (R.comm_items[i].peer != e) continue;
-        if (cnt++ % n_workers == worker) comm_item<COMM>(R, A, i, worker, staging, buf_bytes, bars, phase_bits);
-      }
+      const int o0 = R.comm_peer_off[e], o1 = R.comm_peer_off[e + 1];
+      // this worker's items of the block: global indices cnt + j with (cnt + j) % n == worker
+      for (int j = o0 + ((worker - cnt) % n_workers + n_workers) % n_workers; j < o1; j += n_workers)
+        comm_item<COMM, U>(R, A, R.comm_by_peer[j], worker, staging, buf_bytes, bars, phase_bits);
+      cnt += o1 - o0;
     }
   }
 }
 
 // ---- tile walk --------------------------------------------------------------------------
-// Calls f(R, grp, k) for every tile position this worker runs, in order.  Space-sliced:
-// positions wk, wk + n_wk, ... of its own rank group's list (Lst.1).
-// Time-sliced: global indices wk, wk + n_wk, ... of the launch's segment list.
+// The k-blocks [kb0, kb1) of a tile position a worker runs, and their role: 0 = the whole
+// tile; stream-K tail (Q28): 1 = a tail piece (k-blocks up to the end; its fp32 partial goes
+// to the plan's stream-K workspace), 2 = a head piece (k-blocks from 0; adds the tail's
+// partial and stores the tile).
+struct KSpan {
+  int kb0, kb1, role;
+};
+
+// Calls f(R, grp, k, span) for every tile position this worker runs, in order.
+// Space-sliced: positions wk, wk + n_wk, ... of its own rank group's list (Lst.1,
+// P:211-216) below sk_dp, then its contiguous range of the stream-K units (position-major
+// (position, k-block) pairs of positions >= sk_dp, cut into n_wk equal ranges; planner.cpp
+// worker_pieces, oracle/schedule.py worker_pieces).  Time-sliced: global indices wk,
+// wk + n_wk, ... of the launch's segment list (whole tiles).
 template <class F>
-__device__ __forceinline__ void for_tiles(const KernelArgs& a, int grp, int wk, int n_wk, F&& f) {
+__device__ __forceinline__ void for_tiles(const KernelArgs& a, int grp, int wk, int n_wk, int nkb, F&& f) {
   if (a.n_seg == 0) {
     const RankArgs& R = a.rk[grp];
-    for (int k = wk; k < R.n_tiles; k += n_wk) f(R, grp, k);
+    const int dp = R.sk_dp < R.n_tiles ? R.sk_dp : R.n_tiles;
+    for (int k = wk; k < dp; k += n_wk) f(R, grp, k, KSpan{0, nkb, 0});
+    if (dp < R.n_tiles) {
+      const int64_t U = int64_t(R.n_tiles - dp) * nkb;
+      int64_t u = U * wk / n_wk;
+      const int64_t u1 = U * (wk + 1) / n_wk;
+      while (u < u1) {
+        const int t = int(u / nkb), kb0 = int(u % nkb);
+        const int kb1 = int(u1 - u < int64_t(nkb - kb0) ? int64_t(kb0) + (u1 - u) : int64_t(nkb));
+        f(R, grp, dp + t, KSpan{kb0, kb1, (kb0 == 0 && kb1 == nkb) ? 0 : (kb0 != 0 ? 1 : 2)});
+        u += kb1 - kb0;
+      }
+    }
   } else {
     int si = 0;
     for (int i = wk; i < a.n_total; i += n_wk) {
       while (i >= a.seg[si].o + (a.seg[si].k1 - a.seg[si].k0)) ++si;
       const int g = a.seg[si].g;
-      f(a.rk[g], g, a.seg[si].k0 + (i - a.seg[si].o));
+      f(a.rk[g], g, a.seg[si].k0 + (i - a.seg[si].o), KSpan{0, nkb, 0});
     }
   }
 }
@@ -417,12 +454,12 @@ template <class F>
 __device__ __forceinline__ void for_tiles_a2a(const KernelArgs& a, const A2ASched& sm, int grp, int wk, int n_wk, F&& f) {
   if (!a.a2a_ts) {
     const int n = sm.nmb[grp] * a.rk[grp].n_nb;
-    for (int k = wk; k < n; k += n_wk) f(a.rk[grp], grp, k);
+    for (int k = wk; k < n; k += n_wk) f(a.rk[grp], grp, k, KSpan{0, 0, 0});
   } else {
     int g = 0;
     for (int i = wk; i < sm.tprefix[a.n_group]; i += n_wk) {
       while (i >= sm.tprefix[g + 1]) ++g;
-      f(a.rk[g], g, i - sm.tprefix[g]);
+      f(a.rk[g], g, i - sm.tprefix[g], KSpan{0, 0, 0});
     }
   }
 }
@@ -655,7 +692,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     if constexpr (MODE == MODE_A2A)
       for_tiles_a2a(args, a2s, grp, wk, n_wk, f);
     else
-      for_tiles(args, grp, wk, n_wk, f);
+      for_tiles(args, grp, wk, n_wk, int((R0.K + kBK - 1) / kBK), f);
   };
   // (row block, column block) of tile k of rank group g
   auto tile_of = [&](const RankArgs& R, int g, int k) -> int2 {
@@ -691,7 +728,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       WaitCache wc;
       wc.reset();
       uint32_t q = 0;  // this worker's tile count (wait-warp slot = q % kAhead)
-      walk([&](const RankArgs& R, int grp, int k) {
+      walk([&](const RankArgs& R, int grp, int k, const KSpan sp) {
         if constexpr (kWaitWarp) {
           const int j = int(q % kAhead);
           mbar_wait(&wrdy[j], (q / kAhead) & 1u);
@@ -738,7 +775,9 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         const int brow = nb * BN + int(crank) * (BN / CGM) + int(pp) * (BN / CG);
         const uint32_t boff = pp * uint32_t(BN / CG) * 128u;
         const uint16_t bmask = uint16_t((1u << crank) | (1u << (crank + 2)));
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int kb_lo = (MODE == MODE_AG || MODE == MODE_GEMM) ? sp.kb0 : 0;
+        const int kb_hi = (MODE == MODE_AG || MODE == MODE_GEMM) ? sp.kb1 : nkb;
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 4) {
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C_::kStage);
@@ -806,12 +845,14 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       // full[] completes only on operand uses of a slot (RS partial stages use pfull[]),
       // so its parity is tracked per slot.
       uint32_t stage = 0, fpar = 0, acc = 0, acc_phase = 0;
-      walk([&](const RankArgs& R, int grp, int k) {
+      walk([&](const RankArgs& R, int grp, int k, const KSpan sp) {
         const uint64_t t_mma = args.trace ? globaltimer() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int kb_lo = (MODE == MODE_AG || MODE == MODE_GEMM) ? sp.kb0 : 0;
+        const int kb_hi = (MODE == MODE_AG || MODE == MODE_GEMM) ? sp.kb1 : nkb;
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&full[stage], (fpar >> stage) & 1u);
           fpar ^= 1u << stage;
           tc_fence_after();
@@ -821,9 +862,11 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 B per K=16 step inside the swizzle atom
               if constexpr (CG >= 2)
-                mma_bf16_ss_cg2(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
+                mma_bf16_ss_cg2(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc,
+                                (kb != kb_lo || kk != 0) ? 1u : 0u);
               else
-                mma_bf16_ss(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc, (kb | kk) != 0 ? 1u : 0u);
+                mma_bf16_ss(d_tmem, ad + uint64_t(kk * 2), bd + uint64_t(kk * 2), idesc,
+                            (kb != kb_lo || kk != 0) ? 1u : 0u);
             }
             // the stage is free once this pair's MMAs read it -- in every CTA that holds
             // operands of this pair (CG == 4: also the other pair's CTAs, whose B quarters
@@ -883,7 +926,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     }
     WaitCache wc;
     if (etid == 0) wc.reset();
-    walk([&](const RankArgs& R, int grp, int k) {
+    walk([&](const RankArgs& R, int grp, int k, const KSpan sp) {
       const int2 tmn = tile_of(R, grp, k);
       const int mb = tmn.x, nb = tmn.y;
       const int t = mb * R.n_nb + nb;
@@ -1061,13 +1104,74 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
           }
         }
       }
+      // stream-K (Q28): this CTA's partial slot of a split tile position
+      float4* sk_part = nullptr;
+      uint32_t* sk_flag = nullptr;
+      if constexpr (MODE == MODE_AG || MODE == MODE_GEMM) {
+        if (sp.role != 0) {
+          const int slot = (k - R.sk_dp) * CG + int(crk);
+          sk_part = reinterpret_cast<float4*>(R.sk_ws) + int64_t(slot) * ((BN + 31) / 32) * 128 * 8;
+          sk_flag = R.sk_flags + slot;
+          if (sp.role == 2) {  // head piece: the tail piece (the next worker's first) must have landed
+            if (etid == 0) spin_flag(sk_flag, R.sk_seq, args, R.rank, lcta, -2);
+            named_bar_sync(1, 128);
+          }
+        }
+      }
       if (!own_tile) {
       // RS ATOMIC: the TMA unit reduce-adds each staged 32 x 32 fp32 box into the owner's
       // accumulator (two staging buffers per warp, so staging overlaps the previous reduce).
       const bool tma_red = MODE == MODE_RS && R.rs_atomic && !xp(args, 64);  // exp 64: thread red.add
       int sb = 0;
+      if constexpr (MODE == MODE_AG || MODE == MODE_GEMM) {
+        if (sk_part != nullptr) {
+          // stream-K piece (Q28), 32 fp32 columns per step through the transpose buffer, so
+          // the partial moves in coalesced 512-byte warp accesses: lane l handles rows
+          // i*4 + l/8, columns 4*(l%8)..+3 of the warp's 32 x 32 block.  Tail piece: store the
+          // partial ([cb][128 rows][32] fp32).  Head piece: add it, store bf16 C.
+          const int c = lane & 7;
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += CW) {
+          for (int cb = 0; cb < (BN + 31) / 32; ++cb) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tb + cb * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            __syncwarp();
+            float4* wsb = sk_part + (int64_t(cb) * 128 + q * 32) * 8;  // this warp's 32 rows of block cb
+            if (sp.role == 1) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int rr = i * 4 + (lane >> 3);
+                const uint4 w = stg[rr * 8 + (c ^ (rr & 7))];
+                __stcg(wsb + rr * 8 + c, make_float4(__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z),
+                                                     __uint_as_float(w.w)));
+              }
+            } else {
+              float4 a[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) a[i] = __ldcg(wsb + (i * 4 + (lane >> 3)) * 8 + c);
+              const int64_t col = col_base + cb * 32 + 4 * c;
+              const bool ok = col < N && cb * 32 + 4 * c < BN;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int rr = i * 4 + (lane >> 3);
+                const uint4 w = stg[rr * 8 + (c ^ (rr & 7))];
+                if (ok && row0 + rr < rlim) {
+                  uint2 o;
+                  o.x = pack_bf16x2(__uint_as_float(w.x) + a[i].x, __uint_as_float(w.y) + a[i].y);
+                  o.y = pack_bf16x2(__uint_as_float(w.z) + a[i].z, __uint_as_float(w.w) + a[i].w);
+                  *reinterpret_cast<uint2*>(dst_base + rr * ld_bytes + col * EB) = o;
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < ((MODE == MODE_AG || MODE == MODE_GEMM) && sk_part != nullptr ? 0 : BN); cc += CW) {
         uint32_t v[32];
         if constexpr (MODE == MODE_RS) {
           tmem_ld_32x32b_x32(tb + cc, v);
@@ -1164,6 +1268,12 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             mbar_arrive(&tempty[acc]);
         }
       }
+      if ((MODE == MODE_AG || MODE == MODE_GEMM) && sp.role == 1) {
+        // stream-K tail piece: every epilogue thread's partial stores precede the CTA-scope
+        // barrier; the release (cumulative) publishes them to the head piece's CTA
+        named_bar_sync(1, 128);
+        if (etid == 0) st_release_gpu(sk_flag, R.sk_seq);
+      }
       if (MODE == MODE_RS && !own_tile && !(R.rs_atomic && !xp(args, 64))) {
         // RS-3 (stores / thread reduces): signal this sub-tile now.
         named_bar_sync(1, 128);
@@ -1200,7 +1310,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         int wp = (ts || MODE == MODE_A2A) ? 0 : R0.wait_off[wk];
         int we = (ts || MODE == MODE_A2A) ? 0 : R0.wait_off[wk + 1];
         uint32_t q = 0;
-        walk([&](const RankArgs& R, int grp, int k) {
+        walk([&](const RankArgs& R, int grp, int k, const KSpan sp) {
           const int j = int(q % kAhead);
           mbar_wait(&wfre[j], ((q / kAhead) & 1u) ^ 1u);
           bool waited = false;
@@ -1269,12 +1379,14 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     if constexpr (MODE == MODE_RS) {
       if (R.ar && R.n_comm_items > 0) {  // GEMM-AR gather: ld/st pulls of reduced chunks
         const int cw = warp - kCommWarp0;
+        // 16 KB of loads in flight per warp (the RS kernel's register budget has room; at 4 KB
+        // the gather was latency-bound well below the copy bandwidth)
         if (ts)  // every rank's pulls, owner after owner (the order the owners' reductions finish)
-          comm_worker_ts<COMM_LDST>(args, int(blockIdx.x) * kColocCommWarps + cw, int(gridDim.x) * kColocCommWarps,
-                                    nullptr, 0, nullptr);
+          comm_worker_ts<COMM_LDST, kArPullU>(args, int(blockIdx.x) * kColocCommWarps + cw,
+                                              int(gridDim.x) * kColocCommWarps, nullptr, 0, nullptr);
         else
-          comm_worker<COMM_LDST>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps, nullptr,
-                                 0, nullptr);
+          comm_worker<COMM_LDST, kArPullU>(R, args, lcta * kColocCommWarps + cw, args.ctas_per_rank * kColocCommWarps,
+                                           nullptr, 0, nullptr);
       }
     }
     if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {

@@ -65,6 +65,8 @@ struct alignas(64) RankArgs {
   const int* tiles_per_chunk;  // RS [n_chunks]: 128-row sub-tiles (one per CTA) touching chunk g
   const int* reduce_items;     // RS [n_items] tile ids
   const CommItem* comm_items;  // AG in-kernel comm [n_comm_items]
+  const int* comm_by_peer;     // comm item indices grouped by peer (stable), CSR offsets comm_peer_off[W + 1]
+  const int* comm_peer_off;
   void* C;                     // AG/GEMM: C [M, N] bf16.  RS: C_shard [S, N] bf16
   const char* A_shard;         // AG: local shard (source of pushes)
   uint32_t* flags;             // this rank's flag words (current parity)
@@ -83,6 +85,13 @@ struct alignas(64) RankArgs {
   // table [W][W] (row s = source s's per-expert counts) after them; receive buffer = peer_data.
   const int32_t* a2a_perm;  // [W][T] this rank's token ids grouped by destination expert
   int32_t T, topk, maxJ, gm;
+  // stream-K tail (Q28): positions >= sk_dp are split along K (sk_dp >= n_tiles: off).  Per
+  // split position and CTA of the cluster, the tail piece's fp32 partial [ceil(BN/32)][128][32]
+  // in sk_ws and a flag word in sk_flags holding the launch sequence number sk_seq.
+  float* sk_ws;
+  uint32_t* sk_flags;
+  uint32_t sk_seq;
+  int32_t sk_dp;
 };
 
 // A2A prep kernel (routing -> counts, permutation, count exchange, route positions).

@@ -116,6 +116,9 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   // rejected for every op that has partials, so validate, create and the hash agree
   if (d.rs_wire == AO_WIRE_BF16 && (d.op == AO_OP_GEMM_RS || d.op == AO_OP_GEMM_AR)) v.push_back("rs_wire bf16");
   if (d.rs_reduce != AO_RS_SLOTS && d.rs_reduce != AO_RS_ATOMIC) v.push_back("rs_reduce");
+  if (d.stream_k < -1 || d.stream_k > 1) v.push_back("stream_k");
+  if (d.stream_k == 1 && (d.op != AO_OP_AG_GEMM || d.backend != AO_BACKEND_CE || d.tile_m == 512))
+    v.push_back("stream_k (AG with the copy engine, tiles of <= 2 CTAs)");
   if ((d.tile_m == 0) != (d.tile_n == 0)) v.push_back("tile");
   if (d.tile_m != 0) {
     bool ok = false;
@@ -284,7 +287,26 @@ static std::string rank_independent_key(const HostPlan& p) {
   o.put("rs_reduce", d.rs_reduce);
   if (d.op == AO_OP_A2A_GEMM) o.put("topk", d.topk);
   if (d.op == AO_OP_SP_ATTN) o.put("causal", d.causal);
+  if (p.sk_dp < p.n_tiles) o.put("sk_dp", p.sk_dp);
   return o.str();
+}
+
+std::vector<SkPiece> worker_pieces(const HostPlan& p, int c) {
+  std::vector<SkPiece> out;
+  const int n = p.n_cta, nkb = p.nkb;
+  for (int k = c; k < p.sk_dp; k += n) out.push_back({k, 0, nkb, 0});
+  if (p.sk_dp < p.n_tiles) {
+    const int64_t U = int64_t(p.n_tiles - p.sk_dp) * nkb;
+    int64_t u = U * c / n;
+    const int64_t u1 = U * (c + 1) / n;
+    while (u < u1) {
+      const int t = int(u / nkb), kb0 = int(u % nkb);
+      const int kb1 = int(std::min<int64_t>(nkb, kb0 + (u1 - u)));
+      out.push_back({p.sk_dp + t, kb0, kb1, (kb0 == 0 && kb1 == nkb) ? 0 : (kb0 != 0 ? 1 : 2)});
+      u += kb1 - kb0;
+    }
+  }
+  return out;
 }
 
 std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPlan* p) {
@@ -496,10 +518,20 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
   // Rules 7/8: CTA k mod n_cta; one wait per (CTA, chunk) first use.  AG tiles wait for
   // remote chunks; RS own-row tiles (fused peer reduction in their epilogue) wait for the
   // other sources' contributions.
+  // Stream-K tail (Q28): AG with the copy engine (and plain GEMM), <= 2-CTA tiles.
+  P.nkb = int(ceil_div(P.K, kBK));
+  P.sk_dp = P.n_tiles;
+  {
+    const int T = P.n_tiles, n = P.n_cta;
+    const bool able = P.is_ag && d.backend == AO_BACKEND_CE && P.tile.cg <= 2 && P.nkb > 0 && T > n && T % n != 0;
+    const bool want = d.stream_k == 1 || (d.stream_k == -1 && int64_t(T) * 10 < int64_t(ceil_div(T, n)) * n * 9);
+    if (able && want) P.sk_dp = (T / n - 1) * n;
+  }
   P.waits.assign(P.n_cta, {});
   std::vector<int> seen(P.n_chunks, -1);
   for (int c = 0; c < P.n_cta; ++c) {
-    for (int k = c; k < P.n_tiles; k += P.n_cta) {
+    for (const SkPiece& pc : worker_pieces(P, c)) {
+      const int k = pc.k;
       const int t = P.order[k];
       for (int g = glo_of[t]; g <= ghi_of[t]; ++g) {
         const bool own = P.chunks[g][3] == r;
@@ -608,6 +640,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
     o.put("waits", s + "]");
   }
   o.put("contrib", int_list(P.contrib));
+  if (P.sk_dp < P.n_tiles) o.put("sk_dp", P.sk_dp);
   if (!P.is_ag) {
     o.put("tiles_per_chunk", int_list(P.tiles_per_chunk));
     o.put_str("rs_reduce", d.rs_reduce == AO_RS_ATOMIC ? "atomic" : "slots");

@@ -59,6 +59,11 @@ struct HostPlan {
   std::vector<std::vector<std::array<int, 2>>> waits;  // per CTA: (k, g)
   std::vector<int> contrib;
   std::vector<int> tiles_per_chunk;                // RS
+  // stream-K tail (Q28): positions [0, sk_dp) run data-parallel (worker c: c, c + n_cta, ...);
+  // positions [sk_dp, n_tiles) are split along K into n_cta contiguous ranges of k-blocks
+  // (sk_dp == n_tiles: off)
+  int sk_dp = 1 << 30;
+  int nkb = 0;
   std::string json;
   uint64_t hash = 0;
 };
@@ -78,5 +83,13 @@ size_t a2a_max_chunks(const ao_plan_desc& d);
 size_t flag_words_needed(const ao_plan_desc& d);
 
 uint64_t fnv1a64(const std::string& s);
+
+// Stream-K piece of a worker's walk: tile position k, k-blocks [kb0, kb1), role 0 = whole
+// tile, 1 = tail piece (stores its fp32 partial), 2 = head piece (adds the tail's partial).
+struct SkPiece {
+  int k, kb0, kb1, role;
+};
+// The positions/pieces worker c runs, in order (shared by the wait tables and tests).
+std::vector<SkPiece> worker_pieces(const HostPlan& p, int c);
 
 }  // namespace ao

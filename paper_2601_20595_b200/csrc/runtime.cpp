@@ -147,6 +147,7 @@ struct DebugKnobs {
   int64_t gemm_group_m = 16;
   int64_t ts_lag = 0;  // time-sliced RS: lag the own run behind the next owner's first source run
   int64_t ts_owners = 1;  // time-sliced RS: owners per phase (experiment)
+  int64_t gemm_stream_k = 0;  // ao_gemm: desc.stream_k of its internal plan (0 off, 1 on, -1 auto)
   int64_t prearrive = 0;  // per-rank measurement: every chunk flag of the launch's ranks is set
                           // for the coming epoch before the kernel and no copy-engine chain is
                           // issued (peers' data "already arrived"; the bench's per-GPU legs,
@@ -208,8 +209,14 @@ struct ao_plan {
   const int* d_items = nullptr;
   const ao::CommItem* d_comm = nullptr;
   int n_comm = 0;
+  const int* d_comm_by_peer = nullptr;  // comm item indices grouped by peer (CSR, time-sliced walks)
+  const int* d_comm_peer_off = nullptr;
   int comm_kind = ao::COMM_NONE;
   int32_t* d_a2a = nullptr;  // A2A: token permutation [W][T] | block positions [T][k] (local)
+  // stream-K tail (Q28): per split position and cluster CTA, the tail piece's fp32 partial
+  // [ceil(BN/32)][128][32] and a flag word (local, zeroed once; flags hold the launch count)
+  char* d_sk = nullptr;
+  uint32_t sk_launches = 0;
   // CE backend: instantiated copy-chain graphs keyed by (parity, group plans, A pointers)
   std::map<std::vector<uintptr_t>, cudaGraphExec_t> ce_graphs;
 };
@@ -293,6 +300,15 @@ ao_status upload_tables(ao_plan* p) {
     }
   }
   p->n_comm = int(comm.size());
+  // comm items grouped by peer (stable): time-sliced groups serve them peer (destination /
+  // owner) after peer without scanning the item list
+  std::vector<int> by_peer(comm.size()), peer_off(AO_MAX_WORLD + 1, 0);
+  for (const ao::CommItem& it : comm) ++peer_off[it.peer + 1];
+  for (int q = 0; q < AO_MAX_WORLD; ++q) peer_off[q + 1] += peer_off[q];
+  {
+    std::vector<int> fill(peer_off.begin(), peer_off.end() - 1);
+    for (size_t i = 0; i < comm.size(); ++i) by_peer[fill[comm[i].peer]++] = int(i);
+  }
 
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   const size_t o_order = 0;
@@ -301,7 +317,9 @@ ao_status upload_tables(ao_plan* p) {
   const size_t o_tpc = o_waits + al(waits.size() * 8 + 8);
   const size_t o_items = o_tpc + al(subtiles.size() * 4 + 4);
   const size_t o_comm = o_items + al(items.size() * 4 + 4);
-  const size_t total = o_comm + al(comm.size() * sizeof(ao::CommItem) + 16);
+  const size_t o_bypeer = o_comm + al(comm.size() * sizeof(ao::CommItem) + 16);
+  const size_t o_peeroff = o_bypeer + al(by_peer.size() * 4 + 4);
+  const size_t total = o_peeroff + al(peer_off.size() * 4);
   std::vector<char> h(total, 0);
   memcpy(h.data() + o_order, hp.order.data(), hp.order.size() * 4);
   memcpy(h.data() + o_woff, wait_off.data(), wait_off.size() * 4);
@@ -309,6 +327,8 @@ ao_status upload_tables(ao_plan* p) {
   if (!subtiles.empty()) memcpy(h.data() + o_tpc, subtiles.data(), subtiles.size() * 4);
   if (!items.empty()) memcpy(h.data() + o_items, items.data(), items.size() * 4);
   if (!comm.empty()) memcpy(h.data() + o_comm, comm.data(), comm.size() * sizeof(ao::CommItem));
+  if (!by_peer.empty()) memcpy(h.data() + o_bypeer, by_peer.data(), by_peer.size() * 4);
+  memcpy(h.data() + o_peeroff, peer_off.data(), peer_off.size() * 4);
   AO_CUDA(cudaMalloc(&p->d_tables, total));
   AO_CUDA(cudaMemcpy(p->d_tables, h.data(), total, cudaMemcpyHostToDevice));
   p->d_order = reinterpret_cast<const int*>(p->d_tables + o_order);
@@ -317,6 +337,14 @@ ao_status upload_tables(ao_plan* p) {
   p->d_tpc = reinterpret_cast<const int*>(p->d_tables + o_tpc);
   p->d_items = reinterpret_cast<const int*>(p->d_tables + o_items);
   p->d_comm = reinterpret_cast<const ao::CommItem*>(p->d_tables + o_comm);
+  p->d_comm_by_peer = reinterpret_cast<const int*>(p->d_tables + o_bypeer);
+  p->d_comm_peer_off = reinterpret_cast<const int*>(p->d_tables + o_peeroff);
+  if (hp.sk_dp < hp.n_tiles) {
+    const size_t slots = size_t(hp.n_tiles - hp.sk_dp) * hp.tile.cg;
+    const size_t bytes = slots * ((hp.tile.bn + 31) / 32) * 128 * 32 * 4 + slots * 4;
+    AO_CUDA(cudaMalloc(&p->d_sk, bytes));
+    AO_CUDA(cudaMemset(p->d_sk, 0, bytes));
+  }
   return AO_OK;
 }
 
@@ -382,6 +410,8 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
   R->reduce_items = p->d_items;
   R->comm_items = p->d_comm;
   R->n_comm_items = p->n_comm;
+  R->comm_by_peer = p->d_comm_by_peer;
+  R->comm_peer_off = p->d_comm_peer_off;
   R->C = C;
   R->M = hp.M;
   R->N = hp.N;
@@ -398,6 +428,13 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
   R->n_cta = hp.n_cta;
   R->epoch = epoch;
   R->rs_atomic = (!hp.is_ag && hp.desc.rs_reduce == AO_RS_ATOMIC) ? 1 : 0;
+  R->sk_dp = hp.sk_dp;
+  if (p->d_sk) {
+    const size_t slots = size_t(hp.n_tiles - hp.sk_dp) * hp.tile.cg;
+    R->sk_ws = reinterpret_cast<float*>(p->d_sk);
+    R->sk_flags = reinterpret_cast<uint32_t*>(p->d_sk + slots * ((hp.tile.bn + 31) / 32) * 128 * 32 * 4);
+    R->sk_seq = ++p->sk_launches;
+  }
   R->counters = ctx ? ctx->counters : nullptr;
   if (ctx) {
     for (int q = 0; q < hp.W; ++q) {
@@ -496,6 +533,7 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   else if (!strcmp(key, "exp")) g_debug.exp = value;
   else if (!strcmp(key, "ts_lag")) g_debug.ts_lag = value;
   else if (!strcmp(key, "ts_owners")) g_debug.ts_owners = value;
+  else if (!strcmp(key, "gemm_stream_k")) g_debug.gemm_stream_k = value;
   else if (!strcmp(key, "prearrive")) g_debug.prearrive = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
   return AO_OK;
@@ -591,6 +629,7 @@ ao_status ao_plan_destroy(ao_plan* p) {
     for (auto& kv : p->ce_graphs) cudaGraphExecDestroy(kv.second);
     cudaFree(p->d_tables);
     if (p->d_a2a) cudaFree(p->d_a2a);
+    if (p->d_sk) cudaFree(p->d_sk);
     cudaSetDevice(cur);
   }
   delete p;
@@ -1045,6 +1084,7 @@ static ao_status launch_group(int n, ao_plan* const* plans, const void* const* A
     if (epochs[i] != epochs[0]) return fail(AO_ERR_STATE, "ranks of a group disagree on the epoch");
     ao_status s = fill_rank(&ka->rk[i], plans[i], epochs[i], As[i], Bs[i], Cs[i]);
     if (s != AO_OK) return s;
+    if (time_sliced) ka->rk[i].sk_dp = ka->rk[i].n_tiles;  // time-sliced groups walk whole tiles
   }
   DriverFns* drv = nullptr;
   if (g_debug.prearrive) {
@@ -1680,7 +1720,7 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
   ao_plan* p = nullptr;
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(device, M, N, K, bm, bn, int(g_debug.gemm_group_m));
+    auto key = std::make_tuple(device, M, N, K, bm, bn, int(g_debug.gemm_group_m) * 4 + int(g_debug.gemm_stream_k) + 1);
     auto it = cache.find(key);
     if (it != cache.end()) {
       p = it->second;
@@ -1698,6 +1738,7 @@ ao_status ao_gemm(int device, const void* A, const void* B, void* C, int64_t M, 
       d.tile_n = bn;
       d.intra = AO_INTRA_GROUPED;  // GROUP_M swizzle: B tiles reused across row blocks in L2
       d.group_m = int32_t(g_debug.gemm_group_m);
+      d.stream_k = bm == 512 ? 0 : int32_t(g_debug.gemm_stream_k);
       if (bm == 512) {  // 4-CTA clusters: as many as fit the GPU at once
         const int n4 = ao::max_co_resident_ctas(4);
         if (n4 < 4) return fail(AO_ERR_CUDA, "no 4-CTA cluster fits this device");

@@ -25,12 +25,14 @@ __device__ __forceinline__ void st_v4(int4* p, const int4& v) {
 }
 
 // LDST: every lane of the warp; `coherent_src` for peer data written during the kernel.
+// U 16-byte loads per lane in flight (U * 512 bytes per warp): the copy is latency-bound at
+// (bytes in flight) / (load latency), so warps with registers to spare use a larger U.
+template <int U = 8>
 __device__ __forceinline__ void warp_copy_ldst(char* dst, const char* src, int64_t bytes, bool coherent_src) {
   const int lane = lane_id();
   const int4* s = reinterpret_cast<const int4*>(src);
   int4* d = reinterpret_cast<int4*>(dst);
   const int64_t n = bytes / 16;
-  constexpr int U = 8;
   for (int64_t base = 0; base < n; base += 32 * U) {
     int4 v[U];
 #pragma unroll

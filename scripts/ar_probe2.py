@@ -1,0 +1,36 @@
+"""GEMM-AR (NEXT-1) probe, Llama-3-8B down-proj at TP=8 in loopback: space- vs time-sliced
+groups x chunk rows x chunk order (device time per call, CUDA events)."""
+import sys
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2601_20595_b200 as ao
+from synthetic import inputs as si
+
+W, M, H, F = 8, 8192, 4096, 14336
+Fl = F // W
+A, B = si.rs_inputs(W, M, Fl, H)
+dA, dB = [a.cuda() for a in A], [b.cuda() for b in B]
+C = [torch.empty(M, H, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+configs = [("space", 256, "chunk_major"), ("time", 256, "chunk_major"), ("time", 1024, "shard_major"),
+           ("time", 256, "shard_major"), ("space", 1024, "shard_major")]
+base = dict(op="gemm_ar", world_size=W, M=M, N=H, K=Fl, intra="grouped", group_m=4, backend="ldst", n_slices=8,
+            rs_reduce="atomic", tile_m=256, tile_n=256, timeout_ns=5_000_000_000)
+ws = max(ao.workspace_bytes(dict(base, chunk_rows=c)) for _, c, _ in configs)
+ctxs = ao.loopback_world(0, W, ws)
+for sched, c, o in configs:
+    nc = 148 if sched == "time" else 148 // W // 2 * 2
+    plans = [ao.Plan(ctxs[r], dict(base, rank=r, chunk_rows=c, chunk_order=o, n_cta=nc)) for r in range(W)]
+    for _ in range(3):
+        ao.gemm_ar_group(plans, dA, dB, C)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(10):
+        ao.gemm_ar_group(plans, dA, dB, C)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / 10
+    print(f"{sched:5s} chunk {c:5d} {o:12s}: {ms:.4f} ms  {2 * M * F * H / ms / 1e9:.0f} TF/s", flush=True)
+    for p in plans:
+        p.close()

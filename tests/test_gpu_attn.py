@@ -1,10 +1,12 @@
 """GPU parity of SP attention (NEXT-4: sequence-parallel attention over all-gathered KV,
 consumed in ring/arrival order) vs the fp64 oracle (oracle/attn.py), through the C ABI.
 
-Tolerance: the north-star bound (1e-2 per element relative to max(1, |ref|)) and a
-Frobenius bound of 5e-3: P enters the P.V MMA as bf16 (the method's bf16-in/fp32-accumulate
-arithmetic, Q27), which alone gives ~2^-9/sqrt(3) relative error, plus the bf16
-output rounding."""
+Tolerance: the north-star bound (1e-2 per element relative to max(1, |ref|)); Frobenius:
+2e-3, or -- P enters the P.V MMA as bf16 (bf16-in / fp32-accumulate, Q27) and the
+output is bf16 -- 1.15x the floor of that arithmetic when it is higher: the relative
+Frobenius error of the bf16-P oracle variant (oracle/attn.py attention_p_bf16, pinned in
+tests/test_oracle_attn.py) rounded to bf16, against the exact fp64 result, computed for the
+same inputs (measured ~2.2-2.3e-3 on N(0,1) scores; the kernels measure ~2.3e-3)."""
 import numpy as np
 import pytest
 import torch
@@ -15,7 +17,26 @@ from synthetic import inputs as si
 
 pytestmark = pytest.mark.gpu
 SMS = 148
-FROB = 5e-3
+FROB = 2e-3  # north star; raised to 1.15x the bf16-P floor per case (see _frob_bound)
+
+
+def _frob_bound(ref, ref_p_bf16):
+    floor = np.linalg.norm(oatt.round_bf16(ref_p_bf16) - ref) / np.linalg.norm(ref)
+    return max(FROB, 1.15 * floor)
+
+
+def _check_full(got, Qn, Kn, Vn, r, causal, what):
+    ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=causal)
+    refb = oatt.sp_attention_p_bf16(Qn, Kn, Vn, r, 128 ** -0.5, causal=causal)
+    ok, e, f = on.check_tolerance(got, ref, frob_rel=_frob_bound(ref, refb))
+    assert ok, f"{what}: max elem err {e:.3e}, frob {f:.3e} (bound {_frob_bound(ref, refb):.3e})"
+
+
+def _check_rows(got, Qn, Kn, Vn, r, heads, rows, causal, what):
+    ref = oatt.sp_attention_rows(Qn, Kn, Vn, r, 128 ** -0.5, heads, rows, causal=causal)
+    refb = oatt.sp_attention_rows(Qn, Kn, Vn, r, 128 ** -0.5, heads, rows, causal=causal, p_bf16=True)
+    ok, e, f = on.check_tolerance(got, ref, frob_rel=_frob_bound(ref, refb))
+    assert ok, f"{what}: max elem err {e:.3e}, frob {f:.3e} (bound {_frob_bound(ref, refb):.3e})"
 
 
 @pytest.fixture(scope="module")
@@ -46,10 +67,7 @@ def _run(ao, ctxs, plans, Q, K, V):
 def _check(O, Q, K, V, what):
     Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
     for r in range(len(O)):
-        ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5)
-        got = O[r].float().cpu().numpy()
-        ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
-        assert ok, f"{what} rank {r}: max elem err {e:.3e}, frob {f:.3e}"
+        _check_full(O[r].float().cpu().numpy(), Qn, Kn, Vn, r, False, f"{what} rank {r}")
 
 
 @pytest.mark.parametrize("W,H,S,C", [(1, 1, 128, 128), (1, 2, 256, 128), (2, 2, 256, 256), (4, 2, 128, 128),
@@ -91,10 +109,8 @@ def test_sp_attn_llama_sampled(ao):
     Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
     rows = np.array([0, 127, 128, 1000, 2047])
     for r in (0, 5):
-        ref = oatt.sp_attention_rows(Qn, Kn, Vn, r, 128 ** -0.5, [0, 13, 31], rows)
         got = O[r][[0, 13, 31]][:, rows].float().cpu().numpy()
-        ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
-        assert ok, f"llama sampled rank {r}: {e:.3e} {f:.3e}"
+        _check_rows(got, Qn, Kn, Vn, r, [0, 13, 31], rows, False, f"llama sampled rank {r}")
 
 
 @pytest.mark.parametrize("W,H,S", [(1, 2, 256), (2, 2, 256), (4, 1, 512), (8, 2, 256)])
@@ -107,9 +123,7 @@ def test_sp_attn_causal_vs_oracle(ao, W, H, S, ts):
     O = _run(ao, ctxs, plans, Q, K, V)
     Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
     for r in range(W):
-        ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=True)
-        ok, e, f = on.check_tolerance(O[r].float().cpu().numpy(), ref, frob_rel=FROB)
-        assert ok, f"causal W={W} H={H} S={S} ts={ts} rank {r}: {e:.3e} {f:.3e}"
+        _check_full(O[r].float().cpu().numpy(), Qn, Kn, Vn, r, True, f"causal W={W} H={H} S={S} ts={ts} rank {r}")
 
 
 def test_sp_attn_causal_llama_sampled(ao):
@@ -120,10 +134,8 @@ def test_sp_attn_causal_llama_sampled(ao):
     Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
     rows = np.array([0, 127, 128, 255, 256, 1000, 2047])
     for r in (0, 3, 7):
-        ref = oatt.sp_attention_rows(Qn, Kn, Vn, r, 128 ** -0.5, [0, 31], rows, causal=True)
         got = O[r][[0, 31]][:, rows].float().cpu().numpy()
-        ok, e, f = on.check_tolerance(got, ref, frob_rel=FROB)
-        assert ok, f"causal llama rank {r}: {e:.3e} {f:.3e}"
+        _check_rows(got, Qn, Kn, Vn, r, [0, 31], rows, True, f"causal llama rank {r}")
 
 
 @pytest.mark.parametrize("causal", [0, 1])
@@ -144,9 +156,8 @@ def test_sp_attn_per_rank_calls_on_separate_streams(ao, causal):
         for c in ctxs:
             c.check_async()
         for r in range(W):
-            ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=bool(causal))
-            ok, e, f = on.check_tolerance(O[r].float().cpu().numpy(), ref, frob_rel=FROB)
-            assert ok, f"per-rank attn causal={causal} it={it} r{r}: {e:.3e} {f:.3e}"
+            _check_full(O[r].float().cpu().numpy(), Qn, Kn, Vn, r, bool(causal),
+                        f"per-rank attn causal={causal} it={it} r{r}")
 
 
 @pytest.mark.parametrize("S,causal", [(256, 0), (256, 1), (128, 0)])
@@ -163,9 +174,7 @@ def test_sp_attn_peaked_scores_rescale_and_underflow(ao, S, causal):
     O = _run(ao, ctxs, plans, Q, K, V)
     Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
     for r in range(W):
-        ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=bool(causal))
-        ok, e, f = on.check_tolerance(O[r].float().cpu().numpy(), ref, frob_rel=FROB)
-        assert ok, f"peaked S={S} causal={causal} rank {r}: {e:.3e} {f:.3e}"
+        _check_full(O[r].float().cpu().numpy(), Qn, Kn, Vn, r, bool(causal), f"peaked S={S} causal={causal} rank {r}")
 
 
 @pytest.mark.parametrize("causal", [0, 1])
@@ -211,6 +220,4 @@ def test_sp_attn_causal_epochs_without_host_sync(ao):
         Q, K, V = ins[e]
         Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
         for r in range(W):
-            ref = oatt.sp_attention(Qn, Kn, Vn, r, 128 ** -0.5, causal=True)
-            ok, el, fr = on.check_tolerance(outs[e][0][r].float().cpu().numpy(), ref, frob_rel=FROB)
-            assert ok, f"causal epoch {e} rank {r}: {el:.3e} {fr:.3e}"
+            _check_full(outs[e][0][r].float().cpu().numpy(), Qn, Kn, Vn, r, True, f"causal epoch {e} rank {r}")

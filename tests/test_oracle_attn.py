@@ -111,3 +111,40 @@ def test_causal_last_rank_last_row_equals_full():
     rows = np.array([0, 3, 7])
     np.testing.assert_allclose(oa.sp_attention_rows(Q, K, V, 1, d ** -0.5, [1], rows, causal=True),
                                oa.sp_attention(Q, K, V, 1, d ** -0.5, causal=True)[[1]][:, rows], rtol=1e-13, atol=1e-13)
+
+
+# ---- bf16-P arithmetic floor (Q27) --------------------------------------------
+def test_round_bf16_matches_torch():
+    import torch
+    x = np.random.default_rng(1).standard_normal(200000).astype(np.float32) * 37.0
+    x[:4] = [0.0, 1.0, 2.0 ** -130, 65504.0]
+    assert np.array_equal(oa.round_bf16(x), torch.from_numpy(x).bfloat16().double().numpy())
+
+
+def test_p_bf16_variant_reduces_to_exact_when_p_is_representable():
+    # Q = 0: every score 0, p = 1 exactly (bf16-representable): both variants give mean(V)
+    rng = np.random.default_rng(2)
+    Q = np.zeros((2, 8, 128))
+    K = rng.standard_normal((2, 64, 128))
+    V = rng.standard_normal((2, 64, 128))
+    a = oa.attention(Q, K, V, 128 ** -0.5)
+    b = oa.attention_p_bf16(Q, K, V, 128 ** -0.5)
+    assert np.allclose(a, b, rtol=0, atol=1e-13)
+    assert np.allclose(a, V.mean(axis=1, keepdims=True).repeat(8, axis=1), atol=1e-13)
+
+
+def test_bf16_p_floor_exceeds_the_gemm_bound():
+    """With P rounded to bf16 (the P.V MMA's input) and the output rounded to bf16, the
+    relative Frobenius error against the exact fp64 result is ~2.2e-3 on the bench's
+    N(0,1) scores -- above the north star's 2e-3 for GEMM outputs.  This is why the attention
+    tests bound the kernel by the measured floor of this arithmetic, not by 2e-3."""
+    from synthetic import inputs as si
+    Q, K, V = si.attn_inputs(8, 1, 256, 128, salt=81)
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    a = oa.sp_attention(Qn, Kn, Vn, 0, 128 ** -0.5)
+    b = oa.round_bf16(oa.sp_attention_p_bf16(Qn, Kn, Vn, 0, 128 ** -0.5))
+    frob = np.linalg.norm(b - a) / np.linalg.norm(a)
+    assert 2.0e-3 < frob < 3.0e-3, frob
+    # the P rounding alone: ~2^-9 relative per probability, averaged over the keys
+    p_only = oa.sp_attention_p_bf16(Qn, Kn, Vn, 0, 128 ** -0.5)
+    assert 1.0e-3 < np.linalg.norm(p_only - a) / np.linalg.norm(a) < 2.0e-3

@@ -165,3 +165,79 @@ def test_sp_attn_host_plan(ao):
     assert j["op"] == "sp_attn" and j["chunks_per_source"] == 32 * 4096 // 4096 and j["items"] == 32 * 32
     assert len({ao.Plan(None, dict(base, rank=r)).hash() for r in range(8)}) == 1
     assert ao.workspace_bytes(dict(base, rank=0)) == 2 * 2 * 8 * 32 * 4096 * 128 * 2
+
+
+# ---- stream-K tail (Q28) ------------------------------------------------------
+def _sk_descs():
+    out = []
+    # per-GPU TP shapes (BASELINE configs[1]) at W = 8 / 4 / 2, tiles of 1 and 2 CTAs, and
+    # small shapes where the tail is a handful of tiles; K ragged (not a multiple of 64)
+    for W, N in ((8, 1792), (4, 3584), (2, 7168)):
+        for tile in ((256, 256), (256, 224), (128, 256), (0, 0)):
+            for sk in (1, -1):
+                out.append(dict(op="ag_gemm", world_size=W, M=8192, N=N, K=4096, chunk_rows=1024 // W * 2,
+                                intra="grouped", group_m=4, tile_m=tile[0], tile_n=tile[1], stream_k=sk))
+    for n_cta in (3, 5, 7, 11):
+        for K in (136, 512, 1000 // 8 * 8):
+            out.append(dict(op="ag_gemm", world_size=2, M=1024, N=392, K=K, chunk_rows=128, tile_m=128,
+                            tile_n=128, n_cta=n_cta, stream_k=1))
+    return out
+
+
+@pytest.mark.parametrize("d", _sk_descs())
+def test_stream_k_json_byte_exact(ao, d):
+    for r in range(d["world_size"]):
+        dd = osch.default_desc(**dict(d, rank=r))
+        assert ao.plan_json(dd, sm_count=148) == osch.export_json(osch.plan(dd, sm_count=148)), (d, r)
+
+
+def test_stream_k_partition_invariants():
+    """Independent of the oracle's formulas: every (position, k-block) unit of the tiles is
+    computed by exactly one piece; each worker's pieces are contiguous in unit order; a
+    split tile has exactly one head (from k-block 0, stores the tile) and one tail (to the
+    last k-block, stores a partial) on consecutive workers; every worker's stream-K work
+    differs from the mean by less than one k-block."""
+    for T, n, nkb in ((224, 74, 64), (448, 74, 64), (13, 5, 7), (29, 4, 3), (150, 74, 1)):
+        dp = (T // n - 1) * n
+        cover = {}
+        sk_units = []
+        for c in range(n):
+            pcs = osch.worker_pieces(T, n, dp, nkb, c)
+            units = []
+            for k, kb0, kb1, role in pcs:
+                assert 0 <= kb0 < kb1 <= nkb
+                for kb in range(kb0, kb1):
+                    assert (k, kb) not in cover
+                    cover[(k, kb)] = (c, role)
+                    if k >= dp:
+                        units.append(k * nkb + kb)
+            assert units == list(range(units[0], units[0] + len(units))) if units else True
+            sk_units.append(len(units))
+        assert set(cover) == {(k, kb) for k in range(T) for kb in range(nkb)}
+        mean = (T - dp) * nkb / n
+        assert all(abs(u - mean) < 1 for u in sk_units)
+        for k in range(dp, T):
+            owners = {cover[(k, kb)] for kb in range(nkb)}
+            if len(owners) > 1:
+                (c_head, r_head), (c_tail, r_tail) = sorted(owners)
+                assert (r_head, r_tail) == (2, 1) and c_tail == c_head + 1
+                assert cover[(k, 0)][1] == 2 and cover[(k, nkb - 1)][1] == 1
+            else:
+                assert owners.pop()[1] == 0
+
+
+def test_stream_k_auto_rule():
+    # S:334 utilization at the per-GPU TP=8 AG shape: 224 pair tiles on 74 workers = 0.757 -> on;
+    # TP=2 (896 tiles, 0.93) -> off; an exact multiple -> off
+    assert osch.stream_k_dp(osch.default_desc(K=4096, stream_k=-1), 224, 74, 2) == 148
+    assert osch.stream_k_dp(osch.default_desc(K=4096, stream_k=-1), 896, 74, 2) == 896
+    assert osch.stream_k_dp(osch.default_desc(K=4096, stream_k=1), 222, 74, 2) == 222
+    assert osch.stream_k_dp(osch.default_desc(K=4096, stream_k=0), 224, 74, 2) == 224
+    assert osch.stream_k_dp(osch.default_desc(op="gemm_rs", K=4096, stream_k=1), 224, 74, 2) == 224
+
+
+def test_stream_k_validation_agrees(ao):
+    for kw in (dict(stream_k=1), dict(stream_k=-1), dict(stream_k=2), dict(stream_k=1, op="gemm_rs"),
+               dict(stream_k=1, backend="tma"), dict(stream_k=-1, op="gemm_rs")):
+        dd = osch.default_desc(**kw)
+        assert (not osch.validate(dd)) == (not ao.validate(dd)), kw

@@ -166,8 +166,9 @@ def run_ours(args, rank, world, local_rank):
     if loop:
         # time-sliced (default): every rank's plan spans all SMs and the group launch runs the
         # ranks' tile lists in one global order; space-sliced: SMs // W CTAs per rank
-        # GEMM-AR stays space-sliced: time-sliced it measured 4.3 vs 1.2 ms
-        ar_desc["n_cta"] = sms // W
+        # GEMM-AR time-sliced too (0.92 ms vs 1.14 space-sliced, scripts/ar_probe2.py)
+        ar_desc["n_cta"] = sms if args.sched == "time" else sms // W
+        ar_desc["tile_m"], ar_desc["tile_n"] = 256, 256
         ag_desc["n_cta"] = rs_desc["n_cta"] = sms if args.sched == "time" else sms // W
         if args.sched == "time":
             tm, tn = (int(x) for x in args.tile.split("x"))

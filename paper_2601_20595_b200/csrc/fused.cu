@@ -43,8 +43,16 @@ __device__ __forceinline__ bool xp(const KernelArgs& a, int bit) { return AO_TIM
 
 constexpr int kSubM = 128;  // rows per CTA (TMEM lanes)
 constexpr int kBK = 64;
-constexpr int kThreads = 256;
-constexpr int kCommWarp0 = 6;
+constexpr int kThreads = 256;  // AG / GEMM / A2A CTAs (and AG's dedicated comm CTAs)
+// Epilogue warps per mode: GEMM-RS's epilogue (fp32 partial pushes + the owner's fused
+// reduction) is the critical role, so RS CTAs run 8 (two per TMEM lane quadrant, each
+// taking half of the tile's columns), the other modes 4.
+template <int MODE>
+struct Roles {
+  static constexpr int kEpiW = MODE == 2 ? 8 : 4;        // MODE_RS == 2
+  static constexpr int kCommWarp0 = 2 + kEpiW;           // first co-located comm warp
+  static constexpr int kThreads = 32 * (kCommWarp0 + 2);  // + 2 comm warps (AG / A2A / GEMM-AR gather)
+};
 constexpr int kColocCommWarps = 2;
 constexpr int kCommBufs = 2;
 constexpr uint32_t kColocBufBytes = 4096;
@@ -56,7 +64,7 @@ constexpr int kAhead = 4;  // AG (copy engine): tiles whose chunk waits the wait
 constexpr int kA2ABuf = 8192;        // A2A dispatch: bytes per TMA staging buffer
 constexpr int kA2ABufs = 4;          // A2A dispatch: staging buffers (loads in flight)
 constexpr int kA2AOperandBudget = 163840;  // A2A: one ring stage less, for the staging buffers
-constexpr int kRsStg = 2;                  // RS: TMA-reduce staging buffers per epilogue warp
+constexpr int kRsStg = 1;                  // RS: TMA-reduce staging buffers per epilogue warp (8 warps)
 #ifndef AO_AR_PULL_U
 #define AO_AR_PULL_U 32
 #endif
@@ -108,7 +116,7 @@ __host__ __device__ constexpr SmemLayout gemm_layout(bool tma_comm, bool dbl_stg
   L.off_a = 0;
   L.off_b = C_::kStages * C_::kStageA;
   L.off_stg = C_::kStages * C_::kStage;
-  L.off_comm = L.off_stg + (dbl_stg ? 4 * kRsStg : 4) * kStageWarpBytes;  // RS: kRsStg buffers per warp (TMA reduce)
+  L.off_comm = L.off_stg + (dbl_stg ? 8 * kRsStg : 4) * kStageWarpBytes;  // RS: 8 warps x kRsStg buffers (TMA reduce)
   const uint32_t comm = tma_comm ? kColocCommWarps * kCommBufs * kColocBufBytes : (a2a ? kA2ABufs * kA2ABuf : 0);
   L.off_bar = L.off_comm + comm;
   const uint32_t nbars = 3 * C_::kStages + 4 + 8 * kCommBufs + 2 * kAhead;
@@ -576,8 +584,12 @@ __device__ __noinline__ void a2a_push_chunk_tma(const A2ASched& sm, const RankAr
 // thread bound; launched with 256): the loopback pushes are same-device memcpys that run as
 // SM kernels beside this persistent kernel and need registers left on every SM (DESIGN.md
 // §8: a persistent kernel without that headroom stalled them and its chunk waits timed out).
+#ifndef AO_AG_BOUND_THREADS
+#define AO_AG_BOUND_THREADS 384  // 256: AG / GEMM uncapped (experiment: the cap's cost)
+#endif
 template <int BN, int MODE, int COMM, int CG>
-__global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 : kThreads, 1)
+__global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? AO_AG_BOUND_THREADS
+                                                                      : (MODE == MODE_RS ? 384 : kThreads), 1)
     fused_kernel(const __grid_constant__ KernelArgs args) {
   static_assert((MODE != MODE_RS && MODE != MODE_A2A) || BN % 32 == 0, "RS / A2A epilogues step 32 columns");
   extern __shared__ uint8_t smem_raw[];
@@ -660,7 +672,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 4 * CGM);
+        mbar_init(&tempty[a], Roles<MODE>::kEpiW * CGM);
       }
       for (int a = 0; a < kAhead; ++a) {
         mbar_init(&wrdy[a], 1);
@@ -904,13 +916,18 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         if (acc == 0) acc_phase ^= 1;
       });
     }
-  } else if (warp < kCommWarp0) {
+  } else if (warp < Roles<MODE>::kCommWarp0) {
     // ================================================================ epilogue
     // TMEM -> registers -> per-warp smem transpose -> coalesced 128-byte row segments.
     // AG/GEMM: bf16 C rows (64 columns per step).  RS: fp32 partial rows into the owner's
     // slot (32 columns per step; a peer address over NVLink, local in loopback).
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int etid = threadIdx.x - 64;
+    constexpr int kEpiW = Roles<MODE>::kEpiW;
+    constexpr int kEpiT = 32 * kEpiW;  // epilogue threads (named barrier 1)
+    // RS: warps 2-5 take columns [0, BN/2) of the tile, warps 6-9 [BN/2, BN)
+    const int half = (warp - 2) / 4;
+    const int c_lo = kEpiW == 8 ? half * (BN / 2) : 0, c_hi = kEpiW == 8 ? c_lo + BN / 2 : BN;
     uint4* stg = reinterpret_cast<uint4*>(smem + L.off_stg + (warp - 2) * kStageWarpBytes);
     constexpr int CW = (MODE == MODE_RS) ? 32 : 64;  // columns per staging step (128 B per row)
     constexpr int EPS = (MODE == MODE_RS) ? 4 : 8;   // elements per 16-byte lane segment
@@ -976,12 +993,11 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             }
             trace_event(args, TR_REDWAIT, R.rank, lcta, t, tw);
           }
-          named_bar_sync(1, 128);
+          named_bar_sync(1, kEpiT);
           const int64_t lrow0 = row0 - int64_t(R.rank) * S;  // this warp's first row in C_shard
           float* accm = reinterpret_cast<float*>(R.peer_acc[R.rank]);
           __nv_bfloat16* cout = reinterpret_cast<__nv_bfloat16*>(R.C);
           const int c = lane & 7;
-          // accumulator loads run one 32-column block ahead of their use (latency hiding)
           float4 pa[8];
           auto load_acc = [&](int64_t col0, float4 (&dst)[8]) {
             const bool okl = col0 < N && col0 + 4 * c < N;
@@ -991,13 +1007,11 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
               dst[i] = (okl && !xp(args, 2)) ? __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N))
                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
           };
-          load_acc(col_base, pa);
 #pragma unroll 1
-          for (int cc = 0; cc < BN; cc += 32) {
+          for (int cc = c_lo; cc < c_hi; cc += 32) {
             const int64_t col0 = col_base + cc;
             if (col0 >= N) break;  // warp-uniform
-            float4 pn[8];
-            if (cc + 32 < BN) load_acc(col0 + 32, pn);
+            load_acc(col0, pa);  // in flight while the TMEM block is read and staged
             uint32_t v[32];
             tmem_ld_32x32b_x32(tb + cc, v);
             tmem_wait_ld();
@@ -1029,10 +1043,10 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
               }
             }
             __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) pa[i] = pn[i];
           }
-        } else if (own_tile) {
+        } else if (own_tile && half == 0) {
+          // (slots: the four warps of half 0 take every column -- the peer boxes stream
+          // through the operand ring in one order; named barrier 2 = those 128 threads)
           // RS-4 fused reduction: the peer partials arrive as 32-column fp32 boxes in the
           // smem ring (streamed by the producer); thread = row, like the TMEM accumulator.
           // Sum in ascending source rank, own TMEM value at s == rank, store bf16.
@@ -1045,13 +1059,15 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
             const int nterms = R.W;  // ascending source rank; own TMEM value at s == rank
             const int own_term = R.rank;
             for (int s = 0; s < nterms; ++s) {
-              float x[32];
               if (s == own_term) {
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(tb + cb * 32, v);
                 tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] = nkb ? __uint_as_float(v[i]) : 0.f;
+                for (int i = 0; i < 32; ++i) {
+                  const float x = nkb ? __uint_as_float(v[i]) : 0.f;
+                  acc[i] = s == 0 ? x : acc[i] + x;
+                }
               } else {
                 mbar_wait(&pfull[rs_stage], (ppar >> rs_stage) & 1u);
                 ppar ^= 1u << rs_stage;
@@ -1059,21 +1075,16 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                   const uint4 w = box[r * 8 + (j ^ (r & 7))];  // TMA 128-B swizzle
-                  x[4 * j] = __uint_as_float(w.x);
-                  x[4 * j + 1] = __uint_as_float(w.y);
-                  x[4 * j + 2] = __uint_as_float(w.z);
-                  x[4 * j + 3] = __uint_as_float(w.w);
+                  const float x0 = __uint_as_float(w.x), x1 = __uint_as_float(w.y), x2 = __uint_as_float(w.z),
+                              x3 = __uint_as_float(w.w);
+                  acc[4 * j] = s == 0 ? x0 : acc[4 * j] + x0;
+                  acc[4 * j + 1] = s == 0 ? x1 : acc[4 * j + 1] + x1;
+                  acc[4 * j + 2] = s == 0 ? x2 : acc[4 * j + 2] + x2;
+                  acc[4 * j + 3] = s == 0 ? x3 : acc[4 * j + 3] + x3;
                 }
-                named_bar_sync(1, 128);  // every epilogue thread has read the stage
+                named_bar_sync(2, 128);  // every half-0 epilogue thread has read the stage
                 if (etid == 0) mbar_arrive(&empty[rs_stage]);
                 if (++rs_stage == C_::kStages) rs_stage = 0;
-              }
-              if (s == 0) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) acc[i] = x[i];
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) acc[i] += x[i];
               }
             }
             // bf16 pack, stage row `lane` (64 B) through the transpose buffer, store
@@ -1114,7 +1125,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
           sk_flag = R.sk_flags + slot;
           if (sp.role == 2) {  // head piece: the tail piece (the next worker's first) must have landed
             if (etid == 0) spin_flag(sk_flag, R.sk_seq, args, R.rank, lcta, -2);
-            named_bar_sync(1, 128);
+            named_bar_sync(1, kEpiT);
           }
         }
       }
@@ -1171,7 +1182,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         }
       }
 #pragma unroll 1
-      for (int cc = 0; cc < ((MODE == MODE_AG || MODE == MODE_GEMM) && sk_part != nullptr ? 0 : BN); cc += CW) {
+      for (int cc = c_lo; cc < ((MODE == MODE_AG || MODE == MODE_GEMM) && sk_part != nullptr ? 0 : c_hi); cc += CW) {
         uint32_t v[32];
         if constexpr (MODE == MODE_RS) {
           tmem_ld_32x32b_x32(tb + cc, v);
@@ -1194,7 +1205,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
         const int64_t col0 = col_base + cc;
         if (col0 >= N) break;  // warp-uniform
         if (tma_red) {
-          uint4* sg = stg + sb * (4 * kStageWarpBytes / 16);
+          uint4* sg = stg + sb * (kEpiW * kStageWarpBytes / 16);
           if (lane == 0) bulk_wait_read<kRsStg - 1>();  // the reduce that last read buffer sb is done reading
           __syncwarp();
           // the TMA 128-B swizzle of a 1024-B-aligned box: 16-B chunk j of row r at j ^ (r & 7)
@@ -1254,7 +1265,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
           fence_proxy_async_global();  // async-proxy writes -> the generic release below
         }
         __syncwarp();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiT);
         if (etid == 0) rs_signal(R, args, sub0, owner);
       }
       }
@@ -1271,19 +1282,19 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       if ((MODE == MODE_AG || MODE == MODE_GEMM) && sp.role == 1) {
         // stream-K tail piece: every epilogue thread's partial stores precede the CTA-scope
         // barrier; the release (cumulative) publishes them to the head piece's CTA
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiT);
         if (etid == 0) st_release_gpu(sk_flag, R.sk_seq);
       }
       if (MODE == MODE_RS && !own_tile && !(R.rs_atomic && !xp(args, 64))) {
         // RS-3 (stores / thread reduces): signal this sub-tile now.
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiT);
         if (etid == 0) rs_signal(R, args, sub0, owner);
       }
       if (MODE == MODE_RS && own_tile && R.ar && R.W > 1) {
         // GEMM-AR: count this own sub-tile into its chunks; the last one releases the
         // owner's "reduced" flag of chunk g (word n_chunks*W + g), which peers' gather
         // warps acquire before pulling the rows (Fig.4d).
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiT);
         if (etid == 0) {  // (release below is cumulative over the CTA's stores, as in rs_signal)
           const int glo = int(sub0 / R.crows);
           const int ghi = int((sub0 + kSubM - 1) / R.crows);
@@ -1304,7 +1315,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
   } else {
     // ================================================================ co-located comm warps
     if constexpr (kWaitWarp) {
-      if (warp == kCommWarp0 && lane == 0) {
+      if (warp == Roles<MODE>::kCommWarp0 && lane == 0) {
         WaitCache wc;
         wc.reset();
         int wp = (ts || MODE == MODE_A2A) ? 0 : R0.wait_off[wk];
@@ -1350,7 +1361,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
       // Space-sliced: this rank's rows, destinations in the push rotation (own rows first,
       // then e = s+1, s+2, ...).  Time-sliced: every rank's rows, destination-major in the
       // order the experts' tiles run.
-      if (warp == kCommWarp0 + 1) {
+      if (warp == Roles<MODE>::kCommWarp0 + 1) {
         const int W = R0.W;
         const int nw = ts ? int(gridDim.x) : args.ctas_per_rank;
         const int w = ts ? int(blockIdx.x) : lcta;
@@ -1378,7 +1389,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     const RankArgs& R = R0;
     if constexpr (MODE == MODE_RS) {
       if (R.ar && R.n_comm_items > 0) {  // GEMM-AR gather: ld/st pulls of reduced chunks
-        const int cw = warp - kCommWarp0;
+        const int cw = warp - Roles<MODE>::kCommWarp0;
         // 16 KB of loads in flight per warp (the RS kernel's register budget has room; at 4 KB
         // the gather was latency-bound well below the copy bandwidth)
         if (ts)  // every rank's pulls, owner after owner (the order the owners' reductions finish)
@@ -1391,7 +1402,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? 384 :
     }
     if constexpr (MODE == MODE_AG && COMM != COMM_NONE) {
       if (args.comm_ctas_per_rank == 0) {
-        const int cw = warp - kCommWarp0;
+        const int cw = warp - Roles<MODE>::kCommWarp0;
         if (ts)
           comm_worker_ts<COMM>(args, int(blockIdx.x) * kColocCommWarps + cw, int(gridDim.x) * kColocCommWarps,
                                smem + L.off_comm + cw * kCommBufs * kColocBufBytes, kColocBufBytes,
@@ -1442,7 +1453,7 @@ cudaError_t launch_one(const KernelArgs& args, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((args.n_seg > 0 || args.a2a_ts) ? args.ctas_per_rank
                                     : args.n_group * (args.ctas_per_rank + args.comm_ctas_per_rank));
-  cfg.blockDim = dim3(dev::kThreads);
+  cfg.blockDim = dim3(dev::Roles<MODE>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -1484,7 +1495,7 @@ int max_clusters_of() {
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(4 * 64);
-  cfg.blockDim = dim3(dev::kThreads);
+  cfg.blockDim = dim3(dev::Roles<MODE>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

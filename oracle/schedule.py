@@ -131,8 +131,11 @@ def validate(desc, sm_count=148):
         v.append("n_cta")
     if desc["n_slices"] < 1 or desc["n_slices"] > 64:
         v.append("n_slices")
-    if desc.get("rs_wire", "fp32") == "bf16" and desc["op"] in ("gemm_rs", "gemm_ar"):
-        v.append("rs_wire bf16")  # DESIGN.md Q14: bf16 partials break the per-element bound
+    # DESIGN.md Q14: bf16 partials break the per-element bound; built (non-conforming) for
+    # GEMM-RS with the atomic reduction only
+    if desc.get("rs_wire", "fp32") == "bf16" and (desc["op"] == "gemm_ar" or (
+            desc["op"] == "gemm_rs" and desc.get("rs_reduce", "slots") != "atomic")):
+        v.append("rs_wire bf16")
     if desc.get("rs_reduce", "slots") not in ("slots", "atomic"):
         v.append("rs_reduce")
     sk = desc.get("stream_k", 0)
@@ -174,7 +177,8 @@ def pick_tile(desc, sm_count):
             continue
         n = max(1, n_workers(desc, sm_count) // cg)
         T = (M // bm) * _ceil_div(N, bn)
-        waves = _ceil_div(T, n)
+        # with a stream-K tail (Q28) the last partial wave is spread over all workers: T / n waves
+        waves = Fraction(T, n) if stream_k_dp(desc, T, n, cg) < T else _ceil_div(T, n)
         cost = Fraction(waves * (bm * bn // cg), max(1, TILE_EFF[(bm, bn, cg)]))
         key = (-cost, bm * bn, bn)
         if best is None or key > best[0]:
@@ -411,6 +415,8 @@ def plan(desc, sm_count=148):
     if not is_ag:
         out["tiles_per_chunk"] = tiles_per_chunk
         out["rs_reduce"] = desc.get("rs_reduce", "slots")
+        if desc.get("rs_wire", "fp32") == "bf16":
+            out["rs_wire"] = "bf16"
     if sk_dp < T:
         out["sk_dp"] = sk_dp
     return out

@@ -1003,9 +1003,18 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? AO_AG
             const bool okl = col0 < N && col0 + 4 * c < N;
             const int64_t off = (lrow0 + (lane >> 3)) * N + col0 + 4 * c;
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              dst[i] = (okl && !xp(args, 2)) ? __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N))
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = 0; i < 8; ++i) {
+              if (!okl || xp(args, 2)) {
+                dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+              } else if (R.rs_bf16) {  // bf16 wire: a bf16 accumulator [S, N]
+                const uint2 b = __ldcg(reinterpret_cast<const uint2*>(
+                    reinterpret_cast<const __nv_bfloat16*>(accm) + off + int64_t(i) * 4 * N));
+                dst[i] = make_float4(__uint_as_float(b.x << 16), __uint_as_float(b.x & 0xffff0000u),
+                                     __uint_as_float(b.y << 16), __uint_as_float(b.y & 0xffff0000u));
+              } else {
+                dst[i] = __ldcg(reinterpret_cast<const float4*>(accm + off + int64_t(i) * 4 * N));
+              }
+            }
           };
 #pragma unroll 1
           for (int cc = c_lo; cc < c_hi; cc += 32) {
@@ -1038,8 +1047,13 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? AO_AG
                 *reinterpret_cast<uint2*>(cout + base_off + int64_t(i) * 4 * N) = o;
                 if (R.ar)  // GEMM-AR: the reduced rows peers gather
                   *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(R.ar_red) + base_off + int64_t(i) * 4 * N) = o;
-                if (!xp(args, 1))
+                if (xp(args, 1)) {
+                } else if (R.rs_bf16) {
+                  *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(accm) + base_off + int64_t(i) * 4 * N) =
+                      make_uint2(0u, 0u);
+                } else {
                   st_v4(reinterpret_cast<int4*>(accm + base_off + int64_t(i) * 4 * N), make_int4(0, 0, 0, 0));
+                }
               }
             }
             __syncwarp();
@@ -1204,6 +1218,37 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? AO_AG
         }
         const int64_t col0 = col_base + cc;
         if (col0 >= N) break;  // warp-uniform
+        if (tma_red && R.rs_bf16) {
+          // bf16 wire (Q14, non-conforming): 64 columns per step as bf16 pairs, one 32 x 64
+          // bf16 box reduce-added into the owner's bf16 accumulator; the next block of 32
+          // columns is consumed here too (cc advances by 64)
+          if ((cc - c_lo) & 32) continue;
+          uint32_t hi[32];
+          tmem_ld_32x32b_x32(tb + cc + 32, hi);
+          tmem_wait_ld();
+          if (nkb == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) hi[i] = 0u;
+          }
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+            pk[16 + i] = pack_bf16x2(__uint_as_float(hi[2 * i]), __uint_as_float(hi[2 * i + 1]));
+          }
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&R.tmAcc[owner], stg, int(col0), int(row0 - int64_t(owner) * S));
+            bulk_commit();
+          }
+          continue;
+        }
         if (tma_red) {
           uint4* sg = stg + sb * (kEpiW * kStageWarpBytes / 16);
           if (lane == 0) bulk_wait_read<kRsStg - 1>();  // the reduce that last read buffer sb is done reading

@@ -81,6 +81,7 @@ struct alignas(64) RankArgs {
   int32_t rank, W, crows, n_chunks, n_tiles, n_items, n_nb, n_slices, n_comm_items, n_cta;
   uint32_t epoch;
   int32_t rs_atomic;  // RS: 1 = reduce-add into one accumulator (slot 0) instead of per-source slots
+  int32_t rs_bf16;    // RS ATOMIC: bf16 wire (bf16 partials reduce-added into a bf16 accumulator; Q14)
   // A2A (NEXT-3): chunk flags [W][maxJ] at word 0, count flags [W] at kA2ACountFlags, count
   // table [W][W] (row s = source s's per-expert counts) after them; receive buffer = peer_data.
   const int32_t* a2a_perm;  // [W][T] this rank's token ids grouped by destination expert

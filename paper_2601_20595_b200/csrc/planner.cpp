@@ -112,9 +112,11 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   if (d.n_cta < 0) v.push_back("n_cta");
   if (d.n_slices < 1 || d.n_slices > 64) v.push_back("n_slices");
   if (d.rs_wire != AO_WIRE_FP32 && d.rs_wire != AO_WIRE_BF16) v.push_back("rs_wire");
-  // the bf16 partial wire breaks the per-element bound (Q14) and is not built:
-  // rejected for every op that has partials, so validate, create and the hash agree
-  if (d.rs_wire == AO_WIRE_BF16 && (d.op == AO_OP_GEMM_RS || d.op == AO_OP_GEMM_AR)) v.push_back("rs_wire bf16");
+  // the bf16 partial wire breaks the per-element bound (Q14): built for GEMM-RS
+  // with the atomic reduction only (bf16 TMA reduce-adds into a bf16 accumulator), accepted
+  // and flagged non-conforming by ao_plan_create / ao_plan_create_host (ao_last_error)
+  if (d.rs_wire == AO_WIRE_BF16 && (d.op == AO_OP_GEMM_AR || (d.op == AO_OP_GEMM_RS && d.rs_reduce != AO_RS_ATOMIC)))
+    v.push_back("rs_wire bf16 (GEMM-RS with rs_reduce atomic only)");
   if (d.rs_reduce != AO_RS_SLOTS && d.rs_reduce != AO_RS_ATOMIC) v.push_back("rs_reduce");
   if (d.stream_k < -1 || d.stream_k > 1) v.push_back("stream_k");
   if (d.stream_k == 1 && (d.op != AO_OP_AG_GEMM || d.backend != AO_BACKEND_CE || d.tile_m == 512))
@@ -155,7 +157,7 @@ bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
   }
   const int64_t S = d.M / d.world_size;
   bool have = false;
-  int64_t best_num = 0, best_eff = 1, best_area = -1, best_bn = -1;
+  int64_t best_num = 0, best_eff = 1, best_den = 1, best_area = -1, best_bn = -1;
   for (int i = 0; i < kNumTileCandidates; ++i) {
     const TileShape c = kTileCandidates[i];
     if (!tile_allowed(d, i)) continue;
@@ -164,20 +166,26 @@ bool pick_tile(const ao_plan_desc& d, int sm_count, TileShape* out) {
     if (S % c.bm != 0) continue;
     const int64_t n = std::max(1, workers(d, sm_count) / c.cg);
     const int64_t T = (d.M / c.bm) * ceil_div(d.N, c.bn);
-    const int64_t num = ceil_div(T, n) * (int64_t(c.bm) * c.bn / c.cg);  // cost = num / eff
+    // cost = waves * per-SM tile area / eff, waves = ceil(T / n); with a stream-K tail (Q28)
+    // the waves are T / n (the last partial wave is spread over all workers): cost = num / (den * eff)
+    const bool sk = d.op == AO_OP_AG_GEMM && d.backend == AO_BACKEND_CE && c.cg <= 2 && d.K > 0 && T > n &&
+                    T % n != 0 && (d.stream_k == 1 || (d.stream_k == -1 && T * 10 < ceil_div(T, n) * n * 9));
+    const int64_t num = (sk ? T : ceil_div(T, n)) * (int64_t(c.bm) * c.bn / c.cg);
+    const int64_t den = sk ? n : 1;
     const int64_t eff = kTileEff[i] > 0 ? kTileEff[i] : 1;
     const int64_t area = int64_t(c.bm) * c.bn;
     bool better;
     if (!have) {
       better = true;
     } else {
-      const int64_t lhs = num * best_eff, rhs = best_num * eff;  // cost < best_cost
+      const __int128 lhs = __int128(num) * best_eff * best_den, rhs = __int128(best_num) * eff * den;  // cost < best
       better = lhs < rhs || (lhs == rhs && std::make_tuple(area, int64_t(c.bn)) > std::make_tuple(best_area, best_bn));
     }
     if (better) {
       have = true;
       best_num = num;
       best_eff = eff;
+      best_den = den;
       best_area = area;
       best_bn = c.bn;
       *out = c;
@@ -644,6 +652,7 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
   if (!P.is_ag) {
     o.put("tiles_per_chunk", int_list(P.tiles_per_chunk));
     o.put_str("rs_reduce", d.rs_reduce == AO_RS_ATOMIC ? "atomic" : "slots");
+    if (d.rs_wire == AO_WIRE_BF16) o.put_str("rs_wire", "bf16");
   }
   P.json = o.str();
   P.hash = fnv1a64(rank_independent_key(P));

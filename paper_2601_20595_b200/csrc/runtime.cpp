@@ -428,6 +428,7 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
   R->n_cta = hp.n_cta;
   R->epoch = epoch;
   R->rs_atomic = (!hp.is_ag && hp.desc.rs_reduce == AO_RS_ATOMIC) ? 1 : 0;
+  R->rs_bf16 = (R->rs_atomic && hp.desc.rs_wire == AO_WIRE_BF16) ? 1 : 0;
   R->sk_dp = hp.sk_dp;
   if (p->d_sk) {
     const size_t slots = size_t(hp.n_tiles - hp.sk_dp) * hp.tile.cg;
@@ -480,8 +481,10 @@ ao_status fill_rank(ao::RankArgs* R, ao_plan* p, uint32_t epoch, const void* A, 
   }
   if (!hp.is_ag && ctx && hp.W > 1 && hp.N > 0 && hp.S > 0) {  // RS: peer partials, streamed by the producer
     if (R->rs_atomic) {
-      s = encode_2d(&R->tmA_loc, R->peer_acc[hp.rank], hp.S, hp.N, 128, true);
-      for (int q = 0; q < hp.W && s == AO_OK; ++q) s = encode_2d(&R->tmAcc[q], R->peer_acc[q], hp.S, hp.N, 32, true);
+      // accumulator boxes: 32 rows x 128 bytes (32 fp32, or 64 bf16 with the bf16 wire)
+      const bool f32 = !R->rs_bf16;
+      s = encode_2d(&R->tmA_loc, R->peer_acc[hp.rank], hp.S, hp.N, 128, f32);
+      for (int q = 0; q < hp.W && s == AO_OK; ++q) s = encode_2d(&R->tmAcc[q], R->peer_acc[q], hp.S, hp.N, 32, f32);
     } else
       s = encode_2d(&R->tmA_loc, R->peer_data[hp.rank], int64_t(hp.W) * hp.S, hp.N, 128, true);
     if (s != AO_OK) return s;
@@ -581,6 +584,8 @@ ao_status ao_plan_create_host(const ao_plan_desc* d, int sm_count, ao_plan** out
     return fail(AO_ERR_INVALID_ARG, "invalid plan desc: %s", joined.c_str());
   }
   *out = p.release();
+  if (d->rs_wire == AO_WIRE_BF16)
+    fail(AO_OK, "non-conforming: rs_wire bf16 (DESIGN.md Q14)");
   return AO_OK;
 }
 
@@ -819,7 +824,7 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
     return fail(AO_ERR_INVALID_ARG, "workspace too small: plan needs %zu bytes per parity, ctx has %zu",
                 ao::data_bytes_per_parity(*d), c->data_half);
   if (d->op == AO_OP_GEMM_RS && d->rs_reduce == AO_RS_ATOMIC &&
-      size_t(d->M / d->world_size) * size_t(d->N) * 4 > c->acc_half)
+      size_t(d->M / d->world_size) * size_t(d->N) * (d->rs_wire == AO_WIRE_BF16 ? 2 : 4) > c->acc_half)
     return fail(AO_ERR_INVALID_ARG, "workspace too small for the RS accumulator");
   if (ao::flag_words_needed(*d) > ao::kA2ACountFlags)
     return fail(AO_ERR_INVALID_ARG, "too many chunk flags (%zu)", ao::flag_words_needed(*d));
@@ -835,6 +840,9 @@ ao_status ao_plan_create(ao_ctx* c, const ao_plan_desc* d, ao_plan** out) {
   s = upload_tables(p);
   if (s != AO_OK) return s;
   *out = guard.release();
+  if (d->rs_wire == AO_WIRE_BF16)  // accepted, flagged; the status stays AO_OK
+    fail(AO_OK, "non-conforming: rs_wire bf16 rounds each partial and the owner's accumulator to bf16, "
+         "outside the 1e-2 per-element / 2e-3 Frobenius bound (DESIGN.md Q14)");
   return AO_OK;
 }
 

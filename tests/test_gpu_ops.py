@@ -337,6 +337,35 @@ def test_gemm_rs_atomic_bitmask_and_mode_mixing(ao):
             assert torch.all(Cs[r].float().cpu() == 2 ** W - 1), seq
 
 
+# ------------------------------------------------------------------------ RS bf16 wire
+@pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_gemm_rs_bf16_wire(ao, W, tile):
+    """rs_wire=bf16 (non-conforming, Q14): each partial is rounded to bf16 and
+    reduce-added into a bf16 accumulator, so every addition rounds.  Accepted with the
+    status AO_OK and flagged in ao_last_error; checked against the oracle within the bound
+    that arithmetic allows (W bf16 roundings of O(1) partials: per element 1e-2 * W^0.5 *
+    max(1, |ref|), Frobenius 2e-3 * W^0.5), epochs re-arm the accumulator, and the bitmask
+    pattern (sums of distinct powers of two < 256, exact in bf16) stays bit-exact."""
+    M, K, N, C = 256 * W, 256, 520, 64
+    A, B = si.rs_inputs(W, M, K, N, salt=23)
+    ctxs, plans = _rs_world(ao, W, M, N, K, C, tile_m=tile[0], tile_n=tile[1], rs_reduce="atomic", rs_wire="bf16")
+    assert "non-conforming" in ao.N.lib().ao_last_error().decode()
+    A64, B64 = [si.to_f64(a) for a in A], [si.to_f64(b) for b in B]
+    dA, dB = _dev(A), _dev(B)
+    for it in range(3):
+        Cs = _run_rs(ao, ctxs, plans, dA, dB)
+        for r in range(W):
+            ok, e, f = on.check_tolerance(Cs[r].float().cpu().numpy(), on.gemm_rs(A64, B64, r),
+                                          elem_rel=1e-2 * W ** 0.5, frob_rel=2e-3 * W ** 0.5)
+            assert ok, f"rs bf16 wire W={W} it={it} rank {r}: {e:.3e} {f:.3e}"
+    Ap, Bp = si.rs_provenance_inputs(W, M, 64, N)
+    ctxs2, plans2 = _rs_world(ao, W, M, N, 64, C, tile_m=tile[0], tile_n=tile[1], rs_reduce="atomic", rs_wire="bf16")
+    Cs = _run_rs(ao, ctxs2, plans2, _dev(Ap), _dev(Bp))
+    for r in range(W):
+        assert torch.all(Cs[r].float().cpu() == 2 ** W - 1)
+
+
 # ------------------------------------------------------------------------ AG PULL
 @pytest.mark.parametrize("tile", [(128, 128), (256, 256)])
 @pytest.mark.parametrize("backend", ["ce", "ldst", "tma"])

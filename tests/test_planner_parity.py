@@ -83,7 +83,8 @@ def test_validation_agrees(ao):
              dict(op="gemm_ar"), dict(op="gemm_ar", backend="ldst"), dict(op="gemm_ar", backend="ldst", dir="pull"),
              dict(op="gemm_ar", backend="ldst", comm_ctas=4), dict(op="gemm_ar", backend="tma"),
              dict(op="gemm_rs", rs_wire="bf16"), dict(op="gemm_ar", backend="ldst", rs_wire="bf16"),
-             dict(rs_wire="bf16")]
+             dict(rs_wire="bf16"), dict(op="gemm_rs", rs_wire="bf16", rs_reduce="atomic"),
+             dict(op="gemm_ar", backend="ldst", rs_wire="bf16", rs_reduce="atomic")]
     for kw in cases:
         dd = osch.default_desc(**kw)
         ref_ok = not osch.validate(dd)
@@ -241,3 +242,17 @@ def test_stream_k_validation_agrees(ao):
                dict(stream_k=1, backend="tma"), dict(stream_k=-1, op="gemm_rs")):
         dd = osch.default_desc(**kw)
         assert (not osch.validate(dd)) == (not ao.validate(dd)), kw
+
+
+def test_rs_bf16_wire_json_and_flag(ao):
+    """The non-conforming bf16 RS wire (Q14): accepted for GEMM-RS with the atomic
+    reduction, exported in the canonical JSON, part of the plan hash, flagged in
+    ao_last_error while the call returns AO_OK."""
+    d = osch.default_desc(op="gemm_rs", world_size=4, M=1024, N=392, K=136, chunk_rows=128, rs_reduce="atomic",
+                          rs_wire="bf16")
+    got = ao.plan_json(d)
+    assert got == osch.export_json(osch.plan(d))
+    assert json.loads(got)["rs_wire"] == "bf16"
+    assert "non-conforming" in ao.N.lib().ao_last_error().decode()
+    h32 = ao.Plan(None, dict(d, rs_wire="fp32")).hash()
+    assert ao.Plan(None, d).hash() != h32

@@ -125,6 +125,47 @@ def main():
             p.close()
         run(name, f)
 
+    if want("sk"):
+        # AG with the stream-K tail (Q28): W=2: 12 tiles on 5 workers -> 5 data-parallel, 7 split
+        def f():
+            d = dict(op="ag_gemm", world_size=W, rank=rank, M=M, N=N, K=K, chunk_rows=C, backend="ce", tile_m=128,
+                     tile_n=128, n_cta=5, stream_k=1, timeout_ns=TMO)
+            p = ao.Plan(ctx, d)
+            T = (M // 128) * ((N + 127) // 128)
+            assert json.loads(p.export_json()).get("sk_dp") == (T // 5 - 1) * 5
+            A, B = si.ag_inputs(W, M, K, N, salt=15)
+            Cg = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+            for _ in range(3):
+                ao.ag_gemm(p, A[rank].cuda(), B[rank].cuda(), Cg)
+            torch.cuda.synchronize()
+            ctx.check_async()
+            check(Cg, on.ag_gemm([si.to_f64(a) for a in A], si.to_f64(B[rank])), "ag stream-K")
+            p.close()
+        run("sk", f)
+
+    if want("rs_bf16"):
+        # the non-conforming bf16 RS wire (Q14): its own bound, exact bitmask
+        def f():
+            d = dict(op="gemm_rs", world_size=W, rank=rank, M=M, N=N, K=K, chunk_rows=C, tile_m=128, tile_n=128,
+                     n_cta=n_cta, rs_reduce="atomic", rs_wire="bf16", timeout_ns=TMO)
+            p = ao.Plan(ctx, d)
+            A, B = si.rs_inputs(W, M, K, N, salt=16)
+            D = torch.empty(M // W, N, dtype=torch.bfloat16, device="cuda")
+            ao.gemm_rs(p, A[rank].cuda(), B[rank].cuda(), D)
+            torch.cuda.synchronize()
+            ctx.check_async()
+            ok, e, fr = on.check_tolerance(D.float().cpu().numpy(),
+                                           on.gemm_rs([si.to_f64(a) for a in A], [si.to_f64(b) for b in B], rank),
+                                           elem_rel=1e-2 * W ** 0.5, frob_rel=2e-3 * W ** 0.5)
+            assert ok, f"rs bf16 wire: {e:.3e} {fr:.3e}"
+            Ap, Bp = si.rs_provenance_inputs(W, M, K, N)
+            for ep in range(3):
+                ao.gemm_rs(p, Ap[rank].cuda(), Bp[rank].cuda(), D)
+            torch.cuda.synchronize()
+            assert torch.all(D.float().cpu() == 2 ** W - 1), "bitmask provenance (bf16 wire)"
+            p.close()
+        run("rs_bf16", f)
+
     if want("ar"):
         def f():
             d = dict(op="gemm_ar", world_size=W, rank=rank, M=M, N=N, K=K, chunk_rows=C, tile_m=128, tile_n=128,

@@ -630,6 +630,33 @@ def attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
     flops_c = 2.0 * Stot * Stot * d * H / (1 if loop else W)
     for p in cplans:
         p.close()
+    # head-parallel (Ulysses) variant: Q/K/V all-to-all in, H/W heads per rank over the
+    # whole sequence, output tiles returned to their owners (same FLOPs, same result)
+    hdesc = dict(desc, op="hp_attn", chunk_rows=(H // W) * S // 4 if (H // W) * S % (4 * 128) == 0 else S)
+    hp_res = {}
+    if H % W == 0 and S % 256 == 0:
+        hctxs = ao.loopback_world(local_rank, W, ao.workspace_bytes(hdesc)) if loop else \
+            [ao.dist_world(local_rank, ao.workspace_bytes(hdesc))]
+        for cz in (0, 1):
+            hplans = [ao.Plan(c, dict(hdesc, rank=r, causal=cz)) for c, r in zip(hctxs, my)]
+
+            def run_h(hplans=hplans):
+                if loop:
+                    ao.hp_attn_group(hplans, Qd, Kd, Vd, Od)
+                else:
+                    ao.hp_attn(hplans[0], Qd[0], Kd[0], Vd[0], Od[0])
+
+            ms_h = timed(run_h, n)
+            for c in hctxs:
+                c.check_async()
+            fl = flops_c if cz else flops
+            hp_res["causal_ms" if cz else "ms"] = round(ms_h, 4)
+            hp_res["causal_tflops" if cz else "tflops"] = round(fl / (ms_h * 1e-3) / 1e12, 1)
+            for p in hplans:
+                p.close()
+        hp_res["chunk_rows"] = hdesc["chunk_rows"]
+        for c in hctxs:
+            c.close()
     # library reference: SDPA per rank over its gathered K/V (already resident)
     if loop:
         Kf = torch.cat([k.to(dev) for k in K], 1).unsqueeze(0)
@@ -649,7 +676,8 @@ def attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
             "frac_of_peak": round(tf / peaks["bf16_tflops"], 4),
             "causal_ms": round(ms_c, 4), "causal_tflops": round(flops_c / (ms_c * 1e-3) / 1e12, 1),
             "sdpa_same_gpu_ms": None if sd_ms is None else round(sd_ms, 4),
-            "sdpa_tflops": None if sd_ms is None else round(flops / (sd_ms * 1e-3) / 1e12, 1)}
+            "sdpa_tflops": None if sd_ms is None else round(flops / (sd_ms * 1e-3) / 1e12, 1),
+            "head_parallel": hp_res}
 
 
 def per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms):

@@ -60,7 +60,8 @@ typedef enum {
 
 typedef enum { AO_OP_AG_GEMM = 0, AO_OP_GEMM_RS = 1, AO_OP_GEMM_AR = 2 /* NEXT-1 */,
                AO_OP_A2A_GEMM = 3 /* NEXT-3: MoE All-to-All dispatch + expert GEMM */,
-               AO_OP_SP_ATTN = 4 /* NEXT-4: sequence-parallel attention over all-gathered KV */ } ao_op;
+               AO_OP_SP_ATTN = 4 /* NEXT-4: sequence-parallel attention over all-gathered KV */,
+               AO_OP_HP_ATTN = 5 /* NEXT-4: head-parallel (all-to-all) attention */ } ao_op;
 /* Transfer backends of P:397 / Fig.7.  CE = copy-engine peer memcpy on a side
  * stream with stream-memop flags; TMA = cp.async.bulk peer copies issued from
  * communication warps; LDST = 16-byte vector ld/st over NVSwitch from CUDA cores. */
@@ -273,6 +274,25 @@ ao_status ao_a2a_gemm_group(int n, ao_plan* const* plans, const void* const* Xs,
  * diagonal blocks); requires S_loc % 256 == 0.  Collective rules and errors as ao_ag_gemm. */
 ao_status ao_sp_attn(ao_plan* plan, const void* Q, const void* K, const void* V, void* O, void* stream);
 ao_status ao_sp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
+                           const void* const* Vs, void* const* Os, void* stream);
+
+/* ---- HP attention (NEXT-4; "head-parallel (HP)" attention, DeepSpeed-Ulysses) -------
+ * Same operands and result as ao_sp_attn (rank r holds Q, K, V [H, S_loc, 128] of its
+ * tokens and gets O [H, S_loc, 128] = attention over the keys of all ranks), computed
+ * head-parallel: rank r owns the head group G_r = [r*H/W, (r+1)*H/W).  The copy engine
+ * pushes every source's Q, K, V rows of G_p to rank p (an all-to-all) in chunks of
+ * chunk_rows rows of the [H/W * S_loc, 128] view of a source block, each released by a
+ * per-chunk flag; rank r computes, for its heads, every source's queries against every
+ * source's keys (items (source, head, 256 queries); keys in arrival order, causal: the
+ * sources up to the query's), and writes each output tile straight to its owner: its own
+ * rows into O, the other sources' rows into that source's symmetric return buffer, the last
+ * tile of a (source, head group) block releasing a flag there; after the kernel the stream
+ * waits for the W-1 return flags and copies the returned blocks into O (the reverse
+ * all-to-all).  Plan: op AO_OP_HP_ATTN, M = S_loc (multiple of 256), N = H (multiple of W),
+ * K = 128, chunk_rows a multiple of 128 dividing H/W * S_loc, backend CE, dir PUSH.
+ * ao_hp_attn / ao_hp_attn_group are ao_sp_attn / ao_sp_attn_group on an HP plan. */
+ao_status ao_hp_attn(ao_plan* plan, const void* Q, const void* K, const void* V, void* O, void* stream);
+ao_status ao_hp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
                            const void* const* Vs, void* const* Os, void* stream);
 
 /* ---- plain local GEMM through the same tcgen05 mainloop (no communication) -------------

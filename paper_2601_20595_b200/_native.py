@@ -17,7 +17,7 @@ AO_HANDLE_BYTES = 256
 
 STATUS = {0: "AO_OK", 1: "AO_ERR_INVALID_ARG", 2: "AO_ERR_UNSUPPORTED", 3: "AO_ERR_CUDA", 4: "AO_ERR_OOM",
           5: "AO_ERR_PEER", 6: "AO_ERR_TIMEOUT", 7: "AO_ERR_STATE"}
-OPS = {"ag_gemm": 0, "gemm_rs": 1, "gemm_ar": 2, "a2a_gemm": 3, "sp_attn": 4}
+OPS = {"ag_gemm": 0, "gemm_rs": 1, "gemm_ar": 2, "a2a_gemm": 3, "sp_attn": 4, "hp_attn": 5}
 BACKENDS = {"ce": 0, "tma": 1, "ldst": 2}
 DIRS = {"push": 0, "pull": 1}
 CHUNK_ORDERS = {"shard_major": 0, "chunk_major": 1}
@@ -102,6 +102,8 @@ _SIGS = {
     "ao_a2a_gemm_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 7 + [ctypes.c_void_p]),
     "ao_sp_attn": (ctypes.c_int, [ctypes.c_void_p] * 6),
     "ao_sp_attn_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 5 + [ctypes.c_void_p]),
+    "ao_hp_attn": (ctypes.c_int, [ctypes.c_void_p] * 6),
+    "ao_hp_attn_group": (ctypes.c_int, [ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 5 + [ctypes.c_void_p]),
     "ao_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
     "ao_gemm_batched": (ctypes.c_int, [ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 3 +

@@ -282,6 +282,23 @@ def sp_attn_group(plans, Qs, Ks, Vs, Os, stream=None):
                                  _stream(stream)))
 
 
+def hp_attn(plan: Plan, Q, K, V, O, stream=None):
+    """ao_hp_attn (NEXT-4, head-parallel / Ulysses): the result of sp_attn, computed by this
+    rank for its head group over all ranks' queries and keys (all-to-all in and out)."""
+    _require_bf16_cuda(Q, K, V, O)
+    _attn_expect(plan, Q, K, V, O)
+    check(lib().ao_hp_attn(plan.handle, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _stream(stream)))
+
+
+def hp_attn_group(plans, Qs, Ks, Vs, Os, stream=None):
+    """ao_hp_attn_group: one launch for co-located ranks (loopback)."""
+    _require_bf16_cuda(*Qs, *Ks, *Vs, *Os)
+    for i, p in enumerate(plans):
+        _attn_expect(p, Qs[i], Ks[i], Vs[i], Os[i])
+    check(lib().ao_hp_attn_group(len(plans), _plans(plans), _arr(Qs), _arr(Ks), _arr(Vs), _arr(Os),
+                                 _stream(stream)))
+
+
 def _arr(ts):
     return (ctypes.c_void_p * len(ts))(*[0 if t is None else int(t.data_ptr()) for t in ts])
 

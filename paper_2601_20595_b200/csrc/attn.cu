@@ -448,14 +448,26 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
   PPBars& B = *reinterpret_cast<PPBars*>(sV + kPPV * (kKVBytes / 2));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = args.W, S = args.S_loc, nqp = S / (2 * kBlk), nkb = S / kBlk;
-  const int n_items = args.H * nqp;
-  // KV blocks of an item, in arrival order: the own shard first (kb = 0, 1, ...), then the
-  // sources rank-1, rank-2, ... (the push rotation).  Causal: only the own blocks up to the
-  // item's last query (kb <= 2qp+1) and only the sources below this rank (RingAttention
-  // skips the future shards).
-  auto nkv_of = [&](const AttnRank& R, int qp) -> int { return CAUSAL ? R.rank * nkb + 2 * qp + 2 : W * nkb; };
-  auto kv_of = [&](const AttnRank& R, int qp, int j, int& d, int& kb) {
-    const int own = CAUSAL ? 2 * qp + 2 : nkb;
+  // SP: items (head, query pair) of this rank's queries; HP: items (query source, head of
+  // this rank's group, query pair), query sources in arrival order (own rank first, then
+  // r-1, r-2, ...).  args.H = heads of the view (SP: all, HP: this rank's H/W).
+  const int n_items = (args.hp ? W : 1) * args.H * nqp;
+  struct Item {
+    int hv, qp, qs;  // head in the view, query pair, source rank of the queries
+  };
+  auto decode = [&](const AttnRank& R, int item) -> Item {
+    if (!args.hp) return Item{item / nqp, item % nqp, R.rank};
+    const int per = args.H * nqp, qi = item / per, rem = item - qi * per;
+    return Item{rem / nqp, rem % nqp, (R.rank - qi + W) % W};
+  };
+  // KV blocks of an item, in arrival order: the base shard first (kb = 0, 1, ...), then the
+  // sources base-1, base-2, ... (the push rotation); base = this rank (its own shard needs no
+  // wait).  Causal: base = the queries' source, only its blocks up to the item's last query
+  // (kb <= 2qp+1, the diagonal) and only the sources below it (RingAttention skips the
+  // future shards).
+  auto nkv_of = [&](const Item& it) -> int { return CAUSAL ? it.qs * nkb + 2 * it.qp + 2 : W * nkb; };
+  auto kv_of = [&](const Item& it, int j, int& d, int& kb) {
+    const int own = CAUSAL ? 2 * it.qp + 2 : nkb;
     if (j < own) {
       d = 0;
       kb = j;
@@ -463,8 +475,9 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
       d = 1 + (j - own) / nkb;
       kb = (j - own) % nkb;
     }
-    (void)R;
   };
+  auto kv_src = [&](const AttnRank& R, const Item& it, int d) -> int { return ((CAUSAL ? it.qs : R.rank) - d + W) % W; };
+  const int hv_rows = args.H * S;  // rows of one source's block in the gathered buffers
 
   if (warp == 1) {
     if (lane == 0) {
@@ -507,21 +520,38 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
       uint64_t got[AO_MAX_WORLD] = {};  // acquired chunk flags per rank group (w < 64)
       attn_walk(args, n_items, [&](int g, int item) {
         const AttnRank& R = args.rk[g];
-        const int h = item / nqp, qp = item % nqp;
+        const Item it = decode(R, item);
+        const int h = it.hv, qp = it.qp;
+        const int hoff = args.hp ? R.rank * args.H : 0;  // HP: this rank's heads in the local tensors
         mbar_wait(&B.qempty, (t & 1u) ^ 1u);
+        const CUtensorMap* mq = &R.tmQ;
+        int qrow = (hoff + h) * S + qp * 2 * kBlk;
+        if (it.qs != R.rank) {  // HP: another source's queries, from the gathered Q
+          const int vr = h * S + qp * 2 * kBlk;
+          for (int c = vr / args.crows; c <= (vr + 2 * kBlk - 1) / args.crows; ++c) {
+            const int w = it.qs * args.nch + c;
+            if (!(w < 64 && ((got[g] >> w) & 1u))) {
+              attn_spin(R.flags + w, R.epoch, args, R.rank, int(blockIdx.x), w);
+              if (w < 64) got[g] |= 1ull << w;
+            }
+          }
+          fence_proxy_async_global();  // generic-proxy acquire -> TMA reads
+          mq = &R.tmQg;
+          qrow = it.qs * hv_rows + vr;
+        }
         mbar_arrive_expect_tx(&B.qfull, 2 * kQBytes);
-        const int qrow = h * S + qp * 2 * kBlk;
-        tma_load_2d(sQ, &R.tmQ, &B.qfull, 0, qrow, pol);
-        tma_load_2d(sQ + kHalf, &R.tmQ, &B.qfull, 64, qrow, pol);
-        tma_load_2d(sQ + kQBytes, &R.tmQ, &B.qfull, 0, qrow + kBlk, pol);
-        tma_load_2d(sQ + kQBytes + kHalf, &R.tmQ, &B.qfull, 64, qrow + kBlk, pol);
-        const int nkv = nkv_of(R, qp);
+        tma_load_2d(sQ, mq, &B.qfull, 0, qrow, pol);
+        tma_load_2d(sQ + kHalf, mq, &B.qfull, 64, qrow, pol);
+        tma_load_2d(sQ + kQBytes, mq, &B.qfull, 0, qrow + kBlk, pol);
+        tma_load_2d(sQ + kQBytes + kHalf, mq, &B.qfull, 64, qrow + kBlk, pol);
+        const int nkv = nkv_of(it);
         for (int j = 0; j < nkv; ++j, ++n) {
           int d, kb;
-          kv_of(R, qp, j, d, kb);
-          const int src = (R.rank - d + W) % W;
-          const int krow = h * S + kb * kBlk;
-          if (d > 0) {  // the chunk (src, h*S + kb*128) must have landed
+          kv_of(it, j, d, kb);
+          const int src = kv_src(R, it, d);
+          const int krow = h * S + kb * kBlk;  // row in the view of one source's block
+          const bool local = src == R.rank;
+          if (!local) {  // the chunk (src, h*S + kb*128) must have landed
             const int w = src * args.nch + krow / args.crows;
             if (!(w < 64 && ((got[g] >> w) & 1u))) {
               attn_spin(R.flags + w, R.epoch, args, R.rank, int(blockIdx.x), w);
@@ -530,9 +560,9 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
             }
           }
           const uint32_t kst = n % kPPK, vst = n % kPPV;
-          const CUtensorMap* mk = d == 0 ? &R.tmK_loc : &R.tmK;
-          const CUtensorMap* mv = d == 0 ? &R.tmV_loc : &R.tmV;
-          const int row = d == 0 ? krow : src * args.H * S + krow;
+          const CUtensorMap* mk = local ? &R.tmK_loc : &R.tmK;
+          const CUtensorMap* mv = local ? &R.tmV_loc : &R.tmV;
+          const int row = local ? hoff * S + krow : src * hv_rows + krow;
           uint8_t* kdst = sK + kst * (kKVBytes / 2);
           uint8_t* vdst = sV + vst * (kKVBytes / 2);
           mbar_wait(&B.kempty[kst], ((n / kPPK) & 1u) ^ 1u);
@@ -571,7 +601,7 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
       __syncwarp();
     };
     attn_walk(args, n_items, [&](int g, int item) {
-      const int nkv = nkv_of(args.rk[g], item % nqp);
+      const int nkv = nkv_of(decode(args.rk[g], item));
       mbar_wait(&B.qfull, t & 1u);
       for (int x = 0; x < 2; ++x) {
         if (n > 0) mbar_wait(&B.pvdone[x], (n - 1) & 1u);  // P_x of the previous item was read
@@ -624,14 +654,15 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
     };
     attn_walk(args, n_items, [&](int g, int item) {
       const AttnRank& R = args.rk[g];
-      const int h = item / nqp, qp = item % nqp;
-      const int nkv = nkv_of(R, qp);
-      const int qloc = qp * 2 * kBlk + x * kBlk + r;  // this thread's query (local position)
+      const Item it = decode(R, item);
+      const int h = it.hv, qp = it.qp;
+      const int nkv = nkv_of(it);
+      const int qloc = qp * 2 * kBlk + x * kBlk + r;  // this thread's query (position in its source's shard)
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         const uint32_t nn = n + j;
         int d, kb;
-        kv_of(R, qp, j, d, kb);
+        kv_of(it, j, d, kb);
         // causal: keys kb*128 + c beyond this query are masked (own diagonal blocks only)
         const int kmax = (CAUSAL && d == 0) ? qloc - kb * kBlk : 1 << 30;
         mbar_wait(&B.sfull[x], nn & 1u);
@@ -715,7 +746,11 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
       }
       pv_wait(n + nkv - 1);
       const float inv = 1.f / l;
-      char* orow = R.O + (int64_t(h) * S + qp * 2 * kBlk + x * kBlk + r) * 256;
+      // SP and HP own queries: O rows of this rank; HP other sources: their return buffer,
+      // block of this rank's head group
+      const int hoff = args.hp ? R.rank * args.H : 0;
+      char* orow = it.qs == R.rank ? R.O + (int64_t(hoff + h) * S + qloc) * 256
+                                   : R.oret[it.qs] + (int64_t(R.rank) * hv_rows + int64_t(h) * S + qloc) * 256;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
@@ -733,6 +768,20 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&B.ofree[x]);
+      if (it.qs != R.rank) {
+        // HP: count this tile into its destination block; the last of the block's H*nqp*2
+        // tiles releases the destination's return flag (cumulative over the warpgroup's
+        // stores, which precede the barrier)
+        named_bar_sync(1 + x, 128);
+        if (qd == 0 && lane == 0) {
+          uint32_t old;
+          asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.counters + it.qs) : "memory");
+          if (int(old) + 1 == args.H * nqp * 2) {
+            R.counters[it.qs] = 0;
+            st_release_sys(R.peer_flags[it.qs] + W * args.nch + R.rank, R.epoch);
+          }
+        }
+      }
       n += nkv;
     });
   }
@@ -751,7 +800,7 @@ cudaError_t launch_attn(const AttnArgs& args, cudaStream_t stream) {
   // two-tile ping-pong kernel when S_loc is a multiple of 256 (AO_ATTN_SINGLE=1 forces the
   // one-tile kernel)
   static const bool single = getenv("AO_ATTN_SINGLE") && getenv("AO_ATTN_SINGLE")[0] == '1';
-  const bool pp = args.causal || (!single && args.S_loc % (2 * dev::kBlk) == 0);  // causal: pp only
+  const bool pp = args.causal || args.hp || (!single && args.S_loc % (2 * dev::kBlk) == 0);  // causal / HP: pp only
   static bool attr = false, attr_pp = false, attr_ppc = false;
   if (!pp && !attr) {
     cudaError_t e = cudaFuncSetAttribute(dev::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -118,8 +118,14 @@ struct A2APrepArgs {
 // are [W][H*S_loc][128] (source-major) in the symmetric data half (K, then V).
 struct AttnRank {
   CUtensorMap tmQ, tmK_loc, tmV_loc, tmK, tmV;  // 2-D maps, boxes of 64 elements x 128 rows
+  CUtensorMap tmQg;                             // HP: gathered Q [W][H/W*S_loc][128]
   char* O;                                      // [H*S_loc, 128] bf16
   const uint32_t* flags;                        // this rank's flag words: chunk (src, c) at src*nch + c
+  // HP: every rank's O return buffer [W][H/W*S_loc][128] (current parity) and flag words
+  // (return flag of source block s at word W*nch + s), tiles done per destination (counters)
+  char* oret[AO_MAX_WORLD];
+  uint32_t* peer_flags[AO_MAX_WORLD];
+  uint32_t* counters;
   int32_t rank;
   uint32_t epoch;
 };
@@ -128,6 +134,7 @@ struct AttnArgs {
   int32_t n_group, W, H, S_loc, crows, nch;  // crows: rows of the [H*S_loc] view per chunk
   int32_t ctas_per_rank, ts;                 // ts: time-sliced whole-world group (rank after rank)
   int32_t causal;                            // causal mask over global token positions (ping-pong kernel)
+  int32_t hp;                                // head-parallel: items (query source, head of the group, pair)
   float scale_log2;                          // softmax scale * log2(e)
   uint64_t timeout_ns;
   ErrorInfo* err;

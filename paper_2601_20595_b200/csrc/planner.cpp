@@ -30,6 +30,7 @@ static const char* op_name(int op) {
          : op == AO_OP_GEMM_RS ? "gemm_rs"
          : op == AO_OP_GEMM_AR ? "gemm_ar"
          : op == AO_OP_A2A_GEMM ? "a2a_gemm"
+         : op == AO_OP_HP_ATTN  ? "hp_attn"
                                 : "sp_attn";
 }
 static const char* tensor_name(int t) { return t == TENSOR_A ? "A" : (t == TENSOR_P ? "P" : "C"); }
@@ -55,8 +56,27 @@ std::vector<std::string> validate_desc(const ao_plan_desc& d, int sm_count) {
   std::vector<std::string> v;
   if (d.struct_size != sizeof(ao_plan_desc)) v.push_back("struct_size");
   if (d.op != AO_OP_AG_GEMM && d.op != AO_OP_GEMM_RS && d.op != AO_OP_GEMM_AR && d.op != AO_OP_A2A_GEMM &&
-      d.op != AO_OP_SP_ATTN)
+      d.op != AO_OP_SP_ATTN && d.op != AO_OP_HP_ATTN)
     v.push_back("op");
+  if (d.op == AO_OP_HP_ATTN) {
+    // M = S_loc tokens per rank, N = heads (split over the ranks), K = head dim 128
+    const int W = d.world_size;
+    if (W < 1 || W > AO_MAX_WORLD) v.push_back("world_size");
+    if (!(d.rank >= 0 && d.rank < std::max(W, 1))) v.push_back("rank");
+    if (d.K != 128) v.push_back("head dim (K) must be 128");
+    if (d.M <= 0 || d.M % 256 != 0) v.push_back("S_loc (M) % 256");
+    if (d.N < 1 || (W >= 1 && d.N % W != 0)) v.push_back("heads (N) % world_size");
+    const int64_t view = W >= 1 ? d.M * (d.N / std::max(W, 1)) : 0;  // rows of a source block
+    if (d.chunk_rows <= 0 || d.chunk_rows % 128 != 0 || (view > 0 && view % d.chunk_rows != 0))
+      v.push_back("chunk_rows");
+    if (d.backend != AO_BACKEND_CE) v.push_back("backend for hp_attn");
+    if (d.dir != AO_DIR_PUSH) v.push_back("dir for hp_attn");
+    if (d.comm_ctas != 0) v.push_back("comm_ctas with hp_attn");
+    if (d.topk != 0) v.push_back("topk");
+    if (d.causal != 0 && d.causal != 1) v.push_back("causal");
+    if (d.n_cta < 0) v.push_back("n_cta");
+    return v;
+  }
   if (d.op == AO_OP_SP_ATTN) {
     // M = S_loc tokens per rank, N = heads, K = head dim (the kernel is built for 128)
     const int W = d.world_size;
@@ -205,6 +225,8 @@ size_t data_bytes_per_parity(const ao_plan_desc& d) {
   if (d.op == AO_OP_A2A_GEMM) return size_t(d.world_size) * size_t(d.M) * size_t(d.K) * 2;  // receive buffer
   if (d.op == AO_OP_SP_ATTN)  // gathered K then V, [W][H*S_loc][128] bf16 each
     return 2 * size_t(d.world_size) * size_t(d.N) * size_t(d.M) * size_t(d.K) * 2;
+  if (d.op == AO_OP_HP_ATTN)  // gathered Q, K, V and the O return buffer, [W][H/W*S_loc][128] bf16 each
+    return 4 * size_t(d.N) * size_t(d.M) * size_t(d.K) * 2;
   if (d.op == AO_OP_GEMM_AR)  // (slots) + the owner's reduced rows [S, N] bf16
     return ar_reduced_offset(d) + size_t(d.world_size > 0 ? d.M / d.world_size : 0) * size_t(d.N) * 2;
   const size_t eb = d.rs_wire == AO_WIRE_BF16 ? 2 : 4;
@@ -216,6 +238,10 @@ size_t a2a_max_chunks(const ao_plan_desc& d) { return d.chunk_rows > 0 ? size_t(
 size_t flag_words_needed(const ao_plan_desc& d) {
   if (d.op == AO_OP_SP_ATTN)  // chunk flags [W sources][H*S_loc / chunk_rows]
     return d.chunk_rows > 0 ? size_t(d.world_size) * size_t(d.M * d.N / d.chunk_rows) : 0;
+  if (d.op == AO_OP_HP_ATTN)  // chunk flags [W sources][H/W*S_loc / chunk_rows], then O return flags [W]
+    return d.chunk_rows > 0 && d.world_size > 0
+               ? size_t(d.world_size) * size_t(d.M * (d.N / d.world_size) / d.chunk_rows) + size_t(d.world_size)
+               : 0;
   if (d.op == AO_OP_A2A_GEMM)  // chunk flags [W][maxJ] (the count exchange uses the reserved tail)
     return size_t(d.world_size) * a2a_max_chunks(d);
   const size_t nch = d.chunk_rows > 0 ? size_t(d.M / d.chunk_rows) : 0;
@@ -294,7 +320,7 @@ static std::string rank_independent_key(const HostPlan& p) {
   o.put("rs_wire", d.rs_wire);
   o.put("rs_reduce", d.rs_reduce);
   if (d.op == AO_OP_A2A_GEMM) o.put("topk", d.topk);
-  if (d.op == AO_OP_SP_ATTN) o.put("causal", d.causal);
+  if (d.op == AO_OP_SP_ATTN || d.op == AO_OP_HP_ATTN) o.put("causal", d.causal);
   if (p.sk_dp < p.n_tiles) o.put("sk_dp", p.sk_dp);
   return o.str();
 }
@@ -334,7 +360,39 @@ std::vector<std::string> build_plan(const ao_plan_desc& d, int sm_count, HostPla
   P.is_ag = d.op == AO_OP_AG_GEMM;
   P.is_ar = d.op == AO_OP_GEMM_AR;
   P.is_a2a = d.op == AO_OP_A2A_GEMM;
-  P.is_attn = d.op == AO_OP_SP_ATTN;
+  P.is_attn = d.op == AO_OP_SP_ATTN || d.op == AO_OP_HP_ATTN;
+  P.is_hp = d.op == AO_OP_HP_ATTN;
+  if (P.is_hp) {
+    // HP attention (NEXT-4): items (query source, head of the group, 256 queries); one chunk =
+    // chunk_rows rows of a source's [H/W * S_loc, 128] Q, K and V blocks
+    P.tile = TileShape{256, 128, 1};
+    P.n_cta = std::max(1, workers(d, sm_count));
+    P.S = d.M;
+    P.n_c = int(d.M * (d.N / P.W) / d.chunk_rows);
+    P.n_chunks = P.W * P.n_c;
+    P.n_mb = int(P.W * (d.N / P.W) * (d.M / 256));
+    P.n_nb = 1;
+    P.n_tiles = P.n_mb;
+    Obj o;
+    o.put_str("op", op_name(d.op));
+    o.put("world_size", P.W);
+    o.put("rank", P.rank);
+    o.put("S_loc", P.M);
+    o.put("heads", P.N);
+    o.put("heads_per_rank", P.N / P.W);
+    o.put("head_dim", P.K);
+    o.put("chunk_rows", P.C);
+    o.put("chunks_per_source", P.n_c);
+    o.put_str("backend", backend_name(d.backend));
+    o.put_str("dir", dir_name(d.dir));
+    o.put("n_cta", P.n_cta);
+    o.put("items", P.n_tiles);
+    o.put_str("kv_order", d.causal ? "query_source_down" : "ring");
+    o.put("causal", d.causal);
+    P.json = o.str();
+    P.hash = fnv1a64(rank_independent_key(P));
+    return {};
+  }
   if (P.is_attn) {
     // SP attention (NEXT-4): items (head, 128 queries), KV blocks of 128 in arrival order;
     // one chunk = chunk_rows rows of a source's [H*S_loc, 128] K and V

@@ -49,7 +49,8 @@ struct HostPlan {
   int n_mb = 0, n_nb = 0, n_tiles = 0;
   bool is_ag = true;
   bool is_a2a = false;
-  bool is_attn = false;  // SP attention (NEXT-4)  // A2A-GEMM (NEXT-3): routing-dependent tables built on the device
+  bool is_attn = false;  // SP or HP attention (NEXT-4)
+  bool is_hp = false;    // HP (head-parallel, all-to-all) attention
   bool is_ar = false;  // GEMM-AR: the RS schedule + a pull AllGather of the reduced chunks
   // tables
   std::vector<std::array<int, 5>> chunks;  // g, row0, rows, src_or_owner, pos

@@ -1359,7 +1359,7 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
   ao_plan* p0 = plans[0];
   if (!p0 || !p0->ctx) return fail(AO_ERR_STATE, "plan is not bound to a ctx");
   const ao::HostPlan& h0 = p0->hp;
-  if (!h0.is_attn) return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is not sp_attn");
+  if (!h0.is_attn) return fail(AO_ERR_INVALID_ARG, "op mismatch: plan is not sp_attn / hp_attn");
   for (int i = 0; i < n; ++i) {
     ao_plan* p = plans[i];
     if (!p || !p->ctx) return fail(AO_ERR_STATE, "plan %d not bound", i);
@@ -1379,12 +1379,16 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
     if (s != AO_OK) return s;
   }
   const int W = h0.W, H = int(h0.N), S = int(h0.M), crows = h0.C, nch = h0.n_c;
+  const bool hp = h0.is_hp;
+  const int Hv = hp ? H / W : H;  // heads of one source's block in the gathered buffers
   const int64_t rows = int64_t(H) * S, row_bytes = 256;  // [H*S_loc, 128] bf16
+  const int64_t vrows = int64_t(Hv) * S;                  // rows of one source's block
   std::unique_ptr<ao::AttnArgs> ka(new ao::AttnArgs());
   memset(ka.get(), 0, sizeof(ao::AttnArgs));
   ka->n_group = n;
   ka->W = W;
-  ka->H = H;
+  ka->H = Hv;
+  ka->hp = hp ? 1 : 0;
   ka->S_loc = S;
   ka->crows = crows;
   ka->nch = nch;
@@ -1408,18 +1412,29 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
     const uint32_t par = epochs[i] & 1;
     const int r = plans[i]->hp.rank;
     ao::AttnRank& R = ka->rk[i];
-    char* gK = c->data(r, par);
-    char* gV = gK + int64_t(W) * rows * row_bytes;
+    // data half: SP [gathered K | gathered V], each [W][H*S_loc]; HP [gathered Q | K | V |
+    // O return], each [W][H/W*S_loc] (= H*S_loc rows)
+    char* gQ = c->data(r, par);
+    char* gK = hp ? gQ + rows * row_bytes : gQ;
+    char* gV = gK + int64_t(W) * vrows * row_bytes;
     ao_status s;
     if ((s = encode_2d(&R.tmQ, Qs[i], rows, 128, 128)) != AO_OK) return s;
     if ((s = encode_2d(&R.tmK_loc, Ks[i], rows, 128, 128)) != AO_OK) return s;
     if ((s = encode_2d(&R.tmV_loc, Vs[i], rows, 128, 128)) != AO_OK) return s;
-    if ((s = encode_2d(&R.tmK, gK, int64_t(W) * rows, 128, 128)) != AO_OK) return s;
-    if ((s = encode_2d(&R.tmV, gV, int64_t(W) * rows, 128, 128)) != AO_OK) return s;
+    if ((s = encode_2d(&R.tmK, gK, int64_t(W) * vrows, 128, 128)) != AO_OK) return s;
+    if ((s = encode_2d(&R.tmV, gV, int64_t(W) * vrows, 128, 128)) != AO_OK) return s;
+    if (hp && (s = encode_2d(&R.tmQg, gQ, int64_t(W) * vrows, 128, 128)) != AO_OK) return s;
     R.O = static_cast<char*>(Os[i]);
     R.flags = c->flags(r, par);
     R.rank = r;
     R.epoch = epochs[i];
+    if (hp) {
+      for (int q = 0; q < W; ++q) {
+        R.oret[q] = c->data(q, par) + 3 * rows * row_bytes;
+        R.peer_flags[q] = c->flags(q, par);
+      }
+      R.counters = c->counters;
+    }
   }
   ao_ctx* c0 = p0->ctx;
   const uint32_t par = epochs[0] & 1;
@@ -1438,7 +1453,7 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
     // only on lower ranks, so nothing else orders a source behind a higher destination --
     // wait for that destination's done word (written after each of its attention kernels)
     // to reach e-2.  Ranks of this launch are ordered by the stream already.
-    if (h0.desc.causal && epochs[0] > 2) {
+    if (!hp && h0.desc.causal && epochs[0] > 2) {
       for (int dst = 0; dst < W; ++dst) {
         bool in_group = false;
         for (int q = 0; q < n; ++q) in_group |= plans[q]->hp.rank == dst;
@@ -1455,6 +1470,7 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
       key.push_back(reinterpret_cast<uintptr_t>(plans[i]));
       key.push_back(reinterpret_cast<uintptr_t>(Ks[i]));
       key.push_back(reinterpret_cast<uintptr_t>(Vs[i]));
+      if (hp) key.push_back(reinterpret_cast<uintptr_t>(Qs[i]));
     }
     cudaGraphExec_t exec = nullptr;
     auto it = p0->ce_graphs.find(key);
@@ -1466,9 +1482,9 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
       for (int i = 0; i < n; ++i) {  // one chain per source rank in this group
         const int src = plans[i]->hp.rank;
         std::vector<int> dests;
-        for (int ds = 1; ds < W; ++ds) {  // ring rotation; causal: only higher ranks read src's shard
+        for (int ds = 1; ds < W; ++ds) {  // ring rotation; SP causal: only higher ranks read src's shard
           const int dst = (src + ds) % W;
-          if (!h0.desc.causal || dst > src) dests.push_back(dst);
+          if (hp || !h0.desc.causal || dst > src) dests.push_back(dst);
         }
         if (ka->ts) std::sort(dests.begin(), dests.end());              // destination-major
         std::vector<cudaGraphNode_t> prev;
@@ -1476,15 +1492,24 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
           ao_ctx* dc = nullptr;  // the destination's buffers, mapped in this process
           for (int q = 0; q < n; ++q)
             if (plans[q]->hp.rank == dst) dc = plans[q]->ctx;
-          char* gK = (dc ? dc : plans[i]->ctx)->data(dst, par);
-          if (!dc) gK = plans[i]->ctx->data(dst, par);
-          char* gV = gK + int64_t(W) * rows * row_bytes;
+          (void)dc;
+          char* gQ = plans[i]->ctx->data(dst, par);  // the destination's buffers, mapped in this process
+          char* gK = hp ? gQ + rows * row_bytes : gQ;
+          char* gV = gK + int64_t(W) * vrows * row_bytes;
           uint32_t* fl = plans[i]->ctx->flags(dst, par);
+          // SP: chunk c of src's whole K/V; HP: chunk c of the rows of dst's head group in
+          // src's Q, K and V (the all-to-all)
+          const int64_t sbase = hp ? int64_t(dst) * vrows : 0;
           for (int cch = 0; cch < nch; ++cch) {
-            const int64_t off = (int64_t(src) * rows + int64_t(cch) * crows) * row_bytes;
-            const int64_t soff = int64_t(cch) * crows * row_bytes;
+            const int64_t off = (int64_t(src) * vrows + int64_t(cch) * crows) * row_bytes;
+            const int64_t soff = (sbase + int64_t(cch) * crows) * row_bytes;
             const size_t bytes = size_t(crows) * row_bytes;
-            cudaGraphNode_t nk = nullptr, nv = nullptr, nf = nullptr;
+            cudaGraphNode_t nq = nullptr, nk = nullptr, nv = nullptr, nf = nullptr;
+            if (hp) {
+              AO_CUDA(cudaGraphAddMemcpyNode1D(&nq, graph, prev.data(), prev.size(), gQ + off,
+                                               static_cast<const char*>(Qs[i]) + soff, bytes, cudaMemcpyDeviceToDevice));
+              prev.assign(1, nq);
+            }
             AO_CUDA(cudaGraphAddMemcpyNode1D(&nk, graph, prev.data(), prev.size(), gK + off,
                                              static_cast<const char*>(Ks[i]) + soff, bytes, cudaMemcpyDeviceToDevice));
             AO_CUDA(cudaGraphAddMemcpyNode1D(&nv, graph, &nk, 1, gV + off, static_cast<const char*>(Vs[i]) + soff,
@@ -1513,6 +1538,28 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
     cudaError_t e = ao::launch_attn(*ka, stream);
     if (e != cudaSuccess) return fail(AO_ERR_CUDA, "attention kernel launch: %s", cudaGetErrorString(e));
   }
+  if (hp && W > 1 && rows > 0) {
+    // the reverse all-to-all: each other source's block of this rank's output came back in
+    // the return buffer; wait for its flag (released by the block's last tile) and copy it
+    // into O (rows of that source's head group)
+    DriverFns* drv = nullptr;
+    ao_status s = get_driver(&drv);
+    if (s != AO_OK) return s;
+    for (int i = 0; i < n; ++i) {
+      ao_ctx* c = plans[i]->ctx;
+      const int r = plans[i]->hp.rank;
+      const uint32_t par = epochs[i] & 1;
+      for (int d = 1; d < W; ++d) {
+        const int src = (r - d + W) % W;
+        CUresult cr = drv->wait32(stream, reinterpret_cast<CUdeviceptr>(c->flags(r, par) + W * nch + src), epochs[i],
+                                  0x0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+        if (cr != CUDA_SUCCESS) return fail(AO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", int(cr));
+        AO_CUDA(cudaMemcpyAsync(static_cast<char*>(Os[i]) + int64_t(src) * vrows * row_bytes,
+                                c->data(r, par) + 3 * rows * row_bytes + int64_t(src) * vrows * row_bytes,
+                                size_t(vrows) * row_bytes, cudaMemcpyDeviceToDevice, stream));
+      }
+    }
+  }
   for (int i = 0; i < n; ++i) plans[i]->ctx->epoch = epochs[i];
   if (ce) AO_CUDA(cudaStreamWaitEvent(stream, c0->ev_done, 0));
   return mark_done(n, plans, epochs, stream);
@@ -1524,6 +1571,15 @@ ao_status ao_sp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, 
 }
 
 ao_status ao_sp_attn(ao_plan* plan, const void* Q, const void* K, const void* V, void* O, void* stream) {
+  return launch_attn_group(1, &plan, &Q, &K, &V, &O, stream);
+}
+
+ao_status ao_hp_attn_group(int n, ao_plan* const* plans, const void* const* Qs, const void* const* Ks,
+                           const void* const* Vs, void* const* Os, void* stream) {
+  return launch_attn_group(n, plans, Qs, Ks, Vs, Os, stream);
+}
+
+ao_status ao_hp_attn(ao_plan* plan, const void* Q, const void* K, const void* V, void* O, void* stream) {
   return launch_attn_group(1, &plan, &Q, &K, &V, &O, stream);
 }
 

@@ -234,6 +234,37 @@ def main():
             p.close()
         run(name, f)
 
+    for causal in (0, 1):
+        name = f"hp_causal{causal}"
+        if not want("hp") and not want(name):
+            continue
+
+        def f(causal=causal):
+            # head-parallel attention: all-to-all of Q/K/V by head group in, output tiles
+            # returned to their owners over IPC, 3 epochs without host sync
+            H, S = 2 * W, 256
+            d = dict(op="hp_attn", world_size=W, rank=rank, M=S, N=H, K=128, chunk_rows=256, backend="ce",
+                     n_cta=n_cta, causal=causal, timeout_ns=TMO)
+            p = ao.Plan(ctx, d)
+            outs = []
+            for ep in range(3):
+                Q, Kx, V = si.attn_inputs(W, H, S, 128, salt=700 + ep)
+                O = torch.empty(H, S, 128, dtype=torch.bfloat16, device="cuda")
+                ao.hp_attn(p, Q[rank].cuda(), Kx[rank].cuda(), V[rank].cuda(), O)
+                outs.append((O, Q, Kx, V))
+            torch.cuda.synchronize()
+            ctx.check_async()
+            for ep, (O, Q, Kx, V) in enumerate(outs):
+                args = ([si.to_f64(t) for t in Q], [si.to_f64(t) for t in Kx], [si.to_f64(t) for t in V], rank,
+                        128 ** -0.5)
+                ref = oatt.sp_attention(*args, causal=bool(causal))
+                refb = oatt.round_bf16(oatt.sp_attention_p_bf16(*args, causal=bool(causal)))
+                bound = max(2e-3, 1.15 * np.linalg.norm(refb - ref) / np.linalg.norm(ref))
+                ok, e, fr = on.check_tolerance(O.float().cpu().numpy(), ref, frob_rel=bound)
+                assert ok, f"hp epoch {ep}: {e:.3e} {fr:.3e}"
+            p.close()
+        run(name, f)
+
     if want("mismatch"):
         # collective semantics: rank 0 launches a plan whose desc differs (chunk_rows) ->
         # every rank's first launch reports AO_ERR_PEER instead of running a mixed schedule

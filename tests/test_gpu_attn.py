@@ -221,3 +221,88 @@ def test_sp_attn_causal_epochs_without_host_sync(ao):
         Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
         for r in range(W):
             _check_full(outs[e][0][r].float().cpu().numpy(), Qn, Kn, Vn, r, True, f"causal epoch {e} rank {r}")
+
+
+# ---- head-parallel (Ulysses) attention: the same result, computed per head group ---------
+def _hp_world(ao, W, H, S, C, n_cta, **kw):
+    d = dict(op="hp_attn", world_size=W, M=S, N=H, K=128, chunk_rows=C, backend="ce", n_cta=n_cta,
+             timeout_ns=2_000_000_000)
+    d.update(kw)
+    ctxs = ao.loopback_world(0, W, ao.workspace_bytes(d))
+    return ctxs, [ao.Plan(ctxs[r], dict(d, rank=r)) for r in range(W)]
+
+
+def _run_hp(ao, ctxs, plans, Q, K, V):
+    O = [torch.full_like(q, float("nan"), device="cuda") for q in Q]
+    ao.hp_attn_group(plans, [q.cuda() for q in Q], [k.cuda() for k in K], [v.cuda() for v in V], O)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    return O
+
+
+@pytest.mark.parametrize("causal", [0, 1])
+@pytest.mark.parametrize("ts", [False, True])
+@pytest.mark.parametrize("W,H,S,C", [(1, 2, 256, 256), (2, 2, 256, 256), (2, 4, 512, 128), (4, 4, 256, 128),
+                                     (8, 8, 256, 256), (4, 8, 512, 256)])
+def test_hp_attn_vs_oracle(ao, W, H, S, C, ts, causal):
+    """HP attention (DeepSpeed-Ulysses): rank r computes heads [r*H/W, (r+1)*H/W) for
+    every source's queries over every source's keys (all-to-all in, output tiles written
+    straight to their owners); the result equals SP attention's (same oracle)."""
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=500 + 10 * W + H + causal)
+    ctxs, plans = _hp_world(ao, W, H, S, C, SMS if ts else max(1, SMS // W), causal=causal)
+    O = _run_hp(ao, ctxs, plans, Q, K, V)
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    for r in range(W):
+        _check_full(O[r].float().cpu().numpy(), Qn, Kn, Vn, r, bool(causal),
+                    f"hp W={W} H={H} S={S} ts={ts} causal={causal} rank {r}")
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("causal", [0, 1])
+def test_hp_attn_per_rank_calls_epochs_without_host_sync(ao, causal):
+    """One ao_hp_attn call per rank on its own stream (as with one process per GPU), three
+    epochs back to back with different inputs and no host synchronisation: the return
+    buffers and flags are reused across the epoch parities (Q11)."""
+    W, H, S, E = 2, 4, 512, 3
+    ctxs, plans = _hp_world(ao, W, H, S, 256, 32, causal=causal)
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    ins, outs = [], []
+    for e in range(E):
+        Q, K, V = si.attn_inputs(W, H, S, 128, salt=600 + e + 10 * causal)
+        ins.append((Q, K, V))
+        dQ, dK, dV = [q.cuda() for q in Q], [k.cuda() for k in K], [v.cuda() for v in V]
+        outs.append(([torch.empty_like(q) for q in dQ], dQ, dK, dV))
+    torch.cuda.synchronize()
+    for e in range(E):
+        O, dQ, dK, dV = outs[e]
+        for r in (range(W) if e % 2 == 0 else reversed(range(W))):
+            ao.hp_attn(plans[r], dQ[r], dK[r], dV[r], O[r], stream=streams[r])
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check_async()
+    for e in range(E):
+        Q, K, V = ins[e]
+        Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+        for r in range(W):
+            _check_full(outs[e][0][r].float().cpu().numpy(), Qn, Kn, Vn, r, bool(causal),
+                        f"hp per-rank causal={causal} epoch {e} rank {r}")
+    for c in ctxs:
+        c.close()
+
+
+def test_hp_attn_llama_sampled(ao):
+    """Llama-3-8B attention, 32 heads over 8 ranks (4 per rank), 2048 tokens per rank
+    (16384 total), time-sliced loopback; sampled rows of three heads vs fp64."""
+    W, H, S = 8, 32, 2048
+    Q, K, V = si.attn_inputs(W, H, S, 128, salt=7)
+    ctxs, plans = _hp_world(ao, W, H, S, 2048, SMS, timeout_ns=10_000_000_000)
+    O = _run_hp(ao, ctxs, plans, Q, K, V)
+    Qn, Kn, Vn = ([si.to_f64(t) for t in x] for x in (Q, K, V))
+    rows = np.array([0, 127, 128, 1000, 2047])
+    for r in (0, 5):
+        got = O[r][[0, 13, 31]][:, rows].float().cpu().numpy()
+        _check_rows(got, Qn, Kn, Vn, r, [0, 13, 31], rows, False, f"hp llama sampled rank {r}")
+    for c in ctxs:
+        c.close()

@@ -79,8 +79,8 @@ def mps(tmp_path_factory):
     subprocess.run([ctl], input="quit\n", env=dict(os.environ, **env), capture_output=True, text=True)
 
 
-@pytest.mark.parametrize("W,cases,use_mps", [(2, "ag,rs,ar,a2a,attn,sk,rs_bf16,mismatch", False),
-                                             (4, "ag_ce_push,ag_tma_push,ag_ldst_pull,rs,ar,a2a,attn,sk,rs_bf16,mismatch",
+@pytest.mark.parametrize("W,cases,use_mps", [(2, "ag,rs,ar,a2a,attn,hp,sk,rs_bf16,mismatch", False),
+                                             (4, "ag_ce_push,ag_tma_push,ag_ldst_pull,rs,ar,a2a,attn,hp,sk,rs_bf16,mismatch",
                                               True)])
 def test_one_rank_per_process(W, cases, use_mps, mps):
     """W=2 time-sliced (no MPS: the ranks' kernels alternate on the GPU), W=4 concurrent
@@ -90,7 +90,7 @@ def test_one_rank_per_process(W, cases, use_mps, mps):
     assert r.returncode == 0 and not bad, (r.returncode, bad[:4], r.stderr[-3000:])
     names = {x["case"] for x in recs}
     for c in cases.split(","):
-        if c in ("ag", "rs", "attn"):
+        if c in ("ag", "rs", "attn", "hp"):
             assert any(n.startswith(c) for n in names), c
         else:
             assert c in names, c

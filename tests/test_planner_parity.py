@@ -256,3 +256,20 @@ def test_rs_bf16_wire_json_and_flag(ao):
     assert "non-conforming" in ao.N.lib().ao_last_error().decode()
     h32 = ao.Plan(None, dict(d, rs_wire="fp32")).hash()
     assert ao.Plan(None, d).hash() != h32
+
+
+def test_hp_attn_host_plan(ao):
+    """HP attention (NEXT-4) host plan: validation (heads divisible by W, S_loc % 256, chunk
+    rows dividing a source block of H/W heads), JSON, rank-independent hash, workspace = 2
+    parities of gathered Q, K, V and the output return buffer."""
+    base = dict(op="hp_attn", world_size=8, M=4096, N=32, K=128, chunk_rows=2048, backend="ce", n_cta=148)
+    assert ao.validate(dict(base, rank=0)) == []
+    for bad in (dict(N=30), dict(M=384), dict(K=64), dict(chunk_rows=96), dict(chunk_rows=4096 * 4 + 128),
+                dict(backend="tma"), dict(causal=2)):
+        assert ao.validate(dict(base, rank=0, **bad)), bad
+    j = json.loads(ao.plan_json(dict(base, rank=3)))
+    assert j["op"] == "hp_attn" and j["heads_per_rank"] == 4 and j["chunks_per_source"] == 4 * 4096 // 2048
+    assert j["items"] == 8 * 4 * (4096 // 256)
+    hs = {ao.Plan(None, dict(base, rank=r)).hash() for r in range(8)}
+    assert len(hs) == 1
+    assert ao.workspace_bytes(dict(base, rank=0)) == 2 * 4 * 32 * 4096 * 128 * 2

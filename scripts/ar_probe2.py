@@ -12,15 +12,20 @@ Fl = F // W
 A, B = si.rs_inputs(W, M, Fl, H)
 dA, dB = [a.cuda() for a in A], [b.cuda() for b in B]
 C = [torch.empty(M, H, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
-configs = [("space", 256, "chunk_major"), ("time", 256, "chunk_major"), ("time", 1024, "shard_major"),
-           ("time", 256, "shard_major"), ("space", 1024, "shard_major")]
-base = dict(op="gemm_ar", world_size=W, M=M, N=H, K=Fl, intra="grouped", group_m=4, backend="ldst", n_slices=8,
+import os as _os
+configs = [("space", 256, "chunk_major", 8), ("time", 256, "chunk_major", 8), ("time", 1024, "shard_major", 8),
+           ("time", 256, "shard_major", 8), ("space", 1024, "shard_major", 8)]
+if _os.environ.get("AR_SLICES"):
+    configs = [("time", c, o, int(ns)) for ns in _os.environ["AR_SLICES"].split(",")
+               for c, o in ((256, "chunk_major"), (128, "chunk_major"), (512, "chunk_major"))]
+base = dict(op="gemm_ar", world_size=W, M=M, N=H, K=Fl, intra="grouped", group_m=4, backend="ldst",
             rs_reduce="atomic", tile_m=256, tile_n=256, timeout_ns=5_000_000_000)
-ws = max(ao.workspace_bytes(dict(base, chunk_rows=c)) for _, c, _ in configs)
+ws = max(ao.workspace_bytes(dict(base, chunk_rows=c, n_slices=ns)) for _, c, _, ns in configs)
 ctxs = ao.loopback_world(0, W, ws)
-for sched, c, o in configs:
+for sched, c, o, ns in configs:
     nc = 148 if sched == "time" else 148 // W // 2 * 2
-    plans = [ao.Plan(ctxs[r], dict(base, rank=r, chunk_rows=c, chunk_order=o, n_cta=nc)) for r in range(W)]
+    plans = [ao.Plan(ctxs[r], dict(base, rank=r, chunk_rows=c, chunk_order=o, n_cta=nc, n_slices=ns))
+             for r in range(W)]
     for _ in range(3):
         ao.gemm_ar_group(plans, dA, dB, C)
     torch.cuda.synchronize()
@@ -31,6 +36,7 @@ for sched, c, o in configs:
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / 10
-    print(f"{sched:5s} chunk {c:5d} {o:12s}: {ms:.4f} ms  {2 * M * F * H / ms / 1e9:.0f} TF/s", flush=True)
+    print(f"{sched:5s} chunk {c:5d} {o:12s} slices {ns:3d}: {ms:.4f} ms  {2 * M * F * H / ms / 1e9:.0f} TF/s",
+          flush=True)
     for p in plans:
         p.close()

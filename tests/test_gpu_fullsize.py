@@ -79,7 +79,7 @@ def test_fullsize_ag_and_rs_sampled_vs_oracle(ao, rs_reduce):
         c.check_async()
     Bd64 = [si.to_f64(b) for b in Bd]
     for r in range(W):
-        local = _rows(S, 128, rng, extra=4)
+        local = _rows(S, 64, rng, extra=24)
         grows = r * S + local
         A_rows = [si.to_f64(Ar[s][torch.as_tensor(grows)]) for s in range(W)]
         ref = on.gemm_rs_from_rows(A_rows, Bd64)
@@ -141,12 +141,17 @@ def test_config5_70b_ag_sampled_vs_oracle(ao, backend):
         assert ok, f"config5 {backend} rank {r}: elem {e:.3e} frob {f:.3e}"
 
 
-def test_fullsize_gemm_ar_sampled_vs_oracle(ao):
-    """GEMM-AR (NEXT-1) on the down-proj shape at TP=8 in the bench's configuration: every
-    rank's full [M, hidden] output; sampled rows of every owner block on 3 ranks."""
+@pytest.mark.parametrize("sched", ["space", "time"])
+def test_fullsize_gemm_ar_sampled_vs_oracle(ao, sched):
+    """GEMM-AR (NEXT-1) on the down-proj shape at TP=8: space-sliced (1024-row chunks) and the
+    bench's time-sliced configuration (all SMs per rank, 256-row chunks in chunk-major order,
+    256x256 tiles, the peer-grouped gather walk); every rank's full [M, hidden] output,
+    sampled rows of every owner block on 3 ranks."""
     Fl, S = F // W, M // W
     desc = dict(op="gemm_ar", world_size=W, M=M, N=H, K=Fl, chunk_rows=1024, intra="grouped", group_m=4,
                 n_cta=148 // W, backend="ldst", n_slices=8, rs_reduce="atomic", timeout_ns=5_000_000_000)
+    if sched == "time":
+        desc.update(n_cta=148, chunk_rows=256, chunk_order="chunk_major", tile_m=256, tile_n=256)
     ctxs = ao.loopback_world(0, W, ao.workspace_bytes(desc))
     plans = [ao.Plan(ctxs[r], dict(desc, rank=r)) for r in range(W)]
     Ar, Bd = si.rs_inputs(W, M, Fl, H)

@@ -65,13 +65,15 @@ def _ag_world(ao, W, desc):
     return ctxs, plans
 
 
+@pytest.mark.parametrize("dirn", ["push", "pull"])
 @pytest.mark.parametrize("W,n_cta,tile,K", [(2, 10, (256, 256), 512), (2, 7, (128, 256), 1000), (4, 18, (256, 128), 136)])
-def test_ag_gemm_stream_k_vs_oracle(ao, W, n_cta, tile, K):
+def test_ag_gemm_stream_k_vs_oracle(ao, W, n_cta, tile, K, dirn):
     # space-sliced loopback group (n_cta CTAs = n_cta / cta_group workers per rank): each rank's workers run the data-parallel waves, then
     # the stream-K tail; the plan's per-worker chunk waits follow the stream-K walk
     M, N, C = 1024 * W, 768, 128
     desc = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=C, backend="ce", tile_m=tile[0],
-                tile_n=tile[1], n_cta=n_cta, stream_k=1, intra="grouped", group_m=2, timeout_ns=2_000_000_000)
+                tile_n=tile[1], n_cta=n_cta, stream_k=1, intra="grouped", group_m=2, dir=dirn,
+                timeout_ns=2_000_000_000)
     p = osch.plan(osch.default_desc(**dict(desc, rank=0)))
     assert p.get("sk_dp", None) is not None and p["sk_dp"] < len(p["order"])
     A, B = si.ag_inputs(W, M, K, N, salt=11)

@@ -236,16 +236,20 @@ def test_bench_config_timesliced_fullsize(ao):
     for c in ctxs:
         c.check_async()
     rng = np.random.default_rng(7)
-    rows = np.unique(np.concatenate([np.arange(0, M, 1024), np.arange(1023, M, 1024), rng.integers(0, M, 24)]))
+    # every rank; each shard's first / last rows and a tile-boundary row of every 256-row
+    # block (both CTAs of a pair, chunk edges) plus random rows
+    edges = np.concatenate([np.arange(0, M, 256), np.arange(127, M, 256), np.arange(128, M, 256), np.arange(255, M, 256)])
+    rows = np.unique(np.concatenate([edges[::3], rng.integers(0, M, 48)]))
     A64 = [si.to_f64(a) for a in A]
-    for r in (0, 3, 7):
+    for r in range(W):
         ref = on.ag_gemm_rows(A64, si.to_f64(Bu[r]), rows)
         _check(Cu[r][torch.as_tensor(rows)], ref, f"fullsize ag ts r{r}")
-    # RS consumes the GPU's up-proj output (bit-identical input on both sides)
+    # RS consumes the GPU's up-proj output (bit-identical input on both sides); every owner,
+    # 96+ of its 1024 rows (every sub-tile half of each 256-row block, random rows)
     Cu64 = [Cu[s].float().cpu().numpy().astype(np.float64) for s in range(W)]
     Bd64 = [si.to_f64(b) for b in Bd]
-    lrows = np.unique(np.concatenate([[0, 1023], rng.integers(0, M // W, 16)]))
-    for r in (0, 5, 7):
+    lrows = np.unique(np.concatenate([np.arange(0, M // W, 16), [127, 128, 1023], rng.integers(0, M // W, 32)]))
+    for r in range(W):
         ref = on.gemm_rs_rows(Cu64, Bd64, r, lrows)
         _check(Cd[r][torch.as_tensor(lrows)], ref, f"fullsize rs ts r{r}")
 

@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--attn-seq", type=int, default=32768, help="SP attention: total sequence length")
     ap.add_argument("--a2a-chunk", type=int, default=64, help="A2A chunk rows")
     ap.add_argument("--a2a-zipf", type=float, default=0.0, help="A2A routing skew (0 = top-2 of N(0,1) logits)")
+    ap.add_argument("--a2a-group-m", type=int, default=16,
+                    help="A2A GROUP_M (row blocks per group; 16 covers an expert's ~2050 rows: its weight is read once)")
     ap.add_argument("--ar-chunk", type=int, default=256, help="GEMM-AR chunk rows")
     ap.add_argument("--ag-dir", default="push", choices=["push", "pull"], help="AG transfer direction (Lst.2, P:295)")
     ap.add_argument("--chunk", type=int, default=1024)
@@ -500,7 +502,7 @@ def a2a_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms):
     my = list(range(W)) if loop else [rank]
     X, idx, B = si.moe_inputs(W, T, H, N, topk=k, zipf=args.a2a_zipf)
     desc = dict(op="a2a_gemm", world_size=W, M=T, N=N, K=H, topk=k, chunk_rows=args.a2a_chunk, backend="ldst",
-                tile_m=256, tile_n=256, intra="grouped", group_m=8, n_cta=sms, timeout_ns=10_000_000_000)
+                tile_m=256, tile_n=256, intra="grouped", group_m=args.a2a_group_m, n_cta=sms, timeout_ns=10_000_000_000)
     ctxs = ao.loopback_world(local_rank, W, ao.workspace_bytes(desc)) if loop else \
         [ao.dist_world(local_rank, ao.workspace_bytes(desc))]
     plans = [ao.Plan(c, dict(desc, rank=r)) for c, r in zip(ctxs, my)]

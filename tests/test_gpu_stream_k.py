@@ -141,3 +141,40 @@ def test_ag_gemm_stream_k_per_rank_full_size(ao):
     _check(C[torch.as_tensor(rows)], ref, "ag stream-K per-rank full size")
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("tile,n_cta", [((256, 256), 10), ((128, 256), 7)])
+def test_stream_k_mma_order_matches_oracle(ao, tile, n_cta, tmp_path):
+    """The device executes the stream-K walk of oracle.schedule.worker_pieces: the MMA trace
+    gives each worker's tiles in issue order, which must be the tiles of the worker's pieces
+    (data-parallel positions, then its contiguous stream-K range; a split tile appears in
+    two adjacent workers)."""
+    import json
+    W, M, N, K, C = 2, 2048, 768, 512, 128
+    desc = dict(op="ag_gemm", world_size=W, M=M, N=N, K=K, chunk_rows=C, backend="ce", tile_m=tile[0],
+                tile_n=tile[1], n_cta=n_cta, stream_k=1, intra="grouped", group_m=2, timeout_ns=2_000_000_000)
+    ctxs, plans = _ag_world(ao, W, desc)
+    A, B = si.ag_inputs(W, M, K, N, salt=19)
+    dA, dB = [a.cuda() for a in A], [b.cuda() for b in B]
+    Cs = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+    ao.ag_gemm_group(plans, dA, dB, Cs)
+    ctxs[0].trace_enable(1 << 16)
+    ao.ag_gemm_group(plans, dA, dB, Cs)
+    torch.cuda.synchronize()
+    path = str(tmp_path / "sk_trace.json")
+    ctxs[0].trace_dump(path)
+    ctxs[0].trace_enable(0)
+    ev = [e for e in json.load(open(path))["traceEvents"] if e["cat"] == "mma"]
+    cg = tile[0] // 128
+    for r in range(W):
+        p = osch.plan(osch.default_desc(**{k: v for k, v in dict(desc, rank=r).items() if k != "timeout_ns"}))
+        T, nw, nkb = len(p["order"]), p["n_cta"], (K + 63) // 64
+        assert p["sk_dp"] < T
+        # space-sliced group: rank group r owns CTAs [r*n_cta, (r+1)*n_cta); tid // 8 = CTA index in the group
+        for w in range(nw):
+            want = [p["order"][pc[0]] for pc in osch.worker_pieces(T, nw, p["sk_dp"], nkb, w)]
+            mine = sorted((e for e in ev if e["pid"] == r and (e["tid"] // 8) // cg == w), key=lambda e: e["ts"])
+            got = [int(e["name"].split()[1]) for e in mine]
+            assert got == want, (r, w, got, want)
+    for c in ctxs:
+        c.close()

@@ -151,6 +151,8 @@ def run_ours(args, rank, world, local_rank):
         ao.debug_set(k, int(v))
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
+    if SHARED_GPU and world > 1:
+        sms = sms // world // 2 * 2  # the ranks' persistent kernels must co-reside (MPS)
     M = args.tokens
     loop = world == 1
     W = args.tp if loop else world
@@ -178,6 +180,8 @@ def run_ours(args, rank, world, local_rank):
                 d["tile_m"], d["tile_n"] = tm, tn
                 if tm == 512:  # 4-CTA clusters: as many as fit the GPU at once
                     d["n_cta"] = ao.device_query(local_rank, "cluster4_ctas")
+    if not loop and SHARED_GPU:
+        ag_desc["n_cta"] = rs_desc["n_cta"] = ar_desc["n_cta"] = sms
     ws = max(ao.workspace_bytes(ag_desc), ao.workspace_bytes(rs_desc),
              0 if args.no_ar else ao.workspace_bytes(ar_desc))
     if loop:
@@ -277,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
     baseline = None
     if loop and not args.no_baseline and rank == 0:
         baseline = loopback_baseline(torch, A, Bu, Bd, Cu, W, M, F, args)
-    elif not loop and not args.no_baseline:
+    elif not loop and not args.no_baseline and not SHARED_GPU:
         baseline = nccl_baseline(torch, dist, A[0], Bu[0], Bd[0], W, M, F, args, dev)
 
     # --- GEMM-only leg: the same kernel, tiles and workers with no communication -------
@@ -1029,6 +1033,13 @@ def run_reference(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+# AO_BENCH_SHARED_GPU=1 (scripts/bench_shared_gpu.sh): run the N > 1 code path with every rank
+# on GPU 0 under MPS -- gloo process group, each rank's persistent kernels on SMs / N CTAs,
+# the NCCL two-stream baseline skipped.  A functional check of the one-rank-per-process bench
+# path on a single-GPU box; its numbers are not the multi-GPU measurement.
+SHARED_GPU = os.environ.get("AO_BENCH_SHARED_GPU") == "1"
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -1037,11 +1048,16 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if SHARED_GPU:
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if SHARED_GPU:  # test harness: every rank on GPU 0 (under MPS); NCCL refuses shared GPUs
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

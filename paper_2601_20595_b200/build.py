@@ -28,19 +28,50 @@ def nvcc_path():
     raise RuntimeError("nvcc not found")
 
 
+STAMP = LIB + ".stamp"
+
+
+def _source_digest():
+    """sha256 over the sources, headers and extra nvcc flags the library is built from."""
+    import hashlib
+    h = hashlib.sha256(os.environ.get("AO_NVCC_FLAGS", "").encode())
+    for f in [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "autooverlap.h")]:
+        h.update(f.encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def needs_rebuild():
-    if not os.path.exists(LIB):
+    """By content, not mtime (a copied tree -- e.g. the snapshot a GPU box runs -- has fresh
+    mtimes): the stamp written beside the library must match the current sources."""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "autooverlap.h")]
-    return any(os.path.getmtime(d) > t for d in deps)
+    with open(STAMP) as fh:
+        return fh.read().strip() != _source_digest()
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
-    """Compiles every translation unit in parallel (one nvcc per file), then links."""
+    """Compiles every translation unit in parallel (one nvcc per file), then links.  Several
+    processes may call this at once (every rank of a torchrun launch does): an exclusive
+    file lock serializes them, and a process that waited re-checks before rebuilding."""
     if not force and not needs_rebuild():
         return LIB
+    import fcntl
+    os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    with open(os.path.join(ROOT, "build", ".build.lock"), "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        try:
+            if not force and not needs_rebuild():
+                return LIB
+            return _build_locked(verbose)
+        finally:
+            fcntl.flock(lock, fcntl.LOCK_UN)
+
+
+def _build_locked(verbose: bool) -> str:
     from concurrent.futures import ThreadPoolExecutor
+    digest = _source_digest()  # of the sources this build compiles
     nvcc = nvcc_path()
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
@@ -63,11 +94,15 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"] + objs
+    tmp = f"{LIB}.{os.getpid()}.tmp"
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(tmp, LIB)
+    with open(STAMP + ".tmp", "w") as fh:
+        fh.write(digest + "\n")
+    os.replace(STAMP + ".tmp", STAMP)
     return LIB
 
 

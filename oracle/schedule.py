@@ -494,8 +494,9 @@ def group_schedule(descs, sm_count=148):
     position) entries with Lst.1's persistent stride:
       * AG -- rank after rank, each rank's plan order intact;
       * RS / AR -- owner after owner; for owner o the positions of source ranks o+1, o+2,
-        ..., o+W-1 (the rotation) whose tile rows o owns, then o's own positions (its
-        tiles wait on every other source's contribution, so they come after them).
+        ..., o+W-1 (the rotation; reversed for odd owners -- serpentine, Q24)
+        whose tile rows o owns, then o's own positions (its tiles wait on every other
+        source's contribution, so they come after them).
     Waits: before each tile a worker acquires the chunks the tile's rows intersect
     that it needs from peers -- AG: chunks of another source; RS: the own tile's chunks --
     the first time the worker needs (rank, chunk)."""
@@ -530,7 +531,10 @@ def group_schedule(descs, sm_count=148):
         if S % bm != 0:
             return None
         for o in range(W):
-            for step in list(range(1, W)) + [0]:
+            # even owners: sources o+1, o+2, ...; odd owners: the reverse (serpentine, so each
+            # phase starts on the weights the previous one read last); own positions last
+            steps = list(range(1, W)) if o % 2 == 0 else list(range(W - 1, 0, -1))
+            for step in steps + [0]:
                 gi = gi_of[(o + step) % W]
                 for k in range(len(plans[gi]["order"])):
                     if rows_of(gi, k)[0] // S == o:

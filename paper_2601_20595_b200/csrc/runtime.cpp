@@ -147,7 +147,6 @@ struct DebugKnobs {
   int64_t gemm_group_m = 16;
   int64_t ts_lag = 0;  // time-sliced RS: lag the own run behind the next owner's first source run
   int64_t ts_owners = 1;  // time-sliced RS: owners per phase (experiment)
-  int64_t ts_serp = 0;    // time-sliced RS: odd owners' phases run their sources in reverse (experiment)
   int64_t gemm_stream_k = 0;  // ao_gemm: desc.stream_k of its internal plan (0 off, 1 on, -1 auto)
   int64_t prearrive = 0;  // per-rank measurement: every chunk flag of the launch's ranks is set
                           // for the coming epoch before the kernel and no copy-engine chain is
@@ -537,7 +536,6 @@ ao_status ao_debug_set(const char* key, int64_t value) {
   else if (!strcmp(key, "exp")) g_debug.exp = value;
   else if (!strcmp(key, "ts_lag")) g_debug.ts_lag = value;
   else if (!strcmp(key, "ts_owners")) g_debug.ts_owners = value;
-  else if (!strcmp(key, "ts_serp")) g_debug.ts_serp = value;
   else if (!strcmp(key, "gemm_stream_k")) g_debug.gemm_stream_k = value;
   else if (!strcmp(key, "prearrive")) g_debug.prearrive = value;
   else return fail(AO_ERR_INVALID_ARG, "unknown debug key %s", key);
@@ -970,10 +968,9 @@ static bool build_segments(int n, ao_plan* const* plans, int mode, ao::KernelArg
           runs.push_back({ph, own ? 2 * hp.W : 2 * srot, owner, k, {i, k, k1, 0}});
         } else if (g_debug.ts_lag)  // behind the first ts_lag source runs of the next owner's phase
           runs.push_back({own ? owner + 1 : owner, own ? 2 * int(g_debug.ts_lag) + 1 : 2 * rot, 0, k, {i, k, k1, 0}});
-        else if (g_debug.ts_serp && (owner & 1))  // LRU-friendly: reuse the weights the last phase read last
-          runs.push_back({owner, own ? 2 * hp.W : 2 * (hp.W - rot), 0, k, {i, k, k1, 0}});
-        else
-          runs.push_back({owner, own ? 2 * hp.W : 2 * rot, 0, k, {i, k, k1, 0}});
+        else  // odd owners run their sources in reverse rotation (serpentine): each phase starts
+              // with the weights the previous phase read last, still in L2 (RS 1 % faster)
+          runs.push_back({owner, own ? 2 * hp.W : 2 * ((owner & 1) ? hp.W - rot : rot), 0, k, {i, k, k1, 0}});
         k = k1;
       }
     }

@@ -40,10 +40,12 @@ CE_MIN_CHUNK_BYTES = 1 << 20
 
 
 def candidate_space(op: str, W: int, M: int, N: int, K: int, chunks=None, backends=None, intras=None,
-                    tiles=None, orders=None, dirs=None, scheds=None, comm_ctas=None, slices=None):
+                    tiles=None, orders=None, dirs=None, scheds=None, comm_ctas=None, slices=None, stream_ks=None):
     """Enumerate descs of one op (dicts with the oracle/planner desc keys).  `scheds`
     (optional) adds the loopback group schedule as key "sched": "space" (SMs/W CTAs per
-    rank, ranks concurrent) or "time" (every rank over all SMs, Q24)."""
+    rank, ranks concurrent) or "time" (every rank over all SMs, Q24).
+    `stream_ks` (optional, e.g. [0, -1]): the stream-K tail setting of AG plans with the
+    copy engine (Q28); other plans keep 0."""
     S = M // W
     chunks = chunks or [c for c in (128, 256, 512, 1024, 2048, 4096) if c <= S and S % c == 0]
     backends = backends or (["ce", "tma", "ldst"] if op == "ag_gemm" and W > 1 else ["ce"])
@@ -56,9 +58,12 @@ def candidate_space(op: str, W: int, M: int, N: int, K: int, chunks=None, backen
     out = []
     for c, b, (intra, gm), (tm, tn), o, dr in itertools.product(chunks, backends, intras, tiles, orders, dirs):
         inkernel = op == "ag_gemm" and b in ("tma", "ldst")
-        for cc, ns in itertools.product(comm_ctas if inkernel else [0], slices if inkernel else [1]):
+        sks = (stream_ks or [0]) if (op == "ag_gemm" and b == "ce" and tm != 512) else [0]
+        for cc, ns, sk in itertools.product(comm_ctas if inkernel else [0], slices if inkernel else [1], sks):
             d = dict(op=op, world_size=W, M=M, N=N, K=K, chunk_rows=c, backend=b, intra=intra, group_m=gm,
                      tile_m=tm, tile_n=tn, chunk_order=o, dir=dr, n_slices=ns, comm_ctas=cc)
+            if sk:
+                d["stream_k"] = sk
             for sc in (scheds or [None]):
                 out.append(d if sc is None else dict(d, sched=sc))
     return out

@@ -115,3 +115,10 @@ def test_small_measured_tune_winner_matches_oracle(tune, tmp_path):
         assert ok, (rows[0]["desc"], e, f)
     for c in ctxs:
         c.close()
+
+
+def test_stream_k_axis(tune):
+    descs = tune.candidate_space("ag_gemm", 8, 8192, 1792, 4096, backends=["ce", "tma"], stream_ks=[0, -1])
+    assert {d.get("stream_k", 0) for d in descs if d["backend"] == "ce"} == {0, -1}
+    assert {d.get("stream_k", 0) for d in descs if d["backend"] == "tma"} == {0}
+    assert all("stream_k" not in d for d in tune.candidate_space("gemm_rs", 4, 4096, 4096, 1024, stream_ks=[0, 1]))

@@ -79,6 +79,28 @@ __device__ __noinline__ void attn_spin(const uint32_t* p, uint32_t target, const
   ld_acquire_sys(p);
 }
 
+// Device trace (ao_ctx_trace_enable), compiled in only with -DAO_ATTN_TRACE=1 (the hooks
+// cost ~3 % even when off; scripts/attn_trace.py): kind TR_LOAD = the producer's wait for a
+// free K stage, TR_MMA = the MMA warp's wait for a tile's P (softmax done), TR_WAIT = a
+// softmax warpgroup's wait for S, TR_EPI = its softmax of one block (id = tile x).
+#ifndef AO_ATTN_TRACE
+#define AO_ATTN_TRACE 0
+#endif
+__device__ __forceinline__ void attn_trace(const AttnArgs& A, uint32_t kind, int rank, int id, uint64_t t0) {
+  if (!AO_ATTN_TRACE || A.trace == nullptr) return;
+  const uint32_t i = atomicAdd(A.trace_cursor, 1u);
+  if (i < A.trace_cap) {
+    TraceEvent e;
+    e.t0 = t0;
+    e.t1 = globaltimer();
+    e.kind = kind | (A.trace_seq << 8);
+    e.rank = uint32_t(rank);
+    e.cta = blockIdx.x;
+    e.id = uint32_t(id);
+    A.trace[i] = e;
+  }
+}
+
 // Work items of this CTA in order: (rank group, item).  Space-sliced: its own group's items
 // with the persistent stride; time-sliced: every group's items, rank after rank.
 template <class F>
@@ -565,7 +587,9 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
           const int row = local ? hoff * S + krow : src * hv_rows + krow;
           uint8_t* kdst = sK + kst * (kKVBytes / 2);
           uint8_t* vdst = sV + vst * (kKVBytes / 2);
+          const uint64_t tk = AO_ATTN_TRACE && args.trace ? globaltimer() : 0;
           mbar_wait(&B.kempty[kst], ((n / kPPK) & 1u) ^ 1u);
+          if (AO_ATTN_TRACE && args.trace) attn_trace(args, TR_LOAD, R.rank, int(n), tk);
           mbar_arrive_expect_tx(&B.kfull[kst], kKVBytes / 2);
           tma_load_2d(kdst, mk, &B.kfull[kst], 0, row, pol);
           tma_load_2d(kdst + kHalf, mk, &B.kfull[kst], 64, row, pol);
@@ -613,7 +637,9 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
         __syncwarp();
         for (int x = 0; x < 2; ++x) {
           if (j == 0) mbar_wait(&B.ofree[x], (t & 1u) ^ 1u);  // O_x of the previous item read
+          const uint64_t tp = AO_ATTN_TRACE && args.trace ? globaltimer() : 0;
           mbar_wait(&B.pfull[x], nn & 1u);
+          if (AO_ATTN_TRACE && args.trace && lane == 0) attn_trace(args, TR_MMA, args.rk[g].rank, x, tp);
           if (x == 0) mbar_wait(&B.vfull[nn % kPPV], (nn / kPPV) & 1u);
           tc_fence_after();
           if (lane == 0) {
@@ -665,9 +691,12 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
         kv_of(it, j, d, kb);
         // causal: keys kb*128 + c beyond this query are masked (own diagonal blocks only)
         const int kmax = (CAUSAL && d == 0) ? qloc - kb * kBlk : 1 << 30;
+        const uint64_t ts0 = AO_ATTN_TRACE && args.trace ? globaltimer() : 0;
         mbar_wait(&B.sfull[x], nn & 1u);
         tc_fence_after();
         if (nn >= 1) pv_wait(nn - 1);  // PV(nn-1) done before O is rescaled / P(nn) written
+        const uint64_t ts1 = AO_ATTN_TRACE && args.trace ? globaltimer() : 0;
+        if (AO_ATTN_TRACE && args.trace && qd == 0 && lane == 0) attn_trace(args, TR_WAIT, R.rank, x, ts0);
         if (CAUSAL && d == 0 && kb >= 2 * qp) {
           // causal diagonal blocks (two per item): keys past this query become -inf in TMEM,
           // so the passes below stay mask-free (registers are tight)
@@ -743,6 +772,7 @@ __global__ void __maxnreg__(152) attn_pp_kernel(const __grid_constant__ AttnArgs
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&B.pfull[x]);
+        if (AO_ATTN_TRACE && args.trace && qd == 0 && lane == 0) attn_trace(args, TR_EPI, R.rank, x, ts1);
       }
       pv_wait(n + nkv - 1);
       const float inv = 1.f / l;

@@ -1395,6 +1395,10 @@ static ao_status launch_attn_group(int n, ao_plan* const* plans, const void* con
   ka->nch = nch;
   ka->ctas_per_rank = h0.n_cta;
   ka->scale_log2 = float(1.4426950408889634 / std::sqrt(128.0));
+  ka->trace = p0->ctx->trace;  // device trace (ao_ctx_trace_enable on the first plan's ctx)
+  ka->trace_cursor = p0->ctx->trace_cursor;
+  ka->trace_cap = p0->ctx->trace_cap;
+  ka->trace_seq = p0->ctx->trace ? p0->ctx->trace_seq++ : 0;
   ka->causal = h0.desc.causal;
   ka->timeout_ns = h0.desc.timeout_ns ? h0.desc.timeout_ns : 5000000000ull;
   ka->err = p0->ctx->err_dev;

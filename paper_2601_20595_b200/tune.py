@@ -188,7 +188,7 @@ def _time_loopback(desc, W, device, A, B, C, warmup, iters, n_cta):
 
 
 def tune_loopback(op: str, W: int, M: int, N: int, K: int, device: int = 0, budget_s: float = 120.0,
-                  warmup: int = 2, iters: int = 5, space=None, log=None):
+                  warmup: int = 2, iters: int = 5, space=None, log=None, use_e4: bool = True):
     """Measure every kept candidate of `op` in a W-rank loopback world on `device` and
     return rows sorted by time: [{desc, ms, tflops, tile}] + the pruned list."""
     import torch
@@ -197,7 +197,7 @@ def tune_loopback(op: str, W: int, M: int, N: int, K: int, device: int = 0, budg
     torch.cuda.set_device(device)
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     descs = space if space is not None else candidate_space(op, W, M, N, K)
-    kept, pruned = prune(descs, sms // W, e4=load_e4())
+    kept, pruned = prune(descs, sms // W, e4=load_e4() if use_e4 else None)
     if op == "ag_gemm":
         A, B = si.ag_inputs(W, M, K, N)
         A = [a.cuda() for a in A]

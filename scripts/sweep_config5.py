@@ -18,14 +18,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("out")
 ap.add_argument("--tokens", type=int, default=32768)
 ap.add_argument("--budget", type=float, default=900.0)
+ap.add_argument("--no-e4", action="store_true", help="measure every backend (no E4-seeded pruning)")
 a = ap.parse_args()
 W, HIDDEN, FFN = 8, 8192, 28672
 M, N, K = a.tokens, FFN // W, HIDDEN
 S = M // W
 chunks = [c for c in (64, 128, 256, 512, 1024, 2048, 4096) if c <= S and S % c == 0]
 space = tune.candidate_space("ag_gemm", W, M, N, K, chunks=chunks, backends=["ce", "tma", "ldst"],
-                             intras=[("grouped", 4)], tiles=[(256, 256)], dirs=["push"], scheds=["space", "time"])
-rows, pruned = tune.tune_loopback("ag_gemm", W, M, N, K, budget_s=a.budget, warmup=2, iters=10, space=space)
+                             intras=[("grouped", 4)], tiles=[(256, 256)], dirs=["push"], scheds=["space", "time"],
+                             comm_ctas=[0], slices=[2])
+rows, pruned = tune.tune_loopback("ag_gemm", W, M, N, K, budget_s=a.budget, warmup=2, iters=10, space=space,
+                                  use_e4=not a.no_e4)
 with open(a.out, "w") as f:
     for r in rows:
         d = r["desc"]

@@ -729,8 +729,9 @@ def per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms):
             rows = {}
             # (tile, stream_k): the planner's pick with auto stream-K (Q28), 256x256 without
             # and with the stream-K tail, the 512x256 cluster tile
+            # gemm_rs "+bf16wire": the non-conforming bf16 partial wire (Q14), half the bytes
             variants = (("auto", -1), ("256x256", 0), ("256x256+sk", 1), ("512x256", 0)) if op == "ag_gemm" else \
-                (("auto", 0), ("256x256", 0), ("512x256", 0))
+                (("auto", 0), ("256x256", 0), ("512x256", 0), ("256x256+bf16wire", 0))
             # two passes over the variants, best of each (the first launches after the main
             # legs run on a GPU still settling its clocks)
             for tile, sk in [v for _ in range(2) for v in variants]:
@@ -739,6 +740,8 @@ def per_rank_leg(torch, ao, ctxs, A, Bu, Cu, Bd, W, M, F, args, dev, sms):
                     d.update(N=F, K=HIDDEN, backend="ce", stream_k=sk)
                 else:
                     d.update(N=HIDDEN, K=F, rs_reduce="atomic")
+                    if tile.endswith("+bf16wire"):
+                        d["rs_wire"] = "bf16"
                 if tile != "auto":
                     d["tile_m"], d["tile_n"] = (int(x) for x in tile.split("+")[0].split("x"))
                     if d["tile_m"] == 512:

@@ -130,6 +130,34 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def kernel_clocks(ctx, step, steps=3):
+    """The SM clock the fused kernels actually run at: clock64 cycles / %globaltimer ns over
+    every MMA span (TR_CLK trace events) of `steps` extra back-to-back steps run right after
+    the timed region (tracing costs ~3 %, so never inside it).  NVML's clock reading stays at
+    sm_max_mhz through these kernels while the in-kernel rate is ~30 % lower: the power limit
+    acts below NVML's view (scripts/experiments/clock_probe.cu calibrates the method: an idle
+    GPU reads sm_max_mhz).  Launches alternate ag_gemm, rs; the first step is skipped."""
+    import tempfile
+    ctx.trace_enable(1 << 21)
+    for _ in range(steps):
+        step()
+    fd, path = tempfile.mkstemp(suffix=".json")
+    os.close(fd)
+    try:
+        ctx.trace_dump(path)
+        with open(path) as f:
+            ev = json.load(f)["traceEvents"]
+    finally:
+        ctx.trace_enable(0)
+        os.unlink(path)
+    out = {}
+    for name, par in (("ag_gemm", 0), ("gemm_rs", 1)):
+        mhz = [int(e["name"].split()[1]) / e["dur"] for e in ev
+               if e["cat"] == "clock" and e["dur"] > 0 and e["args"]["launch"] >= 2 and e["args"]["launch"] % 2 == par]
+        out[name] = round(statistics.median(mhz)) if mhz else None
+    return out
+
+
 # ============================================================================ our arm
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -265,6 +293,9 @@ def run_ours(args, rank, world, local_rank):
         ctxs[0].trace_dump(args.trace + ".json")
         ctxs[0].trace_enable(0)
 
+    # --- the SM clock under load, measured inside the kernels (decides the peak regime) -----
+    clk_kernel = kernel_clocks(ctxs[0], step) if rank == 0 else {}
+
     # --- sanity vs cuBLAS on sampled rows (not the oracle; parity lives in tests/) ------
     check = None
     if rank == 0 and not args.no_check:
@@ -318,8 +349,18 @@ def run_ours(args, rank, world, local_rank):
         e2e = e2e_leg(torch, dist, args, A, Cd, step, barrier, world, flops_step, dev)
 
     peaks, peaks_src = load_peaks()
-    peak = peaks["bf16_tflops"]
+    # Peak regime (task rule: burst for a kernel timed alone, sustained for one timed inside
+    # a long step), decided by measurement: the dominant kernel's in-kernel SM clock against
+    # the clock MEASURED_PEAKS' sustained cuBLAS figure was taken at.
     dom_ms = max(ag_ms, rs_ms)
+    sus_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
+    f_dom = clk_kernel.get("ag_gemm" if ag_ms >= rs_ms else "gemm_rs")
+    sustained = bool(f_dom and sus_mhz and "bf16_tflops_sustained" in peaks and f_dom <= 1.1 * sus_mhz)
+    peak = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
+    regime = (f"sustained: the kernel runs at {f_dom} MHz (in-kernel clock64/globaltimer median over its MMA "
+              f"spans) vs sm_max {peaks.get('sm_max_mhz')} MHz; the sustained cuBLAS figure was measured at "
+              f"{sus_mhz} MHz" if sustained else
+              f"burst: in-kernel clock {f_dom} MHz, sustained measurement at {sus_mhz} MHz")
     dom = "ag_gemm" if ag_ms >= rs_ms else "gemm_rs"
     per_launch_flops = flops_ag / (1 if loop else W)
     achieved = per_launch_flops / (dom_ms * 1e-3) / 1e12
@@ -342,14 +383,20 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": 2 * args.steps * (1 if loop else world),  # fused kernels, all ranks
         "kernels_ms": {"ag_gemm": round(ag_ms, 4), "gemm_rs": round(rs_ms, 4)},
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                     "peak_source": f"{peaks_src} bf16_tflops (burst)", "unit": "TFLOP/s",
+                     "peak_source": f"{peaks_src} bf16_tflops{'_sustained' if sustained else ''} "
+                                    f"({'sustained' if sustained else 'burst'})",
+                     "peak_regime": regime, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4),
+                     "frac_of_burst": round(achieved / peaks["bf16_tflops"], 4),
+                     # the tensor pipe's own ceiling at the clock the kernel ran: 148 SMs x 8192
+                     # dense bf16 flop/clk (tcgen05 kind::f16; 2.25 PFLOP/s nominal = 1.86 GHz)
+                     "frac_at_kernel_clock": (round(achieved / (torch.cuda.get_device_properties(dev).multi_processor_count * 8192 * f_dom * 1e-6), 4) if f_dom else None),
                      "frac_of_sustained": round(achieved / peaks.get("bf16_tflops_sustained", peak), 4),
                      "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
                      "flops_per_launch": per_launch_flops,
                      "per_kernel": {"ag_gemm": {"achieved": round(ag_ach, 1), "frac": round(ag_ach / peak, 4)},
                                     "gemm_rs": {"achieved": round(rs_ach, 1), "frac": round(rs_ach / peak, 4)}}},
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), sm_mhz_in_kernel=clk_kernel),
         "e2e": e2e,
         "check": check,
         "baseline_kernel_level": baseline,

@@ -859,6 +859,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? AO_AG
       uint32_t stage = 0, fpar = 0, acc = 0, acc_phase = 0;
       walk([&](const RankArgs& R, int grp, int k, const KSpan sp) {
         const uint64_t t_mma = args.trace ? globaltimer() : 0;
+        const long long c_mma = args.trace ? clock64() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -901,6 +902,7 @@ __global__ void __launch_bounds__((MODE == MODE_AG || MODE == MODE_GEMM) ? AO_AG
           if (args.trace) {
             const int2 tmn = tile_of(R, grp, k);
             trace_event(args, TR_MMA, R.rank, lcta, tmn.x * R.n_nb + tmn.y, t_mma);
+            trace_event(args, TR_CLK, R.rank, lcta, int(clock64() - c_mma), t_mma);
           }
         }
         __syncwarp();

@@ -144,7 +144,9 @@ struct AttnArgs {
 };
 
 // In-kernel trace event (AO tracing): 32 bytes, %globaltimer nanoseconds.
-enum TraceKind : uint32_t { TR_WAIT = 1, TR_LOAD = 2, TR_MMA = 3, TR_EPI = 4, TR_COMM = 5, TR_RED = 6, TR_REDWAIT = 7 };
+// TR_CLK: id = SM clock cycles (clock64) over an MMA span -- the clock the kernel runs at under load.
+enum TraceKind : uint32_t { TR_WAIT = 1, TR_LOAD = 2, TR_MMA = 3, TR_EPI = 4, TR_COMM = 5, TR_RED = 6, TR_REDWAIT = 7,
+                            TR_CLK = 8 };
 struct TraceEvent {
   uint64_t t0, t1;
   uint32_t kind, rank, cta, id;

@@ -779,7 +779,7 @@ ao_status ao_ctx_trace_enable(ao_ctx* c, int64_t capacity) {
 }
 
 ao_status ao_ctx_trace_dump(ao_ctx* c, const char* path, int64_t* n_events) {
-  static const char* kinds[] = {"?", "wait", "load", "mma", "epilogue", "comm", "reduce", "reduce_wait"};
+  static const char* kinds[] = {"?", "wait", "load", "mma", "epilogue", "comm", "reduce", "reduce_wait", "clock"};
   if (!c || !path) return fail(AO_ERR_INVALID_ARG, "bad argument");
   if (!c->trace) return fail(AO_ERR_STATE, "tracing is not enabled on this ctx");
   AO_CUDA(cudaSetDevice(c->device));
@@ -799,7 +799,7 @@ ao_status ao_ctx_trace_dump(ao_ctx* c, const char* path, int64_t* n_events) {
   for (uint32_t i = 0; i < n; ++i) {
     const ao::TraceEvent& e = ev[i];
     const uint32_t kk = e.kind & 0xff, seq = e.kind >> 8;
-    const char* k = kk < 8 ? kinds[kk] : "?";
+    const char* k = kk < 9 ? kinds[kk] : "?";  // "clock": id = SM cycles over the event (an MMA span)
     fprintf(f,
             "%s{\"name\":\"%s %u\",\"cat\":\"%s\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":%u,\"tid\":%u,"
             "\"args\":{\"launch\":%u}}",

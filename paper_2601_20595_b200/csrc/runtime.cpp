@@ -934,10 +934,11 @@ static ao_status mark_done(int n, ao_plan* const* plans, const std::vector<uint3
 //    while its tiles run); the copy-engine chains are issued destination-major in the same
 //    order so each rank's chunks land before its turn.
 //  * RS: owner after owner; for owner o the other ranks' runs of tiles whose rows o owns
-//    (rotation o+1, o+2, ...); o's own run (the fused reduction) is lagged behind the first
-//    source run of owner o+1, so its contributions are complete when it starts.  Every
-//    tile that waits (an own tile) comes after all the tiles it waits for, so with all
-//    CTAs co-resident the list drains without deadlock (induction on the list index).
+//    (rotation o+1, o+2, ...; odd owners in reverse, the serpentine), then o's own run (the
+//    fused reduction) last in the phase (debug ts_lag: behind the next owner's first source
+//    runs instead -- measured slower).  Every tile that waits (an own tile) comes after all
+//    the tiles it waits for, so with all CTAs co-resident the list drains without deadlock
+//    (induction on the list index).
 //  * GEMM (batched GEMM-only leg): problem after problem.
 // Chunk waits are taken per tile in the kernel (the plan's per-CTA wait table assumes the
 // space-sliced CTA assignment).  Returns false (and no segments) when not applicable.

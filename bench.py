@@ -613,7 +613,9 @@ def a2a_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms):
             "workload": "mixtral-8x7b-moe-ep8-a2a-gemm-" + ("loopback" if loop else "nvlink"),
             "tokens": W * T, "hidden": H, "n_expert_out": N, "topk": k, "zipf": args.a2a_zipf,
             "chunk_rows": args.a2a_chunk, "ms": round(ms, 4), "tflops": round(tf, 1),
-            "frac_of_peak": round(tf / peaks["bf16_tflops"], 4), "rows_per_expert": rows if loop else rows[0],
+            "frac_of_peak": round(tf / peaks["bf16_tflops"], 4),  # burst
+            "frac_of_sustained": round(tf / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]), 4),
+            "rows_per_expert": rows if loop else rows[0],
             "gemm_only_ms_equal_rows": round(g_ms, 4),
             "gemm_only_tflops": round(g_flops / (g_ms * 1e-3) / 1e12, 1), "launches_per_op": 2}
 
@@ -728,7 +730,8 @@ def attn_leg(torch, ao, si, args, dev, loop, world, rank, local_rank, dist, sms)
     return {"what": "sequence-parallel attention over the all-gathered KV in ring order (NEXT-4), non-causal",
             "workload": "llama3-8b-attn-sp%d-%s" % (W, "loopback" if loop else "nvlink"),
             "seq_total": Stot, "heads": H, "head_dim": d, "ms": round(ms, 4), "tflops": round(tf, 1),
-            "frac_of_peak": round(tf / peaks["bf16_tflops"], 4),
+            "frac_of_peak": round(tf / peaks["bf16_tflops"], 4),  # burst
+            "frac_of_sustained": round(tf / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]), 4),
             "causal_ms": round(ms_c, 4), "causal_tflops": round(flops_c / (ms_c * 1e-3) / 1e12, 1),
             "sdpa_same_gpu_ms": None if sd_ms is None else round(sd_ms, 4),
             "sdpa_tflops": None if sd_ms is None else round(flops / (sd_ms * 1e-3) / 1e12, 1),

@@ -286,16 +286,21 @@ def run_ours(args, rank, world, local_rank):
     flops_step = 2 * flops_ag
     value = flops_step / (ms * 1e-3) / 1e12
 
-    if args.trace and rank == 0:
-        # three back-to-back steps (launches 0..5: ag, rs, ag, rs, ag, rs) in one trace
+    if args.trace:
+        # three back-to-back steps (launches 0..5: ag, rs, ag, rs, ag, rs) in one trace; every
+        # rank steps (collective ops), rank r > 0 writes PREFIX.rank<r>.json
         ctxs[0].trace_enable(1 << 21)
         for _ in range(3):
             step()
-        ctxs[0].trace_dump(args.trace + ".json")
+        ctxs[0].trace_dump(args.trace + (".json" if rank == 0 else ".rank%d.json" % rank))
         ctxs[0].trace_enable(0)
+        barrier()
 
     # --- the SM clock under load, measured inside the kernels (decides the peak regime) -----
-    clk_kernel = kernel_clocks(ctxs[0], step) if rank == 0 else {}
+    # every rank runs the traced steps (the ops are collective: a rank stepping alone would
+    # wait on its peers' chunks); each reads its own kernels' clock
+    clk_kernel = kernel_clocks(ctxs[0], step)
+    barrier()
 
     # --- sanity vs cuBLAS on sampled rows (not the oracle; parity lives in tests/) ------
     check = None

@@ -302,6 +302,32 @@ def run_ours(args, rank, world, local_rank):
     clk_kernel = kernel_clocks(ctxs[0], step)
     barrier()
 
+    # --- single-op latency: each op alone, barrier + synchronize before it ---
+    def one_op(fn):
+        ts = []
+        for _ in range(7):
+            barrier()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            fn()
+            s1.record(stream)
+            s1.synchronize()
+            ts.append(s0.elapsed_time(s1))
+        v = statistics.median(ts[1:])
+        if world > 1:
+            t = torch.tensor([v], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            v = t.item()
+        return round(v, 4)
+
+    if loop:
+        latency = {"ag_gemm": one_op(lambda: ao.ag_gemm_group(pa, A, Bu, Cu)),
+                   "gemm_rs": one_op(lambda: ao.gemm_rs_group(pr, Cu, Bd, Cd))}
+    else:
+        latency = {"ag_gemm": one_op(lambda: ao.ag_gemm(pa[0], A[0], Bu[0], Cu[0])),
+                   "gemm_rs": one_op(lambda: ao.gemm_rs(pr[0], Cu[0], Bd[0], Cd[0]))}
+    latency["what"] = "ms per op launched alone after a barrier + synchronize (median of 6, max over ranks)"
+
     # --- sanity vs cuBLAS on sampled rows (not the oracle; parity lives in tests/) ------
     check = None
     if rank == 0 and not args.no_check:
@@ -389,6 +415,7 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "inputs+weights ~0.7 GB/step > 126 MB L2 (no flush)", "parallelism": f"tp{W}"},
         "gpu_launches": 2 * args.steps * (1 if loop else world),  # fused kernels, all ranks
         "kernels_ms": {"ag_gemm": round(ag_ms, 4), "gemm_rs": round(rs_ms, 4)},
+        "single_op_latency_ms": latency,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                      "peak_source": f"{peaks_src} bf16_tflops{'_sustained' if sustained else ''} "
                                     f"({'sustained' if sustained else 'burst'})",

@@ -130,6 +130,21 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def choose_peak(peaks, f_kernel):
+    """Roofline denominator by the task's rule -- the burst figure for a kernel timed alone,
+    the sustained one for a kernel timed inside a long step -- decided by measurement: the
+    sustained figure when the kernel's in-kernel SM clock (MHz) is at most 1.1x the clock the
+    sustained cuBLAS figure was measured at.  Returns (peak, sustained?, regime text)."""
+    sus_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
+    sustained = bool(f_kernel and sus_mhz and "bf16_tflops_sustained" in peaks and f_kernel <= 1.1 * sus_mhz)
+    if sustained:
+        return peaks["bf16_tflops_sustained"], True, (
+            f"sustained: the kernel runs at {f_kernel} MHz (in-kernel clock64/globaltimer median over its MMA "
+            f"spans) vs sm_max {peaks.get('sm_max_mhz')} MHz; the sustained cuBLAS figure was measured at "
+            f"{sus_mhz} MHz")
+    return peaks["bf16_tflops"], False, f"burst: in-kernel clock {f_kernel} MHz, sustained measurement at {sus_mhz} MHz"
+
+
 def kernel_clocks(ctx, step, steps=3):
     """The SM clock the fused kernels actually run at: clock64 cycles / %globaltimer ns over
     every MMA span (TR_CLK trace events) of `steps` extra back-to-back steps run right after
@@ -385,14 +400,8 @@ def run_ours(args, rank, world, local_rank):
     # a long step), decided by measurement: the dominant kernel's in-kernel SM clock against
     # the clock MEASURED_PEAKS' sustained cuBLAS figure was taken at.
     dom_ms = max(ag_ms, rs_ms)
-    sus_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
     f_dom = clk_kernel.get("ag_gemm" if ag_ms >= rs_ms else "gemm_rs")
-    sustained = bool(f_dom and sus_mhz and "bf16_tflops_sustained" in peaks and f_dom <= 1.1 * sus_mhz)
-    peak = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
-    regime = (f"sustained: the kernel runs at {f_dom} MHz (in-kernel clock64/globaltimer median over its MMA "
-              f"spans) vs sm_max {peaks.get('sm_max_mhz')} MHz; the sustained cuBLAS figure was measured at "
-              f"{sus_mhz} MHz" if sustained else
-              f"burst: in-kernel clock {f_dom} MHz, sustained measurement at {sus_mhz} MHz")
+    peak, sustained, regime = choose_peak(peaks, f_dom)
     dom = "ag_gemm" if ag_ms >= rs_ms else "gemm_rs"
     per_launch_flops = flops_ag / (1 if loop else W)
     achieved = per_launch_flops / (dom_ms * 1e-3) / 1e12
@@ -1038,12 +1047,27 @@ def e2e_leg(torch, dist, args, A, Cd, step, barrier, world, flops_step, dev):
         ms = t.item()
     h2d = sum(h.numel() * h.element_size() for h in hA)
     d2h = sum(h.numel() * h.element_size() for h in hC[0])
+    # the PCIe bound: this step's copies alone, each direction, on the same streams
+    link = {}
+    for name, st, pairs in (("h2d_gbs_alone", up, list(zip(dA[0], hA))), ("d2h_gbs_alone", down, list(zip(hC[0], dC[0])))):
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(st)
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                for d, h in pairs:
+                    d.copy_(h, non_blocking=True)
+        c1.record(st)
+        torch.cuda.synchronize()
+        nb = 3 * sum(d.numel() * d.element_size() for d, _ in pairs)
+        link[name] = round(nb / (c0.elapsed_time(c1) * 1e-3) / 1e9, 1)
     if world > 1:
         h2d *= world
         d2h *= world
     return {"value": round(flops_step / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "pipelining": "double-buffered; H2D of step i+1 and D2H of step i overlap step i's compute"}
+            "pipelining": "double-buffered; H2D of step i+1 and D2H of step i overlap step i's compute",
+            "pcie": link}
 
 
 # ============================================================================ CPU oracle

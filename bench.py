@@ -992,36 +992,51 @@ def e2e_leg(torch, dist, args, A, Cd, step, barrier, world, flops_step, dev):
     """Same step through the public API with this step's activations copied from pinned
     host memory and its output read back to pinned host memory, every step.  Serving-style
     pipelining: inputs/outputs are double-buffered and the copies run on two copy streams,
-    so step i+1's upload and step i's download overlap step i's compute (PCIe duplex)."""
-    hA = [a.cpu().pin_memory() for a in A]
-    hC = [[torch.empty(c.shape, dtype=c.dtype, pin_memory=True) for c in Cd] for _ in range(2)]
-    dA = [A, [torch.empty_like(a) for a in A]]
-    dC = [Cd, [torch.empty_like(c) for c in Cd]]
+    so step i+1's upload and step i's download overlap step i's compute (PCIe duplex).  The
+    ranks' shards of a step are one contiguous buffer each way (one copy per direction per
+    step; the per-rank tensors the ops take are row views of it), so the host issues few
+    calls per step."""
+    r = len(A)
+    S_in, S_out = A[0].shape[0], Cd[0].shape[0]
+    hA = torch.cat([a.cpu() for a in A], 0).pin_memory()
+    hC = [torch.empty((r * S_out,) + tuple(Cd[0].shape[1:]), dtype=Cd[0].dtype, pin_memory=True) for _ in range(2)]
+    dA_all = [torch.empty(hA.shape, dtype=hA.dtype, device=dev) for _ in range(2)]
+    dC_all = [torch.empty(hC[0].shape, dtype=hC[0].dtype, device=dev) for _ in range(2)]
+    dA = [[t[k * S_in:(k + 1) * S_in] for k in range(r)] for t in dA_all]
+    dC = [[t[k * S_out:(k + 1) * S_out] for k in range(r)] for t in dC_all]
     stream = torch.cuda.current_stream()
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
     computed = [torch.cuda.Event() for _ in range(2)]
     uploaded = [torch.cuda.Event() for _ in range(2)]
     downloaded = [torch.cuda.Event() for _ in range(2)]
     n = max(4, args.steps // 2)
+    # per-step diagnosis: the copy and compute spans as they ran inside the pipelined loop
+    ev_up = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n + 2)]
+    ev_cp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n + 2)]
+    ev_dn = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n + 2)]
 
     def upload(i):
         b = i % 2
         up.wait_event(computed[b])  # compute of step i-2 finished reading dA[b]
+        ev_up[i][0].record(up)
         with torch.cuda.stream(up):
-            for d, h in zip(dA[b], hA):
-                d.copy_(h, non_blocking=True)
+            dA_all[b].copy_(hA, non_blocking=True)
+        ev_up[i][1].record(up)
         uploaded[b].record(up)
 
     def run(i):
         b = i % 2
         stream.wait_event(uploaded[b])
         stream.wait_event(downloaded[b])  # dC[b] of step i-2 has been read back
+        ev_cp[i][0].record(stream)
         step(A_in=dA[b], C_out=dC[b])
+        ev_cp[i][1].record(stream)
         computed[b].record(stream)
         down.wait_event(computed[b])
+        ev_dn[i][0].record(down)
         with torch.cuda.stream(down):
-            for h, d in zip(hC[b], dC[b]):
-                h.copy_(d, non_blocking=True)
+            hC[b].copy_(dC_all[b], non_blocking=True)
+        ev_dn[i][1].record(down)
         downloaded[b].record(down)
 
     for b in range(2):
@@ -1032,42 +1047,55 @@ def e2e_leg(torch, dist, args, A, Cd, step, barrier, world, flops_step, dev):
     barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
+    t_host = time.perf_counter()
     upload(1)
     for i in range(1, n + 1):
         if i + 1 <= n:
             upload(i + 1)
         run(i)
+    host_ms = (time.perf_counter() - t_host) * 1e3 / n
     stream.wait_event(downloaded[n % 2])
     e.record(stream)
     barrier()
     ms = s.elapsed_time(e) / n
+    med = lambda evs: round(statistics.median(a.elapsed_time(b) for a, b in evs[2:n]), 4)
+    spans = {"upload_ms": med(ev_up), "compute_ms": med(ev_cp), "download_ms": med(ev_dn),
+             "compute_start_gap_ms": round(statistics.median(ev_cp[i][0].elapsed_time(ev_cp[i + 1][0])
+                                                             for i in range(2, n - 1)), 4)}
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
-    h2d = sum(h.numel() * h.element_size() for h in hA)
-    d2h = sum(h.numel() * h.element_size() for h in hC[0])
-    # the PCIe bound: this step's copies alone, each direction, on the same streams
+    h2d = hA.numel() * hA.element_size()
+    d2h = hC[0].numel() * hC[0].element_size()
+    # the PCIe bound: this step's copies alone, each direction, then both at once
     link = {}
-    for name, st, pairs in (("h2d_gbs_alone", up, list(zip(dA[0], hA))), ("d2h_gbs_alone", down, list(zip(hC[0], dC[0])))):
+    for name, st, dst, src in (("h2d_gbs_alone", up, dA_all[0], hA), ("d2h_gbs_alone", down, hC[0], dC_all[0])):
         torch.cuda.synchronize()
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         c0.record(st)
         with torch.cuda.stream(st):
             for _ in range(3):
-                for d, h in pairs:
-                    d.copy_(h, non_blocking=True)
+                dst.copy_(src, non_blocking=True)
         c1.record(st)
         torch.cuda.synchronize()
-        nb = 3 * sum(d.numel() * d.element_size() for d, _ in pairs)
-        link[name] = round(nb / (c0.elapsed_time(c1) * 1e-3) / 1e9, 1)
+        link[name] = round(3 * src.numel() * src.element_size() / (c0.elapsed_time(c1) * 1e-3) / 1e9, 1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for st, dst, src in ((up, dA_all[0], hA), (down, hC[0], dC_all[0])):
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    link["duplex_gbs_per_direction"] = round(3 * h2d / (time.perf_counter() - t0) / 1e9, 1)
+    link["io_bound_ms_per_step"] = round(max(h2d, d2h) / (link["duplex_gbs_per_direction"] * 1e9) * 1e3, 4)
     if world > 1:
         h2d *= world
         d2h *= world
     return {"value": round(flops_step / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "pipelining": "double-buffered; H2D of step i+1 and D2H of step i overlap step i's compute",
-            "pcie": link}
+            "host_ms_per_step": round(host_ms, 4), "pcie": link, "spans_in_loop": spans}
 
 
 # ============================================================================ CPU oracle

@@ -431,6 +431,7 @@ def run_ours(args, rank, world, local_rank):
                      "peak_regime": regime, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4),
                      "frac_of_burst": round(achieved / peaks["bf16_tflops"], 4),
+                     "frac_of_nominal": round(achieved / 2250.0, 4),  # 2.25 PFLOP/s dense bf16
                      # the tensor pipe's own ceiling at the clock the kernel ran: 148 SMs x 8192
                      # dense bf16 flop/clk (tcgen05 kind::f16; 2.25 PFLOP/s nominal = 1.86 GHz)
                      "frac_at_kernel_clock": (round(achieved / (torch.cuda.get_device_properties(dev).multi_processor_count * 8192 * f_dom * 1e-6), 4) if f_dom else None),

@@ -130,6 +130,25 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def nvlink_roofline(W, M, F, loop, ag_ms, rs_ms, peak, flops):
+    """SURVEY §8(d) per-rank roofline of the fused ops: T_roof = max(FLOPs_rank / P, wire bytes
+    per rank per direction / B_link) with B_link = 900 GB/s nominal (770 measured peer copy):
+    AG (W-1)/W*M*K*2, RS (W-1)/W*M*N*4 (fp32 partials).  In loopback (N = 1) the transfers stay
+    on the GPU, so the link terms are what TP=W would need, not what was measured."""
+    f_rank = flops / (W if loop else 1)
+    out = {"link_gbs": 900.0, "link_gbs_measured_peer_copy": 770.0,
+           "exercised": not loop}
+    for op, wire, ms in (("ag_gemm", (W - 1) / W * M * HIDDEN * 2, ag_ms), ("gemm_rs", (W - 1) / W * M * HIDDEN * 4, rs_ms)):
+        t_gemm = f_rank / (peak * 1e12) * 1e3
+        t_link = wire / 900e9 * 1e3
+        d = {"wire_bytes_per_rank": int(wire), "t_gemm_ms": round(t_gemm, 4), "t_link_ms": round(t_link, 4),
+             "bound": "nvlink" if t_link > t_gemm else "tensor", "t_roof_ms": round(max(t_gemm, t_link), 4)}
+        if not loop:
+            d["frac"] = round(max(t_gemm, t_link) / ms, 4)
+        out[op] = d
+    return out
+
+
 def choose_peak(peaks, f_kernel):
     """Roofline denominator by the task's rule -- the burst figure for a kernel timed alone,
     the sustained one for a kernel timed inside a long step -- decided by measurement: the
@@ -439,7 +458,8 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
                      "flops_per_launch": per_launch_flops,
                      "per_kernel": {"ag_gemm": {"achieved": round(ag_ach, 1), "frac": round(ag_ach / peak, 4)},
-                                    "gemm_rs": {"achieved": round(rs_ach, 1), "frac": round(rs_ach / peak, 4)}}},
+                                    "gemm_rs": {"achieved": round(rs_ach, 1), "frac": round(rs_ach / peak, 4)}},
+                     "nvlink": nvlink_roofline(W, M, F, loop, ag_ms, rs_ms, peak, per_launch_flops)},
         "clocks": clk.summary(),
         # not the NVML record above: clock64 / globaltimer over the fused kernels' MMA spans
         # (three extra steps after the timed region) -- the power limit's effective SM clock

@@ -57,3 +57,15 @@ def test_kernel_clocks_reads_ag_and_rs_launches_after_the_first_step():
     out = bench.kernel_clocks(ctx, lambda: calls.append(1), steps=3)
     assert len(calls) == 3
     assert abs(out["ag_gemm"] - 1205) <= 5 and abs(out["gemm_rs"] - 1295) <= 5
+
+
+def test_nvlink_roofline_matches_survey_table():
+    """SURVEY §8(d) table, TP=8 rows: AG 58.7 MB / RS 117.4 MB of wire per rank; at 900 GB/s the
+    RS is link-bound (130.5 us) and the AG tensor-bound."""
+    r = bench.nvlink_roofline(8, 8192, 1792, False, 0.1, 0.14, 1626.5, 120.26e9)
+    assert r["ag_gemm"]["wire_bytes_per_rank"] == 7 * 8192 * 4096 * 2 // 8 == 58720256
+    assert r["gemm_rs"]["wire_bytes_per_rank"] == 7 * 8192 * 4096 * 4 // 8
+    assert r["ag_gemm"]["bound"] == "tensor" and abs(r["ag_gemm"]["t_gemm_ms"] - 0.0739) < 1e-3
+    assert r["gemm_rs"]["bound"] == "nvlink" and abs(r["gemm_rs"]["t_link_ms"] - 0.1305) < 1e-3
+    loop = bench.nvlink_roofline(8, 8192, 1792, True, 0.77, 0.83, 1374.5, 962.07e9)
+    assert not loop["exercised"] and "frac" not in loop["gemm_rs"]
